@@ -1,0 +1,539 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+Nothing here compares the oracle with itself or with the CUDA path: every
+expected value is a paper value (tests/golden/, cited), a closed form, a
+textbook relation derived independently in this file (moment-cumulant
+partition formula, textbook BGK equilibrium, Gaussian product distribution),
+an invariant, or brute force on tiny inputs.
+"""
+from __future__ import annotations
+
+import itertools
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+STENCILS = [W.D2Q9, W.D3Q19, W.D3Q27]
+LINEAR_SPACES = [W.POPULATION, W.RAW, W.CENTRAL]
+ALL_REGIMES = [(W.EQ_ABSOLUTE, 0), (W.EQ_DELTA, 1), (W.EQ_ABSOLUTE, 1)]
+
+
+def admissible(space):
+    """(eq, zc) pairs admissible for a space."""
+    if space == W.CUMULANT:
+        return [(W.EQ_ABSOLUTE, 0), (W.EQ_ABSOLUTE, 1)]
+    return ALL_REGIMES
+
+
+def rates_for(stencil, space, value=None, seed=7):
+    if space == W.POPULATION:
+        return np.array([1.3 if value is None else value])
+    if value is not None:
+        return np.full(W.Q_OF[stencil], float(value))
+    return W.rates_random(stencil, seed=seed)
+
+
+def random_cells(stencil, n, amp=2e-2, seed=3, umax=0.08):
+    """Absolute populations near a random equilibrium-ish state (positive)."""
+    xi, opp, w, M, Minv = oracle.tables(stencil)
+    rng = np.random.default_rng(seed)
+    rho = 1.0 + rng.uniform(-0.05, 0.05, n)
+    u = rng.uniform(-umax, umax, (n, 3))
+    if W.DIM_OF[stencil] == 2:
+        u[:, 2] = 0
+    f = textbook_feq(stencil, rho, u)
+    f += amp * w * rng.uniform(-1, 1, f.shape)
+    return f
+
+
+def textbook_feq(stencil, rho, u):
+    """Second-order Hermite equilibrium f_i = w_i rho (1 + 3 xi.u + 9/2 (xi.u)^2 - 3/2 u^2)
+    (textbook, e.g. Krueger et al. 2017 eq. 3.54 — typed here independently)."""
+    xi, opp, w, M, Minv = oracle.tables(stencil)
+    cu = u @ xi.T
+    uu = (u * u).sum(1, keepdims=True)
+    return w * rho[:, None] * (1 + 3 * cu + 4.5 * cu * cu - 1.5 * uu)
+
+
+def product_feq(stencil, rho, u):
+    """Equilibrium whose central moments are the Gaussian's (u-independent):
+    f = rho prod_a phi(xi_a, u_a), phi(0) = 1 - cs2 - u^2, phi(+-1) = (cs2 + u^2 +- u)/2.
+    Typed here from the per-axis moment conditions (sum 1, mean u, var cs2)."""
+    xi, opp, w, M, Minv = oracle.tables(stencil)
+    d = W.DIM_OF[stencil]
+    f = np.ones((rho.size, xi.shape[0])) * rho[:, None]
+    for a in range(d):
+        ua = u[:, a:a + 1]
+        x = xi[None, :, a]
+        phi = np.where(x == 0, 1 - 1 / 3 - ua * ua, (1 / 3 + ua * ua + x * ua) / 2)
+        f = f * phi
+    return f
+
+
+# ---------------------------------------------------------------- stencils ---
+def test_weights_golden():
+    """f0 = M^{-1} m0 reduces to the lattice weights."""
+    gold = {}
+    for line in open(os.path.join(GOLDEN, "weights.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        st, n2, num, den = line.split()
+        gold[(W.STENCILS[st], int(n2))] = int(num) / int(den)
+    for st in STENCILS:
+        xi, opp, w, M, Minv = oracle.tables(st)
+        for i in range(len(w)):
+            n2 = int((xi[i] ** 2).sum())
+            assert w[i] == pytest.approx(gold[(st, n2)], abs=1e-16), (st, i)
+        assert w.sum() == pytest.approx(1.0, abs=1e-15)
+
+
+@pytest.mark.parametrize("st", STENCILS)
+def test_stencil_convention(st):
+    """xi_0 = 0; opposite pairs; slab-axis groups contiguous
+    (interface convention of include/lbm.h)."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    q = W.Q_OF[st]
+    assert xi.shape == (q, 3)
+    assert (xi[0] == 0).all()
+    assert len({tuple(v) for v in xi}) == q
+    for i in range(q):
+        assert (xi[opp[i]] == -xi[i]).all()
+        assert opp[opp[i]] == i
+    slab = 1 if st == W.D2Q9 else 2
+    comp = xi[:, slab]
+    n_up = int((comp == 1).sum())
+    first_up = int(np.argmax(comp == 1))
+    # +1 group contiguous, followed by the -1 group as its negation in the same order
+    assert (comp[first_up:first_up + n_up] == 1).all()
+    assert (comp[first_up + n_up:] == -1).all()
+    for k in range(n_up):
+        assert opp[first_up + k] == first_up + n_up + k
+    assert n_up == {W.D2Q9: 3, W.D3Q19: 5, W.D3Q27: 9}[st]
+    if st == W.D3Q19:
+        assert (np.abs(xi).sum(1) <= 2).all()
+
+
+@pytest.mark.parametrize("st", STENCILS)
+def test_moment_matrix_invertible(st):
+    """M is invertible for the basis: M M^{-1} = I."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    q = W.Q_OF[st]
+    assert np.linalg.matrix_rank(M) == q
+    assert np.abs(M @ Minv - np.eye(q)).max() < 1e-14
+    # row of p = 1 on w gives 1; p = x^2 gives cs^2
+    assert (M[0] @ w) == pytest.approx(1.0, abs=1e-15)
+    xx = (xi[:, 0] ** 2) @ w
+    assert xx == pytest.approx(1 / 3, abs=1e-15)
+
+
+# --------------------------------------------------- central moments / K ---
+def raw_monomials(stencil, f):
+    """m_abc = sum_i f_i xi_x^a xi_y^b xi_z^c (eq:DiscreteRawMomentsDef), all 27."""
+    xi, *_ = oracle.tables(stencil)
+    out = np.zeros((f.shape[0], 27))
+    for k in range(27):
+        e = (k % 3, (k // 3) % 3, k // 9)
+        out[:, k] = f @ (xi[:, 0] ** e[0] * xi[:, 1] ** e[1] * xi[:, 2] ** e[2])
+    return out
+
+
+@pytest.mark.parametrize("st", STENCILS)
+def test_central_moments_binomial(st):
+    """kappa_abc = sum_{a'b'c'} C(a,a')C(b,b')C(c,c') (-u)^... m_a'b'c'
+    (eq:RawToCentralMomentsBinomial); kappa_200 = m_200 - 2u m_100
+    + u^2 m_000; at u = 0 central = raw (K(0) = M)."""
+    f = random_cells(st, 20)
+    k27, C27, rho, u = oracle.central_and_cumulants(st, f)
+    m = raw_monomials(st, f)
+    for k in range(27):
+        e = (k % 3, (k // 3) % 3, k // 9)
+        s = np.zeros(f.shape[0])
+        for a in range(e[0] + 1):
+            for b in range(e[1] + 1):
+                for c in range(e[2] + 1):
+                    coef = math.comb(e[0], a) * math.comb(e[1], b) * math.comb(e[2], c)
+                    s += (coef * (-u[:, 0]) ** (e[0] - a) * (-u[:, 1]) ** (e[1] - b) * (-u[:, 2]) ** (e[2] - c)
+                          * m[:, a + 3 * b + 9 * c])
+        np.testing.assert_allclose(k27[:, k], s, atol=1e-15, rtol=1e-13)
+    np.testing.assert_allclose(k27[:, 2], m[:, 2] - 2 * u[:, 0] * m[:, 1] + u[:, 0] ** 2 * m[:, 0], atol=1e-15)
+    # kappa_000 = rho and kappa_100 = 0 (F = 0)
+    np.testing.assert_allclose(k27[:, 0], rho, rtol=1e-15)
+    assert np.abs(k27[:, [1, 3, 9]]).max() < 1e-16
+    # u = 0: a distribution with zero momentum has central == raw moments
+    xi, opp, w, M, Minv = oracle.tables(st)
+    g = f.copy()
+    g[:, :] = g[:, :] + g[:, opp]  # symmetric => zero momentum
+    k0, _, _, u0 = oracle.central_and_cumulants(st, g)
+    assert np.abs(u0).max() < 1e-16
+    np.testing.assert_allclose(k0, raw_monomials(st, g), atol=1e-15)
+
+
+# --------------------------------------------------------------- cumulants ---
+def set_partitions(items):
+    if not items:
+        yield []
+        return
+    first, rest = items[0], items[1:]
+    for part in set_partitions(rest):
+        for k in range(len(part)):
+            yield part[:k] + [[first] + part[k]] + part[k + 1:]
+        yield [[first]] + part
+
+
+def cumulant_by_partitions(stencil, f, e):
+    """Classical moment-cumulant formula (Leonov-Shiryaev): the joint cumulant of
+    the multiset of axes {x^a y^b z^c} of the normalised distribution f/rho is
+    sum over set partitions pi of (-1)^{|pi|-1} (|pi|-1)! prod_B mu_B, mu = raw moments.
+    Independent of the oracle's generating-function series."""
+    xi, *_ = oracle.tables(stencil)
+    rho = f.sum(1)
+    labels = [0] * e[0] + [1] * e[1] + [2] * e[2]
+    total = np.zeros(f.shape[0])
+    for part in set_partitions(list(range(len(labels)))):
+        k = len(part)
+        term = (-1) ** (k - 1) * math.factorial(k - 1) * np.ones(f.shape[0])
+        for B in part:
+            v = np.ones(xi.shape[0])
+            for idx in B:
+                v = v * xi[:, labels[idx]]
+            term = term * (f @ v) / rho
+        total += term
+    return rho * total  # rescaled C = rho c
+
+
+@pytest.mark.parametrize("st", STENCILS)
+def test_cumulants_partition_formula(st):
+    """Every cumulant of order >= 2 equals the partition formula on raw moments."""
+    f = random_cells(st, 12, amp=5e-2)
+    k27, C27, rho, u = oracle.central_and_cumulants(st, f)
+    for k in range(27):
+        e = (k % 3, (k // 3) % 3, k // 9)
+        if sum(e) < 2:
+            continue
+        if W.DIM_OF[st] == 2 and e[2] > 0:
+            continue
+        ref = cumulant_by_partitions(st, f, e)
+        np.testing.assert_allclose(C27[:, k], ref, atol=2e-15, rtol=1e-12, err_msg=str(e))
+
+
+@pytest.mark.parametrize("st", [W.D2Q9, W.D3Q27])
+def test_cumulants_of_product_distribution(st):
+    """Independent axes => every mixed cumulant vanishes; C_200 = rho Var_x
+    (mutual statistical independence)."""
+    rng = np.random.default_rng(11)
+    xi, *_ = oracle.tables(st)
+    n = 8
+    d = W.DIM_OF[st]
+    f = np.ones((n, xi.shape[0])) * rng.uniform(0.9, 1.1, (n, 1))
+    var = np.zeros((n, 3))
+    for a in range(d):
+        p = rng.uniform(0.2, 1.0, (n, 3))
+        p /= p.sum(1, keepdims=True)
+        f *= p[np.arange(n)[:, None], xi[None, :, a] + 1]
+        mean = p[:, 2] - p[:, 0]
+        var[:, a] = p[:, 2] + p[:, 0] - mean ** 2
+    k27, C27, rho, u = oracle.central_and_cumulants(st, f)
+    for k in range(27):
+        e = (k % 3, (k // 3) % 3, k // 9)
+        if sum(e) < 2:
+            continue
+        nz = sum(1 for v in e if v > 0)
+        if nz >= 2:
+            assert np.abs(C27[:, k]).max() < 1e-16, e
+    for a, k in enumerate([2, 6, 18][:d]):
+        np.testing.assert_allclose(C27[:, k], rho * var[:, a], rtol=1e-14)
+
+
+@pytest.mark.parametrize("st", STENCILS)
+def test_cumulant_series_roundtrip(st):
+    """K = exp(C - Xi.u) inverts C = Xi.u + log K (eq:CumulantAndCentralMomentGenFuncs)."""
+    f = random_cells(st, 6, amp=5e-2)
+    k27, C27, rho, u = oracle.central_and_cumulants(st, f)
+    for c in range(f.shape[0]):
+        back = oracle.cumulant_roundtrip(k27[c], rho[c])
+        np.testing.assert_allclose(back, k27[c], atol=1e-16, rtol=1e-14)
+
+
+# ------------------------------------------------------------- collision ---
+@pytest.mark.parametrize("st", STENCILS)
+@pytest.mark.parametrize("space", [W.POPULATION, W.RAW, W.CENTRAL, W.CUMULANT])
+def test_collision_invariants(st, space):
+    """Per cell: mass and momentum conserved; equilibrium is a fixed point;
+    rates 0 => identity; rates 1 => f_eq."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    fa = random_cells(st, 30)
+    rho = fa.sum(1)
+    u = (fa @ xi) / rho[:, None]
+    for eq, zc in admissible(space):
+        rates = rates_for(st, space)
+        fin = fa - w if zc else fa
+        fo = oracle.collide(st, space, eq, zc, rates, fin)
+        fo_abs = fo + w if zc else fo
+        np.testing.assert_allclose(fo_abs.sum(1), rho, rtol=0, atol=1e-15)
+        np.testing.assert_allclose(fo_abs @ xi, fa @ xi, rtol=0, atol=1e-16)
+        feq = oracle.equilibrium(st, space, eq, zc, rho, u)
+        np.testing.assert_allclose(oracle.collide(st, space, eq, zc, rates, feq), feq, atol=1e-16)
+        r0 = oracle.collide(st, space, eq, zc, rates_for(st, space, 0.0), fin)
+        np.testing.assert_allclose(r0, fin, atol=1e-16)
+        r1 = oracle.collide(st, space, eq, zc, rates_for(st, space, 1.0), fin)
+        np.testing.assert_allclose(r1, feq, atol=1e-16)
+
+
+@pytest.mark.parametrize("st", STENCILS)
+@pytest.mark.parametrize("space", LINEAR_SPACES)
+def test_background_invariance(st, space):
+    """delta f = 0 stays 0 in the deviation-only regime.  For
+    CENTRAL the oracle forms dq_eq = q_eq - T(f0) literally with the
+    numerically inverted f0, so it is zero only to long-double rounding."""
+    q = W.Q_OF[st]
+    fo = oracle.collide(st, space, W.EQ_DELTA, 1, rates_for(st, space), np.zeros((3, q)))
+    if space == W.CENTRAL:
+        assert np.abs(fo).max() < 1e-18
+    else:
+        assert (fo == 0).all()
+
+
+@pytest.mark.parametrize("st", [W.D2Q9, W.D3Q27])
+def test_bgk_equivalence(st):
+    """All rates equal: RAW reduces to BGK with the textbook Hermite f_eq; CENTRAL
+    and CUMULANT (omega = 1) to BGK with the Gaussian product f_eq."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    fa = random_cells(st, 25)
+    rho = fa.sum(1)
+    u = (fa @ xi) / rho[:, None]
+    om = 1.37
+    ref_raw = fa + om * (textbook_feq(st, rho, u) - fa)
+    ref_cm = fa + om * (product_feq(st, rho, u) - fa)
+    for eq, zc in ALL_REGIMES:
+        fin = fa - w if zc else fa
+        back = (lambda x: x + w) if zc else (lambda x: x)
+        np.testing.assert_allclose(back(oracle.collide(st, W.RAW, eq, zc, rates_for(st, W.RAW, om), fin)),
+                                   ref_raw, atol=1e-16)
+        np.testing.assert_allclose(back(oracle.collide(st, W.POPULATION, eq, zc, [om], fin)), ref_raw, atol=1e-16)
+        np.testing.assert_allclose(back(oracle.collide(st, W.CENTRAL, eq, zc, rates_for(st, W.CENTRAL, om), fin)),
+                                   ref_cm, atol=1e-16)
+    for zc in (0, 1):
+        fin = fa - w if zc else fa
+        out = oracle.collide(st, W.CUMULANT, W.EQ_ABSOLUTE, zc, rates_for(st, W.CUMULANT, 1.0), fin)
+        np.testing.assert_allclose(out + (w if zc else 0), product_feq(st, rho, u), atol=1e-16)
+        # and K is NOT BGK at omega != 1 (nonlinear transform)
+        out = oracle.collide(st, W.CUMULANT, W.EQ_ABSOLUTE, zc, rates_for(st, W.CUMULANT, om), fin)
+        assert np.abs(out + (w if zc else 0) - ref_cm).max() > 1e-9
+
+
+def test_d3q19_equilibrium_moments():
+    """On D3Q19 the equilibrium is M^{-1} m_eq with m_eq the Maxwellian moments
+    truncated at O(u^2) (reading R4); hand-derived values."""
+    st = W.D3Q19
+    rng = np.random.default_rng(5)
+    n = 10
+    rho = rng.uniform(0.95, 1.05, n)
+    u = rng.uniform(-0.1, 0.1, (n, 3))
+    f = oracle.equilibrium(st, W.RAW, W.EQ_ABSOLUTE, 0, rho, u)
+    m = raw_monomials(st, f)
+    ux, uy, uz = u.T
+    idx = lambda a, b, c: a + 3 * b + 9 * c
+    np.testing.assert_allclose(m[:, idx(0, 0, 0)], rho, rtol=1e-15)
+    np.testing.assert_allclose(m[:, idx(1, 0, 0)], rho * ux, atol=1e-16)
+    np.testing.assert_allclose(m[:, idx(1, 1, 0)], rho * ux * uy, atol=1e-16)
+    np.testing.assert_allclose(m[:, idx(2, 0, 0)], rho * (1 / 3 + ux ** 2), atol=1e-16)
+    np.testing.assert_allclose(m[:, idx(2, 1, 0)], rho * uy / 3, atol=1e-16)
+    np.testing.assert_allclose(m[:, idx(1, 0, 2)], rho * ux / 3, atol=1e-16)
+    np.testing.assert_allclose(m[:, idx(2, 2, 0)], rho * (1 / 9 + (ux ** 2 + uy ** 2) / 3), atol=1e-16)
+    np.testing.assert_allclose(m[:, idx(0, 2, 2)], rho * (1 / 9 + (uy ** 2 + uz ** 2) / 3), atol=1e-16)
+    # ... which differs from the textbook D3Q19 polynomial by -rho uz^2 / 6 in m_220
+    mt = raw_monomials(st, textbook_feq(st, rho, u))
+    np.testing.assert_allclose(mt[:, idx(2, 2, 0)] - m[:, idx(2, 2, 0)], -rho * uz ** 2 / 6, atol=1e-16)
+
+
+@pytest.mark.parametrize("st", STENCILS)
+@pytest.mark.parametrize("space", [W.POPULATION, W.RAW, W.CENTRAL, W.CUMULANT])
+def test_regime_equivalence(st, space):
+    """absolute == zc + delta eq == zc + absolute eq under delta f = f - f0
+    (SPEC.md:508)."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    fa = random_cells(st, 20)
+    rates = rates_for(st, space)
+    outs = []
+    for eq, zc in admissible(space):
+        fin = fa - w if zc else fa
+        o = oracle.collide(st, space, eq, zc, rates, fin)
+        outs.append(o + w if zc else o)
+    for o in outs[1:]:
+        np.testing.assert_allclose(o, outs[0], atol=1.2e-16, rtol=0)  # ~1 ulp of the absolute populations (double output of + w)
+
+
+# ------------------------------------------------------ streaming / bc ---
+@pytest.mark.parametrize("st", STENCILS)
+def test_pull_moves_population_by_xi(st):
+    """eq:LbStreaming: with an identity collision (rate 0) a single
+    population travels one node along xi_i per step, wrapping periodically."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    q = W.Q_OF[st]
+    nx, ny, nz = (5, 4, 1) if st == W.D2Q9 else (5, 4, 6)
+    sim = oracle.Sim(st, W.POPULATION, W.EQ_DELTA, 1, [0.0], (nx, ny, nz))
+    for i in range(q):
+        f = np.zeros((q, nz, ny, nx))
+        x0, y0, z0 = 4, 0, nz - 1  # at the high/low edges to exercise the wrap
+        f[i, z0, y0, x0] = 1.0
+        sim.set(f)
+        sim.step(2)
+        g = sim.get()
+        x1, y1, z1 = (x0 + 2 * xi[i, 0]) % nx, (y0 + 2 * xi[i, 1]) % ny, (z0 + 2 * xi[i, 2]) % nz
+        assert g[i, z1, y1, x1] == 1.0
+        assert np.count_nonzero(g) == 1
+
+
+def test_bounce_back_reverses_population():
+    """Half-way bounce-back (reading R18): a population leaving through a no-slip
+    face returns to its node in the opposite slot one step later."""
+    st = W.D3Q19
+    xi, opp, w, M, Minv = oracle.tables(st)
+    q = 19
+    nx, ny, nz = 4, 5, 6
+    bc = [[W.PERIODIC, W.PERIODIC], [W.PERIODIC, W.PERIODIC], [W.NOSLIP, W.NOSLIP]]
+    sim = oracle.Sim(st, W.POPULATION, W.EQ_DELTA, 1, [0.0], (nx, ny, nz), bc=bc)
+    for i in range(q):
+        if xi[i, 2] == 0:
+            continue
+        f = np.zeros((q, nz, ny, nx))
+        z0 = nz - 1 if xi[i, 2] > 0 else 0
+        f[i, z0, 2, 1] = 1.0
+        sim.set(f)
+        sim.step(1)
+        g = sim.get()
+        assert g[opp[i], z0, 2, 1] == 1.0 and np.count_nonzero(g) == 1
+
+
+def test_mass_conserved_with_walls():
+    st = W.D3Q27
+    xi, opp, w, M, Minv = oracle.tables(st)
+    nx, ny, nz = 6, 5, 7
+    bc = [[W.NOSLIP, W.NOSLIP], [W.PERIODIC, W.PERIODIC], [W.NOSLIP, W.NOSLIP]]
+    sim = oracle.Sim(st, W.CUMULANT, W.EQ_ABSOLUTE, 1, W.rate_set_p(st), (nx, ny, nz), bc=bc)
+    rng = np.random.default_rng(2)
+    f = 1e-2 * w[:, None, None, None] * rng.uniform(-1, 1, (27, nz, ny, nx))
+    sim.set(f)
+    m0 = f.sum()
+    sim.step(5)
+    assert abs(sim.get().sum() - m0) < 1e-14
+
+
+# ----------------------------------------------------------------- physics ---
+def run_tgv(st, space, eq, zc, nu, u0, L, steps, prec=oracle.LONG_DOUBLE):
+    xi, opp, w, M, Minv = oracle.tables(st)
+    om = W.omega_from_nu(nu)
+    rates = [om] if space == W.POPULATION else W.regularized_rates(st, om)
+    rho, u = W.tgv_fields(L, L, 1, u0)
+    feq = oracle.equilibrium(st, space, eq, zc, rho.reshape(-1), u.reshape(3, -1).T)
+    sim = oracle.Sim(st, space, eq, zc, rates, (L, L, 1), prec=prec)
+    sim.set(np.ascontiguousarray(feq.T.reshape(W.Q_OF[st], 1, L, L)))
+
+    def energy():
+        r, uu = sim.macroscopic()
+        return 0.5 * (r * (uu ** 2).sum(0)).sum()
+
+    e0 = energy()
+    sim.step(steps)
+    return energy() / e0
+
+
+@pytest.mark.parametrize("space,eq,zc,nu", [
+    (W.POPULATION, W.EQ_DELTA, 1, 1 / 6),
+    (W.POPULATION, W.EQ_DELTA, 1, 0.02),
+    (W.RAW, W.EQ_DELTA, 1, 0.05),
+    (W.CENTRAL, W.EQ_ABSOLUTE, 1, 0.05),
+    (W.CUMULANT, W.EQ_ABSOLUTE, 1, 0.05),
+])
+def test_tgv_energy_decay(space, eq, zc, nu):
+    """E/E0 = exp(-4 nu kappa^2 t) (eq:TGA_kin_energy) within 1 %
+    at u0 = 0.05, L = 48, 300 steps; the shear group of reading R3 sets nu."""
+    L, steps = 48, 300
+    ratio = run_tgv(W.D2Q9, space, eq, zc, nu, 0.05, L, steps)
+    ref = W.tgv_energy_ratio(nu, L, steps)
+    assert abs(ratio / ref - 1) < 1e-2, (ratio, ref)
+
+
+def test_shear_wave_between_walls():
+    """Bounce-back pin (reading R18): u_x(y) = u0 sin(pi (y+1/2)/ny) between no-slip
+    walls decays as exp(-nu (pi/ny)^2 t)."""
+    st = W.D2Q9
+    nx, ny, steps, u0, nu = 4, 24, 200, 1e-3, 1 / 6
+    y = np.arange(ny)
+    ux = u0 * np.sin(np.pi * (y + 0.5) / ny)
+    rho = np.ones((ny, nx)).reshape(-1)
+    u = np.zeros((ny * nx, 3))
+    u[:, 0] = np.repeat(ux, nx)
+    feq = oracle.equilibrium(st, W.POPULATION, W.EQ_DELTA, 1, rho, u)
+    bc = [[W.PERIODIC, W.PERIODIC], [W.NOSLIP, W.NOSLIP], [W.PERIODIC, W.PERIODIC]]
+    sim = oracle.Sim(st, W.POPULATION, W.EQ_DELTA, 1, [W.omega_from_nu(nu)], (nx, ny, 1), bc=bc)
+    sim.set(np.ascontiguousarray(feq.T.reshape(9, 1, ny, nx)))
+    sim.step(steps)
+    r, uu = sim.macroscopic()
+    amp = (uu[0, 0, :, 0] * np.sin(np.pi * (y + 0.5) / ny)).sum() / (np.sin(np.pi * (y + 0.5) / ny) ** 2).sum()
+    ref = u0 * math.exp(-nu * (math.pi / ny) ** 2 * steps)
+    assert abs(amp / ref - 1) < 1e-2
+
+
+def test_swe_equilibrium_moments():
+    """Corrected eq:DiscreteShallowWaterEquilibrium (reading R5): sum f = h,
+    sum f xi = h u, sum f xi_a xi_b = h u_a u_b + g h^2/2 delta_ab (Zhou 2002)."""
+    st = W.D2Q9
+    xi, *_ = oracle.tables(st)
+    rng = np.random.default_rng(9)
+    n, g = 10, 0.0613125
+    h = rng.uniform(1.0, 6.0, n)
+    u = np.zeros((n, 3))
+    u[:, :2] = rng.uniform(-0.1, 0.1, (n, 2))
+    f = oracle.equilibrium(st, W.CENTRAL, W.EQ_SWE, 0, h, u, g=g)
+    np.testing.assert_allclose(f.sum(1), h, rtol=1e-15)
+    np.testing.assert_allclose(f @ xi[:, :2], h[:, None] * u[:, :2], atol=1e-15)
+    for a in range(2):
+        for b in range(2):
+            P = f @ (xi[:, a] * xi[:, b])
+            ref = h * u[:, a] * u[:, b] + (g * h * h / 2 if a == b else 0)
+            np.testing.assert_allclose(P, ref, atol=1e-14)
+
+
+def test_swe_collision_conserves():
+    st = W.D2Q9
+    xi, *_ = oracle.tables(st)
+    rng = np.random.default_rng(4)
+    n, g = 10, 0.0613125
+    h = rng.uniform(1.0, 6.0, n)
+    u = np.zeros((n, 3))
+    u[:, :2] = rng.uniform(-0.05, 0.05, (n, 2))
+    f = oracle.equilibrium(st, W.CENTRAL, W.EQ_SWE, 0, h, u, g=g)
+    f *= 1 + 0.02 * rng.uniform(-1, 1, f.shape)
+    rates = W.regularized_rates(st, 0.695652)
+    fo = oracle.collide(st, W.CENTRAL, W.EQ_SWE, 0, rates, f, g=g)
+    np.testing.assert_allclose(fo.sum(1), f.sum(1), rtol=1e-15)
+    np.testing.assert_allclose(fo @ xi, f @ xi, atol=1e-15)
+
+
+def paper_values():
+    vals = {}
+    for line in open(os.path.join(GOLDEN, "paper_values.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        k, v, tol, cite = line.split(None, 3)
+        vals[k] = (float(v), float(tol))
+    return vals
+
+
+def test_paper_values():
+    vals = paper_values()
+    g, nu, om = W.swe_lattice_parameters()
+    v, tol = vals["dam_break_omega_s"]
+    assert abs(om - v) < tol
+    v, tol = vals["tgv_omega_at_nu_1_6"]
+    assert abs(W.omega_from_nu(1 / 6) - v) < tol
+    v, tol = vals["tgv_rho_origin_u0_0.25"]
+    rho, u = W.tgv_fields(8, 8, 1, 0.25)
+    assert abs(rho[0, 0, 0] - v) < tol
