@@ -1,0 +1,184 @@
+/*
+ * lbm.h — C ABI of the B200-native MRT lattice Boltzmann stream–collide library
+ * (liblbm.so), the hot path of arXiv 2211.02435 (Hennig, Holzer, Rüde, lbmpy 1.1).
+ *
+ * One call of lbm_step() performs, for every lattice cell of this rank's slab,
+ * the fused update of eq:LbUpdateScheme:
+ *   pull (or AA in-place) gather of the q populations
+ *   -> conserved quantities rho, u                              (eq:DensityAndVelocity[FromDeviation])
+ *   -> forward Chimera transform to raw moments                 (eq:RawMomentChimeraTransform)
+ *   -> binomial Chimera raw -> central moments             [CENTRAL, CUMULANT]
+ *   -> central moments -> cumulants                             (eq:CumulantAndCentralMomentGenFuncs) [CUMULANT]
+ *   -> relaxation q* = q + S (q_eq - q)                         (eq:MrtUpdateGeneral / ...DeviationOnly /
+ *                                                                ...AbsoluteFromZeroCentered)
+ *   -> the inverse transforms and the store of q populations.
+ *
+ * Conventions
+ * -----------
+ * Units: lattice units, dx = dt = 1, cs^2 = 1/3, background density rho0 = 1.
+ *
+ * Velocity ordering (the paper leaves it free except xi_0 = 0).  The
+ * SLAB AXIS is the last lattice axis (z in 3D, y in 2D).  Order: rest; the velocities with
+ * slab component 0; slab component +1; slab component -1 (the negations of the +1 group in
+ * the same order).  Inside a group the in-plane part runs (0,0),(1,0),(-1,0),(0,1),(0,-1),
+ * (1,1),(-1,-1),(1,-1),(-1,1) (2D: x-part 0, 1, -1), keeping the stencil's members:
+ *   D2Q9  (x,y): 0 (0,0) | 1 (1,0) 2 (-1,0) | 3 (0,1) 4 (1,1) 5 (-1,1) | 6 (0,-1) 7 (-1,-1) 8 (1,-1)
+ *   D3Q19: 0 | 1-8 in-plane | 9-13 (0,0,1),(1,0,1),(-1,0,1),(0,1,1),(0,-1,1) | 14-18 their negations
+ *   D3Q27: 0 | 1-8 in-plane | 9-17 (0,0,1),(1,0,1),(-1,0,1),(0,1,1),(0,-1,1),(1,1,1),(-1,-1,1),
+ *          (1,-1,1),(-1,1,1) | 18-26 their negations
+ * so opposite(i) pairs (1,2),(3,4),(5,6),(7,8) in-plane and i <-> i + n_up across the slab
+ * axis, and the populations crossing a slab face form one contiguous index block.
+ *
+ * Collision-space bases (one relaxation rate per polynomial, in this order; R2):
+ *   D3Q27: 1; x, y, z; xy, xz, yz, x^2-y^2, x^2-z^2 [shear]; x^2+y^2+z^2 [bulk];
+ *          xy^2+xz^2, x^2y+yz^2, x^2z+y^2z; xy^2-xz^2, x^2y-yz^2, x^2z-y^2z; xyz;
+ *          x^2y^2-2x^2z^2+y^2z^2, x^2y^2+x^2z^2-2y^2z^2; x^2y^2+x^2z^2+y^2z^2;
+ *          x^2yz, xy^2z, xyz^2; xy^2z^2, x^2yz^2, x^2y^2z; x^2y^2z^2          (27 rates)
+ *   D3Q19: the D3Q27 list without xyz and without the last seven (orders 4 mixed, 5, 6)   (19 rates)
+ *   D2Q9 : 1; x, y; xy, x^2-y^2 [shear]; x^2+y^2 [bulk]; x^2y, xy^2; x^2y^2               (9 rates)
+ *   POPULATION space (SRT/BGK): a single rate.
+ * Rates of the conserved polynomials (orders 0 and 1) are accepted and ignored.
+ *
+ * Host population arrays: f[i][z][y][x], x fastest, this rank's slab only (2D: f[i][y][x]),
+ * in STORED form (delta f = f - f0 when zero_centered), fp64 regardless of storage precision.
+ * Host macroscopic arrays: rho[z][y][x]; u[d][z][y][x] (d = 2 for D2Q9, 3 otherwise).
+ * For LBM_EQ_SWE the density slot carries the water height h.
+ *
+ * Errors: every call returns lbm_status; on failure a message is available from
+ * lbm_last_error(ctx) (or lbm_last_error(NULL) for a failed lbm_create).  Contexts are
+ * thread-compatible, not thread-safe.  All host arrays are borrowed for the duration of the
+ * call only; the context owns every device buffer it allocates.
+ */
+#ifndef LBM_H
+#define LBM_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lbm_ctx lbm_ctx;
+
+typedef enum {
+  LBM_OK = 0,
+  LBM_EINVAL = -1,       /* bad argument: null pointer, rate outside [0,2], n_rates != q, extent < 4, ... */
+  LBM_EUNSUPPORTED = -2, /* inadmissible combination or not built                     */
+  LBM_ENOMEM = -3,       /* device allocation failed                                                     */
+  LBM_ECUDA = -4,        /* CUDA runtime error / no device                                               */
+  LBM_ENUMERIC = -6      /* non-finite population detected by lbm_check_finite                          */
+} lbm_status;
+
+typedef enum { LBM_D2Q9 = 0, LBM_D3Q19 = 1, LBM_D3Q27 = 2 } lbm_stencil;
+typedef enum {
+  LBM_SPACE_POPULATION = 0, /* SRT / BGK, T = identity                     */
+  LBM_SPACE_RAW = 1,        /* raw moments               */
+  LBM_SPACE_CENTRAL = 2,    /* central moments           */
+  LBM_SPACE_CUMULANT = 3    /* cumulants                 */
+} lbm_space;
+typedef enum {
+  LBM_EQ_ABSOLUTE = 0, /* continuous Maxwellian, absolute form                    */
+  LBM_EQ_DELTA = 1,    /* deviation-only delta equilibrium: zero-centered only,
+                          not with cumulants                                       */
+  LBM_EQ_SWE = 2       /* Zhou shallow-water equilibrium (reading R5): D2Q9 +
+                          CENTRAL + absolute storage only                                             */
+} lbm_equilibrium;
+typedef enum { LBM_FP64 = 0, LBM_FP32 = 1 } lbm_precision;
+typedef enum { LBM_PULL = 0, LBM_AA = 1 } lbm_streaming;
+typedef enum { LBM_BC_PERIODIC = 0, LBM_BC_NOSLIP = 1 } lbm_bc;
+typedef enum { LBM_REGION_ALL = 0, LBM_REGION_BOUNDARY = 1, LBM_REGION_INTERIOR = 2 } lbm_region;
+
+typedef struct {
+  int nx, ny, nz;  /* GLOBAL lattice extents; D2Q9: nz = 1 (the slab axis is then y)        */
+  int bc[3][2];    /* [axis][low, high] lbm_bc; periodic must be set on both faces of an axis */
+  int precision;   /* lbm_precision (storage and arithmetic precision)                        */
+  int streaming;   /* lbm_streaming; LBM_AA needs nranks == 1 and all faces periodic          */
+  double swe_g;    /* lattice gravity g (LBM_EQ_SWE only)                                     */
+  int device;      /* CUDA device ordinal                                                     */
+  void *stream;    /* cudaStream_t to enqueue on, or NULL: the library creates its own        */
+  int rank;        /* slab decomposition along the slab axis: this rank ...                  */
+  int nranks;      /* ... of nranks (nranks must divide the slab extent; slabs >= 2 planes)   */
+} lbm_domain;
+
+/* Device-side halo description of one population grid (nranks > 1).
+   send_lo: local slab plane 0, the slab-component -1 population block -> rank-1's recv_hi
+   send_hi: local plane n-1, the slab-component +1 block               -> rank+1's recv_lo
+   recv_lo/recv_hi: the ghost planes below/above the slab (same population blocks).
+   Every block is contiguous, 'bytes' long. */
+typedef struct {
+  void *send_lo, *send_hi, *recv_lo, *recv_hi;
+  size_t bytes;
+} lbm_halo;
+
+typedef struct {
+  int q, d;                 /* populations per cell, dimensions                          */
+  int offset, extent;       /* this rank's slab along the slab axis (global plane index) */
+  int nx, ny, nz;           /* global extents                                            */
+  size_t pitch;             /* x pitch of the device rows (elements)                      */
+  size_t bytes_per_element; /* 8 (fp64) or 4 (fp32)                                       */
+  size_t device_bytes;      /* population storage allocated on the device                 */
+  long long steps_done;     /* time steps taken since the last init/set                   */
+} lbm_info;
+
+/* Creates a context: validates admissibility, allocates the population grid(s) (two for
+   PULL, one for AA; each with one ghost plane per slab face) and uploads the rates.
+   relaxation_rates: n_rates doubles in basis order (1 for POPULATION, q otherwise).
+   zero_centered: store delta f = f - f0.  On failure *out = NULL. */
+lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equilibrium equilibrium,
+                      const double *relaxation_rates, int n_rates, const lbm_domain *domain,
+                      int zero_centered, lbm_ctx **out);
+lbm_status lbm_destroy(lbm_ctx *ctx);
+const char *lbm_last_error(const lbm_ctx *ctx);
+lbm_status lbm_get_info(const lbm_ctx *ctx, lbm_info *info);
+
+/* Writes the post-collision state f*(x, 0) = f_eq(rho, u) of the method's own equilibrium
+   (stored form) for this rank's slab.  rho: [cells]; u: [d][cells] (host, fp64).  Resets
+   the step counter.  Multi-rank callers must exchange halos of the current grid afterwards. */
+lbm_status lbm_init_macroscopic(lbm_ctx *ctx, const double *rho, const double *u);
+
+/* n fused stream–collide time steps (single rank; asynchronous on the context stream). */
+lbm_status lbm_step(lbm_ctx *ctx, int n);
+
+/* Multi-rank building blocks of one step: update the given planes from the current grid into
+   the next grid on 'stream' (NULL: context stream), then lbm_swap() once all regions are done
+   and the next grid's ghost planes were received. */
+lbm_status lbm_step_region(lbm_ctx *ctx, lbm_region region, void *stream);
+lbm_status lbm_swap(lbm_ctx *ctx);
+/* which = 0: the current grid, 1: the next (destination) grid. */
+lbm_status lbm_get_halo(lbm_ctx *ctx, int which, lbm_halo *out);
+
+lbm_status lbm_sync(lbm_ctx *ctx);
+
+/* rho [cells], u [d][cells] of the canonical post-collision state (host, fp64; synchronises). */
+lbm_status lbm_get_macroscopic(lbm_ctx *ctx, double *rho, double *u);
+/* Canonical post-collision populations f*(x, t) in stored form, independent of the AA parity
+   (reading R11), f[i][z][y][x] fp64 (host; synchronises). */
+lbm_status lbm_get_populations(lbm_ctx *ctx, double *f);
+/* Sets the canonical state (converted to the storage precision); resets the step counter. */
+lbm_status lbm_set_populations(lbm_ctx *ctx, const double *f);
+/* LBM_ENUMERIC if any stored population of the current state is not finite. */
+lbm_status lbm_check_finite(lbm_ctx *ctx);
+
+/* Test hook: the device collision alone (no streaming) on n_cells independent cells,
+   host fp64 f_in/f_out [n_cells][q] in stored form, computed in the storage precision. */
+lbm_status lbm_test_collide(lbm_ctx *ctx, const double *f_in, double *f_out, long long n_cells);
+
+/* Host-only helpers (no GPU needed). */
+/* Stencil of the documented ordering: q, xi [q][3] (2D: xi_z = 0), opposite [q]. */
+lbm_status lbm_stencil_info(lbm_stencil stencil, int *q, int *xi, int *opposite);
+/* Slab of 'rank' out of 'nranks' along an axis of 'extent' planes. */
+lbm_status lbm_slab_extent(int extent, int rank, int nranks, int *offset, int *local_extent);
+const char *lbm_version(void);
+
+/* Diagnostics. */
+/* Registers per thread and local (spill) bytes of this context's pull kernel. */
+lbm_status lbm_kernel_attributes(const lbm_ctx *ctx, int *regs, int *local_bytes);
+/* Device pointer and size of a population grid (which = 0 current, 1 next; AA: the single grid). */
+lbm_status lbm_device_grid(lbm_ctx *ctx, int which, void **ptr, size_t *bytes);
+/* The cudaStream_t the context enqueues on. */
+void *lbm_stream(lbm_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBM_H */

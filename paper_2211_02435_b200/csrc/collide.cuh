@@ -1,0 +1,842 @@
+// collide.cuh — register-resident MRT collision of one lattice cell (device code).
+//
+// The transforms are the paper's Chimera forms, evaluated in registers on a
+// 3^d "cube" of values (f_xyz = f_i if xi_i = (x,y,z) is in the
+// stencil, else 0):
+//   fwd_raw   : eq:RawMomentChimeraTransform, sweeps z, y, x;
+//               per axis (f-, f0, f+) -> (f0 + f+ + f-, f+ - f-, f+ + f-)
+//   bwd_raw   : f* = M^{-1} m* split per axis into symmetric/antisymmetric parts
+//               (eq:RawMomentChimeraBackwardSymmetric):
+//               (m0, m1, m2) -> ((m2 - m1)/2, m0 - m2, (m2 + m1)/2); D3Q19 uses the
+//               same split over its 9 opposite pairs (reduced 19 x 19 inverse)
+//   bin_fwd/bwd : binomial Chimera raw <-> central, per axis
+//               k1 = m1 - u m0, k2 = m2 - 2u m1 + u^2 m0 and its inverse
+//   cumulants : closed forms of C = Xi.u + log K / K = exp(C - Xi.u) for the
+//               monomials of orders 4-6 (eq:CumulantAndCentralMomentGenFuncs,
+//               PAPER.md:680-693) with kappa_100 = 0 collapsed
+//               and no log/exp left
+// Relaxation q*_p = q_p + w_p (q_eq_p - q_p) is applied per basis polynomial
+// (eq:MrtUpdateGeneral) by recombining the monomials of each
+// polynomial group and decomposing afterwards.
+//
+// Regimes (template REG):
+//   REG_ABS      absolute storage, eq:MrtUpdateGeneral
+//   REG_DELTA    zero-centered storage + delta equilibrium, eq:MrtUpdateGeneralDeviationOnly
+//                (linear spaces only; dq_eq written in delta-rho form)
+//   REG_ZC_ABS   zero-centered storage + absolute equilibrium,
+//                eq:MrtUpdateAbsoluteFromZeroCentered: the background raw moments m0
+//                are added after the forward raw transform and removed before the
+//                backward one (T(f0) = M f0 = m0).
+#pragma once
+#include "lattice.cuh"
+
+namespace lbm {
+
+enum { SPACE_POPULATION = 0, SPACE_RAW = 1, SPACE_CENTRAL = 2, SPACE_CUMULANT = 3, SPACE_SWE = 4 };
+enum { REG_ABS = 0, REG_DELTA = 1, REG_ZC_ABS = 2 };
+
+template <class real>
+struct Rates {
+  real w[27];
+};
+
+// --------------------------------------------------------------------------
+// exponent helpers
+// --------------------------------------------------------------------------
+__host__ __device__ constexpr int ex_of(int e) { return e % 3; }
+__host__ __device__ constexpr int ey_of(int e) { return (e / 3) % 3; }
+__host__ __device__ constexpr int ez_of(int e) { return e / 9; }
+__host__ __device__ constexpr int n2_of(int e) {
+  return (ex_of(e) == 2) + (ey_of(e) == 2) + (ez_of(e) == 2);
+}
+__host__ __device__ constexpr int n1_of(int e) {
+  return (ex_of(e) == 1) + (ey_of(e) == 1) + (ez_of(e) == 1);
+}
+__host__ __device__ constexpr double third_pow(int n) {
+  return n == 0 ? 1.0 : (n == 1 ? 1.0 / 3.0 : (n == 2 ? 1.0 / 9.0 : 1.0 / 27.0));
+}
+// Gaussian/background central (= rest raw) moment factor prod_a h(e_a), h = (1, 0, cs2)
+__host__ __device__ constexpr double hprod(int e) { return n1_of(e) ? 0.0 : third_pow(n2_of(e)); }
+
+// --------------------------------------------------------------------------
+// forward raw Chimera with compile-time presence of populations
+// --------------------------------------------------------------------------
+template <class S>
+struct Presence {
+  // populations
+  __host__ __device__ static constexpr bool p0(int a, int b, int c) { return S::present(a, b, c); }
+  // after the z sweep: chimera m_{ab|g}
+  __host__ __device__ static constexpr bool p1(int a, int b, int g) {
+    return g == 0 ? (p0(a, b, 0) || p0(a, b, 1) || p0(a, b, 2)) : (p0(a, b, 0) || p0(a, b, 2));
+  }
+  // after the y sweep: m_{a|be g}
+  __host__ __device__ static constexpr bool p2(int a, int be, int g) {
+    return be == 0 ? (p1(a, 0, g) || p1(a, 1, g) || p1(a, 2, g)) : (p1(a, 0, g) || p1(a, 2, g));
+  }
+  // after the x sweep: m_{al be g}
+  __host__ __device__ static constexpr bool p3(int al, int be, int g) {
+    return al == 0 ? (p2(0, be, g) || p2(1, be, g) || p2(2, be, g)) : (p2(0, be, g) || p2(2, be, g));
+  }
+};
+
+// one axis line (c0, c1, c2) = values at velocity (-1, 0, +1) -> exponents (0, 1, 2)
+template <bool PM, bool P0, bool PP, class real>
+__device__ __forceinline__ void fwd_line(real &c0, real &c1, real &c2) {
+  if constexpr (PM && PP) {
+    const real s = c2 + c0, d = c2 - c0;
+    if constexpr (P0) c0 = c1 + s; else c0 = s;
+    c1 = d;
+    c2 = s;
+  } else if constexpr (PP) {
+    const real p = c2;
+    if constexpr (P0) c0 = c1 + p; else c0 = p;
+    c1 = p;
+    c2 = p;
+  } else if constexpr (PM) {
+    const real m = c0;
+    if constexpr (P0) c0 = c1 + m; else c0 = m;
+    c1 = -m;
+    c2 = m;
+  } else {
+    if constexpr (P0) c0 = c1; else c0 = real(0);
+    c1 = real(0);
+    c2 = real(0);
+  }
+}
+
+template <class S, class real>
+__device__ __forceinline__ void fwd_raw3(real (&c)[27]) {
+  using P = Presence<S>;
+  // z sweep: lines over (a, b)
+  sfor<9>([&](auto L) {
+    constexpr int a = L % 3, b = L / 3;
+    fwd_line<P::p0(a, b, 0), P::p0(a, b, 1), P::p0(a, b, 2)>(c[E(a, b, 0)], c[E(a, b, 1)], c[E(a, b, 2)]);
+  });
+  // y sweep: lines over (a, g)
+  sfor<9>([&](auto L) {
+    constexpr int a = L % 3, g = L / 3;
+    fwd_line<P::p1(a, 0, g), P::p1(a, 1, g), P::p1(a, 2, g)>(c[E(a, 0, g)], c[E(a, 1, g)], c[E(a, 2, g)]);
+  });
+  // x sweep: lines over (be, g)
+  sfor<9>([&](auto L) {
+    constexpr int be = L % 3, g = L / 3;
+    fwd_line<P::p2(0, be, g), P::p2(1, be, g), P::p2(2, be, g)>(c[E(0, be, g)], c[E(1, be, g)],
+                                                                 c[E(2, be, g)]);
+  });
+}
+
+template <class real>
+__device__ __forceinline__ void fwd_raw2(real (&c)[9]) {
+  sfor<3>([&](auto a) { fwd_line<true, true, true>(c[E(a, 0)], c[E(a, 1)], c[E(a, 2)]); });  // y
+  sfor<3>([&](auto b) { fwd_line<true, true, true>(c[E(0, b)], c[E(1, b)], c[E(2, b)]); });  // x
+}
+
+// backward per axis line: (m0, m1, m2) -> (f-, f0, f+)
+template <class real>
+__device__ __forceinline__ void bwd_line(real &c0, real &c1, real &c2) {
+  const real m0 = c0, m2 = c2, h1 = real(0.5) * c1, h2 = real(0.5) * c2;
+  c0 = h2 - h1;
+  c2 = h2 + h1;
+  c1 = m0 - m2;
+}
+
+template <class real>
+__device__ __forceinline__ void bwd_raw3_full(real (&c)[27]) {
+  sfor<9>([&](auto L) {
+    constexpr int be = L % 3, g = L / 3;
+    bwd_line(c[E(0, be, g)], c[E(1, be, g)], c[E(2, be, g)]);
+  });
+  sfor<9>([&](auto L) {
+    constexpr int a = L % 3, g = L / 3;
+    bwd_line(c[E(a, 0, g)], c[E(a, 1, g)], c[E(a, 2, g)]);
+  });
+  sfor<9>([&](auto L) {
+    constexpr int a = L % 3, b = L / 3;
+    bwd_line(c[E(a, b, 0)], c[E(a, b, 1)], c[E(a, b, 2)]);
+  });
+}
+
+template <class real>
+__device__ __forceinline__ void bwd_raw2(real (&c)[9]) {
+  sfor<3>([&](auto b) { bwd_line(c[E(0, b)], c[E(1, b)], c[E(2, b)]); });
+  sfor<3>([&](auto a) { bwd_line(c[E(a, 0)], c[E(a, 1)], c[E(a, 2)]); });
+}
+
+// D3Q19: f* = M^{-1} m* on the 19 basis monomials, as the symmetric/antisymmetric
+// split over the 9 opposite pairs (eq:RawMomentChimeraBackwardSymmetric).
+//   edges   f_{ab0} = (m220 + a m120 + b m210 + ab m110) / 4        (and xz, yz)
+//   faces   f_{+-100} = ((m200 - m220 - m202) +- (m100 - m120 - m102)) / 2
+//   rest    f_000 = m000 - (m200 + m020 + m002) + (m220 + m202 + m022)
+// Output written to cube positions.
+template <class real>
+__device__ __forceinline__ void bwd_raw3_d3q19(real (&c)[27]) {
+  const real m000 = c[E(0, 0, 0)];
+  const real m100 = c[E(1, 0, 0)], m010 = c[E(0, 1, 0)], m001 = c[E(0, 0, 1)];
+  const real m110 = c[E(1, 1, 0)], m101 = c[E(1, 0, 1)], m011 = c[E(0, 1, 1)];
+  const real m200 = c[E(2, 0, 0)], m020 = c[E(0, 2, 0)], m002 = c[E(0, 0, 2)];
+  const real m120 = c[E(1, 2, 0)], m102 = c[E(1, 0, 2)], m210 = c[E(2, 1, 0)];
+  const real m012 = c[E(0, 1, 2)], m201 = c[E(2, 0, 1)], m021 = c[E(0, 2, 1)];
+  const real m220 = c[E(2, 2, 0)], m202 = c[E(2, 0, 2)], m022 = c[E(0, 2, 2)];
+  const real q = real(0.25), h = real(0.5);
+  // xy edges: symmetric part (m220 + ab m110)/4, antisymmetric (a m120 + b m210)/4
+  {
+    const real sp = q * (m220 + m110), sm = q * (m220 - m110);
+    const real ap = q * (m120 + m210), am = q * (m120 - m210);
+    c[E(2, 2, 1)] = sp + ap;  // (+1,+1,0)
+    c[E(0, 0, 1)] = sp - ap;  // (-1,-1,0)
+    c[E(2, 0, 1)] = sm + am;  // (+1,-1,0)
+    c[E(0, 2, 1)] = sm - am;  // (-1,+1,0)
+  }
+  {  // xz edges
+    const real sp = q * (m202 + m101), sm = q * (m202 - m101);
+    const real ap = q * (m102 + m201), am = q * (m102 - m201);
+    c[E(2, 1, 2)] = sp + ap;
+    c[E(0, 1, 0)] = sp - ap;
+    c[E(2, 1, 0)] = sm + am;
+    c[E(0, 1, 2)] = sm - am;
+  }
+  {  // yz edges
+    const real sp = q * (m022 + m011), sm = q * (m022 - m011);
+    const real ap = q * (m012 + m021), am = q * (m012 - m021);
+    c[E(1, 2, 2)] = sp + ap;
+    c[E(1, 0, 0)] = sp - ap;
+    c[E(1, 2, 0)] = sm + am;
+    c[E(1, 0, 2)] = sm - am;
+  }
+  {  // faces
+    const real sx = h * (m200 - m220 - m202), ax = h * (m100 - m120 - m102);
+    const real sy = h * (m020 - m220 - m022), ay = h * (m010 - m210 - m012);
+    const real sz = h * (m002 - m202 - m022), az = h * (m001 - m201 - m021);
+    c[E(2, 1, 1)] = sx + ax;
+    c[E(0, 1, 1)] = sx - ax;
+    c[E(1, 2, 1)] = sy + ay;
+    c[E(1, 0, 1)] = sy - ay;
+    c[E(1, 1, 2)] = sz + az;
+    c[E(1, 1, 0)] = sz - az;
+  }
+  c[E(1, 1, 1)] = m000 - (m200 + m020 + m002) + (m220 + m202 + m022);
+}
+
+// --------------------------------------------------------------------------
+// binomial Chimera
+// --------------------------------------------------------------------------
+template <class real>
+__device__ __forceinline__ void bin_fwd_line(real &c0, real &c1, real &c2, real u) {
+  const real k1 = fma(-u, c0, c1);
+  c2 = fma(-u, c1 + k1, c2);  // m2 - 2u m1 + u^2 m0
+  c1 = k1;
+}
+template <class real>
+__device__ __forceinline__ void bin_bwd_line(real &c0, real &c1, real &c2, real u) {
+  const real m1 = fma(u, c0, c1);
+  c2 = fma(u, c1 + m1, c2);  // k2 + 2u k1 + u^2 k0
+  c1 = m1;
+}
+template <class real>
+__device__ __forceinline__ void bin_fwd3(real (&c)[27], real ux, real uy, real uz) {
+  sfor<9>([&](auto L) {
+    constexpr int a = L % 3, b = L / 3;
+    bin_fwd_line(c[E(a, b, 0)], c[E(a, b, 1)], c[E(a, b, 2)], uz);
+  });
+  sfor<9>([&](auto L) {
+    constexpr int a = L % 3, g = L / 3;
+    bin_fwd_line(c[E(a, 0, g)], c[E(a, 1, g)], c[E(a, 2, g)], uy);
+  });
+  sfor<9>([&](auto L) {
+    constexpr int be = L % 3, g = L / 3;
+    bin_fwd_line(c[E(0, be, g)], c[E(1, be, g)], c[E(2, be, g)], ux);
+  });
+}
+template <class real>
+__device__ __forceinline__ void bin_bwd3(real (&c)[27], real ux, real uy, real uz) {
+  sfor<9>([&](auto L) {
+    constexpr int a = L % 3, b = L / 3;
+    bin_bwd_line(c[E(a, b, 0)], c[E(a, b, 1)], c[E(a, b, 2)], uz);
+  });
+  sfor<9>([&](auto L) {
+    constexpr int a = L % 3, g = L / 3;
+    bin_bwd_line(c[E(a, 0, g)], c[E(a, 1, g)], c[E(a, 2, g)], uy);
+  });
+  sfor<9>([&](auto L) {
+    constexpr int be = L % 3, g = L / 3;
+    bin_bwd_line(c[E(0, be, g)], c[E(1, be, g)], c[E(2, be, g)], ux);
+  });
+}
+template <class real>
+__device__ __forceinline__ void bin_fwd2(real (&c)[9], real ux, real uy) {
+  sfor<3>([&](auto a) { bin_fwd_line(c[E(a, 0)], c[E(a, 1)], c[E(a, 2)], uy); });
+  sfor<3>([&](auto b) { bin_fwd_line(c[E(0, b)], c[E(1, b)], c[E(2, b)], ux); });
+}
+template <class real>
+__device__ __forceinline__ void bin_bwd2(real (&c)[9], real ux, real uy) {
+  sfor<3>([&](auto a) { bin_bwd_line(c[E(a, 0)], c[E(a, 1)], c[E(a, 2)], uy); });
+  sfor<3>([&](auto b) { bin_bwd_line(c[E(0, b)], c[E(1, b)], c[E(2, b)], ux); });
+}
+
+// --------------------------------------------------------------------------
+// equilibria in monomial form (template<int e> get(), static zero<e>())
+// --------------------------------------------------------------------------
+// Maxwellian raw moments truncated at O(u^2) (reading R4):
+//   m_eq_e = rho (hprod(e) + U_e(u)), U_e = the u-terms of prod_a g_{e_a} cut at degree 2
+//   (g0 = 1, g1 = u, g2 = cs2 + u^2).
+template <class real>
+struct RawU {
+  real ux, uy, uz, uxx, uyy, uzz;
+  template <int e>
+  __device__ __forceinline__ real get() const {
+    constexpr int ax = ex_of(e), ay = ey_of(e), az = ez_of(e);
+    constexpr int n1 = n1_of(e), n2 = n2_of(e);
+    if constexpr (n1 == 0) {
+      // (1/3)^(n2-1) * sum of u_a^2 over the squared axes
+      real s = real(0);
+      bool first = true;
+      if constexpr (ax == 2) { s = uxx; first = false; }
+      if constexpr (ay == 2) { s = first ? uyy : s + uyy; first = false; }
+      if constexpr (az == 2) { s = first ? uzz : s + uzz; }
+      if constexpr (n2 == 1) return s;
+      else return real(third_pow(n2 - 1)) * s;
+    } else if constexpr (n1 == 1) {
+      const real v = (ax == 1) ? ux : ((ay == 1) ? uy : uz);
+      if constexpr (n2 == 0) return v;
+      else return real(third_pow(n2)) * v;
+    } else if constexpr (n1 == 2) {
+      const real v = (ax != 1) ? uy * uz : ((ay != 1) ? ux * uz : ux * uy);
+      if constexpr (n2 == 0) return v;
+      else return real(third_pow(n2)) * v;
+    } else {
+      return real(0);
+    }
+  }
+  template <int e>
+  __device__ static constexpr bool zero() {
+    return n1_of(e) == 3 || e == 0;
+  }
+};
+
+// central-moment background prod_a k_{e_a}(u), k0 = 1, k1 = -u, k2 = cs2 + u^2, minus hprod(e):
+//   V_e(u) = K(u) f0 - K(0) f0 on monomial e (closed form; exact for D2Q9/D3Q19/D3Q27)
+template <class real>
+struct CentralV {
+  real ux, uy, uz, uxx, uyy, uzz;
+  template <int a>
+  __device__ __forceinline__ real k(real u, real uu) const {
+    if constexpr (a == 0) return real(1);
+    else if constexpr (a == 1) return -u;
+    else return real(1.0 / 3.0) + uu;
+  }
+  template <int e>
+  __device__ __forceinline__ real get() const {
+    constexpr int ax = ex_of(e), ay = ey_of(e), az = ez_of(e);
+    if constexpr (n1_of(e) == 0) {
+      // prod (1/3 + u_a^2) - (1/3)^n2 over squared axes, expanded without cancellation
+      constexpr int n2 = n2_of(e);
+      if constexpr (n2 == 0) return real(0);
+      real A[3];
+      int n = 0;
+      if constexpr (ax == 2) A[n++] = uxx;
+      if constexpr (ay == 2) A[n++] = uyy;
+      if constexpr (az == 2) A[n++] = uzz;
+      if constexpr (n2 == 1) {
+        return A[0];
+      } else if constexpr (n2 == 2) {
+        return fma(A[0], A[1], real(1.0 / 3.0) * (A[0] + A[1]));
+      } else {
+        const real s1 = A[0] + A[1] + A[2];
+        const real s2 = A[0] * A[1] + A[0] * A[2] + A[1] * A[2];
+        return fma(A[0] * A[1], A[2], fma(real(1.0 / 3.0), s2, real(1.0 / 9.0) * s1));
+      }
+    } else {
+      return k<ax>(ux, uxx) * k<ay>(uy, uyy) * k<az>(uz, uzz);
+    }
+  }
+};
+
+// --------------------------------------------------------------------------
+// relaxation helpers (delta = q_eq - q on monomials)
+// --------------------------------------------------------------------------
+template <class real>
+__device__ __forceinline__ void relax1(real &m, real meq, real w) { m = fma(w, meq - m, m); }
+template <class real>
+__device__ __forceinline__ void relax1_zero(real &m, real w) { m = fma(-w, m, m); }
+// polynomials (a + b) [ws], (a - b) [wd]
+template <class real>
+__device__ __forceinline__ void relax_pair(real &a, real &b, real da, real db, real ws, real wd) {
+  const real S = ws * (da + db), D = wd * (da - db);
+  a = fma(real(0.5), S + D, a);
+  b = fma(real(0.5), S - D, b);
+}
+// polynomials (a - b) [w1], (a - c) [w2], (a + b + c) [w3]
+template <class real>
+__device__ __forceinline__ void relax_diag3(real &a, real &b, real &c, real da, real db, real dc, real w1,
+                                            real w2, real w3) {
+  const real E1 = w1 * (da - db), E2 = w2 * (da - dc), E3 = w3 * (da + db + dc);
+  const real t = real(1.0 / 3.0);
+  a = fma(t, E1 + E2 + E3, a);
+  b = fma(t, E3 + E2 - real(2) * E1, b);
+  c = fma(t, E3 + E1 - real(2) * E2, c);
+}
+// polynomials (a - 2b + c) [w1], (a + b - 2c) [w2], (a + b + c) [w3]
+template <class real>
+__device__ __forceinline__ void relax_quad3(real &a, real &b, real &c, real da, real db, real dc, real w1,
+                                            real w2, real w3) {
+  const real E1 = w1 * (da - real(2) * db + dc), E2 = w2 * (da + db - real(2) * dc), E3 = w3 * (da + db + dc);
+  const real t = real(1.0 / 3.0);
+  a = fma(t, E1 + E2 + E3, a);
+  b = fma(t, E3 - E1, b);
+  c = fma(t, E3 - E2, c);
+}
+
+// Apply the basis relaxation of stencil S to the monomial cube c given an
+// equilibrium provider EQ with get<e>() (value of q_eq on monomial e) and
+// zero<e>() (compile-time: q_eq == 0).
+template <class EQ, int e, class real>
+__device__ __forceinline__ real delta_of(const EQ &eq, const real (&c)[27]) {
+  if constexpr (EQ::template zero<e>()) return -c[e];
+  else return eq.template get<e>() - c[e];
+}
+template <class EQ, int e, class real>
+__device__ __forceinline__ void relax_single(const EQ &eq, real (&c)[27], real w) {
+  if constexpr (EQ::template zero<e>()) relax1_zero(c[e], w);
+  else relax1(c[e], eq.template get<e>(), w);
+}
+
+template <class S, class EQ, class real>
+__device__ __forceinline__ void relax_basis3(real (&c)[27], const EQ &eq, const Rates<real> &r) {
+  constexpr bool Q27 = (S::Q == 27);
+  // second order: xy, xz, yz [4,5,6]; (x^2-y^2, x^2-z^2, x^2+y^2+z^2) [7,8,9]
+  relax_single<EQ, E(1, 1, 0)>(eq, c, r.w[4]);
+  relax_single<EQ, E(1, 0, 1)>(eq, c, r.w[5]);
+  relax_single<EQ, E(0, 1, 1)>(eq, c, r.w[6]);
+  {
+    const real da = delta_of<EQ, E(2, 0, 0)>(eq, c), db = delta_of<EQ, E(0, 2, 0)>(eq, c),
+               dc = delta_of<EQ, E(0, 0, 2)>(eq, c);
+    relax_diag3(c[E(2, 0, 0)], c[E(0, 2, 0)], c[E(0, 0, 2)], da, db, dc, r.w[7], r.w[8], r.w[9]);
+  }
+  // third order pairs: (xy^2, xz^2) [10,13], (x^2y, yz^2) [11,14], (x^2z, y^2z) [12,15]
+  {
+    const real da = delta_of<EQ, E(1, 2, 0)>(eq, c), db = delta_of<EQ, E(1, 0, 2)>(eq, c);
+    relax_pair(c[E(1, 2, 0)], c[E(1, 0, 2)], da, db, r.w[10], r.w[13]);
+  }
+  {
+    const real da = delta_of<EQ, E(2, 1, 0)>(eq, c), db = delta_of<EQ, E(0, 1, 2)>(eq, c);
+    relax_pair(c[E(2, 1, 0)], c[E(0, 1, 2)], da, db, r.w[11], r.w[14]);
+  }
+  {
+    const real da = delta_of<EQ, E(2, 0, 1)>(eq, c), db = delta_of<EQ, E(0, 2, 1)>(eq, c);
+    relax_pair(c[E(2, 0, 1)], c[E(0, 2, 1)], da, db, r.w[12], r.w[15]);
+  }
+  constexpr int o4 = Q27 ? 17 : 16;  // first 4th-order rate index
+  if constexpr (Q27) relax_single<EQ, E(1, 1, 1)>(eq, c, r.w[16]);
+  {
+    const real da = delta_of<EQ, E(2, 2, 0)>(eq, c), db = delta_of<EQ, E(2, 0, 2)>(eq, c),
+               dc = delta_of<EQ, E(0, 2, 2)>(eq, c);
+    relax_quad3(c[E(2, 2, 0)], c[E(2, 0, 2)], c[E(0, 2, 2)], da, db, dc, r.w[o4], r.w[o4 + 1], r.w[o4 + 2]);
+  }
+  if constexpr (Q27) {
+    relax_single<EQ, E(2, 1, 1)>(eq, c, r.w[20]);
+    relax_single<EQ, E(1, 2, 1)>(eq, c, r.w[21]);
+    relax_single<EQ, E(1, 1, 2)>(eq, c, r.w[22]);
+    relax_single<EQ, E(1, 2, 2)>(eq, c, r.w[23]);
+    relax_single<EQ, E(2, 1, 2)>(eq, c, r.w[24]);
+    relax_single<EQ, E(2, 2, 1)>(eq, c, r.w[25]);
+    relax_single<EQ, E(2, 2, 2)>(eq, c, r.w[26]);
+  }
+}
+
+// 2D (D2Q9, de Rosis basis): xy [3]; (x^2-y^2 [4], x^2+y^2 [5]); x^2y [6]; xy^2 [7]; x^2y^2 [8]
+template <class EQ, int e, class real>
+__device__ __forceinline__ real delta_of2(const EQ &eq, const real (&c)[9]) {
+  if constexpr (EQ::template zero<e>()) return -c[e];
+  else return eq.template get<e>() - c[e];
+}
+template <class EQ, int e, class real>
+__device__ __forceinline__ void relax_single2(const EQ &eq, real (&c)[9], real w) {
+  if constexpr (EQ::template zero<e>()) relax1_zero(c[e], w);
+  else relax1(c[e], eq.template get<e>(), w);
+}
+template <class EQ, class real>
+__device__ __forceinline__ void relax_basis2(real (&c)[9], const EQ &eq, const Rates<real> &r) {
+  relax_single2<EQ, E(1, 1)>(eq, c, r.w[3]);
+  {
+    const real da = delta_of2<EQ, E(2, 0)>(eq, c), db = delta_of2<EQ, E(0, 2)>(eq, c);
+    relax_pair(c[E(2, 0)], c[E(0, 2)], da, db, r.w[5], r.w[4]);
+  }
+  relax_single2<EQ, E(2, 1)>(eq, c, r.w[6]);
+  relax_single2<EQ, E(1, 2)>(eq, c, r.w[7]);
+  relax_single2<EQ, E(2, 2)>(eq, c, r.w[8]);
+}
+
+// --------------------------------------------------------------------------
+// equilibrium providers
+// --------------------------------------------------------------------------
+// RAW, absolute: rho (hprod + U)
+template <class real>
+struct EqRawAbs {
+  real rho;
+  RawU<real> U;
+  template <int e>
+  __device__ __forceinline__ real get() const {
+    constexpr double h = hprod(e);
+    if constexpr (h != 0.0) return rho * (real(h) + U.template get<e>());
+    else return rho * U.template get<e>();
+  }
+  template <int e>
+  __device__ static constexpr bool zero() { return n1_of(e) == 3; }
+};
+// RAW, delta: drho hprod + rho U
+template <class real>
+struct EqRawDelta {
+  real drho, rho;
+  RawU<real> U;
+  template <int e>
+  __device__ __forceinline__ real get() const {
+    constexpr double h = hprod(e);
+    if constexpr (h != 0.0) return fma(real(h), drho, rho * U.template get<e>());
+    else return rho * U.template get<e>();
+  }
+  template <int e>
+  __device__ static constexpr bool zero() { return n1_of(e) == 3; }
+};
+// CENTRAL, absolute: Gaussian central moments rho hprod (u-independent, reading R4)
+template <class real>
+struct EqCentralAbs {
+  real rho;
+  template <int e>
+  __device__ __forceinline__ real get() const { return real(hprod(e)) * rho; }
+  template <int e>
+  __device__ static constexpr bool zero() { return hprod(e) == 0.0; }
+};
+// CENTRAL, delta: dk_eq = rho hprod - K(u) f0 = drho hprod - V_e(u)
+template <class real>
+struct EqCentralDelta {
+  real drho;
+  CentralV<real> V;
+  template <int e>
+  __device__ __forceinline__ real get() const {
+    constexpr double h = hprod(e);
+    if constexpr (h != 0.0) return fma(real(h), drho, -V.template get<e>());
+    else return -V.template get<e>();
+  }
+  template <int e>
+  __device__ static constexpr bool zero() { return false; }
+};
+// CUMULANT: C_eq = rho cs2 on the diagonal second-order cumulants, 0 otherwise
+template <class real>
+struct EqCumulant {
+  real rho3;  // rho / 3
+  template <int e>
+  __device__ __forceinline__ real get() const { return rho3; }
+  template <int e>
+  __device__ static constexpr bool zero() {
+    return !(n2_of(e) == 1 && n1_of(e) == 0);
+  }
+};
+// tabulated equilibrium (SWE: kappa_eq = K(u) f_eq computed numerically)
+template <class real, int N>
+struct EqTable {
+  real v[N];
+  template <int e>
+  __device__ __forceinline__ real get() const { return v[e]; }
+  template <int e>
+  __device__ static constexpr bool zero() { return false; }
+};
+
+// --------------------------------------------------------------------------
+// cumulant closed forms (3D).  c holds central moments kappa on entry
+// (kappa_000 = rho, first order = 0); 'inv' = 1/rho.
+// --------------------------------------------------------------------------
+template <class S, class real>
+__device__ __forceinline__ void central_to_cumulant3(real (&c)[27], real inv) {
+  const real k200 = c[E(2, 0, 0)], k020 = c[E(0, 2, 0)], k002 = c[E(0, 0, 2)];
+  const real k110 = c[E(1, 1, 0)], k101 = c[E(1, 0, 1)], k011 = c[E(0, 1, 1)];
+  if constexpr (S::Q == 27) {
+    const real k111 = c[E(1, 1, 1)];
+    const real k210 = c[E(2, 1, 0)], k201 = c[E(2, 0, 1)], k120 = c[E(1, 2, 0)];
+    const real k021 = c[E(0, 2, 1)], k102 = c[E(1, 0, 2)], k012 = c[E(0, 1, 2)];
+    const real k220 = c[E(2, 2, 0)], k202 = c[E(2, 0, 2)], k022 = c[E(0, 2, 2)];
+    const real k211 = c[E(2, 1, 1)], k121 = c[E(1, 2, 1)], k112 = c[E(1, 1, 2)];
+    // order 6 (uses the central moments of order 4 before they are overwritten)
+    {
+      const real s24 = k200 * k022 + k020 * k202 + k002 * k220 +
+                       real(4) * (k110 * k112 + k101 * k121 + k011 * k211);
+      const real s33 = real(2) * (k210 * k012 + k201 * k021 + k120 * k102) + real(4) * k111 * k111;
+      const real s222 = k200 * k020 * k002 +
+                        real(2) * (k200 * k011 * k011 + k020 * k101 * k101 + k002 * k110 * k110) +
+                        real(8) * k110 * k101 * k011;
+      c[E(2, 2, 2)] = c[E(2, 2, 2)] - inv * (s24 + s33) + real(2) * inv * inv * s222;
+    }
+    // order 5
+    c[E(2, 2, 1)] -= inv * (k200 * k021 + k020 * k201 + real(4) * k110 * k111 +
+                            real(2) * (k101 * k120 + k011 * k210));
+    c[E(2, 1, 2)] -= inv * (k200 * k012 + k002 * k210 + real(4) * k101 * k111 +
+                            real(2) * (k110 * k102 + k011 * k201));
+    c[E(1, 2, 2)] -= inv * (k020 * k102 + k002 * k120 + real(4) * k011 * k111 +
+                            real(2) * (k110 * k012 + k101 * k021));
+    // order 4 (mixed)
+    c[E(2, 1, 1)] -= inv * (k200 * k011 + real(2) * k110 * k101);
+    c[E(1, 2, 1)] -= inv * (k020 * k101 + real(2) * k110 * k011);
+    c[E(1, 1, 2)] -= inv * (k002 * k110 + real(2) * k101 * k011);
+  }
+  // order 4 (squares)
+  c[E(2, 2, 0)] -= inv * (k200 * k020 + real(2) * k110 * k110);
+  c[E(2, 0, 2)] -= inv * (k200 * k002 + real(2) * k101 * k101);
+  c[E(0, 2, 2)] -= inv * (k020 * k002 + real(2) * k011 * k011);
+}
+
+// inverse: c holds post-collision cumulants C* (orders 2, 3 equal kappa*)
+template <class S, class real>
+__device__ __forceinline__ void cumulant_to_central3(real (&c)[27], real inv) {
+  const real k200 = c[E(2, 0, 0)], k020 = c[E(0, 2, 0)], k002 = c[E(0, 0, 2)];
+  const real k110 = c[E(1, 1, 0)], k101 = c[E(1, 0, 1)], k011 = c[E(0, 1, 1)];
+  c[E(2, 2, 0)] += inv * (k200 * k020 + real(2) * k110 * k110);
+  c[E(2, 0, 2)] += inv * (k200 * k002 + real(2) * k101 * k101);
+  c[E(0, 2, 2)] += inv * (k020 * k002 + real(2) * k011 * k011);
+  if constexpr (S::Q == 27) {
+    const real k111 = c[E(1, 1, 1)];
+    const real k210 = c[E(2, 1, 0)], k201 = c[E(2, 0, 1)], k120 = c[E(1, 2, 0)];
+    const real k021 = c[E(0, 2, 1)], k102 = c[E(1, 0, 2)], k012 = c[E(0, 1, 2)];
+    c[E(2, 1, 1)] += inv * (k200 * k011 + real(2) * k110 * k101);
+    c[E(1, 2, 1)] += inv * (k020 * k101 + real(2) * k110 * k011);
+    c[E(1, 1, 2)] += inv * (k002 * k110 + real(2) * k101 * k011);
+    c[E(2, 2, 1)] += inv * (k200 * k021 + k020 * k201 + real(4) * k110 * k111 +
+                            real(2) * (k101 * k120 + k011 * k210));
+    c[E(2, 1, 2)] += inv * (k200 * k012 + k002 * k210 + real(4) * k101 * k111 +
+                            real(2) * (k110 * k102 + k011 * k201));
+    c[E(1, 2, 2)] += inv * (k020 * k102 + k002 * k120 + real(4) * k011 * k111 +
+                            real(2) * (k110 * k012 + k101 * k021));
+    const real k220 = c[E(2, 2, 0)], k202 = c[E(2, 0, 2)], k022 = c[E(0, 2, 2)];
+    const real k211 = c[E(2, 1, 1)], k121 = c[E(1, 2, 1)], k112 = c[E(1, 1, 2)];
+    const real s24 = k200 * k022 + k020 * k202 + k002 * k220 +
+                     real(4) * (k110 * k112 + k101 * k121 + k011 * k211);
+    const real s33 = real(2) * (k210 * k012 + k201 * k021 + k120 * k102) + real(4) * k111 * k111;
+    const real s222 = k200 * k020 * k002 +
+                      real(2) * (k200 * k011 * k011 + k020 * k101 * k101 + k002 * k110 * k110) +
+                      real(8) * k110 * k101 * k011;
+    c[E(2, 2, 2)] = c[E(2, 2, 2)] + inv * (s24 + s33) - real(2) * inv * inv * s222;
+  }
+}
+
+template <class real>
+__device__ __forceinline__ void central_to_cumulant2(real (&c)[9], real inv) {
+  const real k20 = c[E(2, 0)], k02 = c[E(0, 2)], k11 = c[E(1, 1)];
+  c[E(2, 2)] -= inv * (k20 * k02 + real(2) * k11 * k11);
+}
+template <class real>
+__device__ __forceinline__ void cumulant_to_central2(real (&c)[9], real inv) {
+  const real k20 = c[E(2, 0)], k02 = c[E(0, 2)], k11 = c[E(1, 1)];
+  c[E(2, 2)] += inv * (k20 * k02 + real(2) * k11 * k11);
+}
+
+// --------------------------------------------------------------------------
+// background raw moments m0_e = hprod(e) (= M f0) add/remove
+// --------------------------------------------------------------------------
+template <int NC, class real>
+__device__ __forceinline__ void add_background(real (&c)[NC], real sgn) {
+  sfor<NC>([&](auto e) {
+    constexpr double h = hprod(e);
+    if constexpr (e != 0 && h != 0.0) c[e] = fma(sgn, real(h), c[e]);
+  });
+}
+
+// --------------------------------------------------------------------------
+// the collision of one cell: f in/out in the documented population order,
+// STORED form (delta f for REG_DELTA / REG_ZC_ABS).
+// --------------------------------------------------------------------------
+template <class S, int SPACE, int REG, class real>
+__device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, real swe_g) {
+  constexpr bool zc = (REG != REG_ABS);
+  constexpr int NC = S::NC;
+  real c[NC];
+  sfor<NC>([&](auto k) { c[k] = real(0); });
+  sfor<S::Q>([&](auto i) { c[S::pos(i)] = f[i]; });
+
+  if constexpr (SPACE == SPACE_POPULATION) {
+    // SRT (BGK): f* = f + w (f_eq - f), f_eq = M^{-1} m_eq (reading R4)
+    if constexpr (S::D == 3) fwd_raw3<S>(c); else fwd_raw2(c);
+    const real m000 = c[0];
+    const real rho = zc ? real(1) + m000 : m000;
+    const real inv = real(1) / rho;
+    const real jx = c[E(1, 0, 0)], jy = c[E(0, 1, 0)];
+    real jz = real(0);
+    if constexpr (S::D == 3) jz = c[E(0, 0, 1)];
+    const real ux = jx * inv, uy = jy * inv, uz = jz * inv;
+    RawU<real> U{ux, uy, uz, ux * ux, uy * uy, uz * uz};
+    real g[NC];
+    if constexpr (REG == REG_DELTA) {
+      EqRawDelta<real> eq{m000, rho, U};
+      sfor<NC>([&](auto e) {
+        if constexpr (EqRawDelta<real>::template zero<e>()) g[e] = real(0);
+        else g[e] = eq.template get<e>();
+      });
+      g[0] = m000;
+    } else {
+      EqRawAbs<real> eq{rho, U};
+      sfor<NC>([&](auto e) {
+        if constexpr (EqRawAbs<real>::template zero<e>()) g[e] = real(0);
+        else g[e] = eq.template get<e>();
+      });
+      g[0] = rho;
+      if constexpr (REG == REG_ZC_ABS) add_background<NC>(g, real(-1)), g[0] = m000;  // f_eq - f0
+    }
+    if constexpr (S::Q == 27) bwd_raw3_full(g);
+    else if constexpr (S::Q == 19) bwd_raw3_d3q19(g);
+    else bwd_raw2(g);
+    const real w = r.w[0];
+    if constexpr (REG == REG_ZC_ABS) {
+      // absolute populations f = df + f0 relaxed against the absolute f_eq
+      sfor<S::Q>([&](auto i) {
+        const real f0 = real(weight<S>(i));
+        const real fa = f[i] + f0;
+        const real feq = g[S::pos(i)] + f0;
+        f[i] = fma(w, feq - fa, fa) - f0;
+      });
+    } else {
+      sfor<S::Q>([&](auto i) { f[i] = fma(w, g[S::pos(i)] - f[i], f[i]); });
+    }
+    return;
+  } else {
+    // ---- forward raw Chimera
+    if constexpr (S::D == 3) fwd_raw3<S>(c); else fwd_raw2(c);
+    // ---- conserved quantities, conserved-quantity rewriting
+    const real m000 = c[0];
+    const real rho = zc ? real(1) + m000 : m000;
+    const real inv = real(1) / rho;
+    const real jx = c[E(1, 0, 0)], jy = c[E(0, 1, 0)];
+    real jz = real(0);
+    if constexpr (S::D == 3) jz = c[E(0, 0, 1)];
+    const real ux = jx * inv, uy = jy * inv, uz = jz * inv;
+    if constexpr (REG == REG_ZC_ABS) {  // q = T(df + f0): add m0 = M f0
+      add_background<NC>(c, real(1));
+      c[0] = rho;
+    }
+
+    if constexpr (SPACE == SPACE_RAW) {
+      RawU<real> U{ux, uy, uz, ux * ux, uy * uy, uz * uz};
+      if constexpr (REG == REG_DELTA) {
+        EqRawDelta<real> eq{m000, rho, U};
+        if constexpr (S::D == 3) relax_basis3<S>(c, eq, r); else relax_basis2(c, eq, r);
+      } else {
+        EqRawAbs<real> eq{rho, U};
+        if constexpr (S::D == 3) relax_basis3<S>(c, eq, r); else relax_basis2(c, eq, r);
+      }
+    } else {
+      // ---- raw -> central (binomial Chimera)
+      if constexpr (S::D == 3) bin_fwd3(c, ux, uy, uz); else bin_fwd2(c, ux, uy);
+      if constexpr (REG != REG_DELTA) {
+        // collapse conserved central moments: kappa_000 = rho, kappa_100 = 0
+        c[0] = rho;
+        c[E(1, 0, 0)] = real(0);
+        c[E(0, 1, 0)] = real(0);
+        if constexpr (S::D == 3) c[E(0, 0, 1)] = real(0);
+      }
+      if constexpr (SPACE == SPACE_CENTRAL) {
+        if constexpr (REG == REG_DELTA) {
+          EqCentralDelta<real> eq{m000, CentralV<real>{ux, uy, uz, ux * ux, uy * uy, uz * uz}};
+          if constexpr (S::D == 3) relax_basis3<S>(c, eq, r); else relax_basis2(c, eq, r);
+        } else {
+          EqCentralAbs<real> eq{rho};
+          if constexpr (S::D == 3) relax_basis3<S>(c, eq, r); else relax_basis2(c, eq, r);
+        }
+      } else if constexpr (SPACE == SPACE_SWE) {
+        // kappa_eq = K(u) f_eq of Zhou's discrete equilibrium
+        static_assert(S::Q == 9, "SWE is D2Q9");
+        const real uu = ux * ux + uy * uy, gh = swe_g * rho;
+        EqTable<real, 9> eq;
+        real *t = eq.v;
+        sfor<9>([&](auto i) {
+          constexpr int vx = S::vx(i), vy = S::vy(i);
+          constexpr int l1 = (vx != 0) + (vy != 0);
+          if constexpr (l1 == 0) {
+            t[S::pos(i)] = rho * (real(1) - real(5.0 / 6.0) * gh - real(2.0 / 3.0) * uu);
+          } else {
+            const real xu = real(vx) * ux + real(vy) * uy;
+            const real lam = (l1 == 1) ? real(1) : real(0.25);
+            t[S::pos(i)] = lam * rho *
+                           (real(1.0 / 6.0) * gh + real(1.0 / 3.0) * xu + real(0.5) * xu * xu - real(1.0 / 6.0) * uu);
+          }
+        });
+        fwd_raw2(eq.v);
+        bin_fwd2(eq.v, ux, uy);
+        relax_basis2(c, eq, r);
+      } else {  // SPACE_CUMULANT
+        if constexpr (S::D == 3) central_to_cumulant3<S>(c, inv); else central_to_cumulant2(c, inv);
+        EqCumulant<real> eq{rho * real(1.0 / 3.0)};
+        if constexpr (S::D == 3) relax_basis3<S>(c, eq, r); else relax_basis2(c, eq, r);
+        if constexpr (S::D == 3) cumulant_to_central3<S>(c, inv); else cumulant_to_central2(c, inv);
+      }
+      // ---- central -> raw
+      if constexpr (S::D == 3) bin_bwd3(c, ux, uy, uz); else bin_bwd2(c, ux, uy);
+    }
+    if constexpr (REG == REG_ZC_ABS) add_background<NC>(c, real(-1));
+    // conserved raw moments pass through unchanged
+    c[0] = m000;
+    c[E(1, 0, 0)] = jx;
+    c[E(0, 1, 0)] = jy;
+    if constexpr (S::D == 3) c[E(0, 0, 1)] = jz;
+    // ---- backward raw transform
+    if constexpr (S::Q == 27) bwd_raw3_full(c);
+    else if constexpr (S::Q == 19) bwd_raw3_d3q19(c);
+    else bwd_raw2(c);
+    sfor<S::Q>([&](auto i) { f[i] = c[S::pos(i)]; });
+  }
+}
+
+// Equilibrium populations of the method at (rho, u) in stored form: f_eq = T^{-1}(q_eq).
+// RAW / POPULATION: M^{-1} m_eq (truncated Maxwellian); CENTRAL / CUMULANT: the Gaussian
+// central moments, i.e. raw moments rho prod_a (1, u_a, cs2 + u_a^2); SWE: Zhou f_eq.
+template <class S, int SPACE, int REG, class real>
+__device__ __forceinline__ void equilibrium(real (&f)[S::Q], real rho, real ux, real uy, real uz, real swe_g) {
+  constexpr int NC = S::NC;
+  constexpr bool zc = (REG != REG_ABS);
+  if constexpr (SPACE == SPACE_SWE) {
+    const real uu = ux * ux + uy * uy, gh = swe_g * rho;
+    sfor<9>([&](auto i) {
+      constexpr int vx = S::vx(i), vy = S::vy(i);
+      constexpr int l1 = (vx != 0) + (vy != 0);
+      if constexpr (l1 == 0) {
+        f[i] = rho * (real(1) - real(5.0 / 6.0) * gh - real(2.0 / 3.0) * uu);
+      } else {
+        const real xu = real(vx) * ux + real(vy) * uy;
+        const real lam = (l1 == 1) ? real(1) : real(0.25);
+        f[i] = lam * rho * (real(1.0 / 6.0) * gh + real(1.0 / 3.0) * xu + real(0.5) * xu * xu - real(1.0 / 6.0) * uu);
+      }
+    });
+    return;
+  } else {
+    const real drho = rho - real(1);
+    real c[NC];
+    if constexpr (SPACE == SPACE_POPULATION || SPACE == SPACE_RAW) {
+      RawU<real> U{ux, uy, uz, ux * ux, uy * uy, uz * uz};
+      sfor<NC>([&](auto e) {
+        constexpr double h = hprod(e);
+        if constexpr (RawU<real>::template zero<e>() && e != 0) c[e] = real(0);
+        else if constexpr (e == 0) c[e] = zc ? drho : rho;
+        else if constexpr (h != 0.0) c[e] = zc ? fma(real(h), drho, rho * U.template get<e>())
+                                              : rho * (real(h) + U.template get<e>());
+        else c[e] = rho * U.template get<e>();
+      });
+    } else {
+      // untruncated Gaussian raw moments rho prod (1, u, cs2 + u^2); zc: minus hprod
+      sfor<NC>([&](auto e) {
+        constexpr int ax = ex_of(e), ay = ey_of(e), az = ez_of(e);
+        auto g = [&](auto a, real u) -> real {
+          if constexpr (decltype(a)::value == 0) return real(1);
+          else if constexpr (decltype(a)::value == 1) return u;
+          else return real(1.0 / 3.0) + u * u;
+        };
+        const real p = g(std::integral_constant<int, ax>{}, ux) * g(std::integral_constant<int, ay>{}, uy) *
+                       g(std::integral_constant<int, az>{}, uz);
+        constexpr double h = hprod(e);
+        if constexpr (e == 0) c[e] = zc ? drho : rho;
+        else if constexpr (h != 0.0) c[e] = zc ? fma(rho, p, real(-h)) : rho * p;
+        else c[e] = rho * p;
+      });
+    }
+    if constexpr (S::Q == 27) bwd_raw3_full(c);
+    else if constexpr (S::Q == 19) bwd_raw3_d3q19(c);
+    else bwd_raw2(c);
+    sfor<S::Q>([&](auto i) { f[i] = c[S::pos(i)]; });
+  }
+}
+
+}  // namespace lbm

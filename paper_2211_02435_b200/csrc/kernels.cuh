@@ -1,0 +1,237 @@
+// kernels.cuh — the fused stream–collide kernels and their small helpers.
+//
+// Device population grid layout (SoA):
+//   element (zz, i, y, x) at  zz * plane + i * pop + y * pitch + x
+//   zz = local slab plane + 1 (zz = 0 and zz = nzl + 1 are ghost planes),
+//   pop = ny * pitch, plane = q * pop, pitch = nx rounded up to 32 elements.
+// With the slab axis outermost and the slab-crossing populations contiguous in i
+// (include/lbm.h ordering), every halo block is one contiguous range.
+//
+// Streaming patterns:
+//   PULL     f_i(x) = src(x - xi_i, i)  -> collide -> dst(x, i)            (two grids)
+//   AA_ODD   state A -> B: f_i(x) = mem(x - xi_i, opp i) -> collide -> mem(x + xi_i, i)
+//   AA_EVEN  state B -> A: f_i(x) = mem(x, i)          -> collide -> mem(x, opp i)
+//   (state A: mem(x, opp i) = f*_i(x);  state B: mem(x + xi_i, i) = f*_i(x); reading R11).
+// Each cell reads and writes the same q slots in both AA parities, so the in-place
+// update is race-free without synchronisation.
+#pragma once
+#include "collide.cuh"
+
+namespace lbm {
+
+enum { PAT_PULL = 0, PAT_AA_EVEN = 1, PAT_AA_ODD = 2 };
+constexpr int BLOCK_X = 128;
+
+struct GridParams {
+  long long plane;  // elements per storage plane = q * ny * pitch
+  long long pop;    // elements per population row block = ny * pitch
+  int pitch;
+  int nx, ny, nzl, nzg, z0;  // local view: x, y, slab axis (nzl local planes from global z0)
+  int zbegin;                // first local plane of this launch
+  int wrapz;                 // single rank: periodic wrap along the slab axis by index
+  int bcmask;                // bit (2 * axis + side): no-slip face (axis 0 x, 1 y, 2 slab)
+};
+
+__device__ __forceinline__ int wrapi(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
+
+template <class real>
+__device__ __forceinline__ real ld_nc(const real *p) { return __ldg(p); }
+
+// ---------------------------------------------------------------------------
+// the fused stream–collide kernel (pull, optionally with half-way bounce-back)
+// ---------------------------------------------------------------------------
+template <class S, int SPACE, int REG, class real, bool BB>
+__global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, real *__restrict__ dst,
+                                                   const GridParams g, const Rates<real> r, const real swe_g) {
+  const int x = blockIdx.x * BLOCK_X + threadIdx.x;
+  if (x >= g.nx) return;
+  const int y = blockIdx.y;
+  const int zl = g.zbegin + blockIdx.z;
+
+  // source coordinates for offsets s = -1, 0, +1 (index s + 1)
+  int xs[3], ys[3];
+  long long zo[3];
+  bool bx[3] = {false, false, false}, by[3] = {false, false, false}, bz[3] = {false, false, false};
+#pragma unroll
+  for (int s = -1; s <= 1; ++s) {
+    const int xv = x + s, yv = y + s, zv = zl + s;
+    xs[s + 1] = wrapi(xv, g.nx);
+    ys[s + 1] = wrapi(yv, g.ny) * g.pitch;
+    const int zz = g.wrapz ? wrapi(zv, g.nzl) + 1 : zv + 1;
+    zo[s + 1] = (long long)zz * g.plane;
+    if constexpr (BB) {
+      bx[s + 1] = (xv < 0 && (g.bcmask & 1)) || (xv >= g.nx && (g.bcmask & 2));
+      by[s + 1] = (yv < 0 && (g.bcmask & 4)) || (yv >= g.ny && (g.bcmask & 8));
+      const int zgv = g.z0 + zv;
+      bz[s + 1] = (zgv < 0 && (g.bcmask & 16)) || (zgv >= g.nzg && (g.bcmask & 32));
+    }
+  }
+  const long long own = (long long)(zl + 1) * g.plane + (long long)y * g.pitch + x;
+
+  real f[S::Q];
+  sfor<S::Q>([&](auto i) {
+    constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+    const long long a = zo[1 - cz] + (long long)i * g.pop + ys[1 - cy] + xs[1 - cx];
+    if constexpr (BB) {
+      const bool bb = bx[1 - cx] || by[1 - cy] || bz[1 - cz];
+      // half-way bounce-back: f_i(x) = f*_{opp i}(x)   (reading R18)
+      const long long ab = own + (long long)S::opp(i) * g.pop;
+      f[i] = ld_nc(src + (bb ? ab : a));
+    } else {
+      f[i] = ld_nc(src + a);
+    }
+  });
+
+  collide<S, SPACE, REG, real>(f, r, swe_g);
+
+  sfor<S::Q>([&](auto i) { dst[own + (long long)i * g.pop] = f[i]; });
+}
+
+// ---------------------------------------------------------------------------
+// AA pattern (single rank, periodic): in-place
+// ---------------------------------------------------------------------------
+template <class S, int SPACE, int REG, class real, int PAT>
+__global__ void __launch_bounds__(BLOCK_X) k_aa(real *mem, const GridParams g, const Rates<real> r,
+                                                 const real swe_g) {
+  const int x = blockIdx.x * BLOCK_X + threadIdx.x;
+  if (x >= g.nx) return;
+  const int y = blockIdx.y;
+  const int zl = g.zbegin + blockIdx.z;
+  real f[S::Q];
+  if constexpr (PAT == PAT_AA_EVEN) {
+    const long long own = (long long)(zl + 1) * g.plane + (long long)y * g.pitch + x;
+    sfor<S::Q>([&](auto i) { f[i] = mem[own + (long long)i * g.pop]; });
+    collide<S, SPACE, REG, real>(f, r, swe_g);
+    sfor<S::Q>([&](auto i) { mem[own + (long long)S::opp(i) * g.pop] = f[i]; });
+  } else {
+    int xs[3], ys[3];
+    long long zo[3];
+#pragma unroll
+    for (int s = -1; s <= 1; ++s) {
+      xs[s + 1] = wrapi(x + s, g.nx);
+      ys[s + 1] = wrapi(y + s, g.ny) * g.pitch;
+      zo[s + 1] = (long long)(wrapi(zl + s, g.nzl) + 1) * g.plane;
+    }
+    // read f_i(x) = mem(x - xi_i, opp i)
+    sfor<S::Q>([&](auto i) {
+      constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+      f[i] = mem[zo[1 - cz] + (long long)S::opp(i) * g.pop + ys[1 - cy] + xs[1 - cx]];
+    });
+    collide<S, SPACE, REG, real>(f, r, swe_g);
+    // write f*_i(x) to mem(x + xi_i, i)
+    sfor<S::Q>([&](auto i) {
+      constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+      mem[zo[1 + cz] + (long long)i * g.pop + ys[1 + cy] + xs[1 + cx]] = f[i];
+    });
+  }
+}
+
+// ---------------------------------------------------------------------------
+// helpers: init from macroscopic fields, canonical get/set, macroscopic moments,
+// collision-only test kernel, finiteness probe.  'state' for AA: 0 = A, 1 = B.
+// ---------------------------------------------------------------------------
+template <class S>
+struct Canon {
+  // element offset of the canonical post-collision value f*_i(x) in the grid
+  template <int i>
+  __device__ static __forceinline__ long long at(const GridParams &g, int x, int y, int zl, int aa, int state) {
+    if (!aa) return (long long)(zl + 1) * g.plane + (long long)i * g.pop + (long long)y * g.pitch + x;
+    if (state == 0)
+      return (long long)(zl + 1) * g.plane + (long long)S::opp(i) * g.pop + (long long)y * g.pitch + x;
+    const int xx = wrapi(x + S::mx(i), g.nx), yy = wrapi(y + S::my(i), g.ny), zz = wrapi(zl + S::mz(i), g.nzl);
+    return (long long)(zz + 1) * g.plane + (long long)i * g.pop + (long long)yy * g.pitch + xx;
+  }
+};
+
+// host staging layouts: f[i][z][y][x] (fp64), rho[z][y][x], u[d][z][y][x]
+template <class S, int SPACE, int REG, class real>
+__global__ void k_init(real *mem, const GridParams g, int aa, const double *__restrict__ rho,
+                       const double *__restrict__ u, real swe_g) {
+  const int x = blockIdx.x * BLOCK_X + threadIdx.x;
+  if (x >= g.nx) return;
+  const int y = blockIdx.y, zl = blockIdx.z;
+  const long long cell = ((long long)zl * g.ny + y) * g.nx + x;
+  const long long ncell = (long long)g.nzl * g.ny * g.nx;
+  const real r = (real)rho[cell];
+  const real ux = (real)u[cell];
+  real uy, uz;
+  if constexpr (S::D == 3) {
+    uy = (real)u[ncell + cell];
+    uz = (real)u[2 * ncell + cell];
+  } else {
+    uy = (real)u[ncell + cell];
+    uz = real(0);
+  }
+  real f[S::Q];
+  equilibrium<S, SPACE, REG, real>(f, r, ux, uy, uz, swe_g);
+  // post-collision state at t = 0 written in state A (AA) or the current grid (pull)
+  sfor<S::Q>([&](auto i) { mem[Canon<S>::template at<i>(g, x, y, zl, aa, 0)] = f[i]; });
+}
+
+template <class S, class real>
+__global__ void k_get_populations(const real *mem, const GridParams g, int aa, int state, double *__restrict__ out) {
+  const int x = blockIdx.x * BLOCK_X + threadIdx.x;
+  if (x >= g.nx) return;
+  const int y = blockIdx.y, zl = blockIdx.z;
+  const long long cell = ((long long)zl * g.ny + y) * g.nx + x;
+  const long long ncell = (long long)g.nzl * g.ny * g.nx;
+  sfor<S::Q>([&](auto i) { out[i * ncell + cell] = (double)mem[Canon<S>::template at<i>(g, x, y, zl, aa, state)]; });
+}
+
+template <class S, class real>
+__global__ void k_set_populations(real *mem, const GridParams g, int aa, const double *__restrict__ in) {
+  const int x = blockIdx.x * BLOCK_X + threadIdx.x;
+  if (x >= g.nx) return;
+  const int y = blockIdx.y, zl = blockIdx.z;
+  const long long cell = ((long long)zl * g.ny + y) * g.nx + x;
+  const long long ncell = (long long)g.nzl * g.ny * g.nx;
+  sfor<S::Q>([&](auto i) { mem[Canon<S>::template at<i>(g, x, y, zl, aa, 0)] = (real)in[i * ncell + cell]; });
+}
+
+// rho = rho0 + sum df (zc) or sum f; u = sum f xi / rho
+template <class S, class real>
+__global__ void k_macroscopic(const real *mem, const GridParams g, int aa, int state, int zc,
+                              double *__restrict__ rho, double *__restrict__ u) {
+  const int x = blockIdx.x * BLOCK_X + threadIdx.x;
+  if (x >= g.nx) return;
+  const int y = blockIdx.y, zl = blockIdx.z;
+  const long long cell = ((long long)zl * g.ny + y) * g.nx + x;
+  const long long ncell = (long long)g.nzl * g.ny * g.nx;
+  double s = 0, jx = 0, jy = 0, jz = 0;
+  sfor<S::Q>([&](auto i) {
+    const double v = (double)mem[Canon<S>::template at<i>(g, x, y, zl, aa, state)];
+    s += v;
+    if constexpr (S::vx(i) != 0) jx += S::vx(i) * v;
+    if constexpr (S::vy(i) != 0) jy += S::vy(i) * v;
+    if constexpr (S::vz(i) != 0) jz += S::vz(i) * v;
+  });
+  const double r = zc ? 1.0 + s : s;
+  rho[cell] = r;
+  u[cell] = jx / r;
+  u[ncell + cell] = jy / r;
+  if constexpr (S::D == 3) u[2 * ncell + cell] = jz / r;
+}
+
+template <class S, int SPACE, int REG, class real>
+__global__ void k_test_collide(const double *__restrict__ fin, double *__restrict__ fout, long long n,
+                               const Rates<real> r, real swe_g) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  real f[S::Q];
+  sfor<S::Q>([&](auto i) { f[i] = (real)fin[c * S::Q + i]; });
+  collide<S, SPACE, REG, real>(f, r, swe_g);
+  sfor<S::Q>([&](auto i) { fout[c * S::Q + i] = (double)f[i]; });
+}
+
+template <class S, class real>
+__global__ void k_check_finite(const real *mem, const GridParams g, int *flag) {
+  const int x = blockIdx.x * BLOCK_X + threadIdx.x;
+  if (x >= g.nx) return;
+  const int y = blockIdx.y, zl = blockIdx.z;
+  bool bad = false;
+  const long long own = (long long)(zl + 1) * g.plane + (long long)y * g.pitch + x;
+  sfor<S::Q>([&](auto i) { bad |= !isfinite((double)mem[own + (long long)i * g.pop]); });
+  if (bad) atomicOr(flag, 1);
+}
+
+}  // namespace lbm

@@ -1,0 +1,99 @@
+// ops.cuh — type-erased launchers of one (stencil, space, regime, precision)
+// instantiation.  Each instantiation lives in its own translation unit
+// (ops_inst.cu compiled once per stencil / precision / space) so that the
+// heavy D3Q27 cumulant kernels compile in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace lbm {
+
+struct Ops {
+  int q, d;
+  // pull stream–collide of planes [zbegin, zbegin + nplanes) from src into dst
+  void (*pull)(const void *src, void *dst, const GridParams &g, const void *rates, double swe_g, int bb,
+               int nplanes, cudaStream_t s);
+  // AA step (pattern PAT_AA_EVEN / PAT_AA_ODD) in place, all planes
+  void (*aa)(void *mem, const GridParams &g, const void *rates, double swe_g, int pattern, cudaStream_t s);
+  void (*init)(void *mem, const GridParams &g, int aa, const double *rho, const double *u, double swe_g,
+               cudaStream_t s);
+  void (*get_pop)(const void *mem, const GridParams &g, int aa, int state, double *out, cudaStream_t s);
+  void (*set_pop)(void *mem, const GridParams &g, int aa, const double *in, cudaStream_t s);
+  void (*macro)(const void *mem, const GridParams &g, int aa, int state, int zc, double *rho, double *u,
+                cudaStream_t s);
+  void (*test_collide)(const double *fin, double *fout, long long n, const void *rates, double swe_g,
+                       cudaStream_t s);
+  void (*check_finite)(const void *mem, const GridParams &g, int *flag, cudaStream_t s);
+  // kernel attributes of the pull kernel (registers / local memory), for diagnostics
+  void (*attributes)(int *regs, int *local_bytes);
+};
+
+inline dim3 cell_grid(const GridParams &g, int nplanes) {
+  return dim3((unsigned)((g.nx + BLOCK_X - 1) / BLOCK_X), (unsigned)g.ny, (unsigned)nplanes);
+}
+
+template <class S, int SPACE, int REG, class real>
+struct OpsImpl {
+  static void pull(const void *src, void *dst, const GridParams &g, const void *rates, double swe_g, int bb,
+                   int nplanes, cudaStream_t s) {
+    if (nplanes <= 0) return;
+    const Rates<real> &r = *static_cast<const Rates<real> *>(rates);
+    if (bb)
+      k_pull<S, SPACE, REG, real, true><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
+          static_cast<const real *>(src), static_cast<real *>(dst), g, r, (real)swe_g);
+    else
+      k_pull<S, SPACE, REG, real, false><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
+          static_cast<const real *>(src), static_cast<real *>(dst), g, r, (real)swe_g);
+  }
+  static void aa(void *mem, const GridParams &g, const void *rates, double swe_g, int pattern, cudaStream_t s) {
+    const Rates<real> &r = *static_cast<const Rates<real> *>(rates);
+    if (pattern == PAT_AA_EVEN)
+      k_aa<S, SPACE, REG, real, PAT_AA_EVEN><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<real *>(mem), g,
+                                                                                     r, (real)swe_g);
+    else
+      k_aa<S, SPACE, REG, real, PAT_AA_ODD><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<real *>(mem), g,
+                                                                                    r, (real)swe_g);
+  }
+  static void init(void *mem, const GridParams &g, int aa, const double *rho, const double *u, double swe_g,
+                   cudaStream_t s) {
+    k_init<S, SPACE, REG, real><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<real *>(mem), g, aa, rho, u,
+                                                                        (real)swe_g);
+  }
+  static void get_pop(const void *mem, const GridParams &g, int aa, int state, double *out, cudaStream_t s) {
+    k_get_populations<S, real><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<const real *>(mem), g, aa,
+                                                                       state, out);
+  }
+  static void set_pop(void *mem, const GridParams &g, int aa, const double *in, cudaStream_t s) {
+    k_set_populations<S, real><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<real *>(mem), g, aa, in);
+  }
+  static void macro(const void *mem, const GridParams &g, int aa, int state, int zc, double *rho, double *u,
+                    cudaStream_t s) {
+    k_macroscopic<S, real><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<const real *>(mem), g, aa, state,
+                                                                   zc, rho, u);
+  }
+  static void test_collide(const double *fin, double *fout, long long n, const void *rates, double swe_g,
+                           cudaStream_t s) {
+    if (n <= 0) return;
+    const Rates<real> &r = *static_cast<const Rates<real> *>(rates);
+    const int B = 128;
+    k_test_collide<S, SPACE, REG, real><<<(unsigned)((n + B - 1) / B), B, 0, s>>>(fin, fout, n, r, (real)swe_g);
+  }
+  static void check_finite(const void *mem, const GridParams &g, int *flag, cudaStream_t s) {
+    k_check_finite<S, real><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<const real *>(mem), g, flag);
+  }
+  static void attributes(int *regs, int *local_bytes) {
+    cudaFuncAttributes a{};
+    if (cudaFuncGetAttributes(&a, k_pull<S, SPACE, REG, real, false>) == cudaSuccess) {
+      *regs = a.numRegs;
+      *local_bytes = (int)a.localSizeBytes;
+    } else {
+      *regs = -1;
+      *local_bytes = -1;
+    }
+  }
+  static constexpr Ops table{S::Q,      S::D,  &pull,         &aa,           &init,      &get_pop,
+                             &set_pop, &macro, &test_collide, &check_finite, &attributes};
+};
+
+}  // namespace lbm

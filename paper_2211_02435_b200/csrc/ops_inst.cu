@@ -1,0 +1,52 @@
+// ops_inst.cu — instantiates the kernels of one (stencil, precision, space)
+// triple.  Compiled once per triple with
+//   -DLBM_STENCIL=D3Q27 -DLBM_REAL=double -DLBM_PREC=f64 -DLBM_SPACE=CUMULANT
+// and exports  const lbm::Ops *lbm_ops_<stencil>_<prec>_<space>(int regime).
+#include "ops.cuh"
+
+#ifndef LBM_STENCIL
+#error "define LBM_STENCIL, LBM_REAL, LBM_PREC, LBM_SPACE"
+#endif
+
+#define LBM_NAME2(st, pr, sp) lbm_ops_##st##_##pr##_##sp
+#define LBM_NAME(st, pr, sp) LBM_NAME2(st, pr, sp)
+
+namespace lbm {
+namespace {
+using St = LBM_STENCIL;
+using Re = LBM_REAL;
+constexpr int POPULATION = SPACE_POPULATION, RAW = SPACE_RAW, CENTRAL = SPACE_CENTRAL,
+              CUMULANT = SPACE_CUMULANT, SWE = SPACE_SWE;
+constexpr int SP = LBM_SPACE;
+}  // namespace
+}  // namespace lbm
+
+namespace lbm {
+template <class St_, class Re_, int SP_>
+const Ops *select_ops(int regime) {
+  if constexpr (SP_ == SPACE_SWE) {
+    if constexpr (St_::Q == 9) {
+      if (regime == REG_ABS) return &OpsImpl<St_, SPACE_SWE, REG_ABS, Re_>::table;
+    }
+    return nullptr;
+  } else if constexpr (SP_ == SPACE_CUMULANT) {
+    // cumulants admit no delta equilibrium
+    switch (regime) {
+      case REG_ABS: return &OpsImpl<St_, SP_, REG_ABS, Re_>::table;
+      case REG_ZC_ABS: return &OpsImpl<St_, SP_, REG_ZC_ABS, Re_>::table;
+      default: return nullptr;
+    }
+  } else {
+    switch (regime) {
+      case REG_ABS: return &OpsImpl<St_, SP_, REG_ABS, Re_>::table;
+      case REG_DELTA: return &OpsImpl<St_, SP_, REG_DELTA, Re_>::table;
+      case REG_ZC_ABS: return &OpsImpl<St_, SP_, REG_ZC_ABS, Re_>::table;
+      default: return nullptr;
+    }
+  }
+}
+}  // namespace lbm
+
+extern "C" const lbm::Ops *LBM_NAME(LBM_STENCIL, LBM_PREC, LBM_SPACE)(int regime) {
+  return lbm::select_ops<lbm::St, lbm::Re, lbm::SP>(regime);
+}

@@ -1,0 +1,565 @@
+// runtime.cu — context, memory and the C ABI of include/lbm.h.
+//
+// Host-side runtime: validates the method (admissibility),
+// lays the population grid out in HBM (kernels.cuh), dispatches to the
+// instantiated kernels (ops_inst.cu) and moves host data in and out.  No
+// arithmetic of the method runs on the host: every population, moment and
+// macroscopic value is produced by the device kernels.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/lbm.h"
+#include "ops.cuh"
+
+using lbm::GridParams;
+using lbm::Ops;
+
+#define LBM_DECL_OPS(st, pr, sp) extern "C" const Ops *lbm_ops_##st##_##pr##_##sp(int regime);
+#define LBM_DECL_ALL(st, pr)          \
+  LBM_DECL_OPS(st, pr, POPULATION)    \
+  LBM_DECL_OPS(st, pr, RAW)           \
+  LBM_DECL_OPS(st, pr, CENTRAL)       \
+  LBM_DECL_OPS(st, pr, CUMULANT)
+LBM_DECL_ALL(D2Q9, f64)
+LBM_DECL_ALL(D2Q9, f32)
+LBM_DECL_ALL(D3Q19, f64)
+LBM_DECL_ALL(D3Q19, f32)
+LBM_DECL_ALL(D3Q27, f64)
+LBM_DECL_ALL(D3Q27, f32)
+LBM_DECL_OPS(D2Q9, f64, SWE)
+LBM_DECL_OPS(D2Q9, f32, SWE)
+
+namespace {
+
+const Ops *find_ops(int stencil, int prec, int space, int regime) {
+#define LBM_CASE_SPACE(st, pr)                              \
+  switch (space) {                                          \
+    case LBM_SPACE_POPULATION: return lbm_ops_##st##_##pr##_POPULATION(regime); \
+    case LBM_SPACE_RAW: return lbm_ops_##st##_##pr##_RAW(regime);               \
+    case LBM_SPACE_CENTRAL: return lbm_ops_##st##_##pr##_CENTRAL(regime);       \
+    case LBM_SPACE_CUMULANT: return lbm_ops_##st##_##pr##_CUMULANT(regime);     \
+    default: return nullptr;                                \
+  }
+  if (space == lbm::SPACE_SWE) {
+    if (stencil != LBM_D2Q9) return nullptr;
+    return prec == LBM_FP64 ? lbm_ops_D2Q9_f64_SWE(regime) : lbm_ops_D2Q9_f32_SWE(regime);
+  }
+  if (stencil == LBM_D2Q9) {
+    if (prec == LBM_FP64) { LBM_CASE_SPACE(D2Q9, f64) } else { LBM_CASE_SPACE(D2Q9, f32) }
+  } else if (stencil == LBM_D3Q19) {
+    if (prec == LBM_FP64) { LBM_CASE_SPACE(D3Q19, f64) } else { LBM_CASE_SPACE(D3Q19, f32) }
+  } else if (stencil == LBM_D3Q27) {
+    if (prec == LBM_FP64) { LBM_CASE_SPACE(D3Q27, f64) } else { LBM_CASE_SPACE(D3Q27, f32) }
+  }
+  return nullptr;
+#undef LBM_CASE_SPACE
+}
+
+thread_local std::string g_create_error;
+
+}  // namespace
+
+struct lbm_ctx {
+  int stencil = 0, space = 0, eq = 0, zc = 0, regime = 0, prec = 0, streaming = 0, kspace = 0;
+  const Ops *ops = nullptr;
+  int q = 0, d = 0;
+  int gnx = 0, gny = 0, gnz = 0;
+  int rank = 0, nranks = 1, offset = 0, extent = 0;
+  int bb = 0;
+  GridParams g{};
+  size_t esize = 8, grid_elems = 0;
+  void *buf[2] = {nullptr, nullptr};
+  int cur = 0;       // pull: index of the current grid
+  int aa_state = 0;  // AA: 0 = state A, 1 = state B
+  long long steps = 0;
+  alignas(16) unsigned char rates[27 * 8];
+  double swe_g = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void *staging = nullptr;
+  size_t staging_bytes = 0;
+  int *flag = nullptr;
+  std::string err;
+};
+
+namespace {
+
+lbm_status fail(lbm_ctx *c, lbm_status s, const std::string &msg) {
+  if (c) c->err = msg;
+  else g_create_error = msg;
+  return s;
+}
+
+lbm_status cuda_fail(lbm_ctx *c, cudaError_t e, const char *what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+  return fail(c, e == cudaErrorMemoryAllocation ? LBM_ENOMEM : LBM_ECUDA, m);
+}
+
+#define LBM_CUDA(c, call)                                   \
+  do {                                                      \
+    cudaError_t e_ = (call);                                \
+    if (e_ != cudaSuccess) return cuda_fail((c), e_, #call); \
+  } while (0)
+
+lbm_status check_launch(lbm_ctx *c, const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(c, e, what);
+  return LBM_OK;
+}
+
+lbm_status ensure_staging(lbm_ctx *c, size_t bytes) {
+  if (c->staging_bytes >= bytes) return LBM_OK;
+  if (c->staging) cudaFree(c->staging);
+  c->staging = nullptr;
+  c->staging_bytes = 0;
+  LBM_CUDA(c, cudaMalloc(&c->staging, bytes));
+  c->staging_bytes = bytes;
+  return LBM_OK;
+}
+
+int q_of(int stencil) { return stencil == LBM_D2Q9 ? 9 : (stencil == LBM_D3Q19 ? 19 : 27); }
+
+long long local_cells(const lbm_ctx *c) { return (long long)c->g.nx * c->g.ny * c->g.nzl; }
+
+void *grid_ptr(lbm_ctx *c, int which) {
+  if (c->streaming == LBM_AA) return c->buf[0];
+  return c->buf[which == 0 ? c->cur : 1 - c->cur];
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *lbm_version(void) { return "lbm-b200 0.1 (sm_100a; arXiv 2211.02435 hot path)"; }
+
+const char *lbm_last_error(const lbm_ctx *ctx) {
+  if (!ctx) return g_create_error.c_str();
+  return ctx->err.c_str();
+}
+
+lbm_status lbm_slab_extent(int extent, int rank, int nranks, int *offset, int *local_extent) {
+  if (!offset || !local_extent) return LBM_EINVAL;
+  if (nranks < 1 || rank < 0 || rank >= nranks || extent < 1) return LBM_EINVAL;
+  if (extent % nranks != 0) return LBM_EINVAL;
+  const int n = extent / nranks;
+  *offset = rank * n;
+  *local_extent = n;
+  return LBM_OK;
+}
+
+lbm_status lbm_stencil_info(lbm_stencil stencil, int *q, int *xi, int *opposite) {
+  if (!q) return LBM_EINVAL;
+  auto fill = [&](auto S) {
+    using St = decltype(S);
+    *q = St::Q;
+    for (int i = 0; i < St::Q; ++i) {
+      if (xi) {
+        xi[3 * i + 0] = St::vx(i);
+        xi[3 * i + 1] = St::vy(i);
+        xi[3 * i + 2] = St::vz(i);
+      }
+      if (opposite) opposite[i] = St::opp(i);
+    }
+  };
+  switch (stencil) {
+    case LBM_D2Q9: fill(lbm::D2Q9{}); return LBM_OK;
+    case LBM_D3Q19: fill(lbm::D3Q19{}); return LBM_OK;
+    case LBM_D3Q27: fill(lbm::D3Q27{}); return LBM_OK;
+    default: return LBM_EINVAL;
+  }
+}
+
+lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equilibrium equilibrium,
+                      const double *relaxation_rates, int n_rates, const lbm_domain *domain, int zero_centered,
+                      lbm_ctx **out) {
+  if (!out) return fail(nullptr, LBM_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!domain) return fail(nullptr, LBM_EINVAL, "domain is NULL");
+  if (!relaxation_rates) return fail(nullptr, LBM_EINVAL, "relaxation_rates is NULL");
+  if (stencil < LBM_D2Q9 || stencil > LBM_D3Q27) return fail(nullptr, LBM_EINVAL, "unknown stencil");
+  if (collision_space < LBM_SPACE_POPULATION || collision_space > LBM_SPACE_CUMULANT)
+    return fail(nullptr, LBM_EINVAL, "unknown collision space");
+  if (equilibrium < LBM_EQ_ABSOLUTE || equilibrium > LBM_EQ_SWE)
+    return fail(nullptr, LBM_EINVAL, "unknown equilibrium");
+  const int zc = zero_centered ? 1 : 0;
+  // admissibility
+  if (equilibrium == LBM_EQ_DELTA && !zc)
+    return fail(nullptr, LBM_EUNSUPPORTED, "delta equilibrium requires zero-centered storage (PAPER.md:546)");
+  if (equilibrium == LBM_EQ_DELTA && collision_space == LBM_SPACE_CUMULANT)
+    return fail(nullptr, LBM_EUNSUPPORTED,
+                "cumulant space is incompatible with the delta equilibrium (PAPER.md:430-431, 547)");
+  if (equilibrium == LBM_EQ_SWE &&
+      !(stencil == LBM_D2Q9 && collision_space == LBM_SPACE_CENTRAL && !zc))
+    return fail(nullptr, LBM_EUNSUPPORTED,
+                "the shallow-water equilibrium is provided for D2Q9, central moments, absolute storage");
+  const int q = q_of(stencil);
+  const int need = (collision_space == LBM_SPACE_POPULATION) ? 1 : q;
+  if (n_rates != need)
+    return fail(nullptr, LBM_EINVAL, "n_rates must be " + std::to_string(need) + " for this method");
+  for (int i = 0; i < n_rates; ++i)
+    if (!std::isfinite(relaxation_rates[i]) || relaxation_rates[i] < 0.0 || relaxation_rates[i] > 2.0)
+      return fail(nullptr, LBM_EINVAL, "relaxation rate " + std::to_string(i) + " outside [0, 2]");
+  const lbm_domain &D = *domain;
+  const bool two_d = (stencil == LBM_D2Q9);
+  if (D.nx < 4 || D.ny < 4 || (two_d ? D.nz != 1 : D.nz < 4))
+    return fail(nullptr, LBM_EINVAL, two_d ? "D2Q9 needs nx, ny >= 4 and nz == 1" : "extents must be >= 4");
+  for (int a = 0; a < 3; ++a) {
+    for (int s = 0; s < 2; ++s)
+      if (D.bc[a][s] != LBM_BC_PERIODIC && D.bc[a][s] != LBM_BC_NOSLIP)
+        return fail(nullptr, LBM_EINVAL, "unknown boundary condition");
+    if ((D.bc[a][0] == LBM_BC_PERIODIC) != (D.bc[a][1] == LBM_BC_PERIODIC))
+      return fail(nullptr, LBM_EINVAL, "periodic must be set on both faces of an axis");
+  }
+  if (D.precision != LBM_FP64 && D.precision != LBM_FP32) return fail(nullptr, LBM_EINVAL, "unknown precision");
+  if (D.streaming != LBM_PULL && D.streaming != LBM_AA) return fail(nullptr, LBM_EINVAL, "unknown streaming");
+  if (D.nranks < 1 || D.rank < 0 || D.rank >= D.nranks) return fail(nullptr, LBM_EINVAL, "bad rank/nranks");
+  const int slab_extent = two_d ? D.ny : D.nz;
+  if (slab_extent % D.nranks != 0)
+    return fail(nullptr, LBM_EINVAL, "nranks must divide the slab-axis extent");
+  if (slab_extent / D.nranks < 2) return fail(nullptr, LBM_EINVAL, "slabs need at least 2 planes");
+  bool any_wall = false;
+  for (int a = 0; a < 3; ++a) any_wall |= (D.bc[a][0] == LBM_BC_NOSLIP);
+  if (D.streaming == LBM_AA && (D.nranks > 1 || any_wall))
+    return fail(nullptr, LBM_EUNSUPPORTED, "AA streaming is provided for a single rank with periodic faces");
+
+  int regime = lbm::REG_ABS;
+  if (zc) regime = (equilibrium == LBM_EQ_DELTA) ? lbm::REG_DELTA : lbm::REG_ZC_ABS;
+  const int kspace = (equilibrium == LBM_EQ_SWE) ? (int)lbm::SPACE_SWE : (int)collision_space;
+  const Ops *ops = find_ops(stencil, D.precision, kspace, regime);
+  if (!ops) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
+
+  lbm_ctx *c = new lbm_ctx;
+  c->stencil = stencil;
+  c->space = collision_space;
+  c->kspace = kspace;
+  c->eq = equilibrium;
+  c->zc = zc;
+  c->regime = regime;
+  c->prec = D.precision;
+  c->streaming = D.streaming;
+  c->ops = ops;
+  c->q = q;
+  c->d = two_d ? 2 : 3;
+  c->gnx = D.nx;
+  c->gny = D.ny;
+  c->gnz = D.nz;
+  c->rank = D.rank;
+  c->nranks = D.nranks;
+  c->swe_g = D.swe_g;
+  c->device = D.device;
+  c->esize = (D.precision == LBM_FP64) ? 8 : 4;
+  lbm_slab_extent(slab_extent, D.rank, D.nranks, &c->offset, &c->extent);
+
+  // memory view: (x, y, slab); D2Q9 maps its physical y onto the slab axis
+  GridParams &g = c->g;
+  g.nx = D.nx;
+  g.ny = two_d ? 1 : D.ny;
+  g.nzl = c->extent;
+  g.nzg = slab_extent;
+  g.z0 = c->offset;
+  g.zbegin = 0;
+  g.wrapz = (D.nranks == 1) ? 1 : 0;
+  const size_t align = 128 / c->esize;  // 128-byte aligned rows
+  g.pitch = (int)(((size_t)D.nx + align - 1) / align * align);
+  g.pop = (long long)g.ny * g.pitch;
+  g.plane = (long long)q * g.pop;
+  int mask = 0;
+  auto wall = [&](int a, int s) { return D.bc[a][s] == LBM_BC_NOSLIP; };
+  if (wall(0, 0)) mask |= 1;
+  if (wall(0, 1)) mask |= 2;
+  if (two_d) {
+    if (wall(1, 0)) mask |= 16;
+    if (wall(1, 1)) mask |= 32;
+  } else {
+    if (wall(1, 0)) mask |= 4;
+    if (wall(1, 1)) mask |= 8;
+    if (wall(2, 0)) mask |= 16;
+    if (wall(2, 1)) mask |= 32;
+  }
+  g.bcmask = mask;
+  c->bb = mask != 0;
+
+  // rates in the storage precision
+  if (c->esize == 8) {
+    double *r = reinterpret_cast<double *>(c->rates);
+    for (int i = 0; i < 27; ++i) r[i] = (i < n_rates) ? relaxation_rates[i] : 0.0;
+  } else {
+    float *r = reinterpret_cast<float *>(c->rates);
+    for (int i = 0; i < 27; ++i) r[i] = (i < n_rates) ? (float)relaxation_rates[i] : 0.0f;
+  }
+
+  auto bail = [&](lbm_status s) {
+    g_create_error = c->err;
+    lbm_destroy(c);
+    return s;
+  };
+  cudaError_t e = cudaSetDevice(D.device);
+  if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaSetDevice"));
+  if (D.stream) {
+    c->stream = (cudaStream_t)D.stream;
+  } else {
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaStreamCreate"));
+    c->own_stream = true;
+  }
+  c->grid_elems = (size_t)(g.nzl + 2) * (size_t)g.plane;
+  const int ngrids = (D.streaming == LBM_AA) ? 1 : 2;
+  for (int k = 0; k < ngrids; ++k) {
+    e = cudaMalloc(&c->buf[k], c->grid_elems * c->esize);
+    if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaMalloc(populations)"));
+    e = cudaMemsetAsync(c->buf[k], 0, c->grid_elems * c->esize, c->stream);
+    if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaMemset"));
+  }
+  e = cudaMalloc(&c->flag, sizeof(int));
+  if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaMalloc(flag)"));
+  e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaStreamSynchronize"));
+  *out = c;
+  return LBM_OK;
+}
+
+lbm_status lbm_destroy(lbm_ctx *c) {
+  if (!c) return LBM_EINVAL;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (int k = 0; k < 2; ++k)
+    if (c->buf[k]) cudaFree(c->buf[k]);
+  if (c->staging) cudaFree(c->staging);
+  if (c->flag) cudaFree(c->flag);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return LBM_OK;
+}
+
+lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
+  if (!c || !info) return LBM_EINVAL;
+  info->q = c->q;
+  info->d = c->d;
+  info->offset = c->offset;
+  info->extent = c->extent;
+  info->nx = c->gnx;
+  info->ny = c->gny;
+  info->nz = c->gnz;
+  info->pitch = (size_t)c->g.pitch;
+  info->bytes_per_element = c->esize;
+  info->device_bytes = c->grid_elems * c->esize * (c->streaming == LBM_AA ? 1 : 2);
+  info->steps_done = c->steps;
+  return LBM_OK;
+}
+
+lbm_status lbm_init_macroscopic(lbm_ctx *c, const double *rho, const double *u) {
+  if (!c || !rho || !u) return fail(c, LBM_EINVAL, "null argument");
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  const long long n = local_cells(c);
+  const size_t bytes = (size_t)n * (1 + c->d) * sizeof(double);
+  lbm_status s = ensure_staging(c, bytes);
+  if (s != LBM_OK) return s;
+  double *dr = static_cast<double *>(c->staging);
+  double *du = dr + n;
+  LBM_CUDA(c, cudaMemcpyAsync(dr, rho, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  LBM_CUDA(c, cudaMemcpyAsync(du, u, (size_t)n * c->d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  const int aa = c->streaming == LBM_AA;
+  GridParams g = c->g;
+  c->cur = 0;
+  c->aa_state = 0;
+  c->ops->init(grid_ptr(c, 0), g, aa, dr, du, c->swe_g, c->stream);
+  s = check_launch(c, "k_init");
+  if (s != LBM_OK) return s;
+  c->steps = 0;
+  LBM_CUDA(c, cudaStreamSynchronize(c->stream));
+  return LBM_OK;
+}
+
+lbm_status lbm_step(lbm_ctx *c, int n) {
+  if (!c) return LBM_EINVAL;
+  if (n < 0) return fail(c, LBM_EINVAL, "negative step count");
+  if (c->nranks > 1)
+    return fail(c, LBM_EUNSUPPORTED, "multi-rank contexts step through lbm_step_region + halo exchange");
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  GridParams g = c->g;
+  for (int t = 0; t < n; ++t) {
+    if (c->streaming == LBM_AA) {
+      const int pat = (c->aa_state == 0) ? lbm::PAT_AA_ODD : lbm::PAT_AA_EVEN;
+      c->ops->aa(c->buf[0], g, c->rates, c->swe_g, pat, c->stream);
+      c->aa_state ^= 1;
+    } else {
+      c->ops->pull(c->buf[c->cur], c->buf[1 - c->cur], g, c->rates, c->swe_g, c->bb, g.nzl, c->stream);
+      c->cur ^= 1;
+    }
+    c->steps++;
+  }
+  return check_launch(c, "stream_collide");
+}
+
+lbm_status lbm_step_region(lbm_ctx *c, lbm_region region, void *stream) {
+  if (!c) return LBM_EINVAL;
+  if (c->streaming != LBM_PULL) return fail(c, LBM_EUNSUPPORTED, "lbm_step_region needs pull streaming");
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+  GridParams g = c->g;
+  const void *src = c->buf[c->cur];
+  void *dst = c->buf[1 - c->cur];
+  const int n = g.nzl;
+  switch (region) {
+    case LBM_REGION_ALL:
+      g.zbegin = 0;
+      c->ops->pull(src, dst, g, c->rates, c->swe_g, c->bb, n, s);
+      break;
+    case LBM_REGION_BOUNDARY:
+      g.zbegin = 0;
+      c->ops->pull(src, dst, g, c->rates, c->swe_g, c->bb, 1, s);
+      g.zbegin = n - 1;
+      c->ops->pull(src, dst, g, c->rates, c->swe_g, c->bb, 1, s);
+      break;
+    case LBM_REGION_INTERIOR:
+      g.zbegin = 1;
+      c->ops->pull(src, dst, g, c->rates, c->swe_g, c->bb, n - 2, s);
+      break;
+    default: return fail(c, LBM_EINVAL, "unknown region");
+  }
+  return check_launch(c, "stream_collide(region)");
+}
+
+lbm_status lbm_swap(lbm_ctx *c) {
+  if (!c) return LBM_EINVAL;
+  if (c->streaming != LBM_PULL) return fail(c, LBM_EUNSUPPORTED, "lbm_swap needs pull streaming");
+  c->cur ^= 1;
+  c->steps++;
+  return LBM_OK;
+}
+
+lbm_status lbm_get_halo(lbm_ctx *c, int which, lbm_halo *out) {
+  if (!c || !out) return LBM_EINVAL;
+  if (c->streaming != LBM_PULL) return fail(c, LBM_EUNSUPPORTED, "halo exchange needs pull streaming");
+  char *base = static_cast<char *>(grid_ptr(c, which));
+  const GridParams &g = c->g;
+  int up0 = 0, nup = 0;
+  if (c->stencil == LBM_D2Q9) { up0 = lbm::D2Q9::UP0; nup = lbm::D2Q9::NUP; }
+  else if (c->stencil == LBM_D3Q19) { up0 = lbm::D3Q19::UP0; nup = lbm::D3Q19::NUP; }
+  else { up0 = lbm::D3Q27::UP0; nup = lbm::D3Q27::NUP; }
+  const size_t E = c->esize;
+  auto at = [&](int zz, int i) { return base + ((size_t)zz * g.plane + (size_t)i * g.pop) * E; };
+  out->send_lo = at(1, up0 + nup);
+  out->send_hi = at(g.nzl, up0);
+  out->recv_lo = at(0, up0);
+  out->recv_hi = at(g.nzl + 1, up0 + nup);
+  out->bytes = (size_t)nup * g.pop * E;
+  return LBM_OK;
+}
+
+lbm_status lbm_sync(lbm_ctx *c) {
+  if (!c) return LBM_EINVAL;
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  LBM_CUDA(c, cudaStreamSynchronize(c->stream));
+  return LBM_OK;
+}
+
+lbm_status lbm_get_macroscopic(lbm_ctx *c, double *rho, double *u) {
+  if (!c || !rho || !u) return fail(c, LBM_EINVAL, "null argument");
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  const long long n = local_cells(c);
+  lbm_status s = ensure_staging(c, (size_t)n * 4 * sizeof(double));
+  if (s != LBM_OK) return s;
+  double *dr = static_cast<double *>(c->staging);
+  double *du = dr + n;
+  const int aa = c->streaming == LBM_AA;
+  c->ops->macro(grid_ptr(c, 0), c->g, aa, c->aa_state, c->zc, dr, du, c->stream);
+  s = check_launch(c, "k_macroscopic");
+  if (s != LBM_OK) return s;
+  LBM_CUDA(c, cudaMemcpyAsync(rho, dr, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  LBM_CUDA(c, cudaMemcpyAsync(u, du, (size_t)n * c->d * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  LBM_CUDA(c, cudaStreamSynchronize(c->stream));
+  return LBM_OK;
+}
+
+lbm_status lbm_get_populations(lbm_ctx *c, double *f) {
+  if (!c || !f) return fail(c, LBM_EINVAL, "null argument");
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  const long long n = local_cells(c);
+  const size_t bytes = (size_t)n * c->q * sizeof(double);
+  lbm_status s = ensure_staging(c, bytes);
+  if (s != LBM_OK) return s;
+  const int aa = c->streaming == LBM_AA;
+  c->ops->get_pop(grid_ptr(c, 0), c->g, aa, c->aa_state, static_cast<double *>(c->staging), c->stream);
+  s = check_launch(c, "k_get_populations");
+  if (s != LBM_OK) return s;
+  LBM_CUDA(c, cudaMemcpyAsync(f, c->staging, bytes, cudaMemcpyDeviceToHost, c->stream));
+  LBM_CUDA(c, cudaStreamSynchronize(c->stream));
+  return LBM_OK;
+}
+
+lbm_status lbm_set_populations(lbm_ctx *c, const double *f) {
+  if (!c || !f) return fail(c, LBM_EINVAL, "null argument");
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  const long long n = local_cells(c);
+  const size_t bytes = (size_t)n * c->q * sizeof(double);
+  lbm_status s = ensure_staging(c, bytes);
+  if (s != LBM_OK) return s;
+  LBM_CUDA(c, cudaMemcpyAsync(c->staging, f, bytes, cudaMemcpyHostToDevice, c->stream));
+  const int aa = c->streaming == LBM_AA;
+  c->cur = 0;
+  c->aa_state = 0;
+  c->ops->set_pop(grid_ptr(c, 0), c->g, aa, static_cast<const double *>(c->staging), c->stream);
+  s = check_launch(c, "k_set_populations");
+  if (s != LBM_OK) return s;
+  c->steps = 0;
+  LBM_CUDA(c, cudaStreamSynchronize(c->stream));
+  return LBM_OK;
+}
+
+lbm_status lbm_check_finite(lbm_ctx *c) {
+  if (!c) return LBM_EINVAL;
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  LBM_CUDA(c, cudaMemsetAsync(c->flag, 0, sizeof(int), c->stream));
+  c->ops->check_finite(grid_ptr(c, 0), c->g, c->flag, c->stream);
+  lbm_status s = check_launch(c, "k_check_finite");
+  if (s != LBM_OK) return s;
+  int h = 0;
+  LBM_CUDA(c, cudaMemcpyAsync(&h, c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  LBM_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (h) return fail(c, LBM_ENUMERIC, "non-finite population after step " + std::to_string(c->steps));
+  return LBM_OK;
+}
+
+lbm_status lbm_test_collide(lbm_ctx *c, const double *f_in, double *f_out, long long n_cells) {
+  if (!c || !f_in || !f_out || n_cells < 0) return fail(c, LBM_EINVAL, "bad argument");
+  if (n_cells == 0) return LBM_OK;
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  const size_t bytes = (size_t)n_cells * c->q * sizeof(double);
+  lbm_status s = ensure_staging(c, 2 * bytes);
+  if (s != LBM_OK) return s;
+  double *din = static_cast<double *>(c->staging);
+  double *dout = din + (size_t)n_cells * c->q;
+  LBM_CUDA(c, cudaMemcpyAsync(din, f_in, bytes, cudaMemcpyHostToDevice, c->stream));
+  c->ops->test_collide(din, dout, n_cells, c->rates, c->swe_g, c->stream);
+  s = check_launch(c, "k_test_collide");
+  if (s != LBM_OK) return s;
+  LBM_CUDA(c, cudaMemcpyAsync(f_out, dout, bytes, cudaMemcpyDeviceToHost, c->stream));
+  LBM_CUDA(c, cudaStreamSynchronize(c->stream));
+  return LBM_OK;
+}
+
+/* diagnostics: registers / local memory of this context's pull kernel */
+lbm_status lbm_kernel_attributes(const lbm_ctx *c, int *regs, int *local_bytes) {
+  if (!c || !regs || !local_bytes) return LBM_EINVAL;
+  c->ops->attributes(regs, local_bytes);
+  return LBM_OK;
+}
+
+/* device pointer of the current population grid (for zero-copy diagnostics) */
+lbm_status lbm_device_grid(lbm_ctx *c, int which, void **ptr, size_t *bytes) {
+  if (!c || !ptr || !bytes) return LBM_EINVAL;
+  *ptr = grid_ptr(c, which);
+  *bytes = c->grid_elems * c->esize;
+  return LBM_OK;
+}
+
+/* the context's CUDA stream (cudaStream_t) */
+void *lbm_stream(lbm_ctx *c) { return c ? (void *)c->stream : nullptr; }
+
+}  // extern "C"

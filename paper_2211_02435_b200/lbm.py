@@ -1,0 +1,268 @@
+"""Thin ctypes binding of include/lbm.h (argument marshalling only).
+
+Every step of the hot path runs in liblbm.so's CUDA kernels; this module only
+converts numpy arrays to pointers and status codes to exceptions.  There is
+no CPU fallback: if liblbm.so cannot be loaded, importing the binding raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblbm.so")
+
+# enums of include/lbm.h
+LBM_OK, LBM_EINVAL, LBM_EUNSUPPORTED, LBM_ENOMEM, LBM_ECUDA, LBM_ENUMERIC = 0, -1, -2, -3, -4, -6
+LBM_D2Q9, LBM_D3Q19, LBM_D3Q27 = 0, 1, 2
+LBM_SPACE_POPULATION, LBM_SPACE_RAW, LBM_SPACE_CENTRAL, LBM_SPACE_CUMULANT = 0, 1, 2, 3
+LBM_EQ_ABSOLUTE, LBM_EQ_DELTA, LBM_EQ_SWE = 0, 1, 2
+LBM_FP64, LBM_FP32 = 0, 1
+LBM_PULL, LBM_AA = 0, 1
+LBM_BC_PERIODIC, LBM_BC_NOSLIP = 0, 1
+LBM_REGION_ALL, LBM_REGION_BOUNDARY, LBM_REGION_INTERIOR = 0, 1, 2
+
+Q_OF = {LBM_D2Q9: 9, LBM_D3Q19: 19, LBM_D3Q27: 27}
+
+STATUS_NAMES = {0: "LBM_OK", -1: "LBM_EINVAL", -2: "LBM_EUNSUPPORTED", -3: "LBM_ENOMEM", -4: "LBM_ECUDA",
+                -6: "LBM_ENUMERIC"}
+
+
+class LbmError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class lbm_domain(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int),
+                ("bc", (ctypes.c_int * 2) * 3), ("precision", ctypes.c_int), ("streaming", ctypes.c_int),
+                ("swe_g", ctypes.c_double), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
+                ("rank", ctypes.c_int), ("nranks", ctypes.c_int)]
+
+
+class lbm_halo(ctypes.Structure):
+    _fields_ = [("send_lo", ctypes.c_void_p), ("send_hi", ctypes.c_void_p), ("recv_lo", ctypes.c_void_p),
+                ("recv_hi", ctypes.c_void_p), ("bytes", ctypes.c_size_t)]
+
+
+class lbm_info(ctypes.Structure):
+    _fields_ = [("q", ctypes.c_int), ("d", ctypes.c_int), ("offset", ctypes.c_int), ("extent", ctypes.c_int),
+                ("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int), ("pitch", ctypes.c_size_t),
+                ("bytes_per_element", ctypes.c_size_t), ("device_bytes", ctypes.c_size_t),
+                ("steps_done", ctypes.c_longlong)]
+
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int)
+_vp = ctypes.c_void_p
+
+# (name, restype, argtypes) for every symbol of include/lbm.h
+SIGNATURES = [
+    ("lbm_create", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, ctypes.c_int,
+                                  ctypes.POINTER(lbm_domain), ctypes.c_int, ctypes.POINTER(_vp)]),
+    ("lbm_destroy", ctypes.c_int, [_vp]),
+    ("lbm_last_error", ctypes.c_char_p, [_vp]),
+    ("lbm_get_info", ctypes.c_int, [_vp, ctypes.POINTER(lbm_info)]),
+    ("lbm_init_macroscopic", ctypes.c_int, [_vp, _dp, _dp]),
+    ("lbm_step", ctypes.c_int, [_vp, ctypes.c_int]),
+    ("lbm_step_region", ctypes.c_int, [_vp, ctypes.c_int, _vp]),
+    ("lbm_swap", ctypes.c_int, [_vp]),
+    ("lbm_get_halo", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(lbm_halo)]),
+    ("lbm_sync", ctypes.c_int, [_vp]),
+    ("lbm_get_macroscopic", ctypes.c_int, [_vp, _dp, _dp]),
+    ("lbm_get_populations", ctypes.c_int, [_vp, _dp]),
+    ("lbm_set_populations", ctypes.c_int, [_vp, _dp]),
+    ("lbm_check_finite", ctypes.c_int, [_vp]),
+    ("lbm_test_collide", ctypes.c_int, [_vp, _dp, _dp, ctypes.c_longlong]),
+    ("lbm_stencil_info", ctypes.c_int, [ctypes.c_int, _ip, _ip, _ip]),
+    ("lbm_slab_extent", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, _ip]),
+    ("lbm_version", ctypes.c_char_p, []),
+    ("lbm_kernel_attributes", ctypes.c_int, [_vp, _ip, _ip]),
+    ("lbm_device_grid", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_size_t)]),
+    ("lbm_stream", _vp, [_vp]),
+]
+
+_lib = None
+
+
+def lib():
+    """The loaded liblbm.so.  Raises if the CUDA library is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run paper_2211_02435_b200.build.build() "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _d(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(_dp)
+
+
+def _check(status: int, ctx=None):
+    if status != LBM_OK:
+        msg = lib().lbm_last_error(ctx)
+        raise LbmError(status, msg.decode() if msg else "")
+
+
+def stencil_info(stencil: int):
+    q = ctypes.c_int()
+    xi = np.zeros(27 * 3, np.int32)
+    opp = np.zeros(27, np.int32)
+    _check(lib().lbm_stencil_info(stencil, ctypes.byref(q), xi.ctypes.data_as(_ip), opp.ctypes.data_as(_ip)))
+    n = q.value
+    return xi[: 3 * n].reshape(n, 3).copy(), opp[:n].copy()
+
+
+def slab_extent(extent: int, rank: int, nranks: int):
+    off, ext = ctypes.c_int(), ctypes.c_int()
+    _check(lib().lbm_slab_extent(extent, rank, nranks, ctypes.byref(off), ctypes.byref(ext)))
+    return off.value, ext.value
+
+
+def version() -> str:
+    return lib().lbm_version().decode()
+
+
+class Lattice:
+    """One lbm_ctx: a rank's slab of an MRT LBM simulation on a CUDA device.
+
+    Arguments mirror lbm_create(); shape = (nx, ny, nz) global (2D: nz = 1);
+    bc = [[x_lo, x_hi], [y_lo, y_hi], [z_lo, z_hi]] of LBM_BC_*.
+    """
+
+    def __init__(self, stencil, space, equilibrium, rates, shape, zero_centered=True, precision=LBM_FP64,
+                 streaming=LBM_PULL, bc=None, swe_g=0.0, device=0, stream=None, rank=0, nranks=1):
+        L = lib()
+        dom = lbm_domain()
+        dom.nx, dom.ny, dom.nz = (int(v) for v in shape)
+        bc = bc if bc is not None else [[LBM_BC_PERIODIC] * 2] * 3
+        for a in range(3):
+            for s in range(2):
+                dom.bc[a][s] = int(bc[a][s])
+        dom.precision = int(precision)
+        dom.streaming = int(streaming)
+        dom.swe_g = float(swe_g)
+        dom.device = int(device)
+        dom.stream = stream
+        dom.rank = int(rank)
+        dom.nranks = int(nranks)
+        r = np.ascontiguousarray(np.asarray(rates, dtype=np.float64).reshape(-1))
+        h = _vp()
+        self._ctx = None
+        _check(L.lbm_create(int(stencil), int(space), int(equilibrium), _d(r), r.size, ctypes.byref(dom),
+                            1 if zero_centered else 0, ctypes.byref(h)))
+        self._ctx = h
+        self.stencil, self.space, self.equilibrium = int(stencil), int(space), int(equilibrium)
+        self.zero_centered = bool(zero_centered)
+        self.precision, self.streaming = int(precision), int(streaming)
+        info = self.info()
+        self.q, self.d = info.q, info.d
+        self.global_shape = (info.nx, info.ny, info.nz)
+        self.offset, self.extent = info.offset, info.extent
+        nx, ny, nz = self.global_shape
+        # host array shape of this rank's slab: [z][y][x] (2D: [1][y_local][x])
+        self.local_shape = (1, self.extent, nx) if self.d == 2 else (self.extent, ny, nx)
+
+    # -- lifecycle
+    def close(self):
+        if self._ctx:
+            lib().lbm_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- C ABI, same names
+    def info(self) -> lbm_info:
+        i = lbm_info()
+        _check(lib().lbm_get_info(self._ctx, ctypes.byref(i)), self._ctx)
+        return i
+
+    @property
+    def cells(self) -> int:
+        z, y, x = self.local_shape
+        return z * y * x
+
+    def init_macroscopic(self, rho, u):
+        rho = np.ascontiguousarray(rho, dtype=np.float64).reshape(-1)
+        u = np.ascontiguousarray(u, dtype=np.float64).reshape(-1)
+        assert rho.size == self.cells and u.size == self.d * self.cells
+        _check(lib().lbm_init_macroscopic(self._ctx, _d(rho), _d(u)), self._ctx)
+
+    def step(self, n=1):
+        _check(lib().lbm_step(self._ctx, int(n)), self._ctx)
+
+    def step_region(self, region, stream=None):
+        _check(lib().lbm_step_region(self._ctx, int(region), stream), self._ctx)
+
+    def swap(self):
+        _check(lib().lbm_swap(self._ctx), self._ctx)
+
+    def get_halo(self, which=0) -> lbm_halo:
+        h = lbm_halo()
+        _check(lib().lbm_get_halo(self._ctx, int(which), ctypes.byref(h)), self._ctx)
+        return h
+
+    def sync(self):
+        _check(lib().lbm_sync(self._ctx), self._ctx)
+
+    def get_macroscopic(self, out=None):
+        z, y, x = self.local_shape
+        rho = np.empty((z, y, x)) if out is None else out[0]
+        u = np.empty((self.d, z, y, x)) if out is None else out[1]
+        _check(lib().lbm_get_macroscopic(self._ctx, _d(rho), _d(u)), self._ctx)
+        return rho, u
+
+    def get_populations(self):
+        f = np.empty((self.q,) + self.local_shape)
+        _check(lib().lbm_get_populations(self._ctx, _d(f)), self._ctx)
+        return f
+
+    def set_populations(self, f):
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        assert f.size == self.q * self.cells
+        _check(lib().lbm_set_populations(self._ctx, _d(f)), self._ctx)
+
+    def check_finite(self):
+        _check(lib().lbm_check_finite(self._ctx), self._ctx)
+
+    def test_collide(self, f_in):
+        f_in = np.ascontiguousarray(f_in, dtype=np.float64)
+        assert f_in.ndim == 2 and f_in.shape[1] == self.q
+        out = np.empty_like(f_in)
+        _check(lib().lbm_test_collide(self._ctx, _d(f_in), _d(out), f_in.shape[0]), self._ctx)
+        return out
+
+    def kernel_attributes(self):
+        r, l = ctypes.c_int(), ctypes.c_int()
+        _check(lib().lbm_kernel_attributes(self._ctx, ctypes.byref(r), ctypes.byref(l)), self._ctx)
+        return r.value, l.value
+
+    def device_grid(self, which=0):
+        p, b = _vp(), ctypes.c_size_t()
+        _check(lib().lbm_device_grid(self._ctx, int(which), ctypes.byref(p), ctypes.byref(b)), self._ctx)
+        return p.value, b.value
+
+    @property
+    def stream(self):
+        return lib().lbm_stream(self._ctx)

@@ -1,0 +1,74 @@
+"""Shared helpers of the GPU parity tests: seeded initial states built by the
+ORACLE (never by the CUDA path) and the parity metric (reading R12)."""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+import workloads as W
+
+F64_TOL = 1e-12  # BASELINE.json north_star: max relative population error, fp64
+F32_TOL = 1e-5   # ... fp32
+
+
+def q_of(st):
+    return W.Q_OF[st]
+
+
+def initial_state(st, space, eq, zc, shape, u0=0.05, noise=1e-3, plane="xz", seed=W.SEED, g=0.0,
+                  z0=0, nz_global=None, dam=None):
+    """Stored-form populations [q][nz][ny][nx] (2D: [q][1][ny][nx]): the oracle's
+    equilibrium of a TGV (or dam-break) field plus seeded noise noise * w_i * U(-1,1)."""
+    nx, ny, nz = shape
+    q = q_of(st)
+    xi, opp, w, M, Minv = oracle.tables(st)
+    if dam is not None:
+        rho, u = W.dam_break_fields(nx, ny, *dam)
+        rho = rho.reshape(1, ny, nx)
+        u = u.reshape(3, 1, ny, nx)
+    elif W.DIM_OF[st] == 2:
+        rho, u = W.tgv_fields(nx, ny, 1, u0, plane="xy")
+    else:
+        rho, u = W.tgv_fields(nx, ny, nz, u0, plane=plane, z0=z0, nz_global=nz_global)
+    feq = oracle.equilibrium(st, space, eq, zc, rho.reshape(-1), u.reshape(3, -1).T, g=g)  # [cells, q]
+    zz = nz if W.DIM_OF[st] == 3 else 1
+    f = np.ascontiguousarray(feq.T.reshape(q, zz, ny, nx))
+    if noise:
+        U = W.noise_field(seed, q, nx, ny, zz, z0=z0)
+        scale = w if dam is None else np.ones(q) * rho.mean()
+        f = f + noise * scale[:, None, None, None] * U
+    return f
+
+
+def absolute(st, f, zc):
+    """Absolute populations f = stored + f0 (zero-centered) or stored."""
+    if not zc:
+        return f
+    w = oracle.tables(st)[2]
+    shape = (-1,) + (1,) * (f.ndim - 1)
+    return f + w.reshape(shape)
+
+
+def gate_error(st, f_gpu, f_ref, zc):
+    """Max over (x, i) of |f_gpu - f_ref| / |f_ref| on absolute populations (reading R12)."""
+    a = absolute(st, f_gpu, zc)
+    b = absolute(st, f_ref, zc)
+    return float(np.max(np.abs(a - b) / np.abs(b)))
+
+
+def field_error(st, f_gpu, f_ref):
+    """Report-only: max |df_gpu - df_ref| / max |df_ref| (stored form)."""
+    return float(np.max(np.abs(f_gpu - f_ref)) / max(np.max(np.abs(f_ref)), 1e-300))
+
+
+def round_to(f, precision):
+    from paper_2211_02435_b200 import lbm as L
+
+    return f.astype(np.float32).astype(np.float64) if precision == L.LBM_FP32 else f
+
+
+def oracle_run(st, space, eq, zc, rates, shape, f0, steps, bc=None, g=0.0):
+    sim = oracle.Sim(st, space, eq, zc, rates, shape, bc=bc, g=g, prec=oracle.LONG_DOUBLE)
+    sim.set(f0)
+    sim.step(steps)
+    return sim.get()

@@ -1,0 +1,65 @@
+"""Slab decomposition on one GPU: N contexts (ranks 0..N-1 of N) in one process,
+connected by LocalTransport, must reproduce the single-rank run BITWISE
+(same per-cell arithmetic; only the ghost-plane plumbing differs), and match
+the oracle at full parity."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import workloads as W
+from gpu_helpers import F64_TOL, gate_error, initial_state, oracle_run
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2211_02435_b200 import distributed as D  # noqa: E402
+from paper_2211_02435_b200 import lbm as L  # noqa: E402
+
+
+def run_slabs(st, space, eq, zc, rates, shape, f0, steps, nranks, bc=None):
+    nx, ny, nz = shape
+    slab_axis = 2 if W.DIM_OF[st] == 2 else 1  # in the [q][z][y][x] host layout (2D: [q][1][y][x])
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, bc=bc, rank=r, nranks=nranks)
+            for r in range(nranks)]
+    for lat in lats:
+        sl = [slice(None)] * 4
+        sl[slab_axis] = slice(lat.offset, lat.offset + lat.extent)
+        lat.set_populations(np.ascontiguousarray(f0[tuple(sl)]))
+    D.prime_local(lats)
+    D.step_local(lats, steps)
+    out = np.concatenate([lat.get_populations() for lat in lats], axis=slab_axis)
+    for lat in lats:
+        lat.close()
+    return out
+
+
+@pytest.mark.parametrize("st,space,eq,zc,nranks", [
+    (W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1, 2),
+    (W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1, 4),
+    (W.D3Q19, W.RAW, W.EQ_DELTA, 1, 3),
+    (W.D2Q9, W.CENTRAL, W.EQ_ABSOLUTE, 0, 4),
+])
+def test_slabs_equal_single_rank_bitwise(st, space, eq, zc, nranks):
+    shape = (20, 12, 1) if st == W.D2Q9 else (20, 10, 12)
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc) as lat:
+        lat.set_populations(f0)
+        lat.step(20)
+        single = lat.get_populations()
+    multi = run_slabs(st, space, eq, zc, rates, shape, f0, 20, nranks)
+    np.testing.assert_array_equal(multi, single)
+
+
+def test_slabs_with_walls_match_oracle():
+    st, space, eq, zc = W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1
+    shape = (16, 10, 16)
+    bc = [[0, 0], [0, 0], [L.LBM_BC_NOSLIP, L.LBM_BC_NOSLIP]]
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape)
+    multi = run_slabs(st, space, eq, zc, rates, shape, f0, 30, 4, bc=bc)
+    ref = oracle_run(st, space, eq, zc, rates, shape, f0, 30, bc=bc)
+    assert gate_error(st, multi, ref, zc) < F64_TOL
