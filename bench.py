@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the fused MRT stream–collide hot path on B200.
+
+Default workload (BASELINE.json metric "MLUPS (D3Q27 cumulant fp64) at 1/2/4/8
+B200; % of HBM roofline", config 4): D3Q27 cumulant LBM, fp64, zero-centered
+storage relaxed against the absolute equilibrium, two-grid pull streaming,
+Taylor-Green vortex (eq:TGA_init, u0 = 0.05) on a z-slab-decomposed periodic box
+of 1024 x 1024 x (128 N) cells, N = number of GPUs (weak scaling: N = 8 is the
+1024^3 box).  One "step" is one time step of the whole lattice.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c3|c2_f64|c2_f32|c1|c5]
+  python bench.py --impl reference ...   # the CPU oracle on the host cores
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+BASELINE_METRIC = "MLUPS (D3Q27 cumulant fp64) at 1/2/4/8 B200; % of HBM roofline"
+
+# (stencil, space, equilibrium, zero_centered, precision, streaming, shape(N), rates, description)
+CONFIGS = {
+    "c4": dict(stencil=W.D3Q27, space=W.CUMULANT, eq=W.EQ_ABSOLUTE, zc=1, prec=0, streaming=0,
+               shape=lambda n: (1024, 1024, 128 * n), slab=2,
+               desc="D3Q27 cumulant TGV 1024x1024x(128*N) z-slabs, fp64, zero-centered + absolute eq, pull"),
+    "c3": dict(stencil=W.D3Q27, space=W.CENTRAL, eq=W.EQ_ABSOLUTE, zc=1, prec=0, streaming=1,
+               shape=lambda n: (384, 384, 384), slab=2,
+               desc="D3Q27 central-moment MRT TGV 384^3, fp64, zero-centered + absolute eq, AA in-place"),
+    "c2_f64": dict(stencil=W.D3Q19, space=W.RAW, eq=W.EQ_DELTA, zc=1, prec=0, streaming=0,
+                   shape=lambda n: (256, 256, 256), slab=2,
+                   desc="D3Q19 raw-moment MRT TGV 256^3, fp64, zero-centered + delta eq, pull"),
+    "c2_f32": dict(stencil=W.D3Q19, space=W.RAW, eq=W.EQ_DELTA, zc=1, prec=1, streaming=0,
+                   shape=lambda n: (256, 256, 256), slab=2,
+                   desc="D3Q19 raw-moment MRT TGV 256^3, fp32, zero-centered + delta eq, pull"),
+    "c1": dict(stencil=W.D2Q9, space=W.POPULATION, eq=W.EQ_DELTA, zc=1, prec=0, streaming=0,
+               shape=lambda n: (64, 64, 1), slab=1,
+               desc="D2Q9 BGK TGV 64x64, fp64, zero-centered + delta eq, pull"),
+    "c5": dict(stencil=W.D2Q9, space=W.CENTRAL, eq=W.EQ_SWE, zc=0, prec=0, streaming=0,
+               shape=lambda n: (8192, 8192, 1), slab=1,
+               desc="D2Q9 shallow-water CM LBM (Zhou eq.) dam break 8192^2, fp64, absolute, pull"),
+}
+
+
+def bytes_per_cell(cfg):
+    q = W.Q_OF[cfg["stencil"]]
+    return 2 * q * (8 if cfg["prec"] == 0 else 4)
+
+
+def rates_of(cfg):
+    st = cfg["stencil"]
+    if cfg["space"] == W.POPULATION:
+        return np.array([1.6])
+    if cfg["eq"] == W.EQ_SWE:
+        return W.regularized_rates(st, W.swe_lattice_parameters()[2])
+    return W.rate_set_p(st)
+
+
+def dtype_name(cfg):
+    return "f64" if cfg["prec"] == 0 else "f32"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config_name, kernel_key, cells):
+    """Per-launch DRAM bytes (read + write) of the timed kernel from the committed
+    ncu --set full capture (profiles/ncu_summary.json: bytes per cell of the same
+    kernel) times this launch's cells, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        e = d.get(config_name)
+        if e and e.get("kernel_key") == kernel_key:
+            return round(float(e["dram_bytes_per_cell"]) * cells)
+    except Exception:
+        return None
+    return None
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for k, name in enumerate(names):
+                if parts[5 + k].lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def oracle_mlups(cfg, target_seconds=15.0, max_cells=None):
+    """Time the CPU oracle (fp64 instantiation, as it stands) on a bounded sample of
+    the same workload: a periodic TGV box with the config's method.  Returns
+    (mlups, cores, sample description)."""
+    import oracle
+
+    st = cfg["stencil"]
+    q = W.Q_OF[st]
+    rates = rates_of(cfg)
+    g = W.swe_lattice_parameters()[0] if cfg["eq"] == W.EQ_SWE else 0.0
+    two_d = W.DIM_OF[st] == 2
+
+    def run(shape, steps):
+        nx, ny, nz = shape
+        if cfg["eq"] == W.EQ_SWE:
+            rho, u = W.dam_break_fields(nx, ny, nx * 2.5 / 40, 6.25, 1.25)
+        else:
+            rho, u = W.tgv_fields(nx, ny, nz, 0.05)
+        feq = oracle.equilibrium(st, cfg["space"], cfg["eq"], cfg["zc"], rho.reshape(-1), u.reshape(3, -1).T, g=g)
+        sim = oracle.Sim(st, cfg["space"], cfg["eq"], cfg["zc"], rates, shape, g=g, prec=oracle.DOUBLE)
+        sim.set(np.ascontiguousarray(feq.T.reshape(q, nz, ny, nx)))
+        t0 = time.perf_counter()
+        sim.step(steps)
+        return time.perf_counter() - t0
+
+    probe = (64, 64, 1) if two_d else (64, 64, 4)
+    t = run(probe, 1)
+    cells = probe[0] * probe[1] * probe[2]
+    per_cell = t / cells
+    want = int(target_seconds / max(per_cell, 1e-12))
+    if max_cells:
+        want = min(want, max_cells)
+    if two_d:
+        ny = max(64, min(8192, (want // 1024) // 8 * 8))
+        shape = (1024, ny, 1)
+    else:
+        nz = max(4, min(256, want // (256 * 256)))
+        shape = (256, 256, nz)
+    t = run(shape, 1)
+    n = shape[0] * shape[1] * shape[2]
+    return n / t / 1e6, oracle.max_threads(), f"1 step of a {shape[0]}x{shape[1]}x{shape[2]} periodic TGV box " \
+                                                f"({n} cells), oracle fp64 instantiation (dense M/K(u), series cumulants)"
+
+
+# ---------------------------------------------------------------------------
+def reference_arm(args, cfg, name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+
+    st = cfg["stencil"]
+    q = W.Q_OF[st]
+    rates = rates_of(cfg)
+    g = W.swe_lattice_parameters()[0] if cfg["eq"] == W.EQ_SWE else 0.0
+    # a bounded sample per step, sized by a probe so the run ends in a few minutes
+    mlups0, cores, _ = oracle_mlups(cfg, target_seconds=2.0)
+    per_step_cells = int(min(4e6, max(4096, mlups0 * 1e6 * 4.0)))  # ~4 s per step
+    if W.DIM_OF[st] == 2:
+        ny = max(64, (per_step_cells // 1024) // 8 * 8)
+        shape = (1024, ny, 1)
+    else:
+        nz = max(4, per_step_cells // (256 * 256))
+        shape = (256, 256, nz)
+    nx, ny, nz = shape
+    if cfg["eq"] == W.EQ_SWE:
+        rho, u = W.dam_break_fields(nx, ny, nx * 2.5 / 40, 6.25, 1.25)
+    else:
+        rho, u = W.tgv_fields(nx, ny, nz, 0.05)
+    feq = oracle.equilibrium(st, cfg["space"], cfg["eq"], cfg["zc"], rho.reshape(-1), u.reshape(3, -1).T, g=g)
+    sim = oracle.Sim(st, cfg["space"], cfg["eq"], cfg["zc"], rates, shape, g=g, prec=oracle.DOUBLE)
+    sim.set(np.ascontiguousarray(feq.T.reshape(q, nz, ny, nx)))
+    sim.step(args.warmup)
+    t0 = time.perf_counter()
+    sim.step(args.steps)
+    dt = time.perf_counter() - t0
+    cells = nx * ny * nz
+    value = cells * args.steps / dt / 1e6
+    sample = f"each step: one time step of a {nx}x{ny}x{nz} periodic box of the same method " \
+             f"({cells} cells), oracle fp64 instantiation"
+    line = {
+        "impl": "reference", "metric": BASELINE_METRIC if name == "c4" else f"MLUPS ({cfg['desc']})",
+        "value": value, "unit": "MLUPS", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": dtype_name(cfg), "data": "synthetic",
+        "config": {"workload": cfg["desc"] + " (CPU oracle sample)", "sample_shape": [nx, ny, nz]},
+        "cpu_baseline": {"value": value, "unit": "MLUPS", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shape", type=int, nargs=3, default=None,
+                    help="override the global lattice shape (profiling runs only)")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return reference_arm(args, cfg, args.config)
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2211_02435_b200 import distributed as D
+    from paper_2211_02435_b200 import lbm as L
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("launch with torchrun for --gpus > 1")
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    n = world
+    st = cfg["stencil"]
+    q = W.Q_OF[st]
+    shape = tuple(args.shape) if args.shape else cfg["shape"](n)
+    nx, ny, nz = shape
+    two_d = W.DIM_OF[st] == 2
+    rates = rates_of(cfg)
+    g = W.swe_lattice_parameters()[0] if cfg["eq"] == W.EQ_SWE else 0.0
+    # a dedicated (non-default) stream: the library enqueues on it and the CUDA
+    # events of the timed region are recorded on the same stream
+    main_stream = torch.cuda.Stream()
+    torch.cuda.set_stream(main_stream)
+    lat = L.Lattice(st, cfg["space"], cfg["eq"], rates, shape, zero_centered=cfg["zc"], precision=cfg["prec"],
+                    streaming=cfg["streaming"], swe_g=g, device=local_rank, stream=main_stream.cuda_stream,
+                    rank=rank, nranks=n)
+    d = lat.d
+    # synthetic initial state of this rank's slab
+    if cfg["eq"] == W.EQ_SWE:
+        rho, u = W.dam_break_fields(nx, ny, nx * 2.5 / 40, 6.25, 1.25, y0=lat.offset, ny_local=lat.extent)
+    elif two_d:
+        rho_g, u_g = W.tgv_fields(nx, ny, 1, 0.05)
+        rho = rho_g[:, lat.offset:lat.offset + lat.extent]
+        u = u_g[:, :, lat.offset:lat.offset + lat.extent]
+    else:
+        rho, u = W.tgv_fields(nx, ny, lat.extent, 0.05, z0=lat.offset)
+    rho = np.ascontiguousarray(rho)
+    u = np.ascontiguousarray(u[:d])
+    lat.init_macroscopic(rho, u)
+    runner = None
+    if n > 1:
+        runner = D.SlabRunner(lat, rank, n)
+        runner.prime()
+
+    def do_steps(k):
+        if runner is None:
+            lat.step(k)
+        else:
+            runner.step(k)
+
+    cells_local = lat.cells
+    # warm-up
+    do_steps(args.warmup)
+    torch.cuda.synchronize()
+    if n > 1:
+        dist.barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if n > 1:
+        dist.barrier()
+    ev0.record(main_stream)
+    do_steps(args.steps)
+    ev1.record(main_stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    if n > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    lat.check_finite()
+    total_cells = nx * ny * nz
+    value = total_cells * args.steps / (ms * 1e-3) / 1e6
+    ms_step = ms / args.steps
+
+    # dominant kernel: the stream–collide kernel (one launch per step at N = 1)
+    peak, peak_src = measured_peaks()
+    bpc = bytes_per_cell(cfg)
+    launches_per_step = 1 if n == 1 else 3
+    kernel_ms = ms_step  # N = 1: one launch per step on this stream
+    achieved = bpc * cells_local / (kernel_ms * 1e-3) / 1e9
+    kkey = f"{args.config}:{dtype_name(cfg)}"
+    traffic = ncu_traffic(args.config, kkey, cells_local)
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "algorithmic_bytes_per_cell": bpc, "cells_per_launch": cells_local,
+                "peak_source": peak_src, "kernel": f"k_pull/k_aa stream-collide ({kkey})"}
+    if n > 1:
+        roofline["note"] = "N > 1: per-step time of boundary + interior launches with the halo exchange"
+
+    # end-to-end through the C ABI with host buffers (pinned): init from host rho/u,
+    # K steps, macroscopic fields back to the host
+    e2e = None
+    if not args.no_e2e:
+        rho_h = torch.from_numpy(rho.reshape(-1)).pin_memory()
+        u_h = torch.from_numpy(u.reshape(-1)).pin_memory()
+        rho_o = torch.empty_like(rho_h).pin_memory()
+        u_o = torch.empty_like(u_h).pin_memory()
+        import ctypes
+
+        dp = ctypes.POINTER(ctypes.c_double)
+        Lb = L.lib()
+        torch.cuda.synchronize()
+        if n > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        st_ = Lb.lbm_init_macroscopic(lat._ctx, ctypes.cast(rho_h.data_ptr(), dp), ctypes.cast(u_h.data_ptr(), dp))
+        assert st_ == 0
+        if runner is not None:
+            runner.prime()
+        do_steps(args.steps)
+        st_ = Lb.lbm_get_macroscopic(lat._ctx, ctypes.cast(rho_o.data_ptr(), dp), ctypes.cast(u_o.data_ptr(), dp))
+        assert st_ == 0
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if n > 1:
+            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        h2d = (rho_h.numel() + u_h.numel()) * 8 * n
+        d2h = (rho_o.numel() + u_o.numel()) * 8 * n
+        e2e = {"value": total_cells * args.steps / dt / 1e6, "unit": "MLUPS",
+               "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+               "what": "lbm_init_macroscopic(host rho,u) + K x lbm_step + lbm_get_macroscopic(host rho,u), "
+                       "pinned host buffers, wall clock"}
+
+    cpu = None
+    if rank == 0 and n == 1 and not args.no_cpu:
+        try:
+            v, cores, sample = oracle_mlups(cfg)
+            cpu = {"value": v, "unit": "MLUPS", "cores": cores, "kind": "oracle", "sample": sample}
+        except Exception as ex:  # report, never fail the bench on the baseline
+            cpu = {"value": None, "unit": "MLUPS", "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
+
+    regs, local = lat.kernel_attributes()
+    if rank == 0:
+        line = {
+            "metric": BASELINE_METRIC if args.config == "c4" else f"MLUPS ({cfg['desc']})",
+            "value": round(value, 1), "unit": "MLUPS", "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": dtype_name(cfg), "data": "synthetic",
+            "config": {"workload": cfg["desc"], "global_shape": [nx, ny, nz], "cells_per_gpu": cells_local,
+                       "rates": "rate set P (SURVEY.md 8(d))" if cfg["space"] != W.POPULATION else "omega = 1.6",
+                       "l2": "inputs larger than L2 (population grids >> 126 MB)" if cells_local * bpc > 1e9
+                       else "small grid: L2-resident", "parallelism": f"z-slab x{n}" if n > 1 else "single GPU",
+                       "kernel_regs": regs, "kernel_local_bytes": local},
+            "roofline": roofline,
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    lat.close()
+    if n > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

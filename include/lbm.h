@@ -110,6 +110,15 @@ typedef struct {
   size_t bytes;
 } lbm_halo;
 
+/* Element layout of one device population grid of a rank's slab (all in ELEMENTS of the
+   storage precision): element (zz, i, y, x) at zz*plane + i*pop + y*pitch + x, zz = local
+   slab plane + 1 (zz = 0 and zz = planes-1 are the ghost planes).  halo_* are the element
+   offsets of the lbm_halo blocks, each halo_elems long. */
+typedef struct {
+  size_t pitch, pop, plane, planes, elements;
+  size_t send_lo, send_hi, recv_lo, recv_hi, halo_elems;
+} lbm_layout;
+
 typedef struct {
   int q, d;                 /* populations per cell, dimensions                          */
   int offset, extent;       /* this rank's slab along the slab axis (global plane index) */
@@ -169,6 +178,9 @@ lbm_status lbm_stencil_info(lbm_stencil stencil, int *q, int *xi, int *opposite)
 /* Slab of 'rank' out of 'nranks' along an axis of 'extent' planes. */
 lbm_status lbm_slab_extent(int extent, int rank, int nranks, int *offset, int *local_extent);
 const char *lbm_version(void);
+/* Device grid layout of 'rank' of 'nranks' for a global (nx, ny, nz) lattice (2D: nz = 1). */
+lbm_status lbm_grid_layout(lbm_stencil stencil, lbm_precision precision, int nx, int ny, int nz, int nranks,
+                           lbm_layout *out);
 
 /* Diagnostics. */
 /* Registers per thread and local (spill) bytes of this context's pull kernel. */

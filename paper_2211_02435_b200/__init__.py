@@ -5,4 +5,4 @@ behind a C ABI.  This package holds its thin Python binding (lbm.py), the
 multi-rank slab driver (distributed.py) and the build script (build.py).
 """
 from .lbm import *  # noqa: F401,F403
-from .lbm import Lattice, LbmError, lib, stencil_info, slab_extent, version  # noqa: F401
+from .lbm import Lattice, LbmError, grid_layout, lib, slab_extent, stencil_info, version  # noqa: F401

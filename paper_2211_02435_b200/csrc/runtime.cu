@@ -152,6 +152,36 @@ lbm_status lbm_slab_extent(int extent, int rank, int nranks, int *offset, int *l
   return LBM_OK;
 }
 
+lbm_status lbm_grid_layout(lbm_stencil stencil, lbm_precision precision, int nx, int ny, int nz, int nranks,
+                           lbm_layout *out) {
+  if (!out) return LBM_EINVAL;
+  if (stencil < LBM_D2Q9 || stencil > LBM_D3Q27) return LBM_EINVAL;
+  if (precision != LBM_FP64 && precision != LBM_FP32) return LBM_EINVAL;
+  if (nx < 1 || ny < 1 || nz < 1 || nranks < 1) return LBM_EINVAL;
+  const bool two_d = (stencil == LBM_D2Q9);
+  const int slab = two_d ? ny : nz;
+  if (slab % nranks != 0) return LBM_EINVAL;
+  const int nzl = slab / nranks;
+  const size_t esize = (precision == LBM_FP64) ? 8 : 4;
+  const size_t align = 128 / esize;
+  const int q = q_of(stencil);
+  out->pitch = ((size_t)nx + align - 1) / align * align;
+  out->pop = (size_t)(two_d ? 1 : ny) * out->pitch;
+  out->plane = (size_t)q * out->pop;
+  out->planes = (size_t)nzl + 2;
+  out->elements = out->planes * out->plane;
+  int up0, nup;
+  if (stencil == LBM_D2Q9) { up0 = lbm::D2Q9::UP0; nup = lbm::D2Q9::NUP; }
+  else if (stencil == LBM_D3Q19) { up0 = lbm::D3Q19::UP0; nup = lbm::D3Q19::NUP; }
+  else { up0 = lbm::D3Q27::UP0; nup = lbm::D3Q27::NUP; }
+  out->send_lo = 1 * out->plane + (size_t)(up0 + nup) * out->pop;
+  out->send_hi = (size_t)nzl * out->plane + (size_t)up0 * out->pop;
+  out->recv_lo = 0 * out->plane + (size_t)up0 * out->pop;
+  out->recv_hi = (size_t)(nzl + 1) * out->plane + (size_t)(up0 + nup) * out->pop;
+  out->halo_elems = (size_t)nup * out->pop;
+  return LBM_OK;
+}
+
 lbm_status lbm_stencil_info(lbm_stencil stencil, int *q, int *xi, int *opposite) {
   if (!q) return LBM_EINVAL;
   auto fill = [&](auto S) {
@@ -437,18 +467,16 @@ lbm_status lbm_get_halo(lbm_ctx *c, int which, lbm_halo *out) {
   if (!c || !out) return LBM_EINVAL;
   if (c->streaming != LBM_PULL) return fail(c, LBM_EUNSUPPORTED, "halo exchange needs pull streaming");
   char *base = static_cast<char *>(grid_ptr(c, which));
-  const GridParams &g = c->g;
-  int up0 = 0, nup = 0;
-  if (c->stencil == LBM_D2Q9) { up0 = lbm::D2Q9::UP0; nup = lbm::D2Q9::NUP; }
-  else if (c->stencil == LBM_D3Q19) { up0 = lbm::D3Q19::UP0; nup = lbm::D3Q19::NUP; }
-  else { up0 = lbm::D3Q27::UP0; nup = lbm::D3Q27::NUP; }
+  lbm_layout lay;
+  lbm_status s = lbm_grid_layout((lbm_stencil)c->stencil, (lbm_precision)c->prec, c->gnx, c->gny, c->gnz,
+                                 c->nranks, &lay);
+  if (s != LBM_OK) return fail(c, s, "layout");
   const size_t E = c->esize;
-  auto at = [&](int zz, int i) { return base + ((size_t)zz * g.plane + (size_t)i * g.pop) * E; };
-  out->send_lo = at(1, up0 + nup);
-  out->send_hi = at(g.nzl, up0);
-  out->recv_lo = at(0, up0);
-  out->recv_hi = at(g.nzl + 1, up0 + nup);
-  out->bytes = (size_t)nup * g.pop * E;
+  out->send_lo = base + lay.send_lo * E;
+  out->send_hi = base + lay.send_hi * E;
+  out->recv_lo = base + lay.recv_lo * E;
+  out->recv_hi = base + lay.recv_hi * E;
+  out->bytes = lay.halo_elems * E;
   return LBM_OK;
 }
 

@@ -48,6 +48,11 @@ class lbm_halo(ctypes.Structure):
                 ("recv_hi", ctypes.c_void_p), ("bytes", ctypes.c_size_t)]
 
 
+class lbm_layout(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_size_t) for n in ("pitch", "pop", "plane", "planes", "elements", "send_lo", "send_hi",
+                                                 "recv_lo", "recv_hi", "halo_elems")]
+
+
 class lbm_info(ctypes.Structure):
     _fields_ = [("q", ctypes.c_int), ("d", ctypes.c_int), ("offset", ctypes.c_int), ("extent", ctypes.c_int),
                 ("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int), ("pitch", ctypes.c_size_t),
@@ -80,6 +85,8 @@ SIGNATURES = [
     ("lbm_stencil_info", ctypes.c_int, [ctypes.c_int, _ip, _ip, _ip]),
     ("lbm_slab_extent", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, _ip]),
     ("lbm_version", ctypes.c_char_p, []),
+    ("lbm_grid_layout", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, ctypes.POINTER(lbm_layout)]),
     ("lbm_kernel_attributes", ctypes.c_int, [_vp, _ip, _ip]),
     ("lbm_device_grid", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_size_t)]),
     ("lbm_stream", _vp, [_vp]),
@@ -128,6 +135,15 @@ def slab_extent(extent: int, rank: int, nranks: int):
     off, ext = ctypes.c_int(), ctypes.c_int()
     _check(lib().lbm_slab_extent(extent, rank, nranks, ctypes.byref(off), ctypes.byref(ext)))
     return off.value, ext.value
+
+
+def grid_layout(stencil: int, precision: int, shape, nranks: int = 1) -> lbm_layout:
+    """Host-only: the device grid layout of a rank's slab (element offsets)."""
+    out = lbm_layout()
+    nx, ny, nz = shape
+    _check(lib().lbm_grid_layout(int(stencil), int(precision), int(nx), int(ny), int(nz), int(nranks),
+                                 ctypes.byref(out)))
+    return out
 
 
 def version() -> str:

@@ -1,0 +1,124 @@
+"""Multi-rank slab plumbing on CPU (gloo, world size 2 and 4): the halo exchange of
+paper_2211_02435_b200.distributed moves exactly the slab-crossing population
+blocks of the library's device grid layout (lbm_grid_layout) into the neighbours'
+ghost planes, with periodic wrap along the slab axis."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2211_02435_b200 as P
+from paper_2211_02435_b200 import distributed as D
+from paper_2211_02435_b200 import lbm as L
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def fill_value(zg, i, y, x):
+    """Code of population i at global slab plane zg, row y, column x."""
+    return zg * 1e6 + i * 1e4 + y * 1e2 + x
+
+
+def make_grid(stencil, prec, shape, rank, nranks):
+    """A rank's grid in the device layout with interior planes coded by global position."""
+    lay = P.grid_layout(stencil, prec, shape, nranks)
+    nx, ny, nz = shape
+    two_d = stencil == L.LBM_D2Q9
+    slab = ny if two_d else nz
+    nyy = 1 if two_d else ny
+    off, ext = P.slab_extent(slab, rank, nranks)
+    q = L.Q_OF[stencil]
+    dt = torch.float64 if prec == L.LBM_FP64 else torch.float32
+    g = torch.full((lay.elements,), -1.0, dtype=dt)
+    v = g.view(lay.planes, q, nyy, lay.pitch)
+    zz = torch.arange(ext).view(-1, 1, 1, 1) + off
+    ii = torch.arange(q).view(1, -1, 1, 1)
+    yy = torch.arange(nyy).view(1, 1, -1, 1)
+    xx = torch.arange(nx).view(1, 1, 1, -1)
+    v[1:ext + 1, :, :, :nx] = fill_value(zz, ii, yy, xx).to(dt)
+    return g, lay, off, ext, q, nyy
+
+
+def _worker(rank, world, port, stencil, prec, shape, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g, lay, off, ext, q, nyy = make_grid(stencil, prec, shape, rank, world)
+        views = D.HaloViews(g[lay.send_lo:lay.send_lo + lay.halo_elems], g[lay.send_hi:lay.send_hi + lay.halo_elems],
+                            g[lay.recv_lo:lay.recv_lo + lay.halo_elems], g[lay.recv_hi:lay.recv_hi + lay.halo_elems])
+        D.exchange(views, rank, world)
+        out[rank] = g.numpy().copy()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("stencil,prec,shape,world", [
+    (L.LBM_D3Q27, L.LBM_FP64, (10, 6, 8), 2),
+    (L.LBM_D3Q19, L.LBM_FP32, (10, 6, 12), 4),
+    (L.LBM_D2Q9, L.LBM_FP64, (12, 8, 1), 2),
+])
+def test_gloo_halo_exchange(stencil, prec, shape, world):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, free_port(), stencil, prec, shape, out), nprocs=world, join=True)
+    xi, opp = P.stencil_info(stencil)
+    slab_ax = 1 if stencil == L.LBM_D2Q9 else 2
+    nx = shape[0]
+    two_d = stencil == L.LBM_D2Q9
+    slab = shape[1] if two_d else shape[2]
+    for r in range(world):
+        g, lay, off, ext, q, nyy = make_grid(stencil, prec, shape, r, world)
+        got = np.asarray(out[r]).reshape(lay.planes, q, nyy, lay.pitch)
+        up = [i for i in range(q) if xi[i, slab_ax] == 1]
+        down = [i for i in range(q) if xi[i, slab_ax] == -1]
+        yy = np.arange(nyy).reshape(-1, 1)
+        xx = np.arange(nx).reshape(1, -1)
+        # bottom ghost: the +1 populations of global plane off - 1 (periodic)
+        zlo = (off - 1) % slab
+        zhi = (off + ext) % slab
+        for i in range(q):
+            lo = got[0, i, :, :nx]
+            hi = got[ext + 1, i, :, :nx]
+            if i in up:
+                np.testing.assert_array_equal(lo, fill_value(zlo, i, yy, xx))
+            else:
+                assert (lo == -1).all()
+            if i in down:
+                np.testing.assert_array_equal(hi, fill_value(zhi, i, yy, xx))
+            else:
+                assert (hi == -1).all()
+        # interior untouched
+        np.testing.assert_array_equal(got[1:ext + 1], g.numpy().reshape(got.shape)[1:ext + 1])
+
+
+def test_halo_blocks_are_the_crossing_populations():
+    """The halo offsets of lbm_grid_layout cover exactly the populations whose slab
+    component is +1 (send_hi / recv_lo) or -1 (send_lo / recv_hi)."""
+    for st in (L.LBM_D2Q9, L.LBM_D3Q19, L.LBM_D3Q27):
+        shape = (16, 8, 1) if st == L.LBM_D2Q9 else (16, 8, 8)
+        lay = P.grid_layout(st, L.LBM_FP64, shape, 2)
+        xi, _ = P.stencil_info(st)
+        ax = 1 if st == L.LBM_D2Q9 else 2
+        up = np.flatnonzero(xi[:, ax] == 1)
+        down = np.flatnonzero(xi[:, ax] == -1)
+        assert lay.halo_elems == len(up) * lay.pop
+        assert lay.send_hi % lay.plane == up[0] * lay.pop and lay.send_hi // lay.plane == lay.planes - 2
+        assert lay.recv_lo // lay.plane == 0 and lay.recv_lo % lay.plane == up[0] * lay.pop
+        assert lay.send_lo // lay.plane == 1 and lay.send_lo % lay.plane == down[0] * lay.pop
+        assert lay.recv_hi // lay.plane == lay.planes - 1
+        assert list(up) == list(range(up[0], up[0] + len(up)))
+        assert list(down) == list(range(down[0], down[0] + len(down)))
+        assert lay.pitch % 16 == 0 and lay.pitch >= shape[0]
