@@ -163,6 +163,10 @@ lbm_status lbm_get_macroscopic(lbm_ctx *ctx, double *rho, double *u);
 /* Canonical post-collision populations f*(x, t) in stored form, independent of the AA parity
    (reading R11), f[i][z][y][x] fp64 (host; synchronises). */
 lbm_status lbm_get_populations(lbm_ctx *ctx, double *f);
+/* Canonical post-collision populations of selected cells: cells[n] are local linear indices
+   x + nx * (y + ny * z) of this rank's slab (2D: x + nx * y); f [n][q] fp64 stored form (host;
+   synchronises).  LBM_EINVAL for an index outside the slab. */
+lbm_status lbm_get_cells(lbm_ctx *ctx, const long long *cells, long long n, double *f);
 /* Sets the canonical state (converted to the storage precision); resets the step counter. */
 lbm_status lbm_set_populations(lbm_ctx *ctx, const double *f);
 /* LBM_ENUMERIC if any stored population of the current state is not finite. */

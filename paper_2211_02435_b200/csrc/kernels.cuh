@@ -223,6 +223,19 @@ __global__ void k_test_collide(const double *__restrict__ fin, double *__restric
   sfor<S::Q>([&](auto i) { fout[c * S::Q + i] = (double)f[i]; });
 }
 
+// canonical populations of selected cells (local linear index x + nx (y + ny z))
+template <class S, class real>
+__global__ void k_get_cells(const real *mem, const GridParams g, int aa, int state, const long long *__restrict__ idx,
+                            long long n, double *__restrict__ out) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const long long c = idx[k];
+  const int x = (int)(c % g.nx);
+  const int y = (int)((c / g.nx) % g.ny);
+  const int zl = (int)(c / ((long long)g.nx * g.ny));
+  sfor<S::Q>([&](auto i) { out[k * S::Q + i] = (double)mem[Canon<S>::template at<i>(g, x, y, zl, aa, state)]; });
+}
+
 template <class S, class real>
 __global__ void k_check_finite(const real *mem, const GridParams g, int *flag) {
   const int x = blockIdx.x * BLOCK_X + threadIdx.x;

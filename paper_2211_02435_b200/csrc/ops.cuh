@@ -25,6 +25,8 @@ struct Ops {
   void (*test_collide)(const double *fin, double *fout, long long n, const void *rates, double swe_g,
                        cudaStream_t s);
   void (*check_finite)(const void *mem, const GridParams &g, int *flag, cudaStream_t s);
+  void (*get_cells)(const void *mem, const GridParams &g, int aa, int state, const long long *idx, long long n,
+                    double *out, cudaStream_t s);
   // kernel attributes of the pull kernel (registers / local memory), for diagnostics
   void (*attributes)(int *regs, int *local_bytes);
 };
@@ -82,6 +84,12 @@ struct OpsImpl {
   static void check_finite(const void *mem, const GridParams &g, int *flag, cudaStream_t s) {
     k_check_finite<S, real><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<const real *>(mem), g, flag);
   }
+  static void get_cells(const void *mem, const GridParams &g, int aa, int state, const long long *idx, long long n,
+                        double *out, cudaStream_t s) {
+    if (n <= 0) return;
+    k_get_cells<S, real><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(static_cast<const real *>(mem), g, aa, state,
+                                                                      idx, n, out);
+  }
   static void attributes(int *regs, int *local_bytes) {
     cudaFuncAttributes a{};
     if (cudaFuncGetAttributes(&a, k_pull<S, SPACE, REG, real, false>) == cudaSuccess) {
@@ -93,7 +101,7 @@ struct OpsImpl {
     }
   }
   static constexpr Ops table{S::Q,      S::D,  &pull,         &aa,           &init,      &get_pop,
-                             &set_pop, &macro, &test_collide, &check_finite, &attributes};
+                             &set_pop, &macro, &test_collide, &check_finite, &get_cells,   &attributes};
 };
 
 }  // namespace lbm

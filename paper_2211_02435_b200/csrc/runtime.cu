@@ -521,6 +521,27 @@ lbm_status lbm_get_populations(lbm_ctx *c, double *f) {
   return LBM_OK;
 }
 
+lbm_status lbm_get_cells(lbm_ctx *c, const long long *cells, long long n, double *f) {
+  if (!c || (n > 0 && (!cells || !f)) || n < 0) return fail(c, LBM_EINVAL, "bad argument");
+  if (n == 0) return LBM_OK;
+  const long long ncell = local_cells(c);
+  for (long long k = 0; k < n; ++k)
+    if (cells[k] < 0 || cells[k] >= ncell) return fail(c, LBM_EINVAL, "cell index out of range");
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  const size_t ibytes = (size_t)n * sizeof(long long), obytes = (size_t)n * c->q * sizeof(double);
+  lbm_status s = ensure_staging(c, ibytes + obytes + 256);
+  if (s != LBM_OK) return s;
+  long long *didx = static_cast<long long *>(c->staging);
+  double *dout = reinterpret_cast<double *>(static_cast<char *>(c->staging) + (ibytes + 255) / 256 * 256);
+  LBM_CUDA(c, cudaMemcpyAsync(didx, cells, ibytes, cudaMemcpyHostToDevice, c->stream));
+  c->ops->get_cells(grid_ptr(c, 0), c->g, c->streaming == LBM_AA, c->aa_state, didx, n, dout, c->stream);
+  s = check_launch(c, "k_get_cells");
+  if (s != LBM_OK) return s;
+  LBM_CUDA(c, cudaMemcpyAsync(f, dout, obytes, cudaMemcpyDeviceToHost, c->stream));
+  LBM_CUDA(c, cudaStreamSynchronize(c->stream));
+  return LBM_OK;
+}
+
 lbm_status lbm_set_populations(lbm_ctx *c, const double *f) {
   if (!c || !f) return fail(c, LBM_EINVAL, "null argument");
   LBM_CUDA(c, cudaSetDevice(c->device));

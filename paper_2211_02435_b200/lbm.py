@@ -80,6 +80,7 @@ SIGNATURES = [
     ("lbm_get_macroscopic", ctypes.c_int, [_vp, _dp, _dp]),
     ("lbm_get_populations", ctypes.c_int, [_vp, _dp]),
     ("lbm_set_populations", ctypes.c_int, [_vp, _dp]),
+    ("lbm_get_cells", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_longlong), ctypes.c_longlong, _dp]),
     ("lbm_check_finite", ctypes.c_int, [_vp]),
     ("lbm_test_collide", ctypes.c_int, [_vp, _dp, _dp, ctypes.c_longlong]),
     ("lbm_stencil_info", ctypes.c_int, [ctypes.c_int, _ip, _ip, _ip]),
@@ -253,6 +254,14 @@ class Lattice:
         f = np.empty((self.q,) + self.local_shape)
         _check(lib().lbm_get_populations(self._ctx, _d(f)), self._ctx)
         return f
+
+    def get_cells(self, cells):
+        """Canonical populations [n][q] of local linear cell indices x + nx (y + ny z)."""
+        idx = np.ascontiguousarray(np.asarray(cells, dtype=np.int64).reshape(-1))
+        out = np.empty((idx.size, self.q))
+        _check(lib().lbm_get_cells(self._ctx, idx.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)), idx.size,
+                                   _d(out)), self._ctx)
+        return out
 
     def set_populations(self, f):
         f = np.ascontiguousarray(f, dtype=np.float64)
