@@ -127,6 +127,12 @@ typedef struct {
   size_t bytes_per_element; /* 8 (fp64) or 4 (fp32)                                       */
   size_t device_bytes;      /* population storage allocated on the device                 */
   long long steps_done;     /* time steps taken since the last init/set                   */
+  int rate_specialization;  /* kernel variant chosen from the rates:
+                               0 general; 1 fully regularised (every rate but the shear
+                               group equals 1, the "R-" methods of PAPER.md:795); 2 higher-
+                               order regularised (D3Q27 orders 5-6 equal 1).  Rates equal to
+                               one become compile-time constants; set the environment
+                               variable LBM_RATE_SPECIALIZATION=0 to force 0.            */
 } lbm_info;
 
 /* Creates a context: validates admissibility, allocates the population grid(s) (two for
@@ -163,6 +169,16 @@ lbm_status lbm_get_macroscopic(lbm_ctx *ctx, double *rho, double *u);
 /* Canonical post-collision populations f*(x, t) in stored form, independent of the AA parity
    (reading R11), f[i][z][y][x] fp64 (host; synchronises). */
 lbm_status lbm_get_populations(lbm_ctx *ctx, double *f);
+/* Global sums over this rank's slab of the canonical state, on the device in fp64 with a
+   fixed (deterministic) summation order: mass = sum rho, momentum = sum rho u (physical
+   x, y, z; 2D: z = 0), kinetic energy = sum rho |u|^2 / 2 (lattice-node form of
+   eq:TGA_kin_energy).  Synchronises. */
+typedef struct {
+  double mass;
+  double momentum[3];
+  double kinetic_energy;
+} lbm_diagnostics;
+lbm_status lbm_get_diagnostics(lbm_ctx *ctx, lbm_diagnostics *out);
 /* Canonical post-collision populations of selected cells: cells[n] are local linear indices
    x + nx * (y + ny * z) of this rank's slab (2D: x + nx * y); f [n][q] fp64 stored form (host;
    synchronises).  LBM_EINVAL for an index outside the slab. */

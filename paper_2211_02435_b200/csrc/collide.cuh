@@ -386,84 +386,116 @@ __device__ __forceinline__ void relax_quad3(real &a, real &b, real &c, real da, 
   c = fma(t, E3 - E2, c);
 }
 
-// Apply the basis relaxation of stencil S to the monomial cube c given an
-// equilibrium provider EQ with get<e>() (value of q_eq on monomial e) and
-// zero<e>() (compile-time: q_eq == 0).
-template <class EQ, int e, class real>
-__device__ __forceinline__ real delta_of(const EQ &eq, const real (&c)[27]) {
+// Rate specialisation: rates known to be one at
+// compile time turn q* = q + w (q_eq - q) into q* = q_eq, so the forward transform of that
+// quantity becomes dead code the compiler removes.
+//   RS_GENERAL  every rate a runtime value
+//   RS_REG      "fully regularised" (R- methods): all but the shear rates = 1
+//   RS_HIGH     "higher-order regularised": rates of orders 5 and 6 = 1 (D3Q27)
+enum { RS_GENERAL = 0, RS_REG = 1, RS_HIGH = 2 };
+
+template <class S, int RS>
+struct RateOf {
+  // index of the first non-shear, non-conserved polynomial of the basis
+  static constexpr int first_nonshear = (S::Q == 9) ? 5 : 9;
+  template <int idx>
+  __device__ static constexpr bool unit() {
+    if constexpr (RS == RS_REG) return idx >= first_nonshear;
+    else if constexpr (RS == RS_HIGH) return S::Q == 27 && idx >= 23;
+    else return false;
+  }
+  template <int idx, class real>
+  __device__ static __forceinline__ real get(const Rates<real> &r) {
+    if constexpr (unit<idx>()) return real(1);
+    else return r.w[idx];
+  }
+};
+
+template <class EQ, int e, class real, int NC>
+__device__ __forceinline__ real eq_value(const EQ &eq) {
+  if constexpr (EQ::template zero<e>()) return real(0);
+  else return eq.template get<e>();
+}
+template <class EQ, int e, class real, int NC>
+__device__ __forceinline__ real delta_v(const EQ &eq, const real (&c)[NC]) {
   if constexpr (EQ::template zero<e>()) return -c[e];
   else return eq.template get<e>() - c[e];
 }
-template <class EQ, int e, class real>
-__device__ __forceinline__ void relax_single(const EQ &eq, real (&c)[27], real w) {
-  if constexpr (EQ::template zero<e>()) relax1_zero(c[e], w);
-  else relax1(c[e], eq.template get<e>(), w);
+template <class R, class EQ, int e, int idx, class real, int NC>
+__device__ __forceinline__ void rs_single(const EQ &eq, real (&c)[NC], const Rates<real> &r) {
+  if constexpr (R::template unit<idx>()) c[e] = eq_value<EQ, e, real, NC>(eq);
+  else if constexpr (EQ::template zero<e>()) relax1_zero(c[e], r.w[idx]);
+  else relax1(c[e], eq.template get<e>(), r.w[idx]);
+}
+// (a + b) [is], (a - b) [id]
+template <class R, class EQ, int ea, int eb, int is, int id, class real, int NC>
+__device__ __forceinline__ void rs_pair(const EQ &eq, real (&c)[NC], const Rates<real> &r) {
+  if constexpr (R::template unit<is>() && R::template unit<id>()) {
+    c[ea] = eq_value<EQ, ea, real, NC>(eq);
+    c[eb] = eq_value<EQ, eb, real, NC>(eq);
+  } else {
+    const real da = delta_v<EQ, ea, real, NC>(eq, c), db = delta_v<EQ, eb, real, NC>(eq, c);
+    relax_pair(c[ea], c[eb], da, db, R::template get<is>(r), R::template get<id>(r));
+  }
+}
+template <class R, class EQ, int ea, int eb, int ec, int i1, int i2, int i3, bool QUAD, class real, int NC>
+__device__ __forceinline__ void rs_triple(const EQ &eq, real (&c)[NC], const Rates<real> &r) {
+  if constexpr (R::template unit<i1>() && R::template unit<i2>() && R::template unit<i3>()) {
+    c[ea] = eq_value<EQ, ea, real, NC>(eq);
+    c[eb] = eq_value<EQ, eb, real, NC>(eq);
+    c[ec] = eq_value<EQ, ec, real, NC>(eq);
+  } else {
+    const real da = delta_v<EQ, ea, real, NC>(eq, c), db = delta_v<EQ, eb, real, NC>(eq, c),
+               dc = delta_v<EQ, ec, real, NC>(eq, c);
+    if constexpr (QUAD)
+      relax_quad3(c[ea], c[eb], c[ec], da, db, dc, R::template get<i1>(r), R::template get<i2>(r),
+                  R::template get<i3>(r));
+    else
+      relax_diag3(c[ea], c[eb], c[ec], da, db, dc, R::template get<i1>(r), R::template get<i2>(r),
+                  R::template get<i3>(r));
+  }
 }
 
-template <class S, class EQ, class real>
+// Apply the basis relaxation of stencil S to the monomial cube c given an
+// equilibrium provider EQ with get<e>() (value of q_eq on monomial e) and
+// zero<e>() (compile-time: q_eq == 0).  Rate indices follow include/lbm.h.
+template <class S, int RS, class EQ, class real>
 __device__ __forceinline__ void relax_basis3(real (&c)[27], const EQ &eq, const Rates<real> &r) {
+  using R = RateOf<S, RS>;
   constexpr bool Q27 = (S::Q == 27);
   // second order: xy, xz, yz [4,5,6]; (x^2-y^2, x^2-z^2, x^2+y^2+z^2) [7,8,9]
-  relax_single<EQ, E(1, 1, 0)>(eq, c, r.w[4]);
-  relax_single<EQ, E(1, 0, 1)>(eq, c, r.w[5]);
-  relax_single<EQ, E(0, 1, 1)>(eq, c, r.w[6]);
-  {
-    const real da = delta_of<EQ, E(2, 0, 0)>(eq, c), db = delta_of<EQ, E(0, 2, 0)>(eq, c),
-               dc = delta_of<EQ, E(0, 0, 2)>(eq, c);
-    relax_diag3(c[E(2, 0, 0)], c[E(0, 2, 0)], c[E(0, 0, 2)], da, db, dc, r.w[7], r.w[8], r.w[9]);
-  }
+  rs_single<R, EQ, E(1, 1, 0), 4>(eq, c, r);
+  rs_single<R, EQ, E(1, 0, 1), 5>(eq, c, r);
+  rs_single<R, EQ, E(0, 1, 1), 6>(eq, c, r);
+  rs_triple<R, EQ, E(2, 0, 0), E(0, 2, 0), E(0, 0, 2), 7, 8, 9, false>(eq, c, r);
   // third order pairs: (xy^2, xz^2) [10,13], (x^2y, yz^2) [11,14], (x^2z, y^2z) [12,15]
-  {
-    const real da = delta_of<EQ, E(1, 2, 0)>(eq, c), db = delta_of<EQ, E(1, 0, 2)>(eq, c);
-    relax_pair(c[E(1, 2, 0)], c[E(1, 0, 2)], da, db, r.w[10], r.w[13]);
-  }
-  {
-    const real da = delta_of<EQ, E(2, 1, 0)>(eq, c), db = delta_of<EQ, E(0, 1, 2)>(eq, c);
-    relax_pair(c[E(2, 1, 0)], c[E(0, 1, 2)], da, db, r.w[11], r.w[14]);
-  }
-  {
-    const real da = delta_of<EQ, E(2, 0, 1)>(eq, c), db = delta_of<EQ, E(0, 2, 1)>(eq, c);
-    relax_pair(c[E(2, 0, 1)], c[E(0, 2, 1)], da, db, r.w[12], r.w[15]);
-  }
-  constexpr int o4 = Q27 ? 17 : 16;  // first 4th-order rate index
-  if constexpr (Q27) relax_single<EQ, E(1, 1, 1)>(eq, c, r.w[16]);
-  {
-    const real da = delta_of<EQ, E(2, 2, 0)>(eq, c), db = delta_of<EQ, E(2, 0, 2)>(eq, c),
-               dc = delta_of<EQ, E(0, 2, 2)>(eq, c);
-    relax_quad3(c[E(2, 2, 0)], c[E(2, 0, 2)], c[E(0, 2, 2)], da, db, dc, r.w[o4], r.w[o4 + 1], r.w[o4 + 2]);
-  }
+  rs_pair<R, EQ, E(1, 2, 0), E(1, 0, 2), 10, 13>(eq, c, r);
+  rs_pair<R, EQ, E(2, 1, 0), E(0, 1, 2), 11, 14>(eq, c, r);
+  rs_pair<R, EQ, E(2, 0, 1), E(0, 2, 1), 12, 15>(eq, c, r);
   if constexpr (Q27) {
-    relax_single<EQ, E(2, 1, 1)>(eq, c, r.w[20]);
-    relax_single<EQ, E(1, 2, 1)>(eq, c, r.w[21]);
-    relax_single<EQ, E(1, 1, 2)>(eq, c, r.w[22]);
-    relax_single<EQ, E(1, 2, 2)>(eq, c, r.w[23]);
-    relax_single<EQ, E(2, 1, 2)>(eq, c, r.w[24]);
-    relax_single<EQ, E(2, 2, 1)>(eq, c, r.w[25]);
-    relax_single<EQ, E(2, 2, 2)>(eq, c, r.w[26]);
+    rs_single<R, EQ, E(1, 1, 1), 16>(eq, c, r);
+    rs_triple<R, EQ, E(2, 2, 0), E(2, 0, 2), E(0, 2, 2), 17, 18, 19, true>(eq, c, r);
+    rs_single<R, EQ, E(2, 1, 1), 20>(eq, c, r);
+    rs_single<R, EQ, E(1, 2, 1), 21>(eq, c, r);
+    rs_single<R, EQ, E(1, 1, 2), 22>(eq, c, r);
+    rs_single<R, EQ, E(1, 2, 2), 23>(eq, c, r);
+    rs_single<R, EQ, E(2, 1, 2), 24>(eq, c, r);
+    rs_single<R, EQ, E(2, 2, 1), 25>(eq, c, r);
+    rs_single<R, EQ, E(2, 2, 2), 26>(eq, c, r);
+  } else {
+    rs_triple<R, EQ, E(2, 2, 0), E(2, 0, 2), E(0, 2, 2), 16, 17, 18, true>(eq, c, r);
   }
 }
 
 // 2D (D2Q9, de Rosis basis): xy [3]; (x^2-y^2 [4], x^2+y^2 [5]); x^2y [6]; xy^2 [7]; x^2y^2 [8]
-template <class EQ, int e, class real>
-__device__ __forceinline__ real delta_of2(const EQ &eq, const real (&c)[9]) {
-  if constexpr (EQ::template zero<e>()) return -c[e];
-  else return eq.template get<e>() - c[e];
-}
-template <class EQ, int e, class real>
-__device__ __forceinline__ void relax_single2(const EQ &eq, real (&c)[9], real w) {
-  if constexpr (EQ::template zero<e>()) relax1_zero(c[e], w);
-  else relax1(c[e], eq.template get<e>(), w);
-}
-template <class EQ, class real>
+template <int RS, class EQ, class real>
 __device__ __forceinline__ void relax_basis2(real (&c)[9], const EQ &eq, const Rates<real> &r) {
-  relax_single2<EQ, E(1, 1)>(eq, c, r.w[3]);
-  {
-    const real da = delta_of2<EQ, E(2, 0)>(eq, c), db = delta_of2<EQ, E(0, 2)>(eq, c);
-    relax_pair(c[E(2, 0)], c[E(0, 2)], da, db, r.w[5], r.w[4]);
-  }
-  relax_single2<EQ, E(2, 1)>(eq, c, r.w[6]);
-  relax_single2<EQ, E(1, 2)>(eq, c, r.w[7]);
-  relax_single2<EQ, E(2, 2)>(eq, c, r.w[8]);
+  using R = RateOf<D2Q9, RS>;
+  rs_single<R, EQ, E(1, 1), 3>(eq, c, r);
+  rs_pair<R, EQ, E(2, 0), E(0, 2), 5, 4>(eq, c, r);
+  rs_single<R, EQ, E(2, 1), 6>(eq, c, r);
+  rs_single<R, EQ, E(1, 2), 7>(eq, c, r);
+  rs_single<R, EQ, E(2, 2), 8>(eq, c, r);
 }
 
 // --------------------------------------------------------------------------
@@ -642,7 +674,7 @@ __device__ __forceinline__ void add_background(real (&c)[NC], real sgn) {
 // the collision of one cell: f in/out in the documented population order,
 // STORED form (delta f for REG_DELTA / REG_ZC_ABS).
 // --------------------------------------------------------------------------
-template <class S, int SPACE, int REG, class real>
+template <class S, int SPACE, int REG, class real, int RS = RS_GENERAL>
 __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, real swe_g) {
   constexpr bool zc = (REG != REG_ABS);
   constexpr int NC = S::NC;
@@ -714,10 +746,10 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
       RawU<real> U{ux, uy, uz, ux * ux, uy * uy, uz * uz};
       if constexpr (REG == REG_DELTA) {
         EqRawDelta<real> eq{m000, rho, U};
-        if constexpr (S::D == 3) relax_basis3<S>(c, eq, r); else relax_basis2(c, eq, r);
+        if constexpr (S::D == 3) relax_basis3<S, RS>(c, eq, r); else relax_basis2<RS>(c, eq, r);
       } else {
         EqRawAbs<real> eq{rho, U};
-        if constexpr (S::D == 3) relax_basis3<S>(c, eq, r); else relax_basis2(c, eq, r);
+        if constexpr (S::D == 3) relax_basis3<S, RS>(c, eq, r); else relax_basis2<RS>(c, eq, r);
       }
     } else {
       // ---- raw -> central (binomial Chimera)
@@ -732,10 +764,10 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
       if constexpr (SPACE == SPACE_CENTRAL) {
         if constexpr (REG == REG_DELTA) {
           EqCentralDelta<real> eq{m000, CentralV<real>{ux, uy, uz, ux * ux, uy * uy, uz * uz}};
-          if constexpr (S::D == 3) relax_basis3<S>(c, eq, r); else relax_basis2(c, eq, r);
+          if constexpr (S::D == 3) relax_basis3<S, RS>(c, eq, r); else relax_basis2<RS>(c, eq, r);
         } else {
           EqCentralAbs<real> eq{rho};
-          if constexpr (S::D == 3) relax_basis3<S>(c, eq, r); else relax_basis2(c, eq, r);
+          if constexpr (S::D == 3) relax_basis3<S, RS>(c, eq, r); else relax_basis2<RS>(c, eq, r);
         }
       } else if constexpr (SPACE == SPACE_SWE) {
         // kappa_eq = K(u) f_eq of Zhou's discrete equilibrium
@@ -757,11 +789,11 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
         });
         fwd_raw2(eq.v);
         bin_fwd2(eq.v, ux, uy);
-        relax_basis2(c, eq, r);
+        relax_basis2<RS>(c, eq, r);
       } else {  // SPACE_CUMULANT
         if constexpr (S::D == 3) central_to_cumulant3<S>(c, inv); else central_to_cumulant2(c, inv);
         EqCumulant<real> eq{rho * real(1.0 / 3.0)};
-        if constexpr (S::D == 3) relax_basis3<S>(c, eq, r); else relax_basis2(c, eq, r);
+        if constexpr (S::D == 3) relax_basis3<S, RS>(c, eq, r); else relax_basis2<RS>(c, eq, r);
         if constexpr (S::D == 3) cumulant_to_central3<S>(c, inv); else cumulant_to_central2(c, inv);
       }
       // ---- central -> raw

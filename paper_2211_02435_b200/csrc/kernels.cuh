@@ -40,7 +40,7 @@ __device__ __forceinline__ real ld_nc(const real *p) { return __ldg(p); }
 // ---------------------------------------------------------------------------
 // the fused stream–collide kernel (pull, optionally with half-way bounce-back)
 // ---------------------------------------------------------------------------
-template <class S, int SPACE, int REG, class real, bool BB>
+template <class S, int SPACE, int REG, class real, bool BB, int RS = RS_GENERAL>
 __global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, real *__restrict__ dst,
                                                    const GridParams g, const Rates<real> r, const real swe_g) {
   const int x = blockIdx.x * BLOCK_X + threadIdx.x;
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, 
     }
   });
 
-  collide<S, SPACE, REG, real>(f, r, swe_g);
+  collide<S, SPACE, REG, real, RS>(f, r, swe_g);
 
   sfor<S::Q>([&](auto i) { dst[own + (long long)i * g.pop] = f[i]; });
 }
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, 
 // ---------------------------------------------------------------------------
 // AA pattern (single rank, periodic): in-place
 // ---------------------------------------------------------------------------
-template <class S, int SPACE, int REG, class real, int PAT>
+template <class S, int SPACE, int REG, class real, int PAT, int RS = RS_GENERAL>
 __global__ void __launch_bounds__(BLOCK_X) k_aa(real *mem, const GridParams g, const Rates<real> r,
                                                  const real swe_g) {
   const int x = blockIdx.x * BLOCK_X + threadIdx.x;
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(BLOCK_X) k_aa(real *mem, const GridParams g, c
   if constexpr (PAT == PAT_AA_EVEN) {
     const long long own = (long long)(zl + 1) * g.plane + (long long)y * g.pitch + x;
     sfor<S::Q>([&](auto i) { f[i] = mem[own + (long long)i * g.pop]; });
-    collide<S, SPACE, REG, real>(f, r, swe_g);
+    collide<S, SPACE, REG, real, RS>(f, r, swe_g);
     sfor<S::Q>([&](auto i) { mem[own + (long long)S::opp(i) * g.pop] = f[i]; });
   } else {
     int xs[3], ys[3];
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(BLOCK_X) k_aa(real *mem, const GridParams g, c
       constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
       f[i] = mem[zo[1 - cz] + (long long)S::opp(i) * g.pop + ys[1 - cy] + xs[1 - cx]];
     });
-    collide<S, SPACE, REG, real>(f, r, swe_g);
+    collide<S, SPACE, REG, real, RS>(f, r, swe_g);
     // write f*_i(x) to mem(x + xi_i, i)
     sfor<S::Q>([&](auto i) {
       constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
@@ -212,15 +212,72 @@ __global__ void k_macroscopic(const real *mem, const GridParams g, int aa, int s
   if constexpr (S::D == 3) u[2 * ncell + cell] = jz / r;
 }
 
-template <class S, int SPACE, int REG, class real>
+template <class S, int SPACE, int REG, class real, int RS = RS_GENERAL>
 __global__ void k_test_collide(const double *__restrict__ fin, double *__restrict__ fout, long long n,
                                const Rates<real> r, real swe_g) {
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   real f[S::Q];
   sfor<S::Q>([&](auto i) { f[i] = (real)fin[c * S::Q + i]; });
-  collide<S, SPACE, REG, real>(f, r, swe_g);
+  collide<S, SPACE, REG, real, RS>(f, r, swe_g);
   sfor<S::Q>([&](auto i) { fout[c * S::Q + i] = (double)f[i]; });
+}
+
+// Global diagnostics of the canonical state: sum rho, sum rho u (3), sum rho |u|^2 / 2
+// (the lattice-node discretisation of eq:TGA_kin_energy).  Fixed grid,
+// per-thread sequential sums in a fixed order, then a fixed-shape tree: deterministic.
+constexpr int DIAG_BLOCK = 256, DIAG_GRID = 1184;  // 148 SMs x 8
+template <class S, class real>
+__global__ void __launch_bounds__(DIAG_BLOCK) k_diag_partial(const real *mem, const GridParams g, int aa, int state,
+                                                             int zc, double *__restrict__ partial) {
+  const long long n = (long long)g.nx * g.ny * g.nzl;
+  double acc[5] = {0, 0, 0, 0, 0};
+  for (long long c = (long long)blockIdx.x * DIAG_BLOCK + threadIdx.x; c < n; c += (long long)DIAG_GRID * DIAG_BLOCK) {
+    const int x = (int)(c % g.nx);
+    const int y = (int)((c / g.nx) % g.ny);
+    const int zl = (int)(c / ((long long)g.nx * g.ny));
+    double s = 0, jx = 0, jy = 0, jz = 0;
+    sfor<S::Q>([&](auto i) {
+      const double v = (double)mem[Canon<S>::template at<i>(g, x, y, zl, aa, state)];
+      s += v;
+      if constexpr (S::vx(i) != 0) jx += S::vx(i) * v;
+      if constexpr (S::vy(i) != 0) jy += S::vy(i) * v;
+      if constexpr (S::vz(i) != 0) jz += S::vz(i) * v;
+    });
+    const double r = zc ? 1.0 + s : s;
+    acc[0] += r;
+    acc[1] += jx;
+    acc[2] += jy;
+    acc[3] += jz;
+    acc[4] += 0.5 * (jx * jx + jy * jy + jz * jz) / r;
+  }
+  __shared__ double sh[5][DIAG_BLOCK];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) sh[k][threadIdx.x] = acc[k];
+  __syncthreads();
+  for (int w = DIAG_BLOCK / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w)
+#pragma unroll
+      for (int k = 0; k < 5; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x < 5) partial[(long long)threadIdx.x * DIAG_GRID + blockIdx.x] = sh[threadIdx.x][0];
+}
+
+__global__ void __launch_bounds__(DIAG_BLOCK) k_diag_final(const double *__restrict__ partial, double *__restrict__ out) {
+  __shared__ double sh[DIAG_BLOCK];
+  for (int k = 0; k < 5; ++k) {
+    double a = 0;
+    for (int b = threadIdx.x; b < DIAG_GRID; b += DIAG_BLOCK) a += partial[(long long)k * DIAG_GRID + b];
+    sh[threadIdx.x] = a;
+    __syncthreads();
+    for (int w = DIAG_BLOCK / 2; w > 0; w >>= 1) {
+      if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[k] = sh[0];
+    __syncthreads();
+  }
 }
 
 // canonical populations of selected cells (local linear index x + nx (y + ny z))

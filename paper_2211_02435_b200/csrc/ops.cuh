@@ -27,6 +27,9 @@ struct Ops {
   void (*check_finite)(const void *mem, const GridParams &g, int *flag, cudaStream_t s);
   void (*get_cells)(const void *mem, const GridParams &g, int aa, int state, const long long *idx, long long n,
                     double *out, cudaStream_t s);
+  // global sums (mass, momentum, kinetic energy): partial[5 * DIAG_GRID] scratch, out[5]
+  void (*diagnostics)(const void *mem, const GridParams &g, int aa, int state, int zc, double *partial,
+                      double *out, cudaStream_t s);
   // kernel attributes of the pull kernel (registers / local memory), for diagnostics
   void (*attributes)(int *regs, int *local_bytes);
 };
@@ -35,26 +38,26 @@ inline dim3 cell_grid(const GridParams &g, int nplanes) {
   return dim3((unsigned)((g.nx + BLOCK_X - 1) / BLOCK_X), (unsigned)g.ny, (unsigned)nplanes);
 }
 
-template <class S, int SPACE, int REG, class real>
+template <class S, int SPACE, int REG, class real, int RS = RS_GENERAL>
 struct OpsImpl {
   static void pull(const void *src, void *dst, const GridParams &g, const void *rates, double swe_g, int bb,
                    int nplanes, cudaStream_t s) {
     if (nplanes <= 0) return;
     const Rates<real> &r = *static_cast<const Rates<real> *>(rates);
     if (bb)
-      k_pull<S, SPACE, REG, real, true><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
+      k_pull<S, SPACE, REG, real, true, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
           static_cast<const real *>(src), static_cast<real *>(dst), g, r, (real)swe_g);
     else
-      k_pull<S, SPACE, REG, real, false><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
+      k_pull<S, SPACE, REG, real, false, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
           static_cast<const real *>(src), static_cast<real *>(dst), g, r, (real)swe_g);
   }
   static void aa(void *mem, const GridParams &g, const void *rates, double swe_g, int pattern, cudaStream_t s) {
     const Rates<real> &r = *static_cast<const Rates<real> *>(rates);
     if (pattern == PAT_AA_EVEN)
-      k_aa<S, SPACE, REG, real, PAT_AA_EVEN><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<real *>(mem), g,
+      k_aa<S, SPACE, REG, real, PAT_AA_EVEN, RS><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<real *>(mem), g,
                                                                                      r, (real)swe_g);
     else
-      k_aa<S, SPACE, REG, real, PAT_AA_ODD><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<real *>(mem), g,
+      k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<real *>(mem), g,
                                                                                     r, (real)swe_g);
   }
   static void init(void *mem, const GridParams &g, int aa, const double *rho, const double *u, double swe_g,
@@ -79,7 +82,7 @@ struct OpsImpl {
     if (n <= 0) return;
     const Rates<real> &r = *static_cast<const Rates<real> *>(rates);
     const int B = 128;
-    k_test_collide<S, SPACE, REG, real><<<(unsigned)((n + B - 1) / B), B, 0, s>>>(fin, fout, n, r, (real)swe_g);
+    k_test_collide<S, SPACE, REG, real, RS><<<(unsigned)((n + B - 1) / B), B, 0, s>>>(fin, fout, n, r, (real)swe_g);
   }
   static void check_finite(const void *mem, const GridParams &g, int *flag, cudaStream_t s) {
     k_check_finite<S, real><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<const real *>(mem), g, flag);
@@ -90,9 +93,15 @@ struct OpsImpl {
     k_get_cells<S, real><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(static_cast<const real *>(mem), g, aa, state,
                                                                       idx, n, out);
   }
+  static void diagnostics(const void *mem, const GridParams &g, int aa, int state, int zc, double *partial,
+                          double *out, cudaStream_t s) {
+    k_diag_partial<S, real><<<DIAG_GRID, DIAG_BLOCK, 0, s>>>(static_cast<const real *>(mem), g, aa, state, zc,
+                                                             partial);
+    k_diag_final<<<1, DIAG_BLOCK, 0, s>>>(partial, out);
+  }
   static void attributes(int *regs, int *local_bytes) {
     cudaFuncAttributes a{};
-    if (cudaFuncGetAttributes(&a, k_pull<S, SPACE, REG, real, false>) == cudaSuccess) {
+    if (cudaFuncGetAttributes(&a, k_pull<S, SPACE, REG, real, false, RS>) == cudaSuccess) {
       *regs = a.numRegs;
       *local_bytes = (int)a.localSizeBytes;
     } else {
@@ -101,7 +110,8 @@ struct OpsImpl {
     }
   }
   static constexpr Ops table{S::Q,      S::D,  &pull,         &aa,           &init,      &get_pop,
-                             &set_pop, &macro, &test_collide, &check_finite, &get_cells,   &attributes};
+                             &set_pop, &macro, &test_collide, &check_finite, &get_cells,   &diagnostics,
+                             &attributes};
 };
 
 }  // namespace lbm

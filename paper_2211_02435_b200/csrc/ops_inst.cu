@@ -22,31 +22,47 @@ constexpr int SP = LBM_SPACE;
 }  // namespace lbm
 
 namespace lbm {
+template <class St_, int SP_, int REG_, class Re_>
+const Ops *with_rs(int rs) {
+  if constexpr (SP_ == SPACE_POPULATION) {
+    return rs == RS_GENERAL ? &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL>::table : nullptr;
+  } else {
+    switch (rs) {
+      case RS_GENERAL: return &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL>::table;
+      case RS_REG: return &OpsImpl<St_, SP_, REG_, Re_, RS_REG>::table;
+      case RS_HIGH:
+        if constexpr (St_::Q == 27) return &OpsImpl<St_, SP_, REG_, Re_, RS_HIGH>::table;
+        return nullptr;
+      default: return nullptr;
+    }
+  }
+}
+
 template <class St_, class Re_, int SP_>
-const Ops *select_ops(int regime) {
+const Ops *select_ops(int regime, int rs) {
   if constexpr (SP_ == SPACE_SWE) {
     if constexpr (St_::Q == 9) {
-      if (regime == REG_ABS) return &OpsImpl<St_, SPACE_SWE, REG_ABS, Re_>::table;
+      if (regime == REG_ABS) return with_rs<St_, SPACE_SWE, REG_ABS, Re_>(rs);
     }
     return nullptr;
   } else if constexpr (SP_ == SPACE_CUMULANT) {
     // cumulants admit no delta equilibrium
     switch (regime) {
-      case REG_ABS: return &OpsImpl<St_, SP_, REG_ABS, Re_>::table;
-      case REG_ZC_ABS: return &OpsImpl<St_, SP_, REG_ZC_ABS, Re_>::table;
+      case REG_ABS: return with_rs<St_, SP_, REG_ABS, Re_>(rs);
+      case REG_ZC_ABS: return with_rs<St_, SP_, REG_ZC_ABS, Re_>(rs);
       default: return nullptr;
     }
   } else {
     switch (regime) {
-      case REG_ABS: return &OpsImpl<St_, SP_, REG_ABS, Re_>::table;
-      case REG_DELTA: return &OpsImpl<St_, SP_, REG_DELTA, Re_>::table;
-      case REG_ZC_ABS: return &OpsImpl<St_, SP_, REG_ZC_ABS, Re_>::table;
+      case REG_ABS: return with_rs<St_, SP_, REG_ABS, Re_>(rs);
+      case REG_DELTA: return with_rs<St_, SP_, REG_DELTA, Re_>(rs);
+      case REG_ZC_ABS: return with_rs<St_, SP_, REG_ZC_ABS, Re_>(rs);
       default: return nullptr;
     }
   }
 }
 }  // namespace lbm
 
-extern "C" const lbm::Ops *LBM_NAME(LBM_STENCIL, LBM_PREC, LBM_SPACE)(int regime) {
-  return lbm::select_ops<lbm::St, lbm::Re, lbm::SP>(regime);
+extern "C" const lbm::Ops *LBM_NAME(LBM_STENCIL, LBM_PREC, LBM_SPACE)(int regime, int rs) {
+  return lbm::select_ops<lbm::St, lbm::Re, lbm::SP>(regime, rs);
 }

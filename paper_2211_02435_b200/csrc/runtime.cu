@@ -9,6 +9,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -18,7 +19,7 @@
 using lbm::GridParams;
 using lbm::Ops;
 
-#define LBM_DECL_OPS(st, pr, sp) extern "C" const Ops *lbm_ops_##st##_##pr##_##sp(int regime);
+#define LBM_DECL_OPS(st, pr, sp) extern "C" const Ops *lbm_ops_##st##_##pr##_##sp(int regime, int rs);
 #define LBM_DECL_ALL(st, pr)          \
   LBM_DECL_OPS(st, pr, POPULATION)    \
   LBM_DECL_OPS(st, pr, RAW)           \
@@ -35,18 +36,18 @@ LBM_DECL_OPS(D2Q9, f32, SWE)
 
 namespace {
 
-const Ops *find_ops(int stencil, int prec, int space, int regime) {
+const Ops *find_ops(int stencil, int prec, int space, int regime, int rs) {
 #define LBM_CASE_SPACE(st, pr)                              \
   switch (space) {                                          \
-    case LBM_SPACE_POPULATION: return lbm_ops_##st##_##pr##_POPULATION(regime); \
-    case LBM_SPACE_RAW: return lbm_ops_##st##_##pr##_RAW(regime);               \
-    case LBM_SPACE_CENTRAL: return lbm_ops_##st##_##pr##_CENTRAL(regime);       \
-    case LBM_SPACE_CUMULANT: return lbm_ops_##st##_##pr##_CUMULANT(regime);     \
+    case LBM_SPACE_POPULATION: return lbm_ops_##st##_##pr##_POPULATION(regime, rs); \
+    case LBM_SPACE_RAW: return lbm_ops_##st##_##pr##_RAW(regime, rs);               \
+    case LBM_SPACE_CENTRAL: return lbm_ops_##st##_##pr##_CENTRAL(regime, rs);       \
+    case LBM_SPACE_CUMULANT: return lbm_ops_##st##_##pr##_CUMULANT(regime, rs);     \
     default: return nullptr;                                \
   }
   if (space == lbm::SPACE_SWE) {
     if (stencil != LBM_D2Q9) return nullptr;
-    return prec == LBM_FP64 ? lbm_ops_D2Q9_f64_SWE(regime) : lbm_ops_D2Q9_f32_SWE(regime);
+    return prec == LBM_FP64 ? lbm_ops_D2Q9_f64_SWE(regime, rs) : lbm_ops_D2Q9_f32_SWE(regime, rs);
   }
   if (stencil == LBM_D2Q9) {
     if (prec == LBM_FP64) { LBM_CASE_SPACE(D2Q9, f64) } else { LBM_CASE_SPACE(D2Q9, f32) }
@@ -70,6 +71,7 @@ struct lbm_ctx {
   int gnx = 0, gny = 0, gnz = 0;
   int rank = 0, nranks = 1, offset = 0, extent = 0;
   int bb = 0;
+  int rs = 0;
   GridParams g{};
   size_t esize = 8, grid_elems = 0;
   void *buf[2] = {nullptr, nullptr};
@@ -260,7 +262,19 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   int regime = lbm::REG_ABS;
   if (zc) regime = (equilibrium == LBM_EQ_DELTA) ? lbm::REG_DELTA : lbm::REG_ZC_ABS;
   const int kspace = (equilibrium == LBM_EQ_SWE) ? (int)lbm::SPACE_SWE : (int)collision_space;
-  const Ops *ops = find_ops(stencil, D.precision, kspace, regime);
+  // rate specialisation: rates equal to one become compile-time constants
+  int rs = lbm::RS_GENERAL;
+  if (collision_space != LBM_SPACE_POPULATION) {
+    const char *env = getenv("LBM_RATE_SPECIALIZATION");
+    const bool allow = !(env && env[0] == '0');
+    const int first_nonshear = (stencil == LBM_D2Q9) ? 5 : 9;
+    bool reg = true, high = (stencil == LBM_D3Q27);
+    for (int i = first_nonshear; i < q; ++i) reg &= (relaxation_rates[i] == 1.0);
+    if (high)
+      for (int i = 23; i < 27; ++i) high &= (relaxation_rates[i] == 1.0);
+    if (allow) rs = reg ? lbm::RS_REG : (high ? lbm::RS_HIGH : lbm::RS_GENERAL);
+  }
+  const Ops *ops = find_ops(stencil, D.precision, kspace, regime, rs);
   if (!ops) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
 
   lbm_ctx *c = new lbm_ctx;
@@ -273,6 +287,7 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   c->prec = D.precision;
   c->streaming = D.streaming;
   c->ops = ops;
+  c->rs = rs;
   c->q = q;
   c->d = two_d ? 2 : 3;
   c->gnx = D.nx;
@@ -379,6 +394,7 @@ lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
   info->bytes_per_element = c->esize;
   info->device_bytes = c->grid_elems * c->esize * (c->streaming == LBM_AA ? 1 : 2);
   info->steps_done = c->steps;
+  info->rate_specialization = c->rs;
   return LBM_OK;
 }
 
@@ -518,6 +534,28 @@ lbm_status lbm_get_populations(lbm_ctx *c, double *f) {
   if (s != LBM_OK) return s;
   LBM_CUDA(c, cudaMemcpyAsync(f, c->staging, bytes, cudaMemcpyDeviceToHost, c->stream));
   LBM_CUDA(c, cudaStreamSynchronize(c->stream));
+  return LBM_OK;
+}
+
+lbm_status lbm_get_diagnostics(lbm_ctx *c, lbm_diagnostics *out) {
+  if (!c || !out) return fail(c, LBM_EINVAL, "null argument");
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  const size_t pbytes = (size_t)5 * lbm::DIAG_GRID * sizeof(double);
+  lbm_status s = ensure_staging(c, pbytes + 5 * sizeof(double));
+  if (s != LBM_OK) return s;
+  double *partial = static_cast<double *>(c->staging);
+  double *dout = partial + 5 * lbm::DIAG_GRID;
+  c->ops->diagnostics(grid_ptr(c, 0), c->g, c->streaming == LBM_AA, c->aa_state, c->zc, partial, dout, c->stream);
+  s = check_launch(c, "k_diag");
+  if (s != LBM_OK) return s;
+  double h[5];
+  LBM_CUDA(c, cudaMemcpyAsync(h, dout, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  LBM_CUDA(c, cudaStreamSynchronize(c->stream));
+  out->mass = h[0];
+  out->momentum[0] = h[1];
+  out->momentum[1] = h[2];
+  out->momentum[2] = h[3];
+  out->kinetic_energy = h[4];
   return LBM_OK;
 }
 

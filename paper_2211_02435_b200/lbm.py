@@ -53,11 +53,15 @@ class lbm_layout(ctypes.Structure):
                                                  "recv_lo", "recv_hi", "halo_elems")]
 
 
+class lbm_diagnostics(ctypes.Structure):
+    _fields_ = [("mass", ctypes.c_double), ("momentum", ctypes.c_double * 3), ("kinetic_energy", ctypes.c_double)]
+
+
 class lbm_info(ctypes.Structure):
     _fields_ = [("q", ctypes.c_int), ("d", ctypes.c_int), ("offset", ctypes.c_int), ("extent", ctypes.c_int),
                 ("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int), ("pitch", ctypes.c_size_t),
                 ("bytes_per_element", ctypes.c_size_t), ("device_bytes", ctypes.c_size_t),
-                ("steps_done", ctypes.c_longlong)]
+                ("steps_done", ctypes.c_longlong), ("rate_specialization", ctypes.c_int)]
 
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -81,6 +85,7 @@ SIGNATURES = [
     ("lbm_get_populations", ctypes.c_int, [_vp, _dp]),
     ("lbm_set_populations", ctypes.c_int, [_vp, _dp]),
     ("lbm_get_cells", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_longlong), ctypes.c_longlong, _dp]),
+    ("lbm_get_diagnostics", ctypes.c_int, [_vp, ctypes.POINTER(lbm_diagnostics)]),
     ("lbm_check_finite", ctypes.c_int, [_vp]),
     ("lbm_test_collide", ctypes.c_int, [_vp, _dp, _dp, ctypes.c_longlong]),
     ("lbm_stencil_info", ctypes.c_int, [ctypes.c_int, _ip, _ip, _ip]),
@@ -254,6 +259,12 @@ class Lattice:
         f = np.empty((self.q,) + self.local_shape)
         _check(lib().lbm_get_populations(self._ctx, _d(f)), self._ctx)
         return f
+
+    def get_diagnostics(self):
+        """dict(mass, momentum[3], kinetic_energy) of this slab (device sums, fp64)."""
+        d = lbm_diagnostics()
+        _check(lib().lbm_get_diagnostics(self._ctx, ctypes.byref(d)), self._ctx)
+        return {"mass": d.mass, "momentum": list(d.momentum), "kinetic_energy": d.kinetic_energy}
 
     def get_cells(self, cells):
         """Canonical populations [n][q] of local linear cell indices x + nx (y + ny z)."""
