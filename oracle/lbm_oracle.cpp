@@ -595,7 +595,9 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
   matvec(q, m.Rmono.data(), Cmono, Cpoly);
   // equilibrium cumulants of the Maxwellian: log M = log rho + Xi.u + cs2 |Xi|^2 / 2
   // (eq:ContMaxwellian, eq:CumulantGeneratingFunction) => C_200 = C_020 = C_002 = rho cs2,
-  // all other cumulants of order >= 2 vanish.
+  // all other cumulants of order >= 2 vanish.  Shallow water (Venturi):
+  // the same Maxwellian with cs2 = g h / 2, h = the local water height.
+  const R cs2 = (m.eq == EQ_SWE) ? m.g * rho / R(2) : R(CS2);
   for (int p = 0; p < q; ++p) {
     int ord = order_of(m.basis[p]);
     if (ord < 2) {
@@ -605,7 +607,7 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
     R ceq = 0;
     for (auto &t : m.basis[p]) {
       bool diag2 = (t.e[0] + t.e[1] + t.e[2] == 2) && (t.e[0] == 2 || t.e[1] == 2 || t.e[2] == 2);
-      if (diag2) ceq += R(t.c) * rho * R(CS2);
+      if (diag2) ceq += R(t.c) * rho * cs2;
     }
     Cstar_poly[p] = Cpoly[p] + m.omega[p] * (ceq - Cpoly[p]);
   }
@@ -639,7 +641,7 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
 template <class R> static bool equilibrium_cell(const Method<R> &m, R rho, const R u[3], R *f) {
   const int q = m.q;
   R qeq[27];
-  if (m.eq == EQ_SWE) {
+  if (m.eq == EQ_SWE && m.space != SP_CUMULANT) {
     swe_equilibrium(m, rho, u, f);
     if (m.zc) return false;
     return true;
@@ -656,9 +658,10 @@ template <class R> static bool equilibrium_cell(const Method<R> &m, R rho, const
       Series<R> Ce;
       for (int k = 0; k < 27; ++k) Ce.c[k] = 0;
       const int e200[3] = {2, 0, 0}, e020[3] = {0, 2, 0}, e002[3] = {0, 0, 2};
-      Ce.c[sidx(e200)] = rho * R(CS2);
-      Ce.c[sidx(e020)] = rho * R(CS2);
-      if (m.d == 3) Ce.c[sidx(e002)] = rho * R(CS2);
+      const R cs2 = (m.eq == EQ_SWE) ? m.g * rho / R(2) : R(CS2);  // Venturi SWE
+      Ce.c[sidx(e200)] = rho * cs2;
+      Ce.c[sidx(e020)] = rho * cs2;
+      if (m.d == 3) Ce.c[sidx(e002)] = rho * cs2;
       R k27[27];
       central_from_cumulants(Ce, rho, k27);
       for (int p = 0; p < q; ++p) {

@@ -264,8 +264,9 @@ __global__ void __launch_bounds__(DIAG_BLOCK) k_diag_partial(const real *mem, co
   if (threadIdx.x < 5) partial[(long long)threadIdx.x * DIAG_GRID + blockIdx.x] = sh[threadIdx.x][0];
 }
 
-__global__ void __launch_bounds__(DIAG_BLOCK) k_diag_final(const double *__restrict__ partial, double *__restrict__ out) {
-  __shared__ double sh[DIAG_BLOCK];
+template <class T>
+__global__ void __launch_bounds__(DIAG_BLOCK) k_diag_final(const T *__restrict__ partial, T *__restrict__ out) {
+  __shared__ T sh[DIAG_BLOCK];
   for (int k = 0; k < 5; ++k) {
     double a = 0;
     for (int b = threadIdx.x; b < DIAG_GRID; b += DIAG_BLOCK) a += partial[(long long)k * DIAG_GRID + b];

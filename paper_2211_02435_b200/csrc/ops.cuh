@@ -97,7 +97,7 @@ struct OpsImpl {
                           double *out, cudaStream_t s) {
     k_diag_partial<S, real><<<DIAG_GRID, DIAG_BLOCK, 0, s>>>(static_cast<const real *>(mem), g, aa, state, zc,
                                                              partial);
-    k_diag_final<<<1, DIAG_BLOCK, 0, s>>>(partial, out);
+    k_diag_final<double><<<1, DIAG_BLOCK, 0, s>>>(partial, out);
   }
   static void attributes(int *regs, int *local_bytes) {
     cudaFuncAttributes a{};
