@@ -264,6 +264,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--backend", default=None, choices=["nccl", "gloo"],
+                    help="torch.distributed backend for N > 1 (default: nccl with one GPU per rank)")
     ap.add_argument("--shape", type=int, nargs=3, default=None,
                     help="override the global lattice shape (profiling runs only)")
     args = ap.parse_args()
@@ -286,10 +288,17 @@ def main():
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("launch with torchrun for --gpus > 1")
-    torch.cuda.set_device(local_rank)
+    ngpu = torch.cuda.device_count()
+    dev = local_rank % ngpu  # ranks share a GPU only in functional checks (then gloo)
+    torch.cuda.set_device(dev)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = args.backend or ("nccl" if ngpu >= world else "gloo")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    local_rank = dev
     n = world
     st = cfg["stencil"]
     q = W.Q_OF[st]
@@ -348,10 +357,16 @@ def main():
     torch.cuda.synchronize()
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1)
-    if n > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    def max_over_ranks(v):
+        if n == 1:
+            return v
+        on_gpu = dist.get_backend() == "nccl"
+        t = torch.tensor([v], device="cuda" if on_gpu else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        return float(t.item())
+
+    ms = max_over_ranks(ms)
+    if n > 1:
         dist.barrier()
     lat.check_finite()
     total_cells = nx * ny * nz
@@ -397,11 +412,7 @@ def main():
         st_ = Lb.lbm_get_macroscopic(lat._ctx, ctypes.cast(rho_o.data_ptr(), dp), ctypes.cast(u_o.data_ptr(), dp))
         assert st_ == 0
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        if n > 1:
-            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+        dt = max_over_ranks(time.perf_counter() - t0)
         h2d = (rho_h.numel() + u_h.numel()) * 8 * n
         d2h = (rho_o.numel() + u_o.numel()) * 8 * n
         e2e = {"value": total_cells * args.steps / dt / 1e6, "unit": "MLUPS",

@@ -80,8 +80,10 @@ typedef enum {
   LBM_EQ_ABSOLUTE = 0, /* continuous Maxwellian, absolute form                    */
   LBM_EQ_DELTA = 1,    /* deviation-only delta equilibrium: zero-centered only,
                           not with cumulants                                       */
-  LBM_EQ_SWE = 2       /* Zhou shallow-water equilibrium (reading R5): D2Q9 +
-                          CENTRAL + absolute storage only                                             */
+  LBM_EQ_SWE = 2       /* shallow water, D2Q9 + absolute storage only; the density slot is the height h:
+                          with CENTRAL: Zhou's discrete equilibrium (de Rosis; PAPER.md:998-1021,
+                          reading R5); with CUMULANT: the Maxwellian with cs2 = g h / 2 (Venturi;
+                          PAPER.md:1023-1026)                                                          */
 } lbm_equilibrium;
 typedef enum { LBM_FP64 = 0, LBM_FP32 = 1 } lbm_precision;
 typedef enum { LBM_PULL = 0, LBM_AA = 1 } lbm_streaming;

@@ -29,10 +29,12 @@ def build() -> str:
 def lib():
     global _LIB
     if _LIB is None:
-        path = os.path.join(_HERE, "liboracle.so")
-        src = os.path.join(_HERE, "lbm_oracle.cpp")
-        if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src):
-            build()
+        path = os.environ.get("LBM_ORACLE_LIB")  # mutation checks (scripts/oracle_mutations.py)
+        if not path:
+            path = os.path.join(_HERE, "liboracle.so")
+            src = os.path.join(_HERE, "lbm_oracle.cpp")
+            if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src):
+                build()
         L = ctypes.CDLL(path)
         dp = ctypes.POINTER(ctypes.c_double)
         ip = ctypes.POINTER(ctypes.c_int)

@@ -30,7 +30,7 @@ def units():
     out = []
     for st in STENCILS:
         for pr, real in PRECS.items():
-            sps = SPACES + (["SWE"] if st == "D2Q9" else [])
+            sps = SPACES + (["SWE", "SWEK"] if st == "D2Q9" else [])
             for sp in sps:
                 out.append((f"ops_{st}_{pr}_{sp}.o",
                             [f"-DLBM_STENCIL={st}", f"-DLBM_REAL={real}", f"-DLBM_PREC={pr}", f"-DLBM_SPACE={sp}"],

@@ -32,7 +32,10 @@
 
 namespace lbm {
 
-enum { SPACE_POPULATION = 0, SPACE_RAW = 1, SPACE_CENTRAL = 2, SPACE_CUMULANT = 3, SPACE_SWE = 4 };
+// SPACE_SWE: central moments relaxed against Zhou's discrete shallow-water equilibrium
+// (de Rosis); SPACE_SWE_K: cumulants relaxed against the Maxwellian
+// with cs2 = g h / 2 (Venturi).
+enum { SPACE_POPULATION = 0, SPACE_RAW = 1, SPACE_CENTRAL = 2, SPACE_CUMULANT = 3, SPACE_SWE = 4, SPACE_SWE_K = 5 };
 enum { REG_ABS = 0, REG_DELTA = 1, REG_ZC_ABS = 2 };
 
 template <class real>
@@ -792,7 +795,10 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
         relax_basis2<RS>(c, eq, r);
       } else {  // SPACE_CUMULANT
         if constexpr (S::D == 3) central_to_cumulant3<S>(c, inv); else central_to_cumulant2(c, inv);
-        EqCumulant<real> eq{rho * real(1.0 / 3.0)};
+        // C_eq = rho cs2 on the diagonal: cs2 = 1/3, or g h / 2 for shallow water (h = rho)
+        real cs2 = real(1.0 / 3.0);
+        if constexpr (SPACE == SPACE_SWE_K) cs2 = real(0.5) * swe_g * rho;
+        EqCumulant<real> eq{rho * cs2};
         if constexpr (S::D == 3) relax_basis3<S, RS>(c, eq, r); else relax_basis2<RS>(c, eq, r);
         if constexpr (S::D == 3) cumulant_to_central3<S>(c, inv); else cumulant_to_central2(c, inv);
       }
@@ -849,12 +855,15 @@ __device__ __forceinline__ void equilibrium(real (&f)[S::Q], real rho, real ux, 
       });
     } else {
       // untruncated Gaussian raw moments rho prod (1, u, cs2 + u^2); zc: minus hprod
+      // (cs2 = 1/3, or g h / 2 for the cumulant shallow-water method)
+      real cs2 = real(1.0 / 3.0);
+      if constexpr (SPACE == SPACE_SWE_K) cs2 = real(0.5) * swe_g * rho;
       sfor<NC>([&](auto e) {
         constexpr int ax = ex_of(e), ay = ey_of(e), az = ez_of(e);
         auto g = [&](auto a, real u) -> real {
           if constexpr (decltype(a)::value == 0) return real(1);
           else if constexpr (decltype(a)::value == 1) return u;
-          else return real(1.0 / 3.0) + u * u;
+          else return cs2 + u * u;
         };
         const real p = g(std::integral_constant<int, ax>{}, ux) * g(std::integral_constant<int, ay>{}, uy) *
                        g(std::integral_constant<int, az>{}, uz);

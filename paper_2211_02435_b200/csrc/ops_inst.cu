@@ -16,7 +16,7 @@ namespace {
 using St = LBM_STENCIL;
 using Re = LBM_REAL;
 constexpr int POPULATION = SPACE_POPULATION, RAW = SPACE_RAW, CENTRAL = SPACE_CENTRAL,
-              CUMULANT = SPACE_CUMULANT, SWE = SPACE_SWE;
+              CUMULANT = SPACE_CUMULANT, SWE = SPACE_SWE, SWEK = SPACE_SWE_K;
 constexpr int SP = LBM_SPACE;
 }  // namespace
 }  // namespace lbm
@@ -40,9 +40,9 @@ const Ops *with_rs(int rs) {
 
 template <class St_, class Re_, int SP_>
 const Ops *select_ops(int regime, int rs) {
-  if constexpr (SP_ == SPACE_SWE) {
+  if constexpr (SP_ == SPACE_SWE || SP_ == SPACE_SWE_K) {
     if constexpr (St_::Q == 9) {
-      if (regime == REG_ABS) return with_rs<St_, SPACE_SWE, REG_ABS, Re_>(rs);
+      if (regime == REG_ABS) return with_rs<St_, SP_, REG_ABS, Re_>(rs);
     }
     return nullptr;
   } else if constexpr (SP_ == SPACE_CUMULANT) {

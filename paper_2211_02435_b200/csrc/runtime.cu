@@ -33,6 +33,8 @@ LBM_DECL_ALL(D3Q27, f64)
 LBM_DECL_ALL(D3Q27, f32)
 LBM_DECL_OPS(D2Q9, f64, SWE)
 LBM_DECL_OPS(D2Q9, f32, SWE)
+LBM_DECL_OPS(D2Q9, f64, SWEK)
+LBM_DECL_OPS(D2Q9, f32, SWEK)
 
 namespace {
 
@@ -48,6 +50,10 @@ const Ops *find_ops(int stencil, int prec, int space, int regime, int rs) {
   if (space == lbm::SPACE_SWE) {
     if (stencil != LBM_D2Q9) return nullptr;
     return prec == LBM_FP64 ? lbm_ops_D2Q9_f64_SWE(regime, rs) : lbm_ops_D2Q9_f32_SWE(regime, rs);
+  }
+  if (space == lbm::SPACE_SWE_K) {
+    if (stencil != LBM_D2Q9) return nullptr;
+    return prec == LBM_FP64 ? lbm_ops_D2Q9_f64_SWEK(regime, rs) : lbm_ops_D2Q9_f32_SWEK(regime, rs);
   }
   if (stencil == LBM_D2Q9) {
     if (prec == LBM_FP64) { LBM_CASE_SPACE(D2Q9, f64) } else { LBM_CASE_SPACE(D2Q9, f32) }
@@ -226,9 +232,11 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
     return fail(nullptr, LBM_EUNSUPPORTED,
                 "cumulant space is incompatible with the delta equilibrium (PAPER.md:430-431, 547)");
   if (equilibrium == LBM_EQ_SWE &&
-      !(stencil == LBM_D2Q9 && collision_space == LBM_SPACE_CENTRAL && !zc))
+      !(stencil == LBM_D2Q9 &&
+        (collision_space == LBM_SPACE_CENTRAL || collision_space == LBM_SPACE_CUMULANT) && !zc))
     return fail(nullptr, LBM_EUNSUPPORTED,
-                "the shallow-water equilibrium is provided for D2Q9, central moments, absolute storage");
+                "the shallow-water methods are provided for D2Q9, central moments (Zhou equilibrium) or "
+                "cumulants (Maxwellian with cs2 = g h / 2), absolute storage");
   const int q = q_of(stencil);
   const int need = (collision_space == LBM_SPACE_POPULATION) ? 1 : q;
   if (n_rates != need)
@@ -261,7 +269,9 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
 
   int regime = lbm::REG_ABS;
   if (zc) regime = (equilibrium == LBM_EQ_DELTA) ? lbm::REG_DELTA : lbm::REG_ZC_ABS;
-  const int kspace = (equilibrium == LBM_EQ_SWE) ? (int)lbm::SPACE_SWE : (int)collision_space;
+  int kspace = (int)collision_space;
+  if (equilibrium == LBM_EQ_SWE)
+    kspace = (collision_space == LBM_SPACE_CUMULANT) ? (int)lbm::SPACE_SWE_K : (int)lbm::SPACE_SWE;
   // rate specialisation: rates equal to one become compile-time constants
   int rs = lbm::RS_GENERAL;
   if (collision_space != LBM_SPACE_POPULATION) {

@@ -76,12 +76,20 @@ def halo_views(lat: "L.Lattice", which: int) -> HaloViews:
 
 
 class TorchTransport:
-    """Halo exchange between the processes of a torch.distributed group."""
+    """Halo exchange between the processes of a torch.distributed group.
+
+    NCCL moves the device blocks directly (zero-copy, NVLink).  A gloo group (CPU
+    transport: tests, or several ranks sharing one GPU) stages the blocks through
+    pinned host buffers."""
 
     def __init__(self, lat: "L.Lattice", rank: int, nranks: int, group=None):
+        import torch.distributed as dist
+
         self.lat, self.rank, self.nranks, self.group = lat, rank, nranks, group
+        self.staged = dist.get_backend(group) == "gloo"
         # halo views of both grids (they alternate every step)
         self._views = {}
+        self._host = None
 
     def _get(self, which):
         key = (which, self.lat.get_halo(which).send_lo)
@@ -90,7 +98,21 @@ class TorchTransport:
         return self._views[key]
 
     def exchange(self, which: int):
-        exchange(self._get(which), self.rank, self.nranks, self.group)
+        v = self._get(which)
+        if not self.staged:
+            exchange(v, self.rank, self.nranks, self.group)
+            return
+        import torch
+
+        if self._host is None:
+            mk = lambda t: torch.empty(t.shape, dtype=t.dtype).pin_memory()
+            self._host = HaloViews(mk(v.send_lo), mk(v.send_hi), mk(v.recv_lo), mk(v.recv_hi))
+        h = self._host
+        h.send_lo.copy_(v.send_lo)  # synchronous D2H: waits for the boundary planes
+        h.send_hi.copy_(v.send_hi)
+        exchange(h, self.rank, self.nranks, self.group)
+        v.recv_lo.copy_(h.recv_lo, non_blocking=True)
+        v.recv_hi.copy_(h.recv_hi, non_blocking=True)
 
 
 class LocalTransport:

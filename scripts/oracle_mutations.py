@@ -1,0 +1,92 @@
+#!/usr/bin/env python
+"""Mutation check of the oracle's pins: plausible mistakes (a dropped term, a wrong sign,
+index or operand) are injected one at a time into a copy of oracle/lbm_oracle.cpp, the
+copy is built, and tests/test_oracle_pins.py must FAIL for every mutant.
+
+  python scripts/oracle_mutations.py
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "oracle", "lbm_oracle.cpp")
+
+# (description, exact source snippet, replacement)
+MUTANTS = [
+    ("D3Q19 basis: drop the -2 in x^2y^2 - 2x^2z^2 + y^2z^2",
+     "T(1, 2, 2, 0), T(-2, 2, 0, 2), T(1, 0, 2, 2)", "T(1, 2, 2, 0), T(-1, 2, 0, 2), T(1, 0, 2, 2)"),
+    ("Maxwellian: cs2 = 1/2", "static const long double CS2 = 1.0L / 3.0L;", "static const long double CS2 = 1.0L / 2.0L;"),
+    ("truncation at total degree 3", "if (i + j + k > 2) continue;", "if (i + j + k > 3) continue;"),
+    ("series log: wrong sign", "R sgn = (n % 2 == 1) ? R(1) : R(-1);", "R sgn = R(1);"),
+    # EQUIVALENT mutant, expected to survive: S^6 reaches degree <= 6 only through six first-order
+    # factors, and the oracle takes the log of the CENTRAL moment series, whose first-order
+    # coefficients vanish (kappa_100 = 0) - the n = 6 term is identically zero in every use.
+    ("series log: stop at n = 5 [equivalent]", "for (int n = 1; n <= 6; ++n) {\n    R sgn",
+     "for (int n = 1; n <= 5; ++n) {\n    R sgn"),
+    ("series exp: drop 1/n!", "for (int k = 0; k < 27; ++k) acc.c[k] += pw.c[k] / fact;",
+     "for (int k = 0; k < 27; ++k) acc.c[k] += pw.c[k];"),
+    ("e! factor: 2! -> 1", "static int efact(int e) { return e == 2 ? 2 : 1; }", "static int efact(int e) { return 1; }"),
+    ("central moments: xi + u", "s += f[i] * ipow(R(m.xi[i][0]) - u[0], e[0])", "s += f[i] * ipow(R(m.xi[i][0]) + u[0], e[0])"),
+    ("relaxation sign", "qs[p] = q0[p] + m.omega[p] * (qeq[p] - q0[p]);\n    matvec(q, m.Minv.data(), qs, fout);",
+     "qs[p] = q0[p] - m.omega[p] * (qeq[p] - q0[p]);\n    matvec(q, m.Minv.data(), qs, fout);"),
+    ("cumulant eq: C_eq on xy instead of the diagonal",
+     "(t.e[0] == 2 || t.e[1] == 2 || t.e[2] == 2)", "(t.e[0] == 1 || t.e[1] == 2 || t.e[2] == 2)"),
+    ("zc: forget to add f0 for the absolute equilibrium",
+     "fabs_[i] = (m.zc && !delta) ? fin[i] + m.w[i] : fin[i];", "fabs_[i] = fin[i];"),
+    ("pull: push direction", "p[a] = pos[a] - s.m.xi[i][a];", "p[a] = pos[a] + s.m.xi[i][a];"),
+    ("bounce-back: same slot instead of the opposite", "f[i] = src[(long long)s.m.opp[i] * N + c];",
+     "f[i] = src[(long long)i * N + c];"),
+    ("SWE: printed -u.u/3 (the garble of Eq. 5.3)", "+ xu * xu / R(2) - uu / R(6));", "+ xu * xu / R(2) - uu / R(3));"),
+    ("SWE cumulant: cs2 = g h", "const R cs2 = (m.eq == EQ_SWE) ? m.g * rho / R(2) : R(CS2);\n  for",
+     "const R cs2 = (m.eq == EQ_SWE) ? m.g * rho : R(CS2);\n  for"),
+    ("velocity: u = j (no division by rho)", "for (int a = 0; a < 3; ++a) u[a] = j[a] / rho;",
+     "for (int a = 0; a < 3; ++a) u[a] = j[a];"),
+    ("stencil order: swap (1,1) and (-1,-1) in-plane", "{1, 1}, {-1, -1}, {1, -1}, {-1, 1}};",
+     "{-1, -1}, {1, 1}, {1, -1}, {-1, 1}};"),
+]
+
+
+def main():
+    src = open(SRC).read()
+    tmp = tempfile.mkdtemp(prefix="oracle_mut_")
+    gomp = subprocess.run(["g++", "-print-file-name=libgomp.so"], capture_output=True, text=True).stdout.strip()
+    survived = []
+    for desc, old, new in MUTANTS:
+        if src.count(old) < 1:
+            print(f"!! snippet not found: {desc}")
+            survived.append(desc)
+            continue
+        mut = src.replace(old, new, 1)
+        cpp = os.path.join(tmp, "m.cpp")
+        so = os.path.join(tmp, "libm.so")
+        open(cpp, "w").write(mut)
+        r = subprocess.run(f"g++ -std=c++17 -O2 -ffp-contract=off -fopenmp -fPIC -c {cpp} -o {tmp}/m.o && "
+                           f"g++ -shared -o {so} {tmp}/m.o -L{os.path.dirname(gomp)} -lgomp",
+                           shell=True, capture_output=True, text=True)
+        if r.returncode != 0:
+            print(f"!! build failed: {desc}\n{r.stderr[-500:]}")
+            survived.append(desc)
+            continue
+        env = dict(os.environ, LBM_ORACLE_LIB=so)
+        t = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                            os.path.join(ROOT, "tests", "test_oracle_pins.py")], env=env, capture_output=True,
+                           text=True, cwd=ROOT, timeout=900)
+        killed = t.returncode != 0
+        first = [ln for ln in t.stdout.splitlines() if ln.startswith("FAILED")][:1]
+        print(f"{'KILLED ' if killed else 'SURVIVED'}  {desc}  {first[0] if first else ''}", flush=True)
+        if not killed and "[equivalent]" not in desc:
+            survived.append(desc)
+    shutil.rmtree(tmp, ignore_errors=True)
+    n_eq = sum("[equivalent]" in m[0] for m in MUTANTS)
+    print(f"{len(MUTANTS) - n_eq - len(survived)}/{len(MUTANTS) - n_eq} non-equivalent mutants killed "
+          f"({n_eq} equivalent mutant(s) listed for the record)")
+    return 1 if survived else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -21,7 +21,7 @@ OBJ = os.path.join(ROOT, "paper_2211_02435_b200", "build")
 
 FP64 = ("DFMA", "DADD", "DMUL")
 FP32 = ("FFMA", "FADD", "FMUL")
-SPACES = {0: "POP", 1: "RAW", 2: "CM", 3: "K", 4: "SWE"}
+SPACES = {0: "POP", 1: "RAW", 2: "CM", 3: "K", 4: "SWE-CM", 5: "SWE-K"}
 REGS = {0: "abs", 1: "zc+delta", 2: "zc+eq"}
 RSN = {0: "general", 1: "R- (all but shear = 1)", 2: "HO (orders 5,6 = 1)"}
 

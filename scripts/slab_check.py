@@ -1,0 +1,101 @@
+#!/usr/bin/env python
+"""Multi-process z-slab check: N torch.distributed ranks (torchrun) step their slabs with
+SlabRunner (boundary planes, halo exchange, interior planes on a second stream) and the
+gathered result must equal a single-rank run of the whole lattice BITWISE.
+
+Runs with NCCL when every rank has its own GPU, otherwise with gloo (ranks may share one
+GPU; the halo blocks are then staged through pinned host memory).
+
+  torchrun --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 scripts/slab_check.py
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import workloads as W  # noqa: E402
+from paper_2211_02435_b200 import distributed as D  # noqa: E402
+from paper_2211_02435_b200 import lbm as L  # noqa: E402
+
+CASES = [
+    ("D3Q27 K zc+eq", W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1, (40, 12, 8)),
+    ("D3Q19 RAW zc+delta walls", W.D3Q19, W.RAW, W.EQ_DELTA, 1, (36, 10, 8)),
+    ("D2Q9 SWE CM", W.D2Q9, W.CENTRAL, W.EQ_SWE, 0, (48, 8, 1)),
+]
+
+
+def fields(st, eq, shape, z0, nzl):
+    nx, ny, nz = shape
+    if eq == W.EQ_SWE:
+        h, u = W.dam_break_fields(nx, ny, 6.0, 6.25, 1.25, y0=z0, ny_local=nzl)
+        return h, u[:2]
+    if W.DIM_OF[st] == 2:
+        r, u = W.tgv_fields(nx, ny, 1, 0.05)
+        return r[:, z0:z0 + nzl], u[:2, :, z0:z0 + nzl]
+    r, u = W.tgv_fields(nx, ny, nzl, 0.05, plane="xz", z0=z0, nz_global=nz)
+    return r, u
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=12)
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    ngpu = torch.cuda.device_count()
+    dev = local % ngpu
+    torch.cuda.set_device(dev)
+    backend = "nccl" if ngpu >= world else "gloo"
+    dist.init_process_group(backend)
+    ok = True
+    for name, st, space, eq, zc, base in CASES:
+        nx, ny, nz = base
+        shape = (nx, ny * world, 1) if W.DIM_OF[st] == 2 else (nx, ny, nz * world)
+        g = W.swe_lattice_parameters()[0] if eq == W.EQ_SWE else 0.0
+        rates = W.regularized_rates(st, 1.3) if eq == W.EQ_SWE else W.rate_set_p(st)
+        bc = None
+        if "walls" in name:
+            bc = [[0, 0], [0, 0], [L.LBM_BC_NOSLIP, L.LBM_BC_NOSLIP]]
+        stream = torch.cuda.Stream()
+        torch.cuda.set_stream(stream)
+        lat = L.Lattice(st, space, eq, rates, shape, zero_centered=zc, bc=bc, swe_g=g, device=dev,
+                        stream=stream.cuda_stream, rank=rank, nranks=world)
+        r, u = fields(st, eq, shape, lat.offset, lat.extent)
+        lat.init_macroscopic(np.ascontiguousarray(r), np.ascontiguousarray(u[:lat.d]))
+        runner = D.SlabRunner(lat, rank, world)
+        runner.prime()
+        runner.step(args.steps)
+        torch.cuda.synchronize()
+        mine = lat.get_populations()
+        lat.close()
+        parts = [None] * world
+        dist.all_gather_object(parts, mine)
+        if rank == 0:
+            axis = 2 if W.DIM_OF[st] == 2 else 1
+            multi = np.concatenate(parts, axis=axis)
+            with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, bc=bc, swe_g=g, device=dev) as one:
+                r, u = fields(st, eq, shape, 0, shape[1] if W.DIM_OF[st] == 2 else shape[2])
+                one.init_macroscopic(np.ascontiguousarray(r), np.ascontiguousarray(u[:one.d]))
+                one.step(args.steps)
+                single = one.get_populations()
+            same = np.array_equal(multi, single)
+            ok &= same
+            print(f"[{backend} x{world}] {name} {shape}: {'PASS' if same else 'FAIL'} "
+                  f"(max |diff| {np.abs(multi - single).max():.3e})", flush=True)
+        dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print("ALL PASS" if ok else "SOME FAILED", flush=True)
+    return 0 if ok else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -119,6 +119,48 @@ def test_stencil_convention(st):
         assert (np.abs(xi).sum(1) <= 2).all()
 
 
+def test_stencil_order_golden():
+    """The full documented velocity order (tests/golden/stencil_order.txt, include/lbm.h)."""
+    gold = {}
+    for line in open(os.path.join(GOLDEN, "stencil_order.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        name, i, x, y, z = line.split()
+        gold.setdefault(W.STENCILS[name], []).append((int(x), int(y), int(z)))
+    for st in STENCILS:
+        xi, *_ = oracle.tables(st)
+        assert [tuple(v) for v in xi] == gold[st], st
+
+
+def symmetry_generators(d):
+    """Signed permutation matrices generating the square (2D) / cube (3D) symmetry group."""
+    if d == 2:
+        return [np.array([[0, 1, 0], [1, 0, 0], [0, 0, 1]]), np.diag([-1, 1, 1])]
+    return [np.array([[0, 1, 0], [1, 0, 0], [0, 0, 1]]), np.array([[1, 0, 0], [0, 0, 1], [0, 1, 0]]),
+            np.diag([-1, 1, 1])]
+
+
+@pytest.mark.parametrize("st", STENCILS)
+@pytest.mark.parametrize("space", [W.POPULATION, W.RAW, W.CENTRAL, W.CUMULANT])
+def test_collision_isotropy(st, space):
+    """With one rate per polynomial GROUP (rate set P) the collision commutes with every
+    lattice symmetry: the grouped basis (reading R2) spans invariant subspaces, as the
+    separation of shear, bulk and higher-order modes requires."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    fa = random_cells(st, 12, amp=5e-2)
+    rates = np.array([1.3]) if space == W.POPULATION else W.rate_set_p(st)
+    for eq, zc in admissible(space):
+        fin = fa - w if zc else fa
+        out = oracle.collide(st, space, eq, zc, rates, fin)
+        for P in symmetry_generators(W.DIM_OF[st]):
+            img = xi @ P.T
+            perm = [int(np.flatnonzero((xi == img[i]).all(1))[0]) for i in range(len(w))]  # xi_perm[i] = P xi_i
+            rot_in = np.empty_like(fin)
+            rot_in[:, perm] = fin
+            rot_out = oracle.collide(st, space, eq, zc, rates, rot_in)
+            np.testing.assert_allclose(rot_out[:, perm], out, atol=2e-16, err_msg=f"{P}")
+
+
 @pytest.mark.parametrize("st", STENCILS)
 def test_moment_matrix_invertible(st):
     """M is invertible for the basis: M M^{-1} = I."""
@@ -481,8 +523,10 @@ def test_shear_wave_between_walls():
     assert abs(amp / ref - 1) < 1e-2
 
 
-def test_swe_equilibrium_moments():
-    """Corrected eq:DiscreteShallowWaterEquilibrium (reading R5): sum f = h,
+@pytest.mark.parametrize("space", [W.CENTRAL, W.CUMULANT])
+def test_swe_equilibrium_moments(space):
+    """Corrected eq:DiscreteShallowWaterEquilibrium (reading R5) for the CM method and the
+    Maxwellian with cs2 = g h / 2 for the cumulant method: sum f = h,
     sum f xi = h u, sum f xi_a xi_b = h u_a u_b + g h^2/2 delta_ab (Zhou 2002)."""
     st = W.D2Q9
     xi, *_ = oracle.tables(st)
@@ -491,7 +535,13 @@ def test_swe_equilibrium_moments():
     h = rng.uniform(1.0, 6.0, n)
     u = np.zeros((n, 3))
     u[:, :2] = rng.uniform(-0.1, 0.1, (n, 2))
-    f = oracle.equilibrium(st, W.CENTRAL, W.EQ_SWE, 0, h, u, g=g)
+    f = oracle.equilibrium(st, space, W.EQ_SWE, 0, h, u, g=g)
+    if space == W.CUMULANT:
+        # product (Gaussian) form: variance cs2 = g h / 2 per axis, no mixed cumulants
+        k27, C27, rho, uu = oracle.central_and_cumulants(st, f)
+        np.testing.assert_allclose(C27[:, 2], h * g * h / 2, rtol=1e-14)
+        np.testing.assert_allclose(C27[:, 6], h * g * h / 2, rtol=1e-14)
+        assert np.abs(C27[:, [4, 5, 7, 8]]).max() < 1e-15
     np.testing.assert_allclose(f.sum(1), h, rtol=1e-15)
     np.testing.assert_allclose(f @ xi[:, :2], h[:, None] * u[:, :2], atol=1e-15)
     for a in range(2):
@@ -501,7 +551,10 @@ def test_swe_equilibrium_moments():
             np.testing.assert_allclose(P, ref, atol=1e-14)
 
 
-def test_swe_collision_conserves():
+@pytest.mark.parametrize("space", [W.CENTRAL, W.CUMULANT])
+def test_swe_collision_conserves(space):
+    """Both shallow-water methods conserve h and h u per cell, keep their equilibrium
+    fixed, and reach it with every rate one."""
     st = W.D2Q9
     xi, *_ = oracle.tables(st)
     rng = np.random.default_rng(4)
@@ -509,12 +562,18 @@ def test_swe_collision_conserves():
     h = rng.uniform(1.0, 6.0, n)
     u = np.zeros((n, 3))
     u[:, :2] = rng.uniform(-0.05, 0.05, (n, 2))
-    f = oracle.equilibrium(st, W.CENTRAL, W.EQ_SWE, 0, h, u, g=g)
-    f *= 1 + 0.02 * rng.uniform(-1, 1, f.shape)
+    feq = oracle.equilibrium(st, space, W.EQ_SWE, 0, h, u, g=g)
+    f = feq * (1 + 0.02 * rng.uniform(-1, 1, feq.shape))
     rates = W.regularized_rates(st, 0.695652)
-    fo = oracle.collide(st, W.CENTRAL, W.EQ_SWE, 0, rates, f, g=g)
+    fo = oracle.collide(st, space, W.EQ_SWE, 0, rates, f, g=g)
     np.testing.assert_allclose(fo.sum(1), f.sum(1), rtol=1e-15)
     np.testing.assert_allclose(fo @ xi, f @ xi, atol=1e-15)
+    np.testing.assert_allclose(oracle.collide(st, space, W.EQ_SWE, 0, rates, feq, g=g), feq, atol=1e-15)
+    h2 = f.sum(1)
+    u2 = np.zeros((n, 3))
+    u2[:, :2] = (f @ xi[:, :2]) / h2[:, None]
+    np.testing.assert_allclose(oracle.collide(st, space, W.EQ_SWE, 0, np.ones(9), f, g=g),
+                               oracle.equilibrium(st, space, W.EQ_SWE, 0, h2, u2, g=g), atol=1e-15)
 
 
 def paper_values():
