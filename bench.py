@@ -166,6 +166,8 @@ def oracle_mlups(cfg, target_seconds=15.0, max_cells=None):
     (mlups, cores, sample description)."""
     import oracle
 
+    # every host core (torchrun exports OMP_NUM_THREADS=1 to its ranks)
+    oracle.set_threads(len(os.sched_getaffinity(0)))
     st = cfg["stencil"]
     q = W.Q_OF[st]
     rates = rates_of(cfg)

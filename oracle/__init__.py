@@ -54,6 +54,7 @@ def lib():
         L.oracle_sim_step.argtypes = [ctypes.c_void_p, ctypes.c_int]
         L.oracle_sim_macroscopic.argtypes = [ctypes.c_void_p, dp, dp]
         L.oracle_max_threads.restype = ctypes.c_int
+        L.oracle_set_threads.argtypes = [ctypes.c_int]
         _LIB = L
     return _LIB
 
@@ -169,3 +170,8 @@ class Sim:
 
 def max_threads() -> int:
     return lib().oracle_max_threads()
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle (torchrun exports OMP_NUM_THREADS=1 to every rank)."""
+    lib().oracle_set_threads(int(n))
