@@ -40,6 +40,14 @@ CONFIGS = {
     "c4": dict(stencil=W.D3Q27, space=W.CUMULANT, eq=W.EQ_ABSOLUTE, zc=1, prec=0, streaming=0,
                shape=lambda n: (1024, 1024, 128 * n), slab=2,
                desc="D3Q27 cumulant TGV 1024x1024x(128*N) z-slabs, fp64, zero-centered + absolute eq, pull"),
+    "c4aa": dict(stencil=W.D3Q27, space=W.CUMULANT, eq=W.EQ_ABSOLUTE, zc=1, prec=0, streaming=1,
+                 shape=lambda n: (1024, 1024, 128 * n), slab=2,
+                 desc="D3Q27 cumulant TGV 1024x1024x(128*N) z-slabs, fp64, zero-centered + absolute eq, "
+                      "AA in-place (one grid)"),
+    "c4_strong": dict(stencil=W.D3Q27, space=W.CUMULANT, eq=W.EQ_ABSOLUTE, zc=1, prec=0, streaming=1,
+                      shape=lambda n: (1024, 1024, 1024), slab=2, scaling="strong",
+                      desc="D3Q27 cumulant TGV 1024^3 (strong scaling, N >= 2: 232 GB in AA), fp64, "
+                           "zero-centered + absolute eq, AA in-place"),
     "c3": dict(stencil=W.D3Q27, space=W.CENTRAL, eq=W.EQ_ABSOLUTE, zc=1, prec=0, streaming=1,
                shape=lambda n: (384, 384, 384), slab=2,
                desc="D3Q27 central-moment MRT TGV 384^3, fp64, zero-centered + absolute eq, AA in-place"),
@@ -435,7 +443,7 @@ def main():
         line = {
             "metric": BASELINE_METRIC if args.config == "c4" else f"MLUPS ({cfg['desc']})",
             "value": round(value, 1), "unit": "MLUPS", "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": cfg.get("scaling", "weak"),
             "vs_baseline": None, "dtype": dtype_name(cfg), "data": "synthetic",
             "config": {"workload": cfg["desc"], "global_shape": [nx, ny, nz], "cells_per_gpu": cells_local,
                        "rates": "rate set P (SURVEY.md 8(d))" if cfg["space"] != W.POPULATION else "omega = 1.6",

@@ -118,7 +118,9 @@ typedef struct {
    offsets of the lbm_halo blocks, each halo_elems long. */
 typedef struct {
   size_t pitch, pop, plane, planes, elements;
-  size_t send_lo, send_hi, recv_lo, recv_hi, halo_elems;
+  size_t send_lo, send_hi, recv_lo, recv_hi, halo_elems;  /* pull                              */
+  size_t aa_pre_send_lo, aa_pre_send_hi, aa_pre_recv_lo, aa_pre_recv_hi;      /* AA, before odd */
+  size_t aa_post_send_lo, aa_post_send_hi, aa_post_recv_lo, aa_post_recv_hi;  /* AA, after odd  */
 } lbm_layout;
 
 typedef struct {
@@ -156,12 +158,17 @@ lbm_status lbm_init_macroscopic(lbm_ctx *ctx, const double *rho, const double *u
 /* n fused stream–collide time steps (single rank; asynchronous on the context stream). */
 lbm_status lbm_step(lbm_ctx *ctx, int n);
 
-/* Multi-rank building blocks of one step: update the given planes from the current grid into
-   the next grid on 'stream' (NULL: context stream), then lbm_swap() once all regions are done
-   and the next grid's ghost planes were received. */
+/* Multi-rank building blocks of one step: run the step's kernel on the given planes on
+   'stream' (NULL: context stream), then lbm_swap() once all regions are done and the halos
+   were exchanged.  PULL: updates the current grid into the next grid; exchange the next
+   grid's halo (lbm_get_halo(1)) before lbm_swap.  AA: the step's kernel is the odd one when
+   lbm_info.steps_done is even (state A), else the even one; before an odd step exchange
+   lbm_get_halo(0) ("pre": the neighbours' boundary slots the odd step reads), after it
+   lbm_get_halo(1) ("post": what the boundary cells wrote into the ghost planes returns to
+   the neighbours); even steps touch only their own cells and need no exchange. */
 lbm_status lbm_step_region(lbm_ctx *ctx, lbm_region region, void *stream);
 lbm_status lbm_swap(lbm_ctx *ctx);
-/* which = 0: the current grid, 1: the next (destination) grid. */
+/* PULL: which = 0 the current grid, 1 the next grid.  AA: which = 0 pre-odd, 1 post-odd. */
 lbm_status lbm_get_halo(lbm_ctx *ctx, int which, lbm_halo *out);
 
 lbm_status lbm_sync(lbm_ctx *ctx);

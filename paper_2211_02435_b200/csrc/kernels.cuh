@@ -110,7 +110,9 @@ __global__ void __launch_bounds__(BLOCK_X) k_aa(real *mem, const GridParams g, c
     for (int s = -1; s <= 1; ++s) {
       xs[s + 1] = wrapi(x + s, g.nx);
       ys[s + 1] = wrapi(y + s, g.ny) * g.pitch;
-      zo[s + 1] = (long long)(wrapi(zl + s, g.nzl) + 1) * g.plane;
+      // single rank: periodic by index; several ranks: the ghost planes (filled before
+      // and returned after the odd step, distributed.py)
+      zo[s + 1] = (long long)((g.wrapz ? wrapi(zl + s, g.nzl) : zl + s) + 1) * g.plane;
     }
     // read f_i(x) = mem(x - xi_i, opp i)
     sfor<S::Q>([&](auto i) {
@@ -138,7 +140,8 @@ struct Canon {
     if (!aa) return (long long)(zl + 1) * g.plane + (long long)i * g.pop + (long long)y * g.pitch + x;
     if (state == 0)
       return (long long)(zl + 1) * g.plane + (long long)S::opp(i) * g.pop + (long long)y * g.pitch + x;
-    const int xx = wrapi(x + S::mx(i), g.nx), yy = wrapi(y + S::my(i), g.ny), zz = wrapi(zl + S::mz(i), g.nzl);
+    const int xx = wrapi(x + S::mx(i), g.nx), yy = wrapi(y + S::my(i), g.ny);
+    const int zz = g.wrapz ? wrapi(zl + S::mz(i), g.nzl) : zl + S::mz(i);  // multi-rank: ghost plane
     return (long long)(zz + 1) * g.plane + (long long)i * g.pop + (long long)yy * g.pitch + xx;
   }
 };

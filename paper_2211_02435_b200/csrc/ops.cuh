@@ -14,8 +14,9 @@ struct Ops {
   // pull stream–collide of planes [zbegin, zbegin + nplanes) from src into dst
   void (*pull)(const void *src, void *dst, const GridParams &g, const void *rates, double swe_g, int bb,
                int nplanes, cudaStream_t s);
-  // AA step (pattern PAT_AA_EVEN / PAT_AA_ODD) in place, all planes
-  void (*aa)(void *mem, const GridParams &g, const void *rates, double swe_g, int pattern, cudaStream_t s);
+  // AA step (pattern PAT_AA_EVEN / PAT_AA_ODD) in place, planes [zbegin, zbegin + nplanes)
+  void (*aa)(void *mem, const GridParams &g, const void *rates, double swe_g, int pattern, int nplanes,
+             cudaStream_t s);
   void (*init)(void *mem, const GridParams &g, int aa, const double *rho, const double *u, double swe_g,
                cudaStream_t s);
   void (*get_pop)(const void *mem, const GridParams &g, int aa, int state, double *out, cudaStream_t s);
@@ -51,14 +52,16 @@ struct OpsImpl {
       k_pull<S, SPACE, REG, real, false, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
           static_cast<const real *>(src), static_cast<real *>(dst), g, r, (real)swe_g);
   }
-  static void aa(void *mem, const GridParams &g, const void *rates, double swe_g, int pattern, cudaStream_t s) {
+  static void aa(void *mem, const GridParams &g, const void *rates, double swe_g, int pattern, int nplanes,
+                 cudaStream_t s) {
+    if (nplanes <= 0) return;
     const Rates<real> &r = *static_cast<const Rates<real> *>(rates);
     if (pattern == PAT_AA_EVEN)
-      k_aa<S, SPACE, REG, real, PAT_AA_EVEN, RS><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<real *>(mem), g,
-                                                                                     r, (real)swe_g);
+      k_aa<S, SPACE, REG, real, PAT_AA_EVEN, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(static_cast<real *>(mem),
+                                                                                        g, r, (real)swe_g);
     else
-      k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<real *>(mem), g,
-                                                                                    r, (real)swe_g);
+      k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(static_cast<real *>(mem),
+                                                                                       g, r, (real)swe_g);
   }
   static void init(void *mem, const GridParams &g, int aa, const double *rho, const double *u, double swe_g,
                    cudaStream_t s) {

@@ -182,10 +182,24 @@ lbm_status lbm_grid_layout(lbm_stencil stencil, lbm_precision precision, int nx,
   if (stencil == LBM_D2Q9) { up0 = lbm::D2Q9::UP0; nup = lbm::D2Q9::NUP; }
   else if (stencil == LBM_D3Q19) { up0 = lbm::D3Q19::UP0; nup = lbm::D3Q19::NUP; }
   else { up0 = lbm::D3Q27::UP0; nup = lbm::D3Q27::NUP; }
-  out->send_lo = 1 * out->plane + (size_t)(up0 + nup) * out->pop;
-  out->send_hi = (size_t)nzl * out->plane + (size_t)up0 * out->pop;
-  out->recv_lo = 0 * out->plane + (size_t)up0 * out->pop;
-  out->recv_hi = (size_t)(nzl + 1) * out->plane + (size_t)(up0 + nup) * out->pop;
+  const size_t UP = (size_t)up0 * out->pop, DN = (size_t)(up0 + nup) * out->pop;
+  const size_t z0 = 0, z1 = out->plane, zn = (size_t)nzl * out->plane, zt = (size_t)(nzl + 1) * out->plane;
+  // pull: the next grid's boundary planes feed the neighbours' ghost planes
+  out->send_lo = z1 + DN;
+  out->send_hi = zn + UP;
+  out->recv_lo = z0 + UP;
+  out->recv_hi = zt + DN;
+  // AA, before the odd step: the boundary planes' slots the neighbours' odd step reads
+  out->aa_pre_send_lo = z1 + UP;
+  out->aa_pre_send_hi = zn + DN;
+  out->aa_pre_recv_lo = z0 + DN;
+  out->aa_pre_recv_hi = zt + UP;
+  // AA, after the odd step: what this slab's boundary cells wrote into the ghost planes
+  // goes back to the neighbours' boundary planes
+  out->aa_post_send_lo = z0 + DN;
+  out->aa_post_send_hi = zt + UP;
+  out->aa_post_recv_lo = z1 + UP;
+  out->aa_post_recv_hi = zn + DN;
   out->halo_elems = (size_t)nup * out->pop;
   return LBM_OK;
 }
@@ -264,8 +278,8 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   if (slab_extent / D.nranks < 2) return fail(nullptr, LBM_EINVAL, "slabs need at least 2 planes");
   bool any_wall = false;
   for (int a = 0; a < 3; ++a) any_wall |= (D.bc[a][0] == LBM_BC_NOSLIP);
-  if (D.streaming == LBM_AA && (D.nranks > 1 || any_wall))
-    return fail(nullptr, LBM_EUNSUPPORTED, "AA streaming is provided for a single rank with periodic faces");
+  if (D.streaming == LBM_AA && any_wall)
+    return fail(nullptr, LBM_EUNSUPPORTED, "AA streaming is provided for periodic faces");
 
   int regime = lbm::REG_ABS;
   if (zc) regime = (equilibrium == LBM_EQ_DELTA) ? lbm::REG_DELTA : lbm::REG_ZC_ABS;
@@ -441,7 +455,7 @@ lbm_status lbm_step(lbm_ctx *c, int n) {
   for (int t = 0; t < n; ++t) {
     if (c->streaming == LBM_AA) {
       const int pat = (c->aa_state == 0) ? lbm::PAT_AA_ODD : lbm::PAT_AA_EVEN;
-      c->ops->aa(c->buf[0], g, c->rates, c->swe_g, pat, c->stream);
+      c->ops->aa(c->buf[0], g, c->rates, c->swe_g, pat, g.nzl, c->stream);
       c->aa_state ^= 1;
     } else {
       c->ops->pull(c->buf[c->cur], c->buf[1 - c->cur], g, c->rates, c->swe_g, c->bb, g.nzl, c->stream);
@@ -454,28 +468,27 @@ lbm_status lbm_step(lbm_ctx *c, int n) {
 
 lbm_status lbm_step_region(lbm_ctx *c, lbm_region region, void *stream) {
   if (!c) return LBM_EINVAL;
-  if (c->streaming != LBM_PULL) return fail(c, LBM_EUNSUPPORTED, "lbm_step_region needs pull streaming");
   LBM_CUDA(c, cudaSetDevice(c->device));
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
   GridParams g = c->g;
-  const void *src = c->buf[c->cur];
-  void *dst = c->buf[1 - c->cur];
   const int n = g.nzl;
+  // launch the step's kernel on planes [z0, z0 + np)
+  auto run = [&](int z0, int np) {
+    g.zbegin = z0;
+    if (c->streaming == LBM_AA) {
+      const int pat = (c->aa_state == 0) ? lbm::PAT_AA_ODD : lbm::PAT_AA_EVEN;
+      c->ops->aa(c->buf[0], g, c->rates, c->swe_g, pat, np, s);
+    } else {
+      c->ops->pull(c->buf[c->cur], c->buf[1 - c->cur], g, c->rates, c->swe_g, c->bb, np, s);
+    }
+  };
   switch (region) {
-    case LBM_REGION_ALL:
-      g.zbegin = 0;
-      c->ops->pull(src, dst, g, c->rates, c->swe_g, c->bb, n, s);
-      break;
+    case LBM_REGION_ALL: run(0, n); break;
     case LBM_REGION_BOUNDARY:
-      g.zbegin = 0;
-      c->ops->pull(src, dst, g, c->rates, c->swe_g, c->bb, 1, s);
-      g.zbegin = n - 1;
-      c->ops->pull(src, dst, g, c->rates, c->swe_g, c->bb, 1, s);
+      run(0, 1);
+      run(n - 1, 1);
       break;
-    case LBM_REGION_INTERIOR:
-      g.zbegin = 1;
-      c->ops->pull(src, dst, g, c->rates, c->swe_g, c->bb, n - 2, s);
-      break;
+    case LBM_REGION_INTERIOR: run(1, n - 2); break;
     default: return fail(c, LBM_EINVAL, "unknown region");
   }
   return check_launch(c, "stream_collide(region)");
@@ -483,25 +496,30 @@ lbm_status lbm_step_region(lbm_ctx *c, lbm_region region, void *stream) {
 
 lbm_status lbm_swap(lbm_ctx *c) {
   if (!c) return LBM_EINVAL;
-  if (c->streaming != LBM_PULL) return fail(c, LBM_EUNSUPPORTED, "lbm_swap needs pull streaming");
-  c->cur ^= 1;
+  if (c->streaming == LBM_AA) c->aa_state ^= 1;
+  else c->cur ^= 1;
   c->steps++;
   return LBM_OK;
 }
 
 lbm_status lbm_get_halo(lbm_ctx *c, int which, lbm_halo *out) {
   if (!c || !out) return LBM_EINVAL;
-  if (c->streaming != LBM_PULL) return fail(c, LBM_EUNSUPPORTED, "halo exchange needs pull streaming");
   char *base = static_cast<char *>(grid_ptr(c, which));
   lbm_layout lay;
   lbm_status s = lbm_grid_layout((lbm_stencil)c->stencil, (lbm_precision)c->prec, c->gnx, c->gny, c->gnz,
                                  c->nranks, &lay);
   if (s != LBM_OK) return fail(c, s, "layout");
   const size_t E = c->esize;
-  out->send_lo = base + lay.send_lo * E;
-  out->send_hi = base + lay.send_hi * E;
-  out->recv_lo = base + lay.recv_lo * E;
-  out->recv_hi = base + lay.recv_hi * E;
+  size_t o[4] = {lay.send_lo, lay.send_hi, lay.recv_lo, lay.recv_hi};
+  if (c->streaming == LBM_AA) {
+    const size_t pre[4] = {lay.aa_pre_send_lo, lay.aa_pre_send_hi, lay.aa_pre_recv_lo, lay.aa_pre_recv_hi};
+    const size_t post[4] = {lay.aa_post_send_lo, lay.aa_post_send_hi, lay.aa_post_recv_lo, lay.aa_post_recv_hi};
+    for (int k = 0; k < 4; ++k) o[k] = (which == 0) ? pre[k] : post[k];
+  }
+  out->send_lo = base + o[0] * E;
+  out->send_hi = base + o[1] * E;
+  out->recv_lo = base + o[2] * E;
+  out->recv_hi = base + o[3] * E;
   out->bytes = lay.halo_elems * E;
   return LBM_OK;
 }

@@ -134,16 +134,28 @@ class LocalTransport:
         torch.cuda.synchronize()
 
 
+def exchange_after_boundary(lat: "L.Lattice") -> int:
+    """Which halo (lbm_get_halo) to exchange once the boundary planes of this step are done:
+    pull: the next grid (1).  AA (lbm.h): after an odd step the ghost-plane writes return
+    to the neighbours ("post", 1); after an even step the boundary slots the next odd step
+    reads go out ("pre", 0)."""
+    if lat.streaming == L.LBM_PULL:
+        return 1
+    odd = lat.info().steps_done % 2 == 0  # state A -> this step runs the odd kernel
+    return 1 if odd else 0
+
+
 def step_local(lats, n: int):
     """n time steps of all slab contexts of one process (LocalTransport), with the
     same boundary/interior split as the multi-process driver."""
     tr = LocalTransport(lats)
     for _ in range(n):
+        which = exchange_after_boundary(lats[0])
         for l in lats:
             l.step_region(L.LBM_REGION_BOUNDARY)
         for l in lats:
             l.sync()
-        tr.exchange_all(1)
+        tr.exchange_all(which)
         for l in lats:
             l.step_region(L.LBM_REGION_INTERIOR)
         for l in lats:
@@ -152,7 +164,7 @@ def step_local(lats, n: int):
 
 
 def prime_local(lats):
-    """Fill the ghost planes of the current grids after init/set."""
+    """Fill the ghost planes after init/set (pull: current grid; AA: the pre-odd halo)."""
     LocalTransport(lats).exchange_all(0)
 
 
@@ -177,6 +189,7 @@ class SlabRunner:
 
         main = self.s_main
         for _ in range(n):
+            which = exchange_after_boundary(self.lat)
             # boundary planes on the main stream, then the exchange (NCCL waits on main)
             self.lat.step_region(L.LBM_REGION_BOUNDARY, main.cuda_stream)
             ev = torch.cuda.Event()
@@ -184,7 +197,7 @@ class SlabRunner:
             self.s_int.wait_event(ev)
             self.lat.step_region(L.LBM_REGION_INTERIOR, self.s_int.cuda_stream)
             with torch.cuda.stream(main):
-                self.tr.exchange(1)
+                self.tr.exchange(which)
             main.wait_stream(self.s_int)
             self.lat.swap()
 

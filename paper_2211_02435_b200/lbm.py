@@ -49,8 +49,10 @@ class lbm_halo(ctypes.Structure):
 
 
 class lbm_layout(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_size_t) for n in ("pitch", "pop", "plane", "planes", "elements", "send_lo", "send_hi",
-                                                 "recv_lo", "recv_hi", "halo_elems")]
+    _fields_ = [(n, ctypes.c_size_t) for n in (
+        "pitch", "pop", "plane", "planes", "elements", "send_lo", "send_hi", "recv_lo", "recv_hi", "halo_elems",
+        "aa_pre_send_lo", "aa_pre_send_hi", "aa_pre_recv_lo", "aa_pre_recv_hi",
+        "aa_post_send_lo", "aa_post_send_hi", "aa_post_recv_lo", "aa_post_recv_hi")]
 
 
 class lbm_diagnostics(ctypes.Structure):

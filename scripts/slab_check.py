@@ -29,6 +29,8 @@ CASES = [
     ("D3Q27 K zc+eq", W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1, (40, 12, 8)),
     ("D3Q19 RAW zc+delta walls", W.D3Q19, W.RAW, W.EQ_DELTA, 1, (36, 10, 8)),
     ("D2Q9 SWE CM", W.D2Q9, W.CENTRAL, W.EQ_SWE, 0, (48, 8, 1)),
+    ("D3Q27 CM zc+eq AA", W.D3Q27, W.CENTRAL, W.EQ_ABSOLUTE, 1, (40, 12, 8)),
+    ("D2Q9 K AA", W.D2Q9, W.CUMULANT, W.EQ_ABSOLUTE, 1, (48, 8, 1)),
 ]
 
 
@@ -64,10 +66,11 @@ def main():
         bc = None
         if "walls" in name:
             bc = [[0, 0], [0, 0], [L.LBM_BC_NOSLIP, L.LBM_BC_NOSLIP]]
+        streaming = L.LBM_AA if name.endswith("AA") else L.LBM_PULL
         stream = torch.cuda.Stream()
         torch.cuda.set_stream(stream)
         lat = L.Lattice(st, space, eq, rates, shape, zero_centered=zc, bc=bc, swe_g=g, device=dev,
-                        stream=stream.cuda_stream, rank=rank, nranks=world)
+                        stream=stream.cuda_stream, rank=rank, nranks=world, streaming=streaming)
         r, u = fields(st, eq, shape, lat.offset, lat.extent)
         lat.init_macroscopic(np.ascontiguousarray(r), np.ascontiguousarray(u[:lat.d]))
         runner = D.SlabRunner(lat, rank, world)

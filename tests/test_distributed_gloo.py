@@ -122,3 +122,13 @@ def test_halo_blocks_are_the_crossing_populations():
         assert list(up) == list(range(up[0], up[0] + len(up)))
         assert list(down) == list(range(down[0], down[0] + len(down)))
         assert lay.pitch % 16 == 0 and lay.pitch >= shape[0]
+        # AA (lbm.h): before the odd step the neighbours' boundary slots the odd step reads come
+        # in (ghost below: the -1 block, ghost above: the +1 block); after it the ghost-plane
+        # writes go back out - the post exchange is the pre exchange with send and recv swapped
+        top, bot = lay.planes - 2, 1
+        assert (lay.aa_pre_recv_lo // lay.plane, lay.aa_pre_recv_lo % lay.plane) == (0, down[0] * lay.pop)
+        assert (lay.aa_pre_recv_hi // lay.plane, lay.aa_pre_recv_hi % lay.plane) == (top + 1, up[0] * lay.pop)
+        assert (lay.aa_pre_send_lo // lay.plane, lay.aa_pre_send_lo % lay.plane) == (bot, up[0] * lay.pop)
+        assert (lay.aa_pre_send_hi // lay.plane, lay.aa_pre_send_hi % lay.plane) == (top, down[0] * lay.pop)
+        assert (lay.aa_post_send_lo, lay.aa_post_send_hi) == (lay.aa_pre_recv_lo, lay.aa_pre_recv_hi)
+        assert (lay.aa_post_recv_lo, lay.aa_post_recv_hi) == (lay.aa_pre_send_lo, lay.aa_pre_send_hi)

@@ -19,11 +19,11 @@ from paper_2211_02435_b200 import distributed as D  # noqa: E402
 from paper_2211_02435_b200 import lbm as L  # noqa: E402
 
 
-def run_slabs(st, space, eq, zc, rates, shape, f0, steps, nranks, bc=None):
+def run_slabs(st, space, eq, zc, rates, shape, f0, steps, nranks, bc=None, streaming=L.LBM_PULL):
     nx, ny, nz = shape
     slab_axis = 2 if W.DIM_OF[st] == 2 else 1  # in the [q][z][y][x] host layout (2D: [q][1][y][x])
-    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, bc=bc, rank=r, nranks=nranks)
-            for r in range(nranks)]
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, bc=bc, rank=r, nranks=nranks,
+                      streaming=streaming) for r in range(nranks)]
     for lat in lats:
         sl = [slice(None)] * 4
         sl[slab_axis] = slice(lat.offset, lat.offset + lat.extent)
@@ -63,3 +63,23 @@ def test_slabs_with_walls_match_oracle():
     multi = run_slabs(st, space, eq, zc, rates, shape, f0, 30, 4, bc=bc)
     ref = oracle_run(st, space, eq, zc, rates, shape, f0, 30, bc=bc)
     assert gate_error(st, multi, ref, zc) < F64_TOL
+
+
+@pytest.mark.parametrize("st,space,eq,zc,nranks", [
+    (W.D3Q27, W.CENTRAL, W.EQ_ABSOLUTE, 1, 2),
+    (W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1, 3),
+    (W.D2Q9, W.RAW, W.EQ_DELTA, 1, 4),
+])
+@pytest.mark.parametrize("steps", [7, 8])
+def test_aa_slabs_equal_single_rank_bitwise(st, space, eq, zc, nranks, steps):
+    """Multi-rank AA (row f4): the pre-odd / post-odd ghost exchange reproduces the
+    single-rank AA run (itself == pull, reading R11) bitwise at both parities."""
+    shape = (20, 12, 1) if st == W.D2Q9 else (20, 10, 12)
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc) as lat:
+        lat.set_populations(f0)
+        lat.step(steps)
+        single = lat.get_populations()
+    multi = run_slabs(st, space, eq, zc, rates, shape, f0, steps, nranks, streaming=L.LBM_AA)
+    np.testing.assert_array_equal(multi, single)
