@@ -178,6 +178,14 @@ lbm_status lbm_get_macroscopic(lbm_ctx *ctx, double *rho, double *u);
 /* Canonical post-collision populations f*(x, t) in stored form, independent of the AA parity
    (reading R11), f[i][z][y][x] fp64 (host; synchronises). */
 lbm_status lbm_get_populations(lbm_ctx *ctx, double *f);
+/* Uniform body force density force[3] (lattice units, physical axes; 2D: force[2] = 0) for the
+   following steps: Guo forcing in the paper's source term q^F of eq:MrtUpdateGeneral
+   (reading R23): u = (j + F/2) / rho and q^F = (I - S/2) T(F^G) with
+   F^G_i = w_i [3 xi.F + 9 (xi.u)(xi.F) - 3 u.F]; the momentum gains F per step (kappa_100 = -F/2
+   before, +F/2 after the collision).  Velocities reported for the
+   post-collision state are (j - F/2) / rho.  LBM_EUNSUPPORTED for cumulant and shallow-water
+   methods.  A zero force restores the unforced kernels. */
+lbm_status lbm_set_force(lbm_ctx *ctx, const double *force);
 /* Global sums over this rank's slab of the canonical state, on the device in fp64 with a
    fixed (deterministic) summation order: mass = sum rho, momentum = sum rho u (physical
    x, y, z; 2D: z = 0), kinetic energy = sum rho |u|^2 / 2 (lattice-node form of

@@ -53,6 +53,9 @@ def lib():
         L.oracle_sim_get.argtypes = [ctypes.c_void_p, dp]
         L.oracle_sim_step.argtypes = [ctypes.c_void_p, ctypes.c_int]
         L.oracle_sim_macroscopic.argtypes = [ctypes.c_void_p, dp, dp]
+        L.oracle_collide_forced.argtypes = [ctypes.c_int] * 4 + [dp, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                                                 dp, dp, dp, ctypes.c_longlong]
+        L.oracle_sim_set_force.argtypes = [ctypes.c_void_p, dp]
         L.oracle_max_threads.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         _LIB = L
@@ -84,13 +87,19 @@ def tables(stencil: int):
             M[: n * n].reshape(n, n).copy(), Minv[: n * n].reshape(n, n).copy())
 
 
-def collide(stencil, space, eq, zc, rates, f_in, g=0.0, prec=LONG_DOUBLE):
-    """Collision of independent cells; f_in [n, q] in stored form."""
+def collide(stencil, space, eq, zc, rates, f_in, g=0.0, prec=LONG_DOUBLE, force=None):
+    """Collision of independent cells; f_in [n, q] in stored form; optional uniform body
+    force density force[3] (Guo forcing, reading R23)."""
     f_in = np.ascontiguousarray(f_in, dtype=np.float64)
     out = np.empty_like(f_in)
     r = np.ascontiguousarray(rates, dtype=np.float64).reshape(-1)
-    rc = lib().oracle_collide(stencil, space, eq, int(zc), _dp(r), r.size, float(g), prec, _dp(f_in), _dp(out),
-                              f_in.shape[0])
+    if force is not None:
+        F = np.ascontiguousarray(np.asarray(force, dtype=np.float64).reshape(3))
+        rc = lib().oracle_collide_forced(stencil, space, eq, int(zc), _dp(r), r.size, float(g), prec, _dp(F),
+                                         _dp(f_in), _dp(out), f_in.shape[0])
+    else:
+        rc = lib().oracle_collide(stencil, space, eq, int(zc), _dp(r), r.size, float(g), prec, _dp(f_in),
+                                  _dp(out), f_in.shape[0])
     if rc != 0:
         raise RuntimeError(f"oracle_collide failed ({rc})")
     return out
@@ -153,6 +162,10 @@ class Sim:
 
     def step(self, n=1):
         lib().oracle_sim_step(self._h, int(n))
+
+    def set_force(self, force):
+        F = np.ascontiguousarray(np.asarray(force, dtype=np.float64).reshape(3))
+        lib().oracle_sim_set_force(self._h, _dp(F))
 
     def macroscopic(self):
         q, nz, ny, nx = self.shape

@@ -303,6 +303,8 @@ static int efact(int e) { return e == 2 ? 2 : 1; }  // e! for e in {0,1,2}
 template <class R> struct Method {
   int stencil = 0, d = 0, q = 0, space = 0, eq = 0, zc = 0;
   R g = 0;  // SWE lattice gravity
+  R F[3] = {0, 0, 0};  // uniform body force density (lattice units)
+  bool forced = false;
   std::vector<std::array<int, 3>> xi;
   std::vector<int> opp;
   std::vector<Poly> basis;
@@ -421,14 +423,32 @@ static bool build_method(Method<R> &m, int stencil, int space, int eq, int zc, c
 
 /* macroscopic quantities (eq:DensityAndVelocity PAPER.md:247-251;            */
 /* eq:DensityAndVelocityFromDeviation PAPER.md:254-259, rho0 = 1)             */
-template <class R> static void macroscopic(const Method<R> &m, const R *f, R &rho, R u[3]) {
+/* With a body force F (reading R23, Guo et al. 2002) the velocity is shifted by half the  */
+/* force: pre-collision u = (j + F/2) / rho (half = +1), post-collision u = (j - F/2) / rho */
+/* (half = -1, the canonical post-collision state of a step).                             */
+template <class R>
+static void macroscopic(const Method<R> &m, const R *f, R &rho, R u[3], int half = 1) {
   R s = 0, j[3] = {0, 0, 0};
   for (int i = 0; i < m.q; ++i) {
     s += f[i];
     for (int a = 0; a < 3; ++a) j[a] += f[i] * R(m.xi[i][a]);
   }
   rho = m.zc ? R(1) + s : s;
-  for (int a = 0; a < 3; ++a) u[a] = j[a] / rho;
+  for (int a = 0; a < 3; ++a) u[a] = (j[a] + R(half) * m.F[a] / R(2)) / rho;
+}
+
+/* Guo's discrete force term F^G_i = w_i [3 xi.F + 9 (xi.u)(xi.F) - 3 u.F] (c_s^2 = 1/3);  */
+/* the source of eq:MrtUpdateGeneral is q^F = (I - S/2) T(F^G) (reading R23).             */
+template <class R> static void guo_force(const Method<R> &m, const R u[3], R *FG) {
+  R uF = u[0] * m.F[0] + u[1] * m.F[1] + u[2] * m.F[2];
+  for (int i = 0; i < m.q; ++i) {
+    R xF = 0, xu = 0;
+    for (int a = 0; a < 3; ++a) {
+      xF += R(m.xi[i][a]) * m.F[a];
+      xu += R(m.xi[i][a]) * u[a];
+    }
+    FG[i] = m.w[i] * (R(3) * xF + R(9) * xu * xF - R(3) * uF);
+  }
 }
 
 /* K(u)[p][i] = p(xi_i - u) */
@@ -535,6 +555,13 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
   const R u0[3] = {0, 0, 0};                // background state rho0 = 1, u = 0
   // absolute populations for the absolute-equilibrium regimes
   for (int i = 0; i < q; ++i) fabs_[i] = (m.zc && !delta) ? fin[i] + m.w[i] : fin[i];
+  // force term (source q^F of eq:MrtUpdateGeneral)
+  R FG[27], qF[27];
+  for (int i = 0; i < q; ++i) FG[i] = 0;
+  if (m.forced) {
+    if (m.space == SP_CUMULANT || m.eq == EQ_SWE) return false;  // not provided (reading R23)
+    guo_force(m, u, FG);
+  }
 
   if (m.space == SP_POPULATION) {
     // T = identity; f_eq = M^{-1} m_eq (reading R4)
@@ -544,18 +571,21 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
       if (delta) meq[p] -= raw_eq_poly(m, p, R(1), u0);
     }
     matvec(q, m.Minv.data(), meq, feq);
-    for (int i = 0; i < q; ++i) qs[i] = fabs_[i] + m.omega[0] * (feq[i] - fabs_[i]);
+    for (int i = 0; i < q; ++i)
+      qs[i] = fabs_[i] + m.omega[0] * (feq[i] - fabs_[i]) + (R(1) - m.omega[0] / R(2)) * FG[i];
     for (int i = 0; i < q; ++i) fout[i] = (m.zc && !delta) ? qs[i] - m.w[i] : qs[i];
     return true;
   }
 
   if (m.space == SP_RAW) {
     matvec(q, m.M.data(), fabs_, q0);  // q = M f   (eq:DiscreteRawMomentsDef)
+    matvec(q, m.M.data(), FG, qF);
     for (int p = 0; p < q; ++p) {
       qeq[p] = raw_eq_poly(m, p, rho, u);
       if (delta) qeq[p] -= raw_eq_poly(m, p, R(1), u0);  // dq_eq = q_eq - q0
     }
-    for (int p = 0; p < q; ++p) qs[p] = q0[p] + m.omega[p] * (qeq[p] - q0[p]);
+    for (int p = 0; p < q; ++p)
+      qs[p] = q0[p] + m.omega[p] * (qeq[p] - q0[p]) + (R(1) - m.omega[p] / R(2)) * qF[p];
     matvec(q, m.Minv.data(), qs, fout);
     if (m.zc && !delta)
       for (int i = 0; i < q; ++i) fout[i] -= m.w[i];
@@ -578,7 +608,9 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
         for (int p = 0; p < q; ++p) qeq[p] -= kw[p];
       }
     }
-    for (int p = 0; p < q; ++p) qs[p] = q0[p] + m.omega[p] * (qeq[p] - q0[p]);
+    matvec(q, K, FG, qF);  // kappa^F = K(u) F^G
+    for (int p = 0; p < q; ++p)
+      qs[p] = q0[p] + m.omega[p] * (qeq[p] - q0[p]) + (R(1) - m.omega[p] / R(2)) * qF[p];
     std::vector<R> A(K, K + q * q);
     if (!solve(q, A.data(), qs)) return false;
     for (int i = 0; i < q; ++i) fout[i] = (m.zc && !delta) ? qs[i] - m.w[i] : qs[i];
@@ -766,34 +798,47 @@ int oracle_weights_ld(int stencil, long double *w) {
   return m.q;
 }
 
+}  // extern "C"
+
+namespace {
+template <class R>
+int collide_cells(int stencil, int space, int eq, int zc, const double *rates, int nrates, double g,
+                  const double *force, const double *fin, double *fout, long long n) {
+  Method<R> m;
+  if (!build_method(m, stencil, space, eq, zc, rates, nrates, g)) return -1;
+  if (force) {
+    for (int a = 0; a < 3; ++a) m.F[a] = R(force[a]);
+    m.forced = true;
+  }
+  int bad = 0;
+#pragma omp parallel for reduction(+ : bad)
+  for (long long c = 0; c < n; ++c) {
+    R f[27], fs[27];
+    for (int i = 0; i < m.q; ++i) f[i] = fin[c * m.q + i];
+    if (!collide_cell(m, f, fs)) bad++;
+    for (int i = 0; i < m.q; ++i) fout[c * m.q + i] = (double)fs[i];
+  }
+  return bad ? -2 : 0;
+}
+}  // namespace
+
+extern "C" {
+
 /* collision of n independent cells; f_in/f_out [n][q] stored form (double) */
 int oracle_collide(int stencil, int space, int eq, int zc, const double *rates, int nrates,
                    double g, int prec, const double *fin, double *fout, long long n) {
-  if (prec == 1) {
-    Method<long double> m;
-    if (!build_method(m, stencil, space, eq, zc, rates, nrates, g)) return -1;
-    int bad = 0;
-#pragma omp parallel for reduction(+ : bad)
-    for (long long c = 0; c < n; ++c) {
-      long double f[27], fs[27];
-      for (int i = 0; i < m.q; ++i) f[i] = fin[c * m.q + i];
-      if (!collide_cell(m, f, fs)) bad++;
-      for (int i = 0; i < m.q; ++i) fout[c * m.q + i] = (double)fs[i];
-    }
-    return bad ? -2 : 0;
-  } else {
-    Method<double> m;
-    if (!build_method(m, stencil, space, eq, zc, rates, nrates, g)) return -1;
-    int bad = 0;
-#pragma omp parallel for reduction(+ : bad)
-    for (long long c = 0; c < n; ++c) {
-      double f[27], fs[27];
-      for (int i = 0; i < m.q; ++i) f[i] = fin[c * m.q + i];
-      if (!collide_cell(m, f, fs)) bad++;
-      for (int i = 0; i < m.q; ++i) fout[c * m.q + i] = fs[i];
-    }
-    return bad ? -2 : 0;
-  }
+  if (prec == 1)
+    return collide_cells<long double>(stencil, space, eq, zc, rates, nrates, g, nullptr, fin, fout, n);
+  return collide_cells<double>(stencil, space, eq, zc, rates, nrates, g, nullptr, fin, fout, n);
+}
+
+/* the same with a uniform body force density force[3] (Guo; reading R23) */
+int oracle_collide_forced(int stencil, int space, int eq, int zc, const double *rates, int nrates,
+                          double g, int prec, const double *force, const double *fin, double *fout,
+                          long long n) {
+  if (prec == 1)
+    return collide_cells<long double>(stencil, space, eq, zc, rates, nrates, g, force, fin, fout, n);
+  return collide_cells<double>(stencil, space, eq, zc, rates, nrates, g, force, fin, fout, n);
 }
 
 /* equilibrium populations at given (rho, u[d]) per cell: f [n][q] stored form */
@@ -936,10 +981,25 @@ int oracle_sim_macroscopic(void *h, double *rho, double *u) {
     for (long long c = 0; c < N; ++c) {
       R f[27], r, uu[3];
       for (int i = 0; i < s->m.q; ++i) f[i] = s->a[(long long)i * N + c];
-      macroscopic(s->m, f, r, uu);
+      macroscopic(s->m, f, r, uu, -1);  // canonical post-collision state: u = (j - F/2) / rho
       rho[c] = (double)r;
       for (int a = 0; a < 3; ++a) u[(long long)a * N + c] = (double)uu[a];
     }
+  };
+  if (as->prec == 1)
+    doit((Sim<long double> *)as->p);
+  else
+    doit((Sim<double> *)as->p);
+  return 0;
+}
+
+/* uniform body force density for the following steps (Guo; reading R23) */
+int oracle_sim_set_force(void *h, const double *force) {
+  AnySim *as = (AnySim *)h;
+  auto doit = [&](auto *s) {
+    using R = typename std::remove_reference<decltype(s->a[0])>::type;
+    for (int a = 0; a < 3; ++a) s->m.F[a] = R(force[a]);
+    s->m.forced = true;
   };
   if (as->prec == 1)
     doit((Sim<long double> *)as->p);

@@ -677,10 +677,49 @@ __device__ __forceinline__ void add_background(real (&c)[NC], real sgn) {
 // the collision of one cell: f in/out in the documented population order,
 // STORED form (delta f for REG_DELTA / REG_ZC_ABS).
 // --------------------------------------------------------------------------
+// --------------------------------------------------------------------------
+// body force (reading R23; Guo et al. 2002, the paper's q^F):
+// u = (j + F/2) / rho, and the source q^F = (I - S/2) T(F^G) of the discrete Guo term
+// F^G_i = w_i [3 xi.F + 9 (xi.u)(xi.F) - 3 u.F] is added after relaxation.  The momentum
+// gains exactly F (kappa_100: -F/2 before, +F/2 after).
+// --------------------------------------------------------------------------
+enum { RS_FORCE = 4 };  // flag bit of the RS template parameter
+
+template <class real>
+struct Force {
+  real F[3];         // force density along the physical axes (2D: x, y)
+  Rates<real> half;  // w / 2 per polynomial: the S/2 of (I - S/2)
+};
+
+template <class real>
+struct EqZeroAll {
+  template <int e>
+  __device__ __forceinline__ real get() const { return real(0); }
+  template <int e>
+  __device__ static constexpr bool zero() { return true; }
+};
+
+template <class S, class real, int NC>
+__device__ __forceinline__ void guo_cube(real (&s)[NC], const Force<real> &fr, real ux, real uy, real uz) {
+  const real uF = ux * fr.F[0] + uy * fr.F[1] + uz * fr.F[2];
+  sfor<NC>([&](auto k) { s[k] = real(0); });
+  sfor<S::Q>([&](auto i) {
+    constexpr int vx = S::vx(i), vy = S::vy(i), vz = S::vz(i);
+    const real xF = real(vx) * fr.F[0] + real(vy) * fr.F[1] + real(vz) * fr.F[2];
+    const real xu = real(vx) * ux + real(vy) * uy + real(vz) * uz;
+    s[S::pos(i)] = real(weight<S>(i)) * (real(3) * xF + real(9) * xu * xF - real(3) * uF);
+  });
+}
+
 template <class S, int SPACE, int REG, class real, int RS = RS_GENERAL>
-__device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, real swe_g) {
+__device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, real swe_g,
+                                        const Force<real> &fr) {
   constexpr bool zc = (REG != REG_ABS);
   constexpr int NC = S::NC;
+  constexpr bool FORCED = (RS & RS_FORCE) != 0;
+  static_assert(!FORCED || SPACE == SPACE_POPULATION || SPACE == SPACE_RAW || SPACE == SPACE_CENTRAL,
+                "forcing is provided for population, raw and central-moment collisions");
+  constexpr int RSR = RS & 3;  // rate specialisation proper
   real c[NC];
   sfor<NC>([&](auto k) { c[k] = real(0); });
   sfor<S::Q>([&](auto i) { c[S::pos(i)] = f[i]; });
@@ -694,7 +733,12 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
     const real jx = c[E(1, 0, 0)], jy = c[E(0, 1, 0)];
     real jz = real(0);
     if constexpr (S::D == 3) jz = c[E(0, 0, 1)];
-    const real ux = jx * inv, uy = jy * inv, uz = jz * inv;
+    real ux = jx * inv, uy = jy * inv, uz = jz * inv;
+    if constexpr (FORCED) {
+      ux = fma(real(0.5) * fr.F[0], inv, ux);
+      uy = fma(real(0.5) * fr.F[1], inv, uy);
+      uz = fma(real(0.5) * fr.F[2], inv, uz);
+    }
     RawU<real> U{ux, uy, uz, ux * ux, uy * uy, uz * uz};
     real g[NC];
     if constexpr (REG == REG_DELTA) {
@@ -728,6 +772,12 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
     } else {
       sfor<S::Q>([&](auto i) { f[i] = fma(w, g[S::pos(i)] - f[i], f[i]); });
     }
+    if constexpr (FORCED) {  // + (1 - w/2) F^G_i
+      real s[NC];
+      guo_cube<S>(s, fr, ux, uy, uz);
+      const real a = real(1) - fr.half.w[0];
+      sfor<S::Q>([&](auto i) { f[i] = fma(a, s[S::pos(i)], f[i]); });
+    }
     return;
   } else {
     // ---- forward raw Chimera
@@ -739,39 +789,60 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
     const real jx = c[E(1, 0, 0)], jy = c[E(0, 1, 0)];
     real jz = real(0);
     if constexpr (S::D == 3) jz = c[E(0, 0, 1)];
-    const real ux = jx * inv, uy = jy * inv, uz = jz * inv;
+    real ux = jx * inv, uy = jy * inv, uz = jz * inv;
+    if constexpr (FORCED) {  // u = (j + F/2) / rho
+      ux = fma(real(0.5) * fr.F[0], inv, ux);
+      uy = fma(real(0.5) * fr.F[1], inv, uy);
+      uz = fma(real(0.5) * fr.F[2], inv, uz);
+    }
     if constexpr (REG == REG_ZC_ABS) {  // q = T(df + f0): add m0 = M f0
       add_background<NC>(c, real(1));
       c[0] = rho;
     }
+    // source term q^F = (I - S/2) T(F^G) added after relaxation (FORCED only)
+    auto add_force = [&](auto central) {
+      real s[NC];
+      guo_cube<S>(s, fr, ux, uy, uz);
+      if constexpr (S::D == 3) fwd_raw3<S>(s); else fwd_raw2(s);
+      if constexpr (decltype(central)::value) {
+        if constexpr (S::D == 3) bin_fwd3(s, ux, uy, uz); else bin_fwd2(s, ux, uy);
+      }
+      EqZeroAll<real> z;
+      if constexpr (S::D == 3) relax_basis3<S, RSR>(s, z, fr.half); else relax_basis2<RSR>(s, z, fr.half);
+      sfor<NC>([&](auto e) { c[e] += s[e]; });
+    };
 
     if constexpr (SPACE == SPACE_RAW) {
       RawU<real> U{ux, uy, uz, ux * ux, uy * uy, uz * uz};
       if constexpr (REG == REG_DELTA) {
         EqRawDelta<real> eq{m000, rho, U};
-        if constexpr (S::D == 3) relax_basis3<S, RS>(c, eq, r); else relax_basis2<RS>(c, eq, r);
+        if constexpr (S::D == 3) relax_basis3<S, RSR>(c, eq, r); else relax_basis2<RSR>(c, eq, r);
       } else {
         EqRawAbs<real> eq{rho, U};
-        if constexpr (S::D == 3) relax_basis3<S, RS>(c, eq, r); else relax_basis2<RS>(c, eq, r);
+        if constexpr (S::D == 3) relax_basis3<S, RSR>(c, eq, r); else relax_basis2<RSR>(c, eq, r);
       }
+      if constexpr (FORCED) add_force(std::false_type{});
     } else {
       // ---- raw -> central (binomial Chimera)
       if constexpr (S::D == 3) bin_fwd3(c, ux, uy, uz); else bin_fwd2(c, ux, uy);
       if constexpr (REG != REG_DELTA) {
-        // collapse conserved central moments: kappa_000 = rho, kappa_100 = 0
+        // collapse conserved central moments: kappa_000 = rho, kappa_100 = -F_x/2 (= 0 without a
+        // force)
         c[0] = rho;
-        c[E(1, 0, 0)] = real(0);
-        c[E(0, 1, 0)] = real(0);
-        if constexpr (S::D == 3) c[E(0, 0, 1)] = real(0);
+        c[E(1, 0, 0)] = FORCED ? real(-0.5) * fr.F[0] : real(0);
+        c[E(0, 1, 0)] = FORCED ? real(-0.5) * fr.F[1] : real(0);
+        if constexpr (S::D == 3) c[E(0, 0, 1)] = FORCED ? real(-0.5) * fr.F[2] : real(0);
       }
       if constexpr (SPACE == SPACE_CENTRAL) {
         if constexpr (REG == REG_DELTA) {
           EqCentralDelta<real> eq{m000, CentralV<real>{ux, uy, uz, ux * ux, uy * uy, uz * uz}};
-          if constexpr (S::D == 3) relax_basis3<S, RS>(c, eq, r); else relax_basis2<RS>(c, eq, r);
+          if constexpr (S::D == 3) relax_basis3<S, RSR>(c, eq, r); else relax_basis2<RSR>(c, eq, r);
         } else {
           EqCentralAbs<real> eq{rho};
-          if constexpr (S::D == 3) relax_basis3<S, RS>(c, eq, r); else relax_basis2<RS>(c, eq, r);
+          if constexpr (S::D == 3) relax_basis3<S, RSR>(c, eq, r); else relax_basis2<RSR>(c, eq, r);
         }
+        // kappa*_100 = kappa_100 + F_x: -F_x/2 -> +F_x/2
+        if constexpr (FORCED) add_force(std::true_type{});
       } else if constexpr (SPACE == SPACE_SWE) {
         // kappa_eq = K(u) f_eq of Zhou's discrete equilibrium
         static_assert(S::Q == 9, "SWE is D2Q9");
@@ -792,25 +863,26 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
         });
         fwd_raw2(eq.v);
         bin_fwd2(eq.v, ux, uy);
-        relax_basis2<RS>(c, eq, r);
+        relax_basis2<RSR>(c, eq, r);
       } else {  // SPACE_CUMULANT
         if constexpr (S::D == 3) central_to_cumulant3<S>(c, inv); else central_to_cumulant2(c, inv);
         // C_eq = rho cs2 on the diagonal: cs2 = 1/3, or g h / 2 for shallow water (h = rho)
         real cs2 = real(1.0 / 3.0);
         if constexpr (SPACE == SPACE_SWE_K) cs2 = real(0.5) * swe_g * rho;
         EqCumulant<real> eq{rho * cs2};
-        if constexpr (S::D == 3) relax_basis3<S, RS>(c, eq, r); else relax_basis2<RS>(c, eq, r);
+        if constexpr (S::D == 3) relax_basis3<S, RSR>(c, eq, r); else relax_basis2<RSR>(c, eq, r);
         if constexpr (S::D == 3) cumulant_to_central3<S>(c, inv); else cumulant_to_central2(c, inv);
       }
       // ---- central -> raw
       if constexpr (S::D == 3) bin_bwd3(c, ux, uy, uz); else bin_bwd2(c, ux, uy);
     }
     if constexpr (REG == REG_ZC_ABS) add_background<NC>(c, real(-1));
-    // conserved raw moments pass through unchanged
+    // conserved raw moments pass through unchanged, the momentum gains the
+    // force: m*_100 = rho u_x + F_x/2 = j_x + F_x
     c[0] = m000;
-    c[E(1, 0, 0)] = jx;
-    c[E(0, 1, 0)] = jy;
-    if constexpr (S::D == 3) c[E(0, 0, 1)] = jz;
+    c[E(1, 0, 0)] = FORCED ? jx + fr.F[0] : jx;
+    c[E(0, 1, 0)] = FORCED ? jy + fr.F[1] : jy;
+    if constexpr (S::D == 3) c[E(0, 0, 1)] = FORCED ? jz + fr.F[2] : jz;
     // ---- backward raw transform
     if constexpr (S::Q == 27) bwd_raw3_full(c);
     else if constexpr (S::Q == 19) bwd_raw3_d3q19(c);

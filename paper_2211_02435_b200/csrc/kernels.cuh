@@ -42,7 +42,8 @@ __device__ __forceinline__ real ld_nc(const real *p) { return __ldg(p); }
 // ---------------------------------------------------------------------------
 template <class S, int SPACE, int REG, class real, bool BB, int RS = RS_GENERAL>
 __global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, real *__restrict__ dst,
-                                                   const GridParams g, const Rates<real> r, const real swe_g) {
+                                                   const GridParams g, const Rates<real> r, const real swe_g,
+                                                   const Force<real> fr) {
   const int x = blockIdx.x * BLOCK_X + threadIdx.x;
   if (x >= g.nx) return;
   const int y = blockIdx.y;
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, 
     }
   });
 
-  collide<S, SPACE, REG, real, RS>(f, r, swe_g);
+  collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
 
   sfor<S::Q>([&](auto i) { dst[own + (long long)i * g.pop] = f[i]; });
 }
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, 
 // at 5 blocks/SM (96 registers, 4 B spill) beats 123 registers at 4 blocks (+3 %, B200).
 template <class S, int SPACE, int REG, class real, int PAT, int RS = RS_GENERAL>
 __global__ void __launch_bounds__(BLOCK_X, (PAT == PAT_AA_ODD ? 5 : 1))
-    k_aa(real *mem, const GridParams g, const Rates<real> r, const real swe_g) {
+    k_aa(real *mem, const GridParams g, const Rates<real> r, const real swe_g, const Force<real> fr) {
   const int x = blockIdx.x * BLOCK_X + threadIdx.x;
   if (x >= g.nx) return;
   const int y = blockIdx.y;
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(BLOCK_X, (PAT == PAT_AA_ODD ? 5 : 1))
     const long long own = (long long)(zl + 1) * g.plane + (long long)y * g.pitch + x;
     // read-only path is safe in place: every slot is read, then written, by the same thread
     sfor<S::Q>([&](auto i) { f[i] = ld_nc(mem + own + (long long)i * g.pop); });
-    collide<S, SPACE, REG, real, RS>(f, r, swe_g);
+    collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
     sfor<S::Q>([&](auto i) { mem[own + (long long)S::opp(i) * g.pop] = f[i]; });
   } else {
     int xs[3], ys[3];
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(BLOCK_X, (PAT == PAT_AA_ODD ? 5 : 1))
       constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
       f[i] = ld_nc(mem + zo[1 - cz] + (long long)S::opp(i) * g.pop + ys[1 - cy] + xs[1 - cx]);
     });
-    collide<S, SPACE, REG, real, RS>(f, r, swe_g);
+    collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
     // write f*_i(x) to mem(x + xi_i, i)
     sfor<S::Q>([&](auto i) {
       constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
@@ -194,10 +195,11 @@ __global__ void k_set_populations(real *mem, const GridParams g, int aa, const d
   sfor<S::Q>([&](auto i) { mem[Canon<S>::template at<i>(g, x, y, zl, aa, 0)] = (real)in[i * ncell + cell]; });
 }
 
-// rho = rho0 + sum df (zc) or sum f; u = sum f xi / rho
+// rho = rho0 + sum df (zc) or sum f; u = (sum f xi + dj) / rho;
+// dj = -F/2 for the post-collision state of a forced method (reading R23), else 0
 template <class S, class real>
 __global__ void k_macroscopic(const real *mem, const GridParams g, int aa, int state, int zc,
-                              double *__restrict__ rho, double *__restrict__ u) {
+                              double *__restrict__ rho, double *__restrict__ u, const double3 dj) {
   const int x = blockIdx.x * BLOCK_X + threadIdx.x;
   if (x >= g.nx) return;
   const int y = blockIdx.y, zl = blockIdx.z;
@@ -213,19 +215,19 @@ __global__ void k_macroscopic(const real *mem, const GridParams g, int aa, int s
   });
   const double r = zc ? 1.0 + s : s;
   rho[cell] = r;
-  u[cell] = jx / r;
-  u[ncell + cell] = jy / r;
-  if constexpr (S::D == 3) u[2 * ncell + cell] = jz / r;
+  u[cell] = (jx + dj.x) / r;
+  u[ncell + cell] = (jy + dj.y) / r;
+  if constexpr (S::D == 3) u[2 * ncell + cell] = (jz + dj.z) / r;
 }
 
 template <class S, int SPACE, int REG, class real, int RS = RS_GENERAL>
 __global__ void k_test_collide(const double *__restrict__ fin, double *__restrict__ fout, long long n,
-                               const Rates<real> r, real swe_g) {
+                               const Rates<real> r, real swe_g, const Force<real> fr) {
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   real f[S::Q];
   sfor<S::Q>([&](auto i) { f[i] = (real)fin[c * S::Q + i]; });
-  collide<S, SPACE, REG, real, RS>(f, r, swe_g);
+  collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
   sfor<S::Q>([&](auto i) { fout[c * S::Q + i] = (double)f[i]; });
 }
 
@@ -235,7 +237,8 @@ __global__ void k_test_collide(const double *__restrict__ fin, double *__restric
 constexpr int DIAG_BLOCK = 256, DIAG_GRID = 1184;  // 148 SMs x 8
 template <class S, class real>
 __global__ void __launch_bounds__(DIAG_BLOCK) k_diag_partial(const real *mem, const GridParams g, int aa, int state,
-                                                             int zc, double *__restrict__ partial) {
+                                                             int zc, double *__restrict__ partial,
+                                                             const double3 dj) {
   const long long n = (long long)g.nx * g.ny * g.nzl;
   double acc[5] = {0, 0, 0, 0, 0};
   for (long long c = (long long)blockIdx.x * DIAG_BLOCK + threadIdx.x; c < n; c += (long long)DIAG_GRID * DIAG_BLOCK) {
@@ -251,6 +254,9 @@ __global__ void __launch_bounds__(DIAG_BLOCK) k_diag_partial(const real *mem, co
       if constexpr (S::vz(i) != 0) jz += S::vz(i) * v;
     });
     const double r = zc ? 1.0 + s : s;
+    jx += dj.x;
+    jy += dj.y;
+    jz += dj.z;
     acc[0] += r;
     acc[1] += jx;
     acc[2] += jy;

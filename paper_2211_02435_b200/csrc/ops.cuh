@@ -9,28 +9,37 @@
 
 namespace lbm {
 
+// Method parameters of the collision, in the storage precision (host blob, copied into
+// the kernel parameters at launch).
+template <class real>
+struct MethodParams {
+  Rates<real> rates;
+  Force<real> force;  // used by the RS_FORCE instantiations only
+};
+
 struct Ops {
   int q, d;
   // pull stream–collide of planes [zbegin, zbegin + nplanes) from src into dst
-  void (*pull)(const void *src, void *dst, const GridParams &g, const void *rates, double swe_g, int bb,
+  void (*pull)(const void *src, void *dst, const GridParams &g, const void *params, double swe_g, int bb,
                int nplanes, cudaStream_t s);
   // AA step (pattern PAT_AA_EVEN / PAT_AA_ODD) in place, planes [zbegin, zbegin + nplanes)
-  void (*aa)(void *mem, const GridParams &g, const void *rates, double swe_g, int pattern, int nplanes,
+  void (*aa)(void *mem, const GridParams &g, const void *params, double swe_g, int pattern, int nplanes,
              cudaStream_t s);
   void (*init)(void *mem, const GridParams &g, int aa, const double *rho, const double *u, double swe_g,
                cudaStream_t s);
   void (*get_pop)(const void *mem, const GridParams &g, int aa, int state, double *out, cudaStream_t s);
   void (*set_pop)(void *mem, const GridParams &g, int aa, const double *in, cudaStream_t s);
+  // dj: momentum correction of the post-collision state (-F/2 with a body force)
   void (*macro)(const void *mem, const GridParams &g, int aa, int state, int zc, double *rho, double *u,
-                cudaStream_t s);
-  void (*test_collide)(const double *fin, double *fout, long long n, const void *rates, double swe_g,
+                double3 dj, cudaStream_t s);
+  void (*test_collide)(const double *fin, double *fout, long long n, const void *params, double swe_g,
                        cudaStream_t s);
   void (*check_finite)(const void *mem, const GridParams &g, int *flag, cudaStream_t s);
   void (*get_cells)(const void *mem, const GridParams &g, int aa, int state, const long long *idx, long long n,
                     double *out, cudaStream_t s);
   // global sums (mass, momentum, kinetic energy): partial[5 * DIAG_GRID] scratch, out[5]
   void (*diagnostics)(const void *mem, const GridParams &g, int aa, int state, int zc, double *partial,
-                      double *out, cudaStream_t s);
+                      double *out, double3 dj, cudaStream_t s);
   // kernel attributes of the pull kernel (registers / local memory), for diagnostics
   void (*attributes)(int *regs, int *local_bytes);
 };
@@ -41,27 +50,27 @@ inline dim3 cell_grid(const GridParams &g, int nplanes) {
 
 template <class S, int SPACE, int REG, class real, int RS = RS_GENERAL>
 struct OpsImpl {
-  static void pull(const void *src, void *dst, const GridParams &g, const void *rates, double swe_g, int bb,
+  static void pull(const void *src, void *dst, const GridParams &g, const void *params, double swe_g, int bb,
                    int nplanes, cudaStream_t s) {
     if (nplanes <= 0) return;
-    const Rates<real> &r = *static_cast<const Rates<real> *>(rates);
+    const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
     if (bb)
       k_pull<S, SPACE, REG, real, true, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
-          static_cast<const real *>(src), static_cast<real *>(dst), g, r, (real)swe_g);
+          static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
     else
       k_pull<S, SPACE, REG, real, false, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
-          static_cast<const real *>(src), static_cast<real *>(dst), g, r, (real)swe_g);
+          static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
   }
-  static void aa(void *mem, const GridParams &g, const void *rates, double swe_g, int pattern, int nplanes,
+  static void aa(void *mem, const GridParams &g, const void *params, double swe_g, int pattern, int nplanes,
                  cudaStream_t s) {
     if (nplanes <= 0) return;
-    const Rates<real> &r = *static_cast<const Rates<real> *>(rates);
+    const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
     if (pattern == PAT_AA_EVEN)
-      k_aa<S, SPACE, REG, real, PAT_AA_EVEN, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(static_cast<real *>(mem),
-                                                                                        g, r, (real)swe_g);
+      k_aa<S, SPACE, REG, real, PAT_AA_EVEN, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
+          static_cast<real *>(mem), g, p.rates, (real)swe_g, p.force);
     else
-      k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(static_cast<real *>(mem),
-                                                                                       g, r, (real)swe_g);
+      k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
+          static_cast<real *>(mem), g, p.rates, (real)swe_g, p.force);
   }
   static void init(void *mem, const GridParams &g, int aa, const double *rho, const double *u, double swe_g,
                    cudaStream_t s) {
@@ -76,16 +85,17 @@ struct OpsImpl {
     k_set_populations<S, real><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<real *>(mem), g, aa, in);
   }
   static void macro(const void *mem, const GridParams &g, int aa, int state, int zc, double *rho, double *u,
-                    cudaStream_t s) {
+                    double3 dj, cudaStream_t s) {
     k_macroscopic<S, real><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<const real *>(mem), g, aa, state,
-                                                                   zc, rho, u);
+                                                                   zc, rho, u, dj);
   }
-  static void test_collide(const double *fin, double *fout, long long n, const void *rates, double swe_g,
+  static void test_collide(const double *fin, double *fout, long long n, const void *params, double swe_g,
                            cudaStream_t s) {
     if (n <= 0) return;
-    const Rates<real> &r = *static_cast<const Rates<real> *>(rates);
+    const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
     const int B = 128;
-    k_test_collide<S, SPACE, REG, real, RS><<<(unsigned)((n + B - 1) / B), B, 0, s>>>(fin, fout, n, r, (real)swe_g);
+    k_test_collide<S, SPACE, REG, real, RS><<<(unsigned)((n + B - 1) / B), B, 0, s>>>(fin, fout, n, p.rates,
+                                                                                     (real)swe_g, p.force);
   }
   static void check_finite(const void *mem, const GridParams &g, int *flag, cudaStream_t s) {
     k_check_finite<S, real><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<const real *>(mem), g, flag);
@@ -97,9 +107,9 @@ struct OpsImpl {
                                                                       idx, n, out);
   }
   static void diagnostics(const void *mem, const GridParams &g, int aa, int state, int zc, double *partial,
-                          double *out, cudaStream_t s) {
+                          double *out, double3 dj, cudaStream_t s) {
     k_diag_partial<S, real><<<DIAG_GRID, DIAG_BLOCK, 0, s>>>(static_cast<const real *>(mem), g, aa, state, zc,
-                                                             partial);
+                                                             partial, dj);
     k_diag_final<double><<<1, DIAG_BLOCK, 0, s>>>(partial, out);
   }
   static void attributes(int *regs, int *local_bytes) {
@@ -113,7 +123,7 @@ struct OpsImpl {
     }
   }
   static constexpr Ops table{S::Q,      S::D,  &pull,         &aa,           &init,      &get_pop,
-                             &set_pop, &macro, &test_collide, &check_finite, &get_cells,   &diagnostics,
+                             &set_pop, &macro, &test_collide, &check_finite, &get_cells, &diagnostics,
                              &attributes};
 };
 

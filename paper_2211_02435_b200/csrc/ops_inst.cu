@@ -24,6 +24,11 @@ constexpr int SP = LBM_SPACE;
 namespace lbm {
 template <class St_, int SP_, int REG_, class Re_>
 const Ops *with_rs(int rs) {
+  // body force (Guo, reading R23): population, raw and central-moment collisions
+  if constexpr (SP_ == SPACE_POPULATION || SP_ == SPACE_RAW || SP_ == SPACE_CENTRAL) {
+    if (rs == (RS_GENERAL | RS_FORCE)) return &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL | RS_FORCE>::table;
+  }
+  if (rs & RS_FORCE) return nullptr;
   if constexpr (SP_ == SPACE_POPULATION) {
     return rs == RS_GENERAL ? &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL>::table : nullptr;
   } else {

@@ -84,7 +84,11 @@ struct lbm_ctx {
   int cur = 0;       // pull: index of the current grid
   int aa_state = 0;  // AA: 0 = state A, 1 = state B
   long long steps = 0;
-  alignas(16) unsigned char rates[27 * 8];
+  alignas(16) unsigned char params[sizeof(lbm::MethodParams<double>)];  // MethodParams<real>
+  double rates_d[27] = {0};
+  double force[3] = {0, 0, 0};
+  bool forced = false;
+  const Ops *ops_plain = nullptr;  // the unforced kernels chosen at create
   double swe_g = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -137,6 +141,28 @@ long long local_cells(const lbm_ctx *c) { return (long long)c->g.nx * c->g.ny * 
 void *grid_ptr(lbm_ctx *c, int which) {
   if (c->streaming == LBM_AA) return c->buf[0];
   return c->buf[which == 0 ? c->cur : 1 - c->cur];
+}
+
+// the kernels' method parameters in the storage precision
+template <class real>
+void fill_params_t(lbm_ctx *c) {
+  lbm::MethodParams<real> p{};
+  for (int i = 0; i < 27; ++i) {
+    p.rates.w[i] = (real)c->rates_d[i];
+    p.force.half.w[i] = (real)(0.5 * c->rates_d[i]);
+  }
+  for (int a = 0; a < 3; ++a) p.force.F[a] = (real)c->force[a];
+  std::memcpy(c->params, &p, sizeof(p));
+}
+void fill_params(lbm_ctx *c) {
+  if (c->esize == 8) fill_params_t<double>(c);
+  else fill_params_t<float>(c);
+}
+
+// momentum correction of the canonical post-collision state: u = (j - F/2) / rho
+double3 post_shift(const lbm_ctx *c) {
+  if (!c->forced) return make_double3(0, 0, 0);
+  return make_double3(-0.5 * c->force[0], -0.5 * c->force[1], -0.5 * c->force[2]);
 }
 
 }  // namespace
@@ -353,14 +379,10 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   g.bcmask = mask;
   c->bb = mask != 0;
 
-  // rates in the storage precision
-  if (c->esize == 8) {
-    double *r = reinterpret_cast<double *>(c->rates);
-    for (int i = 0; i < 27; ++i) r[i] = (i < n_rates) ? relaxation_rates[i] : 0.0;
-  } else {
-    float *r = reinterpret_cast<float *>(c->rates);
-    for (int i = 0; i < 27; ++i) r[i] = (i < n_rates) ? (float)relaxation_rates[i] : 0.0f;
-  }
+  // rates (and a zero force) in the storage precision
+  for (int i = 0; i < 27; ++i) c->rates_d[i] = (i < n_rates) ? relaxation_rates[i] : 0.0;
+  c->ops_plain = ops;
+  fill_params(c);
 
   auto bail = [&](lbm_status s) {
     g_create_error = c->err;
@@ -455,10 +477,10 @@ lbm_status lbm_step(lbm_ctx *c, int n) {
   for (int t = 0; t < n; ++t) {
     if (c->streaming == LBM_AA) {
       const int pat = (c->aa_state == 0) ? lbm::PAT_AA_ODD : lbm::PAT_AA_EVEN;
-      c->ops->aa(c->buf[0], g, c->rates, c->swe_g, pat, g.nzl, c->stream);
+      c->ops->aa(c->buf[0], g, c->params, c->swe_g, pat, g.nzl, c->stream);
       c->aa_state ^= 1;
     } else {
-      c->ops->pull(c->buf[c->cur], c->buf[1 - c->cur], g, c->rates, c->swe_g, c->bb, g.nzl, c->stream);
+      c->ops->pull(c->buf[c->cur], c->buf[1 - c->cur], g, c->params, c->swe_g, c->bb, g.nzl, c->stream);
       c->cur ^= 1;
     }
     c->steps++;
@@ -477,9 +499,9 @@ lbm_status lbm_step_region(lbm_ctx *c, lbm_region region, void *stream) {
     g.zbegin = z0;
     if (c->streaming == LBM_AA) {
       const int pat = (c->aa_state == 0) ? lbm::PAT_AA_ODD : lbm::PAT_AA_EVEN;
-      c->ops->aa(c->buf[0], g, c->rates, c->swe_g, pat, np, s);
+      c->ops->aa(c->buf[0], g, c->params, c->swe_g, pat, np, s);
     } else {
-      c->ops->pull(c->buf[c->cur], c->buf[1 - c->cur], g, c->rates, c->swe_g, c->bb, np, s);
+      c->ops->pull(c->buf[c->cur], c->buf[1 - c->cur], g, c->params, c->swe_g, c->bb, np, s);
     }
   };
   switch (region) {
@@ -540,7 +562,7 @@ lbm_status lbm_get_macroscopic(lbm_ctx *c, double *rho, double *u) {
   double *dr = static_cast<double *>(c->staging);
   double *du = dr + n;
   const int aa = c->streaming == LBM_AA;
-  c->ops->macro(grid_ptr(c, 0), c->g, aa, c->aa_state, c->zc, dr, du, c->stream);
+  c->ops->macro(grid_ptr(c, 0), c->g, aa, c->aa_state, c->zc, dr, du, post_shift(c), c->stream);
   s = check_launch(c, "k_macroscopic");
   if (s != LBM_OK) return s;
   LBM_CUDA(c, cudaMemcpyAsync(rho, dr, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -565,6 +587,28 @@ lbm_status lbm_get_populations(lbm_ctx *c, double *f) {
   return LBM_OK;
 }
 
+lbm_status lbm_set_force(lbm_ctx *c, const double *force) {
+  if (!c || !force) return fail(c, LBM_EINVAL, "null argument");
+  for (int a = 0; a < 3; ++a)
+    if (!std::isfinite(force[a])) return fail(c, LBM_EINVAL, "non-finite force");
+  if (c->d == 2 && force[2] != 0.0) return fail(c, LBM_EINVAL, "a D2Q9 force has no z component");
+  const bool any = force[0] != 0.0 || force[1] != 0.0 || force[2] != 0.0;
+  if (any) {
+    if (!(c->kspace == LBM_SPACE_POPULATION || c->kspace == LBM_SPACE_RAW || c->kspace == LBM_SPACE_CENTRAL))
+      return fail(c, LBM_EUNSUPPORTED,
+                  "a body force is provided for population, raw- and central-moment collisions (reading R23)");
+    const Ops *f = find_ops(c->stencil, c->prec, c->kspace, c->regime, lbm::RS_GENERAL | lbm::RS_FORCE);
+    if (!f) return fail(c, LBM_EUNSUPPORTED, "no forced kernel instantiated for this combination");
+    c->ops = f;
+  } else {
+    c->ops = c->ops_plain;
+  }
+  for (int a = 0; a < 3; ++a) c->force[a] = force[a];
+  c->forced = any;
+  fill_params(c);
+  return LBM_OK;
+}
+
 lbm_status lbm_get_diagnostics(lbm_ctx *c, lbm_diagnostics *out) {
   if (!c || !out) return fail(c, LBM_EINVAL, "null argument");
   LBM_CUDA(c, cudaSetDevice(c->device));
@@ -573,7 +617,8 @@ lbm_status lbm_get_diagnostics(lbm_ctx *c, lbm_diagnostics *out) {
   if (s != LBM_OK) return s;
   double *partial = static_cast<double *>(c->staging);
   double *dout = partial + 5 * lbm::DIAG_GRID;
-  c->ops->diagnostics(grid_ptr(c, 0), c->g, c->streaming == LBM_AA, c->aa_state, c->zc, partial, dout, c->stream);
+  c->ops->diagnostics(grid_ptr(c, 0), c->g, c->streaming == LBM_AA, c->aa_state, c->zc, partial, dout,
+                      post_shift(c), c->stream);
   s = check_launch(c, "k_diag");
   if (s != LBM_OK) return s;
   double h[5];
@@ -651,7 +696,7 @@ lbm_status lbm_test_collide(lbm_ctx *c, const double *f_in, double *f_out, long 
   double *din = static_cast<double *>(c->staging);
   double *dout = din + (size_t)n_cells * c->q;
   LBM_CUDA(c, cudaMemcpyAsync(din, f_in, bytes, cudaMemcpyHostToDevice, c->stream));
-  c->ops->test_collide(din, dout, n_cells, c->rates, c->swe_g, c->stream);
+  c->ops->test_collide(din, dout, n_cells, c->params, c->swe_g, c->stream);
   s = check_launch(c, "k_test_collide");
   if (s != LBM_OK) return s;
   LBM_CUDA(c, cudaMemcpyAsync(f_out, dout, bytes, cudaMemcpyDeviceToHost, c->stream));

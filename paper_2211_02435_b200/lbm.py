@@ -88,6 +88,7 @@ SIGNATURES = [
     ("lbm_set_populations", ctypes.c_int, [_vp, _dp]),
     ("lbm_get_cells", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_longlong), ctypes.c_longlong, _dp]),
     ("lbm_get_diagnostics", ctypes.c_int, [_vp, ctypes.POINTER(lbm_diagnostics)]),
+    ("lbm_set_force", ctypes.c_int, [_vp, _dp]),
     ("lbm_check_finite", ctypes.c_int, [_vp]),
     ("lbm_test_collide", ctypes.c_int, [_vp, _dp, _dp, ctypes.c_longlong]),
     ("lbm_stencil_info", ctypes.c_int, [ctypes.c_int, _ip, _ip, _ip]),
@@ -261,6 +262,12 @@ class Lattice:
         f = np.empty((self.q,) + self.local_shape)
         _check(lib().lbm_get_populations(self._ctx, _d(f)), self._ctx)
         return f
+
+    def set_force(self, force):
+        """Uniform body force density (Guo forcing, include/lbm.h lbm_set_force)."""
+        F = np.ascontiguousarray(np.asarray(force, dtype=np.float64).reshape(-1))
+        F = np.concatenate([F, np.zeros(3 - F.size)]) if F.size < 3 else F
+        _check(lib().lbm_set_force(self._ctx, _d(np.ascontiguousarray(F))), self._ctx)
 
     def get_diagnostics(self):
         """dict(mass, momentum[3], kinetic_energy) of this slab (device sums, fp64)."""

@@ -502,6 +502,71 @@ def test_tgv_energy_decay(space, eq, zc, nu):
     assert abs(ratio / ref - 1) < 1e-2, (ratio, ref)
 
 
+FORCE = np.array([2e-4, -1e-4, 3e-4])
+
+
+@pytest.mark.parametrize("st", STENCILS)
+@pytest.mark.parametrize("space", [W.POPULATION, W.RAW, W.CENTRAL])
+def test_force_momentum_and_paper_example(st, space):
+    """Body force (reading R23): per cell the mass is unchanged and the momentum gains F;
+    written as the paper's worked example: with u = (j + F/2)/rho the
+    post-collision first-order raw moment is m*_{10|0} = rho u_x + F_x / 2."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    F = FORCE.copy()
+    if W.DIM_OF[st] == 2:
+        F[2] = 0
+    fa = random_cells(st, 20)
+    rho = fa.sum(1)
+    u = (fa @ xi + F / 2) / rho[:, None]  # pre-collision velocity with the half-force shift
+    for eq, zc in admissible(space):
+        fin = fa - w if zc else fa
+        fo = oracle.collide(st, space, eq, zc, rates_for(st, space), fin, force=F)
+        fo_abs = fo + w if zc else fo
+        np.testing.assert_allclose(fo_abs.sum(1), rho, atol=1e-15)
+        np.testing.assert_allclose(fo_abs @ xi, rho[:, None] * u + F / 2, atol=1e-16)
+    with pytest.raises(RuntimeError):
+        oracle.collide(st, W.CUMULANT, W.EQ_ABSOLUTE, 1, rates_for(st, W.CUMULANT), fa - w, force=F)
+
+
+@pytest.mark.parametrize("st", STENCILS)
+@pytest.mark.parametrize("space", [W.POPULATION, W.RAW, W.CENTRAL])
+def test_force_isotropy(st, space):
+    """Rotating the cell and the force together commutes with the forced collision."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    F = FORCE.copy()
+    if W.DIM_OF[st] == 2:
+        F[2] = 0
+    fa = random_cells(st, 8)
+    rates = np.array([1.3]) if space == W.POPULATION else W.rate_set_p(st)
+    out = oracle.collide(st, space, W.EQ_DELTA, 1, rates, fa - w, force=F)
+    for P in symmetry_generators(W.DIM_OF[st]):
+        img = xi @ P.T
+        perm = [int(np.flatnonzero((xi == img[i]).all(1))[0]) for i in range(len(w))]
+        rot_in = np.empty_like(fa)
+        rot_in[:, perm] = fa - w
+        rot_out = oracle.collide(st, space, W.EQ_DELTA, 1, rates, rot_in, force=P @ F)
+        np.testing.assert_allclose(rot_out[:, perm], out, atol=2e-16)
+
+
+@pytest.mark.parametrize("space,nu", [(W.POPULATION, 1 / 6), (W.RAW, 0.1), (W.CENTRAL, 0.05)])
+def test_poiseuille_flow(space, nu):
+    """Force-driven channel between half-way bounce-back walls (readings R18, R23): the steady
+    profile is u_x(y) = F / (2 nu) (y + 1/2)(H - 1/2 - y) (walls half a node outside)."""
+    st, nx, ny, Fx = W.D2Q9, 4, 24, 1e-6
+    om = W.omega_from_nu(nu)
+    rates = [om] if space == W.POPULATION else W.regularized_rates(st, om)
+    bc = [[W.PERIODIC, W.PERIODIC], [W.NOSLIP, W.NOSLIP], [W.PERIODIC, W.PERIODIC]]
+    sim = oracle.Sim(st, space, W.EQ_DELTA, 1, rates, (nx, ny, 1), bc=bc)
+    sim.set(np.zeros((9, 1, ny, nx)))
+    sim.set_force([Fx, 0, 0])
+    sim.step(int(8 * ny * ny / nu))
+    r, u = sim.macroscopic()
+    y = np.arange(ny)
+    ref = Fx / (2 * nu) * (y + 0.5) * (ny - 0.5 - y)
+    assert np.abs(u[0, 0, :, 0] - ref).max() < 1e-2 * ref.max()
+    assert np.abs(u[1]).max() < 1e-12 * ref.max()
+
+
 def test_shear_wave_between_walls():
     """Bounce-back pin (reading R18): u_x(y) = u0 sin(pi (y+1/2)/ny) between no-slip
     walls decays as exp(-nu (pi/ny)^2 t)."""
