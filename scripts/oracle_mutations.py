@@ -32,8 +32,13 @@ MUTANTS = [
      "for (int k = 0; k < 27; ++k) acc.c[k] += pw.c[k];"),
     ("e! factor: 2! -> 1", "static int efact(int e) { return e == 2 ? 2 : 1; }", "static int efact(int e) { return 1; }"),
     ("central moments: xi + u", "s += f[i] * ipow(R(m.xi[i][0]) - u[0], e[0])", "s += f[i] * ipow(R(m.xi[i][0]) + u[0], e[0])"),
-    ("relaxation sign", "qs[p] = q0[p] + m.omega[p] * (qeq[p] - q0[p]);\n    matvec(q, m.Minv.data(), qs, fout);",
-     "qs[p] = q0[p] - m.omega[p] * (qeq[p] - q0[p]);\n    matvec(q, m.Minv.data(), qs, fout);"),
+    ("relaxation sign (raw)", "qs[p] = q0[p] + m.omega[p] * (qeq[p] - q0[p]) + (R(1) - m.omega[p] / R(2)) * qF[p];\n"
+     "    matvec(q, m.Minv", "qs[p] = q0[p] - m.omega[p] * (qeq[p] - q0[p]) + (R(1) - m.omega[p] / R(2)) * qF[p];\n"
+     "    matvec(q, m.Minv"),
+    ("force: drop the (1 - w/2) factor (raw)", "+ (R(1) - m.omega[p] / R(2)) * qF[p];\n    matvec(q, m.Minv",
+     "+ qF[p];\n    matvec(q, m.Minv"),
+    ("force: no half-force velocity shift", "u[a] = (j[a] + R(half) * m.F[a] / R(2)) / rho;", "u[a] = j[a] / rho;"),
+    ("force: 9 -> 3 in the Guo term", "R(3) * xF + R(9) * xu * xF - R(3) * uF", "R(3) * xF + R(3) * xu * xF - R(3) * uF"),
     ("cumulant eq: C_eq on xy instead of the diagonal",
      "(t.e[0] == 2 || t.e[1] == 2 || t.e[2] == 2)", "(t.e[0] == 1 || t.e[1] == 2 || t.e[2] == 2)"),
     ("zc: forget to add f0 for the absolute equilibrium",
@@ -44,8 +49,8 @@ MUTANTS = [
     ("SWE: printed -u.u/3 (the garble of Eq. 5.3)", "+ xu * xu / R(2) - uu / R(6));", "+ xu * xu / R(2) - uu / R(3));"),
     ("SWE cumulant: cs2 = g h", "const R cs2 = (m.eq == EQ_SWE) ? m.g * rho / R(2) : R(CS2);\n  for",
      "const R cs2 = (m.eq == EQ_SWE) ? m.g * rho : R(CS2);\n  for"),
-    ("velocity: u = j (no division by rho)", "for (int a = 0; a < 3; ++a) u[a] = j[a] / rho;",
-     "for (int a = 0; a < 3; ++a) u[a] = j[a];"),
+    ("velocity: u = j (no division by rho)", "u[a] = (j[a] + R(half) * m.F[a] / R(2)) / rho;",
+     "u[a] = (j[a] + R(half) * m.F[a] / R(2));"),
     ("stencil order: swap (1,1) and (-1,-1) in-plane", "{1, 1}, {-1, -1}, {1, -1}, {-1, 1}};",
      "{-1, -1}, {1, 1}, {1, -1}, {-1, 1}};"),
 ]
