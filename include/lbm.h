@@ -86,7 +86,9 @@ typedef enum {
                           PAPER.md:1023-1026)                                                          */
 } lbm_equilibrium;
 typedef enum { LBM_FP64 = 0, LBM_FP32 = 1 } lbm_precision;
-typedef enum { LBM_PULL = 0, LBM_AA = 1 } lbm_streaming;
+/* Streaming patterns: two-grid pull; in place: AA (Bailey 2009; single or
+   several ranks, periodic) and Esoteric Pull (Lehmann 2022; single rank, periodic). */
+typedef enum { LBM_PULL = 0, LBM_AA = 1, LBM_ESOTERIC_PULL = 2 } lbm_streaming;
 typedef enum { LBM_BC_PERIODIC = 0, LBM_BC_NOSLIP = 1 } lbm_bc;
 typedef enum { LBM_REGION_ALL = 0, LBM_REGION_BOUNDARY = 1, LBM_REGION_INTERIOR = 2 } lbm_region;
 

@@ -133,20 +133,81 @@ __global__ void __launch_bounds__(BLOCK_X, (PAT == PAT_AA_ODD ? 5 : 1))
 }
 
 // ---------------------------------------------------------------------------
+// Esoteric Pull (Lehmann 2022, cited at PAPER.md:862; single rank, periodic): in place,
+// one kernel shape every step, half of each opposite pair (i, opp i) exchanged with the
+// neighbour x + xi_i, i the "first" member (i < opp i):
+//   odd  (state E -> O): f_i = mem(x, i),     f_opp = mem(x + xi_i, opp)  -> collide ->
+//                        mem(x + xi_i, opp) = f*_i, mem(x, i) = f*_opp
+//   even (state O -> E): f_i = mem(x, opp),   f_opp = mem(x + xi_i, i)    -> collide ->
+//                        mem(x + xi_i, i) = f*_i,   mem(x, opp) = f*_opp
+// (state E: mem(x + xi_i, i) = f*_i(x), mem(x, opp) = f*_opp(x); state O swaps the slots;
+// every slot is read and written by one cell only: race-free in place.)
+// ---------------------------------------------------------------------------
+template <class S>
+__host__ __device__ constexpr bool first_of_pair(int i) {
+  return i != 0 && i < S::opp(i);
+}
+
+enum { PAT_ESO_EVEN = 3, PAT_ESO_ODD = 4 };
+
+template <class S, int SPACE, int REG, class real, int PAT, int RS = RS_GENERAL>
+__global__ void __launch_bounds__(BLOCK_X)
+    k_eso(real *mem, const GridParams g, const Rates<real> r, const real swe_g, const Force<real> fr) {
+  const int x = blockIdx.x * BLOCK_X + threadIdx.x;
+  if (x >= g.nx) return;
+  const int y = blockIdx.y;
+  const int zl = g.zbegin + blockIdx.z;
+  constexpr bool odd = (PAT == PAT_ESO_ODD);
+  const long long own = (long long)(zl + 1) * g.plane + (long long)y * g.pitch + x;
+  int xs[3], ys[3];
+  long long zo[3];
+#pragma unroll
+  for (int s = -1; s <= 1; ++s) {
+    xs[s + 1] = wrapi(x + s, g.nx);
+    ys[s + 1] = wrapi(y + s, g.ny) * g.pitch;
+    zo[s + 1] = (long long)(wrapi(zl + s, g.nzl) + 1) * g.plane;
+  }
+  real f[S::Q];
+  f[0] = ld_nc(mem + own);
+  sfor<S::Q>([&](auto i) {
+    if constexpr (first_of_pair<S>(i)) {
+      constexpr int o = S::opp(i), cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+      const long long nb = zo[1 + cz] + ys[1 + cy] + xs[1 + cx];  // cell x + xi_i
+      f[i] = ld_nc(mem + own + (long long)(odd ? i : o) * g.pop);
+      f[o] = ld_nc(mem + nb + (long long)(odd ? o : i) * g.pop);
+    }
+  });
+  collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
+  mem[own] = f[0];
+  sfor<S::Q>([&](auto i) {
+    if constexpr (first_of_pair<S>(i)) {
+      constexpr int o = S::opp(i), cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+      const long long nb = zo[1 + cz] + ys[1 + cy] + xs[1 + cx];
+      mem[nb + (long long)(odd ? o : i) * g.pop] = f[i];
+      mem[own + (long long)(odd ? i : o) * g.pop] = f[o];
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
 // helpers: init from macroscopic fields, canonical get/set, macroscopic moments,
-// collision-only test kernel, finiteness probe.  'state' for AA: 0 = A, 1 = B.
+// collision-only test kernel, finiteness probe.  'pat' = lbm_streaming (0 pull, 1 AA,
+// 2 Esoteric Pull); 'state' for AA: 0 = A, 1 = B; for Esoteric Pull: 0 = E, 1 = O.
 // ---------------------------------------------------------------------------
 template <class S>
 struct Canon {
   // element offset of the canonical post-collision value f*_i(x) in the grid
   template <int i>
-  __device__ static __forceinline__ long long at(const GridParams &g, int x, int y, int zl, int aa, int state) {
-    if (!aa) return (long long)(zl + 1) * g.plane + (long long)i * g.pop + (long long)y * g.pitch + x;
-    if (state == 0)
-      return (long long)(zl + 1) * g.plane + (long long)S::opp(i) * g.pop + (long long)y * g.pitch + x;
+  __device__ static __forceinline__ long long at(const GridParams &g, int x, int y, int zl, int pat, int state) {
+    const long long own = (long long)(zl + 1) * g.plane + (long long)y * g.pitch + x;
+    if (pat == 0) return own + (long long)i * g.pop;
     const int xx = wrapi(x + S::mx(i), g.nx), yy = wrapi(y + S::my(i), g.ny);
     const int zz = g.wrapz ? wrapi(zl + S::mz(i), g.nzl) : zl + S::mz(i);  // multi-rank: ghost plane
-    return (long long)(zz + 1) * g.plane + (long long)i * g.pop + (long long)yy * g.pitch + xx;
+    const long long nb = (long long)(zz + 1) * g.plane + (long long)yy * g.pitch + xx;  // cell x + xi_i
+    if (pat == 1) return state == 0 ? own + (long long)S::opp(i) * g.pop : nb + (long long)i * g.pop;
+    if constexpr (i == 0) return own;
+    const int slot = state == 0 ? i : S::opp(i);
+    return (first_of_pair<S>(i) ? nb : own) + (long long)slot * g.pop;
   }
 };
 

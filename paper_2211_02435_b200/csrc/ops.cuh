@@ -22,7 +22,7 @@ struct Ops {
   // pull stream–collide of planes [zbegin, zbegin + nplanes) from src into dst
   void (*pull)(const void *src, void *dst, const GridParams &g, const void *params, double swe_g, int bb,
                int nplanes, cudaStream_t s);
-  // AA step (pattern PAT_AA_EVEN / PAT_AA_ODD) in place, planes [zbegin, zbegin + nplanes)
+  // in-place step (PAT_AA_EVEN / PAT_AA_ODD / PAT_ESO_EVEN / PAT_ESO_ODD), planes [zbegin, zbegin + nplanes)
   void (*aa)(void *mem, const GridParams &g, const void *params, double swe_g, int pattern, int nplanes,
              cudaStream_t s);
   void (*init)(void *mem, const GridParams &g, int aa, const double *rho, const double *u, double swe_g,
@@ -65,12 +65,25 @@ struct OpsImpl {
                  cudaStream_t s) {
     if (nplanes <= 0) return;
     const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
-    if (pattern == PAT_AA_EVEN)
-      k_aa<S, SPACE, REG, real, PAT_AA_EVEN, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
-          static_cast<real *>(mem), g, p.rates, (real)swe_g, p.force);
-    else
-      k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
-          static_cast<real *>(mem), g, p.rates, (real)swe_g, p.force);
+    real *m = static_cast<real *>(mem);
+    switch (pattern) {
+      case PAT_AA_EVEN:
+        k_aa<S, SPACE, REG, real, PAT_AA_EVEN, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,
+                                                                                          (real)swe_g, p.force);
+        break;
+      case PAT_AA_ODD:
+        k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,
+                                                                                         (real)swe_g, p.force);
+        break;
+      case PAT_ESO_EVEN:
+        k_eso<S, SPACE, REG, real, PAT_ESO_EVEN, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,
+                                                                                            (real)swe_g, p.force);
+        break;
+      default:
+        k_eso<S, SPACE, REG, real, PAT_ESO_ODD, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,
+                                                                                           (real)swe_g, p.force);
+        break;
+    }
   }
   static void init(void *mem, const GridParams &g, int aa, const double *rho, const double *u, double swe_g,
                    cudaStream_t s) {

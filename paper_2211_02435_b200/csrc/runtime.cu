@@ -139,7 +139,7 @@ int q_of(int stencil) { return stencil == LBM_D2Q9 ? 9 : (stencil == LBM_D3Q19 ?
 long long local_cells(const lbm_ctx *c) { return (long long)c->g.nx * c->g.ny * c->g.nzl; }
 
 void *grid_ptr(lbm_ctx *c, int which) {
-  if (c->streaming == LBM_AA) return c->buf[0];
+  if (c->streaming != LBM_PULL) return c->buf[0];  // in place: one grid
   return c->buf[which == 0 ? c->cur : 1 - c->cur];
 }
 
@@ -157,6 +157,12 @@ void fill_params_t(lbm_ctx *c) {
 void fill_params(lbm_ctx *c) {
   if (c->esize == 8) fill_params_t<double>(c);
   else fill_params_t<float>(c);
+}
+
+// kernel of the next in-place step: AA odd/even, Esoteric Pull odd/even (state 0 -> odd)
+int inplace_pattern(const lbm_ctx *c) {
+  if (c->streaming == LBM_AA) return c->aa_state == 0 ? lbm::PAT_AA_ODD : lbm::PAT_AA_EVEN;
+  return c->aa_state == 0 ? lbm::PAT_ESO_ODD : lbm::PAT_ESO_EVEN;
 }
 
 // momentum correction of the canonical post-collision state: u = (j - F/2) / rho
@@ -296,7 +302,8 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
       return fail(nullptr, LBM_EINVAL, "periodic must be set on both faces of an axis");
   }
   if (D.precision != LBM_FP64 && D.precision != LBM_FP32) return fail(nullptr, LBM_EINVAL, "unknown precision");
-  if (D.streaming != LBM_PULL && D.streaming != LBM_AA) return fail(nullptr, LBM_EINVAL, "unknown streaming");
+  if (D.streaming != LBM_PULL && D.streaming != LBM_AA && D.streaming != LBM_ESOTERIC_PULL)
+    return fail(nullptr, LBM_EINVAL, "unknown streaming");
   if (D.nranks < 1 || D.rank < 0 || D.rank >= D.nranks) return fail(nullptr, LBM_EINVAL, "bad rank/nranks");
   const int slab_extent = two_d ? D.ny : D.nz;
   if (slab_extent % D.nranks != 0)
@@ -306,6 +313,8 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   for (int a = 0; a < 3; ++a) any_wall |= (D.bc[a][0] == LBM_BC_NOSLIP);
   if (D.streaming == LBM_AA && any_wall)
     return fail(nullptr, LBM_EUNSUPPORTED, "AA streaming is provided for periodic faces");
+  if (D.streaming == LBM_ESOTERIC_PULL && (any_wall || D.nranks > 1))
+    return fail(nullptr, LBM_EUNSUPPORTED, "Esoteric Pull is provided for a single rank with periodic faces");
 
   int regime = lbm::REG_ABS;
   if (zc) regime = (equilibrium == LBM_EQ_DELTA) ? lbm::REG_DELTA : lbm::REG_ZC_ABS;
@@ -399,7 +408,7 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
     c->own_stream = true;
   }
   c->grid_elems = (size_t)(g.nzl + 2) * (size_t)g.plane;
-  const int ngrids = (D.streaming == LBM_AA) ? 1 : 2;
+  const int ngrids = (D.streaming == LBM_PULL) ? 2 : 1;
   for (int k = 0; k < ngrids; ++k) {
     e = cudaMalloc(&c->buf[k], c->grid_elems * c->esize);
     if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaMalloc(populations)"));
@@ -438,7 +447,7 @@ lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
   info->nz = c->gnz;
   info->pitch = (size_t)c->g.pitch;
   info->bytes_per_element = c->esize;
-  info->device_bytes = c->grid_elems * c->esize * (c->streaming == LBM_AA ? 1 : 2);
+  info->device_bytes = c->grid_elems * c->esize * (c->streaming == LBM_PULL ? 2 : 1);
   info->steps_done = c->steps;
   info->rate_specialization = c->rs;
   return LBM_OK;
@@ -455,7 +464,7 @@ lbm_status lbm_init_macroscopic(lbm_ctx *c, const double *rho, const double *u) 
   double *du = dr + n;
   LBM_CUDA(c, cudaMemcpyAsync(dr, rho, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   LBM_CUDA(c, cudaMemcpyAsync(du, u, (size_t)n * c->d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  const int aa = c->streaming == LBM_AA;
+  const int aa = c->streaming;  // storage pattern of the canonical state (kernels.cuh Canon)
   GridParams g = c->g;
   c->cur = 0;
   c->aa_state = 0;
@@ -475,9 +484,8 @@ lbm_status lbm_step(lbm_ctx *c, int n) {
   LBM_CUDA(c, cudaSetDevice(c->device));
   GridParams g = c->g;
   for (int t = 0; t < n; ++t) {
-    if (c->streaming == LBM_AA) {
-      const int pat = (c->aa_state == 0) ? lbm::PAT_AA_ODD : lbm::PAT_AA_EVEN;
-      c->ops->aa(c->buf[0], g, c->params, c->swe_g, pat, g.nzl, c->stream);
+    if (c->streaming != LBM_PULL) {
+      c->ops->aa(c->buf[0], g, c->params, c->swe_g, inplace_pattern(c), g.nzl, c->stream);
       c->aa_state ^= 1;
     } else {
       c->ops->pull(c->buf[c->cur], c->buf[1 - c->cur], g, c->params, c->swe_g, c->bb, g.nzl, c->stream);
@@ -497,9 +505,8 @@ lbm_status lbm_step_region(lbm_ctx *c, lbm_region region, void *stream) {
   // launch the step's kernel on planes [z0, z0 + np)
   auto run = [&](int z0, int np) {
     g.zbegin = z0;
-    if (c->streaming == LBM_AA) {
-      const int pat = (c->aa_state == 0) ? lbm::PAT_AA_ODD : lbm::PAT_AA_EVEN;
-      c->ops->aa(c->buf[0], g, c->params, c->swe_g, pat, np, s);
+    if (c->streaming != LBM_PULL) {
+      c->ops->aa(c->buf[0], g, c->params, c->swe_g, inplace_pattern(c), np, s);
     } else {
       c->ops->pull(c->buf[c->cur], c->buf[1 - c->cur], g, c->params, c->swe_g, c->bb, np, s);
     }
@@ -518,7 +525,7 @@ lbm_status lbm_step_region(lbm_ctx *c, lbm_region region, void *stream) {
 
 lbm_status lbm_swap(lbm_ctx *c) {
   if (!c) return LBM_EINVAL;
-  if (c->streaming == LBM_AA) c->aa_state ^= 1;
+  if (c->streaming != LBM_PULL) c->aa_state ^= 1;
   else c->cur ^= 1;
   c->steps++;
   return LBM_OK;
@@ -526,6 +533,7 @@ lbm_status lbm_swap(lbm_ctx *c) {
 
 lbm_status lbm_get_halo(lbm_ctx *c, int which, lbm_halo *out) {
   if (!c || !out) return LBM_EINVAL;
+  if (c->streaming == LBM_ESOTERIC_PULL) return fail(c, LBM_EUNSUPPORTED, "Esoteric Pull is single-rank");
   char *base = static_cast<char *>(grid_ptr(c, which));
   lbm_layout lay;
   lbm_status s = lbm_grid_layout((lbm_stencil)c->stencil, (lbm_precision)c->prec, c->gnx, c->gny, c->gnz,
@@ -561,7 +569,7 @@ lbm_status lbm_get_macroscopic(lbm_ctx *c, double *rho, double *u) {
   if (s != LBM_OK) return s;
   double *dr = static_cast<double *>(c->staging);
   double *du = dr + n;
-  const int aa = c->streaming == LBM_AA;
+  const int aa = c->streaming;  // storage pattern of the canonical state (kernels.cuh Canon)
   c->ops->macro(grid_ptr(c, 0), c->g, aa, c->aa_state, c->zc, dr, du, post_shift(c), c->stream);
   s = check_launch(c, "k_macroscopic");
   if (s != LBM_OK) return s;
@@ -578,7 +586,7 @@ lbm_status lbm_get_populations(lbm_ctx *c, double *f) {
   const size_t bytes = (size_t)n * c->q * sizeof(double);
   lbm_status s = ensure_staging(c, bytes);
   if (s != LBM_OK) return s;
-  const int aa = c->streaming == LBM_AA;
+  const int aa = c->streaming;  // storage pattern of the canonical state (kernels.cuh Canon)
   c->ops->get_pop(grid_ptr(c, 0), c->g, aa, c->aa_state, static_cast<double *>(c->staging), c->stream);
   s = check_launch(c, "k_get_populations");
   if (s != LBM_OK) return s;
@@ -617,7 +625,7 @@ lbm_status lbm_get_diagnostics(lbm_ctx *c, lbm_diagnostics *out) {
   if (s != LBM_OK) return s;
   double *partial = static_cast<double *>(c->staging);
   double *dout = partial + 5 * lbm::DIAG_GRID;
-  c->ops->diagnostics(grid_ptr(c, 0), c->g, c->streaming == LBM_AA, c->aa_state, c->zc, partial, dout,
+  c->ops->diagnostics(grid_ptr(c, 0), c->g, c->streaming, c->aa_state, c->zc, partial, dout,
                       post_shift(c), c->stream);
   s = check_launch(c, "k_diag");
   if (s != LBM_OK) return s;
@@ -645,7 +653,7 @@ lbm_status lbm_get_cells(lbm_ctx *c, const long long *cells, long long n, double
   long long *didx = static_cast<long long *>(c->staging);
   double *dout = reinterpret_cast<double *>(static_cast<char *>(c->staging) + (ibytes + 255) / 256 * 256);
   LBM_CUDA(c, cudaMemcpyAsync(didx, cells, ibytes, cudaMemcpyHostToDevice, c->stream));
-  c->ops->get_cells(grid_ptr(c, 0), c->g, c->streaming == LBM_AA, c->aa_state, didx, n, dout, c->stream);
+  c->ops->get_cells(grid_ptr(c, 0), c->g, c->streaming, c->aa_state, didx, n, dout, c->stream);
   s = check_launch(c, "k_get_cells");
   if (s != LBM_OK) return s;
   LBM_CUDA(c, cudaMemcpyAsync(f, dout, obytes, cudaMemcpyDeviceToHost, c->stream));
@@ -661,7 +669,7 @@ lbm_status lbm_set_populations(lbm_ctx *c, const double *f) {
   lbm_status s = ensure_staging(c, bytes);
   if (s != LBM_OK) return s;
   LBM_CUDA(c, cudaMemcpyAsync(c->staging, f, bytes, cudaMemcpyHostToDevice, c->stream));
-  const int aa = c->streaming == LBM_AA;
+  const int aa = c->streaming;  // storage pattern of the canonical state (kernels.cuh Canon)
   c->cur = 0;
   c->aa_state = 0;
   c->ops->set_pop(grid_ptr(c, 0), c->g, aa, static_cast<const double *>(c->staging), c->stream);

@@ -20,7 +20,7 @@ LBM_D2Q9, LBM_D3Q19, LBM_D3Q27 = 0, 1, 2
 LBM_SPACE_POPULATION, LBM_SPACE_RAW, LBM_SPACE_CENTRAL, LBM_SPACE_CUMULANT = 0, 1, 2, 3
 LBM_EQ_ABSOLUTE, LBM_EQ_DELTA, LBM_EQ_SWE = 0, 1, 2
 LBM_FP64, LBM_FP32 = 0, 1
-LBM_PULL, LBM_AA = 0, 1
+LBM_PULL, LBM_AA, LBM_ESOTERIC_PULL = 0, 1, 2
 LBM_BC_PERIODIC, LBM_BC_NOSLIP = 0, 1
 LBM_REGION_ALL, LBM_REGION_BOUNDARY, LBM_REGION_INTERIOR = 0, 1, 2
 

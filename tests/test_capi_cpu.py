@@ -96,6 +96,10 @@ def test_admissibility_errors():
     assert st == L.LBM_EUNSUPPORTED
     st, _ = create_status(eq=L.LBM_EQ_SWE, stencil=L.LBM_D2Q9, space=L.LBM_SPACE_CENTRAL, zc=1, shape=(8, 8, 1))
     assert st == L.LBM_EUNSUPPORTED
+    st, _ = create_status(streaming=L.LBM_ESOTERIC_PULL, nranks=2, rank=0)
+    assert st == L.LBM_EUNSUPPORTED
+    st, _ = create_status(streaming=L.LBM_ESOTERIC_PULL, bc=[[0, 0], [1, 1], [0, 0]])
+    assert st == L.LBM_EUNSUPPORTED
     st, _ = create_status(streaming=L.LBM_AA, bc=[[1, 1], [0, 0], [0, 0]])
     assert st == L.LBM_EUNSUPPORTED
 
