@@ -13,8 +13,17 @@
 #include <cstring>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for Nsight timelines
+
 #include "../../include/lbm.h"
 #include "ops.cuh"
+
+namespace {
+struct NvtxRange {  // scoped NVTX range around the C-ABI entry points (tracing)
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 using lbm::GridParams;
 using lbm::Ops;
@@ -454,6 +463,7 @@ lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
 }
 
 lbm_status lbm_init_macroscopic(lbm_ctx *c, const double *rho, const double *u) {
+  NvtxRange nvtx_("lbm_init_macroscopic");
   if (!c || !rho || !u) return fail(c, LBM_EINVAL, "null argument");
   LBM_CUDA(c, cudaSetDevice(c->device));
   const long long n = local_cells(c);
@@ -477,6 +487,7 @@ lbm_status lbm_init_macroscopic(lbm_ctx *c, const double *rho, const double *u) 
 }
 
 lbm_status lbm_step(lbm_ctx *c, int n) {
+  NvtxRange nvtx_("lbm_step");
   if (!c) return LBM_EINVAL;
   if (n < 0) return fail(c, LBM_EINVAL, "negative step count");
   if (c->nranks > 1)
@@ -497,6 +508,7 @@ lbm_status lbm_step(lbm_ctx *c, int n) {
 }
 
 lbm_status lbm_step_region(lbm_ctx *c, lbm_region region, void *stream) {
+  NvtxRange nvtx_("lbm_step_region");
   if (!c) return LBM_EINVAL;
   LBM_CUDA(c, cudaSetDevice(c->device));
   cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
@@ -562,6 +574,7 @@ lbm_status lbm_sync(lbm_ctx *c) {
 }
 
 lbm_status lbm_get_macroscopic(lbm_ctx *c, double *rho, double *u) {
+  NvtxRange nvtx_("lbm_get_macroscopic");
   if (!c || !rho || !u) return fail(c, LBM_EINVAL, "null argument");
   LBM_CUDA(c, cudaSetDevice(c->device));
   const long long n = local_cells(c);
@@ -580,6 +593,7 @@ lbm_status lbm_get_macroscopic(lbm_ctx *c, double *rho, double *u) {
 }
 
 lbm_status lbm_get_populations(lbm_ctx *c, double *f) {
+  NvtxRange nvtx_("lbm_get_populations");
   if (!c || !f) return fail(c, LBM_EINVAL, "null argument");
   LBM_CUDA(c, cudaSetDevice(c->device));
   const long long n = local_cells(c);
@@ -618,6 +632,7 @@ lbm_status lbm_set_force(lbm_ctx *c, const double *force) {
 }
 
 lbm_status lbm_get_diagnostics(lbm_ctx *c, lbm_diagnostics *out) {
+  NvtxRange nvtx_("lbm_get_diagnostics");
   if (!c || !out) return fail(c, LBM_EINVAL, "null argument");
   LBM_CUDA(c, cudaSetDevice(c->device));
   const size_t pbytes = (size_t)5 * lbm::DIAG_GRID * sizeof(double);
@@ -662,6 +677,7 @@ lbm_status lbm_get_cells(lbm_ctx *c, const long long *cells, long long n, double
 }
 
 lbm_status lbm_set_populations(lbm_ctx *c, const double *f) {
+  NvtxRange nvtx_("lbm_set_populations");
   if (!c || !f) return fail(c, LBM_EINVAL, "null argument");
   LBM_CUDA(c, cudaSetDevice(c->device));
   const long long n = local_cells(c);

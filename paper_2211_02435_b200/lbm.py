@@ -291,6 +291,41 @@ class Lattice:
     def check_finite(self):
         _check(lib().lbm_check_finite(self._ctx), self._ctx)
 
+    def run(self, n, check_every=0, callback=None, every=0):
+        """n steps; optionally lbm_check_finite every `check_every` steps (raises LbmError
+        LBM_ENUMERIC with the step index) and callback(self, steps_done) every `every` steps."""
+        done = 0
+        chunk = min(x for x in (check_every, every, n) if x > 0) if n > 0 else 0
+        while done < n:
+            k = min(chunk, n - done)
+            self.step(k)
+            done += k
+            steps = self.info().steps_done
+            if check_every and steps % check_every == 0:
+                self.check_finite()
+            if callback is not None and every and steps % every == 0:
+                callback(self, steps)
+
+    # -- checkpoint / restart: the canonical state (independent of the streaming pattern)
+    def save(self, path):
+        """Checkpoint of this rank's slab: canonical populations + method metadata (npz)."""
+        info = self.info()
+        np.savez(path, f=self.get_populations(), steps=info.steps_done, stencil=self.stencil, space=self.space,
+                 equilibrium=self.equilibrium, zero_centered=self.zero_centered, shape=np.array(self.global_shape),
+                 offset=self.offset, extent=self.extent)
+
+    def load(self, path):
+        """Restore a checkpoint written by save() for the same method and slab."""
+        d = np.load(path)
+        for k, v in (("stencil", self.stencil), ("space", self.space), ("equilibrium", self.equilibrium),
+                     ("zero_centered", self.zero_centered), ("offset", self.offset), ("extent", self.extent)):
+            if int(d[k]) != int(v):
+                raise ValueError(f"checkpoint {k} = {d[k]} does not match this lattice ({v})")
+        if tuple(d["shape"]) != tuple(self.global_shape):
+            raise ValueError("checkpoint lattice shape differs")
+        self.set_populations(d["f"])
+        return int(d["steps"])
+
     def test_collide(self, f_in):
         f_in = np.ascontiguousarray(f_in, dtype=np.float64)
         assert f_in.ndim == 2 and f_in.shape[1] == self.q

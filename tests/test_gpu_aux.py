@@ -1,0 +1,74 @@
+"""Auxiliary subsystems on the GPU: checkpoint/restart through the canonical state
+(across streaming patterns), failure detection during runs, fp32 in-place patterns."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import workloads as W
+from gpu_helpers import initial_state
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2211_02435_b200 import lbm as L  # noqa: E402
+
+
+def test_checkpoint_restart_across_patterns(tmp_path):
+    """Saving after 11 steps and continuing 6 more equals 17 uninterrupted steps bitwise, also
+    when the checkpoint is written by an AA run and resumed by Esoteric Pull / pull runs."""
+    st, space, eq, zc = W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1
+    shape = (21, 10, 12)
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc) as lat:
+        lat.set_populations(f0)
+        lat.step(17)
+        ref = lat.get_populations()
+    ck = tmp_path / "ck.npz"
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, streaming=L.LBM_AA) as lat:
+        lat.set_populations(f0)
+        lat.step(11)
+        lat.save(ck)
+    for streaming in (L.LBM_PULL, L.LBM_AA, L.LBM_ESOTERIC_PULL):
+        with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, streaming=streaming) as lat:
+            assert lat.load(ck) == 11
+            lat.step(6)
+            np.testing.assert_array_equal(lat.get_populations(), ref)
+    with L.Lattice(st, W.CENTRAL, eq, rates, shape, zero_centered=zc) as lat:
+        with pytest.raises(ValueError):
+            lat.load(ck)
+
+
+def test_run_detects_non_finite_state():
+    st = W.D2Q9
+    shape = (16, 12, 1)
+    f0 = initial_state(st, W.RAW, W.EQ_DELTA, 1, shape)
+    f0[4, 0, 5, 7] = np.inf
+    seen = []
+    with L.Lattice(st, W.RAW, W.EQ_DELTA, W.rate_set_p(st), shape) as lat:
+        lat.set_populations(f0)
+        with pytest.raises(L.LbmError) as e:
+            lat.run(10, check_every=2, callback=lambda l, s: seen.append(s), every=1)
+        assert e.value.status == L.LBM_ENUMERIC
+        assert "step 2" in str(e.value)
+    assert seen == [1]
+
+
+@pytest.mark.parametrize("st", [W.D2Q9, W.D3Q19, W.D3Q27])
+def test_fp32_in_place_patterns_equal_pull(st):
+    shape = (20, 12, 1) if st == W.D2Q9 else (20, 10, 12)
+    space, eq, zc = W.CENTRAL, W.EQ_ABSOLUTE, 1
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape).astype(np.float32).astype(np.float64)
+    outs = []
+    for streaming in (L.LBM_PULL, L.LBM_AA, L.LBM_ESOTERIC_PULL):
+        with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, precision=L.LBM_FP32,
+                       streaming=streaming) as lat:
+            lat.set_populations(f0)
+            lat.step(7)
+            outs.append(lat.get_populations())
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[0], outs[2])
