@@ -354,6 +354,77 @@ __global__ void __launch_bounds__(DIAG_BLOCK) k_diag_final(const T *__restrict__
   }
 }
 
+// ---------------------------------------------------------------------------
+// Temporal blocking: TWO fused pull steps per sweep (single rank, periodic, 3D).
+// A CTA owns a TX x TY column of the lattice and sweeps the slab axis.  At plane k it
+// computes step t+1 on the (TX+2) x (TY+2) halo-extended tile (pulling step t from HBM)
+// into a 3-plane shared-memory ring, then step t+2 on plane k-1 of the tile interior
+// (pulling step t+1 from the ring) and stores it.  Every population of step t is read
+// from HBM once and step t+2 written once: 2 updates per HBM round trip (plus the halo),
+// and the step t+1 values never leave the SM.  Same per-cell arithmetic as k_pull, so
+// the result equals two k_pull launches bitwise.
+// ---------------------------------------------------------------------------
+template <int TX, int TY>
+struct Tile2 {
+  static constexpr int HX = TX + 2, HY = TY + 2, HW = HX * HY;
+  static constexpr int THREADS = (HW + 31) / 32 * 32;
+};
+
+template <class S, int SPACE, int REG, class real, int RS, int TX, int TY>
+__global__ void __launch_bounds__(Tile2<TX, TY>::THREADS, 1)
+    k_pull2(const real *__restrict__ src, real *__restrict__ dst, const GridParams g, const Rates<real> r,
+            const real swe_g, const Force<real> fr) {
+  using T = Tile2<TX, TY>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  real *ring = reinterpret_cast<real *>(smem_raw);  // [3][Q][HW]
+  const int t = threadIdx.x;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  // step t+1 cell of this thread on the halo-extended tile
+  const bool act1 = t < T::HW;
+  const int hx = t % T::HX, hy = t / T::HX;
+  const int gx = wrapi(x0 - 1 + hx, g.nx), gy = wrapi(y0 - 1 + hy, g.ny);
+  int xs[3], ys[3];
+#pragma unroll
+  for (int s = -1; s <= 1; ++s) {
+    xs[s + 1] = wrapi(gx + s, g.nx);
+    ys[s + 1] = wrapi(gy + s, g.ny) * g.pitch;
+  }
+  // step t+2 cell (tile interior)
+  const bool act2 = t < TX * TY;
+  const int ix = t % TX, iy = t / TX;
+  const int n = g.nzl;
+  for (int k = -1; k <= n; ++k) {
+    if (act1) {
+      const int zc = wrapi(k, n);
+      long long zo[3];
+#pragma unroll
+      for (int s = -1; s <= 1; ++s) zo[s + 1] = (long long)(wrapi(zc + s, n) + 1) * g.plane;
+      real f[S::Q];
+      sfor<S::Q>([&](auto i) {
+        constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+        f[i] = ld_nc(src + zo[1 - cz] + (long long)i * g.pop + ys[1 - cy] + xs[1 - cx]);
+      });
+      collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
+      real *slot = ring + (size_t)((k + 3) % 3) * S::Q * T::HW;
+      sfor<S::Q>([&](auto i) { slot[i * T::HW + t] = f[i]; });
+    }
+    __syncthreads();
+    if (k >= 1 && act2) {
+      const int p = k - 1;  // plane of step t+2
+      real f[S::Q];
+      sfor<S::Q>([&](auto i) {
+        constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+        const real *slot = ring + (size_t)((p - cz + 3) % 3) * S::Q * T::HW;
+        f[i] = slot[i * T::HW + (iy + 1 - cy) * T::HX + (ix + 1 - cx)];
+      });
+      collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
+      const long long own = (long long)(p + 1) * g.plane + (long long)(y0 + iy) * g.pitch + (x0 + ix);
+      sfor<S::Q>([&](auto i) { dst[own + (long long)i * g.pop] = f[i]; });
+    }
+    __syncthreads();
+  }
+}
+
 // canonical populations of selected cells (local linear index x + nx (y + ny z))
 template <class S, class real>
 __global__ void k_get_cells(const real *mem, const GridParams g, int aa, int state, const long long *__restrict__ idx,

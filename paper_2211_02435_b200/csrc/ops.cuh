@@ -42,7 +42,14 @@ struct Ops {
                       double *out, double3 dj, cudaStream_t s);
   // kernel attributes of the pull kernel (registers / local memory), for diagnostics
   void (*attributes)(int *regs, int *local_bytes);
+  // two fused pull steps (temporal blocking; 3D, single rank, periodic); tile TX x TY
+  // (0 x 0: not provided).  Requires nx % TX == 0 and ny % TY == 0.
+  void (*pull2)(const void *src, void *dst, const GridParams &g, const void *params, double swe_g,
+                cudaStream_t s);
+  int tile_x, tile_y;
 };
+
+constexpr int TB_TX = 32, TB_TY = 8;  // temporal-blocking tile (k_pull2)
 
 inline dim3 cell_grid(const GridParams &g, int nplanes) {
   return dim3((unsigned)((g.nx + BLOCK_X - 1) / BLOCK_X), (unsigned)g.ny, (unsigned)nplanes);
@@ -125,6 +132,22 @@ struct OpsImpl {
                                                              partial, dj);
     k_diag_final<double><<<1, DIAG_BLOCK, 0, s>>>(partial, out);
   }
+  static void pull2(const void *src, void *dst, const GridParams &g, const void *params, double swe_g,
+                    cudaStream_t s) {
+    if constexpr (S::D == 3) {
+      using T = Tile2<TB_TX, TB_TY>;
+      const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
+      const size_t smem = (size_t)3 * S::Q * T::HW * sizeof(real);
+      auto kern = k_pull2<S, SPACE, REG, real, RS, TB_TX, TB_TY>;
+      static bool configured = false;  // opt in to > 48 KB of dynamic shared memory once
+      if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+      }
+      kern<<<dim3((unsigned)(g.nx / TB_TX), (unsigned)(g.ny / TB_TY), 1), T::THREADS, smem, s>>>(
+          static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
+    }
+  }
   static void attributes(int *regs, int *local_bytes) {
     cudaFuncAttributes a{};
     if (cudaFuncGetAttributes(&a, k_pull<S, SPACE, REG, real, false, RS>) == cudaSuccess) {
@@ -137,7 +160,10 @@ struct OpsImpl {
   }
   static constexpr Ops table{S::Q,      S::D,  &pull,         &aa,           &init,      &get_pop,
                              &set_pop, &macro, &test_collide, &check_finite, &get_cells, &diagnostics,
-                             &attributes};
+                             &attributes,
+                             S::D == 3 ? &pull2 : nullptr,
+                             S::D == 3 ? TB_TX : 0,
+                             S::D == 3 ? TB_TY : 0};
 };
 
 }  // namespace lbm

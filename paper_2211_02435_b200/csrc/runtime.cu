@@ -98,6 +98,7 @@ struct lbm_ctx {
   double force[3] = {0, 0, 0};
   bool forced = false;
   const Ops *ops_plain = nullptr;  // the unforced kernels chosen at create
+  bool tb_allowed = false;         // temporal blocking (two fused steps) eligible
   double swe_g = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -166,6 +167,12 @@ void fill_params_t(lbm_ctx *c) {
 void fill_params(lbm_ctx *c) {
   if (c->esize == 8) fill_params_t<double>(c);
   else fill_params_t<float>(c);
+}
+
+// two fused pull steps available for this context and its current kernels
+bool use_temporal_blocking(const lbm_ctx *c) {
+  return c->tb_allowed && c->ops->pull2 && c->ops->tile_x > 0 && c->g.nx % c->ops->tile_x == 0 &&
+         c->g.ny % c->ops->tile_y == 0;
 }
 
 // kernel of the next in-place step: AA odd/even, Esoteric Pull odd/even (state 0 -> odd)
@@ -401,6 +408,10 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   for (int i = 0; i < 27; ++i) c->rates_d[i] = (i < n_rates) ? relaxation_rates[i] : 0.0;
   c->ops_plain = ops;
   fill_params(c);
+  {  // temporal blocking: single rank, pull, periodic (LBM_TEMPORAL_BLOCKING=0 disables)
+    const char *env = getenv("LBM_TEMPORAL_BLOCKING");
+    c->tb_allowed = !(env && env[0] == '0') && D.streaming == LBM_PULL && D.nranks == 1 && !c->bb;
+  }
 
   auto bail = [&](lbm_status s) {
     g_create_error = c->err;
@@ -459,6 +470,7 @@ lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
   info->device_bytes = c->grid_elems * c->esize * (c->streaming == LBM_PULL ? 2 : 1);
   info->steps_done = c->steps;
   info->rate_specialization = c->rs;
+  info->temporal_blocking = use_temporal_blocking(c) ? 2 : 1;
   return LBM_OK;
 }
 
@@ -494,7 +506,15 @@ lbm_status lbm_step(lbm_ctx *c, int n) {
     return fail(c, LBM_EUNSUPPORTED, "multi-rank contexts step through lbm_step_region + halo exchange");
   LBM_CUDA(c, cudaSetDevice(c->device));
   GridParams g = c->g;
-  for (int t = 0; t < n; ++t) {
+  int t = 0;
+  if (use_temporal_blocking(c)) {  // pairs of steps fused in one sweep (k_pull2)
+    for (; t + 2 <= n; t += 2) {
+      c->ops->pull2(c->buf[c->cur], c->buf[1 - c->cur], g, c->params, c->swe_g, c->stream);
+      c->cur ^= 1;
+      c->steps += 2;
+    }
+  }
+  for (; t < n; ++t) {
     if (c->streaming != LBM_PULL) {
       c->ops->aa(c->buf[0], g, c->params, c->swe_g, inplace_pattern(c), g.nzl, c->stream);
       c->aa_state ^= 1;

@@ -63,7 +63,8 @@ class lbm_info(ctypes.Structure):
     _fields_ = [("q", ctypes.c_int), ("d", ctypes.c_int), ("offset", ctypes.c_int), ("extent", ctypes.c_int),
                 ("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int), ("pitch", ctypes.c_size_t),
                 ("bytes_per_element", ctypes.c_size_t), ("device_bytes", ctypes.c_size_t),
-                ("steps_done", ctypes.c_longlong), ("rate_specialization", ctypes.c_int)]
+                ("steps_done", ctypes.c_longlong), ("rate_specialization", ctypes.c_int),
+                ("temporal_blocking", ctypes.c_int)]
 
 
 _dp = ctypes.POINTER(ctypes.c_double)
