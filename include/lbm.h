@@ -140,7 +140,7 @@ typedef struct {
                                one become compile-time constants; set the environment
                                variable LBM_RATE_SPECIALIZATION=0 to force 0.            */
   int temporal_blocking;    /* time steps per sweep of lbm_step: 2 when pairs of steps are
-                               fused (3D, pull, single rank, periodic, nx % 32 == 0,
+                               fused (D3Q19, pull, single rank, periodic, nx % 16 == 0,
                                ny % 8 == 0; the intermediate step stays in shared memory;
                                same arithmetic, bitwise equal), else 1.  The environment
                                variable LBM_TEMPORAL_BLOCKING=0 (read at create) forces 1. */

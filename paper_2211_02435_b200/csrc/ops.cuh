@@ -49,7 +49,15 @@ struct Ops {
   int tile_x, tile_y;
 };
 
-constexpr int TB_TX = 32, TB_TY = 8;  // temporal-blocking tile (k_pull2)
+// Temporal-blocking tile of k_pull2 per stencil (scripts/tb_variants.cu on B200,
+// profiles/r1/tb_variants.txt): D3Q19 16 x 8 (2 CTAs/SM; fp64 -17 % time per 2 steps,
+// fp32 -4 %).  D3Q27: not used — 27 fp64 populations per cell leave shared memory for too
+// few warps to hide the fp64 collision latency (+55 % time at best).
+template <class S>
+struct TbTile {
+  static constexpr int TX = (S::Q == 19) ? 16 : 0;
+  static constexpr int TY = (S::Q == 19) ? 8 : 0;
+};
 
 inline dim3 cell_grid(const GridParams &g, int nplanes) {
   return dim3((unsigned)((g.nx + BLOCK_X - 1) / BLOCK_X), (unsigned)g.ny, (unsigned)nplanes);
@@ -134,17 +142,18 @@ struct OpsImpl {
   }
   static void pull2(const void *src, void *dst, const GridParams &g, const void *params, double swe_g,
                     cudaStream_t s) {
-    if constexpr (S::D == 3) {
-      using T = Tile2<TB_TX, TB_TY>;
+    constexpr int TX = TbTile<S>::TX, TY = TbTile<S>::TY;
+    if constexpr (S::D == 3 && TX > 0) {
+      using T = Tile2<TX, TY>;
       const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
       const size_t smem = (size_t)3 * S::Q * T::HW * sizeof(real);
-      auto kern = k_pull2<S, SPACE, REG, real, RS, TB_TX, TB_TY>;
+      auto kern = k_pull2<S, SPACE, REG, real, RS, TX, TY>;
       static bool configured = false;  // opt in to > 48 KB of dynamic shared memory once
       if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
       }
-      kern<<<dim3((unsigned)(g.nx / TB_TX), (unsigned)(g.ny / TB_TY), 1), T::THREADS, smem, s>>>(
+      kern<<<dim3((unsigned)(g.nx / TX), (unsigned)(g.ny / TY), 1), T::THREADS, smem, s>>>(
           static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
     }
   }
@@ -161,9 +170,9 @@ struct OpsImpl {
   static constexpr Ops table{S::Q,      S::D,  &pull,         &aa,           &init,      &get_pop,
                              &set_pop, &macro, &test_collide, &check_finite, &get_cells, &diagnostics,
                              &attributes,
-                             S::D == 3 ? &pull2 : nullptr,
-                             S::D == 3 ? TB_TX : 0,
-                             S::D == 3 ? TB_TY : 0};
+                             (S::D == 3 && TbTile<S>::TX > 0) ? &pull2 : nullptr,
+                             TbTile<S>::TX,
+                             TbTile<S>::TY};
 };
 
 }  // namespace lbm
