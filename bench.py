@@ -386,18 +386,21 @@ def main():
     value = total_cells * args.steps / (ms * 1e-3) / 1e6
     ms_step = ms / args.steps
 
-    # dominant kernel: the stream–collide kernel (one launch per step at N = 1)
+    # dominant kernel: the stream–collide kernel (one launch per step at N = 1, or one launch
+    # per TWO steps when the library fuses pairs of steps: temporal blocking, D3Q19)
     peak, peak_src = measured_peaks()
-    bpc = bytes_per_cell(cfg)
-    launches_per_step = 1 if n == 1 else 3
-    kernel_ms = ms_step  # N = 1: one launch per step on this stream
+    bpc = bytes_per_cell(cfg)  # every population read once and written once per launch
+    tb = lat.info().temporal_blocking if n == 1 else 1
+    launches_per_step = (1.0 / tb) if n == 1 else 3
+    kernel_ms = ms_step * tb  # one launch covers tb steps on this stream
     achieved = bpc * cells_local / (kernel_ms * 1e-3) / 1e9
     kkey = f"{args.config}:{dtype_name(cfg)}"
     traffic = ncu_traffic(args.config, kkey, cells_local)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "algorithmic_bytes_per_cell": bpc, "cells_per_launch": cells_local,
-                "peak_source": peak_src, "kernel": f"k_pull/k_aa stream-collide ({kkey})"}
+                "time_steps_per_launch": tb, "peak_source": peak_src,
+                "kernel": ("k_pull2 (two fused steps)" if tb == 2 else "k_pull/k_aa stream-collide") + f" ({kkey})"}
     if n > 1:
         roofline["note"] = "N > 1: per-step time of boundary + interior launches with the halo exchange"
 
@@ -456,7 +459,7 @@ def main():
             "roofline": roofline,
             "clocks": clocks,
             "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": int(math.ceil(launches_per_step * args.steps)),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

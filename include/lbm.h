@@ -140,10 +140,11 @@ typedef struct {
                                one become compile-time constants; set the environment
                                variable LBM_RATE_SPECIALIZATION=0 to force 0.            */
   int temporal_blocking;    /* time steps per sweep of lbm_step: 2 when pairs of steps are
-                               fused (D3Q19, pull, single rank, periodic, nx % 16 == 0,
-                               ny % 8 == 0; the intermediate step stays in shared memory;
-                               same arithmetic, bitwise equal), else 1.  The environment
-                               variable LBM_TEMPORAL_BLOCKING=0 (read at create) forces 1. */
+                               fused (D3Q19 fp64, pull, single rank, periodic, nx % 16 == 0,
+                               ny % 8 == 0, >= 1184 16x8 tile columns; the intermediate step
+                               stays in shared memory; same arithmetic, bitwise equal), else
+                               1.  Environment LBM_TEMPORAL_BLOCKING: 0 (read at create)
+                               forces 1; 1 drops the tile-count condition.                 */
 } lbm_info;
 
 /* Creates a context: validates admissibility, allocates the population grid(s) (two for

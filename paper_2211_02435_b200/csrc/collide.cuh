@@ -699,15 +699,23 @@ struct EqZeroAll {
   __device__ static constexpr bool zero() { return true; }
 };
 
+// (written with explicit fma and exact signed sums so that no kernel context can contract it
+// differently: the fused two-step kernel must reproduce the single-step bits)
+template <int v, class real>
+__device__ __forceinline__ real signed_add(real acc, real a) {
+  if constexpr (v > 0) return acc + a;
+  else if constexpr (v < 0) return acc - a;
+  else return acc;
+}
 template <class S, class real, int NC>
 __device__ __forceinline__ void guo_cube(real (&s)[NC], const Force<real> &fr, real ux, real uy, real uz) {
-  const real uF = ux * fr.F[0] + uy * fr.F[1] + uz * fr.F[2];
+  const real uF = fma(uz, fr.F[2], fma(uy, fr.F[1], ux * fr.F[0]));
   sfor<NC>([&](auto k) { s[k] = real(0); });
   sfor<S::Q>([&](auto i) {
     constexpr int vx = S::vx(i), vy = S::vy(i), vz = S::vz(i);
-    const real xF = real(vx) * fr.F[0] + real(vy) * fr.F[1] + real(vz) * fr.F[2];
-    const real xu = real(vx) * ux + real(vy) * uy + real(vz) * uz;
-    s[S::pos(i)] = real(weight<S>(i)) * (real(3) * xF + real(9) * xu * xF - real(3) * uF);
+    const real xF = signed_add<vz>(signed_add<vy>(signed_add<vx>(real(0), fr.F[0]), fr.F[1]), fr.F[2]);
+    const real xu = signed_add<vz>(signed_add<vy>(signed_add<vx>(real(0), ux), uy), uz);
+    s[S::pos(i)] = real(weight<S>(i)) * fma(real(9) * xu, xF, real(3) * (xF - uF));
   });
 }
 

@@ -49,14 +49,16 @@ struct Ops {
   int tile_x, tile_y;
 };
 
-// Temporal-blocking tile of k_pull2 per stencil (scripts/tb_variants.cu on B200,
-// profiles/r1/tb_variants.txt): D3Q19 16 x 8 (2 CTAs/SM; fp64 -17 % time per 2 steps,
-// fp32 -4 %).  D3Q27: not used — 27 fp64 populations per cell leave shared memory for too
-// few warps to hide the fp64 collision latency (+55 % time at best).
-template <class S>
+// Temporal-blocking tile of k_pull2 (scripts/tb_variants.cu on B200,
+// profiles/r1/tb_variants.txt): D3Q19 fp64 16 x 8 (2 CTAs/SM; -17 % time per 2 steps on a
+// 1024^2 x 128 lattice).  Not used for fp32 (+-5 %, worse on 256^3) nor D3Q27 — 27 fp64
+// populations per cell leave shared memory for too few warps to hide the fp64 collision
+// latency (+55 % time at best).  The runtime also requires >= 4 waves of tiles.
+template <class S, class real>
 struct TbTile {
-  static constexpr int TX = (S::Q == 19) ? 16 : 0;
-  static constexpr int TY = (S::Q == 19) ? 8 : 0;
+  static constexpr bool on = (S::Q == 19) && sizeof(real) == 8;
+  static constexpr int TX = on ? 16 : 0;
+  static constexpr int TY = on ? 8 : 0;
 };
 
 inline dim3 cell_grid(const GridParams &g, int nplanes) {
@@ -142,7 +144,7 @@ struct OpsImpl {
   }
   static void pull2(const void *src, void *dst, const GridParams &g, const void *params, double swe_g,
                     cudaStream_t s) {
-    constexpr int TX = TbTile<S>::TX, TY = TbTile<S>::TY;
+    constexpr int TX = TbTile<S, real>::TX, TY = TbTile<S, real>::TY;
     if constexpr (S::D == 3 && TX > 0) {
       using T = Tile2<TX, TY>;
       const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
@@ -170,9 +172,9 @@ struct OpsImpl {
   static constexpr Ops table{S::Q,      S::D,  &pull,         &aa,           &init,      &get_pop,
                              &set_pop, &macro, &test_collide, &check_finite, &get_cells, &diagnostics,
                              &attributes,
-                             (S::D == 3 && TbTile<S>::TX > 0) ? &pull2 : nullptr,
-                             TbTile<S>::TX,
-                             TbTile<S>::TY};
+                             (S::D == 3 && TbTile<S, real>::TX > 0) ? &pull2 : nullptr,
+                             TbTile<S, real>::TX,
+                             TbTile<S, real>::TY};
 };
 
 }  // namespace lbm

@@ -171,8 +171,13 @@ void fill_params(lbm_ctx *c) {
 
 // two fused pull steps available for this context and its current kernels
 bool use_temporal_blocking(const lbm_ctx *c) {
-  return c->tb_allowed && c->ops->pull2 && c->ops->tile_x > 0 && c->g.nx % c->ops->tile_x == 0 &&
-         c->g.ny % c->ops->tile_y == 0;
+  if (!(c->tb_allowed && c->ops->pull2 && c->ops->tile_x > 0 && c->g.nx % c->ops->tile_x == 0 &&
+        c->g.ny % c->ops->tile_y == 0))
+    return false;
+  // >= 4 waves of tile columns (148 SMs x 2 CTAs): fewer leave the fused sweep tail-bound
+  const long long tiles = (long long)(c->g.nx / c->ops->tile_x) * (c->g.ny / c->ops->tile_y);
+  const char *env = getenv("LBM_TEMPORAL_BLOCKING");
+  return tiles >= 4 * 2 * 148 || (env && env[0] == '1');
 }
 
 // kernel of the next in-place step: AA odd/even, Esoteric Pull odd/even (state 0 -> odd)
