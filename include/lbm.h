@@ -145,6 +145,13 @@ typedef struct {
                                stays in shared memory; same arithmetic, bitwise equal), else
                                1.  Environment LBM_TEMPORAL_BLOCKING: 0 (read at create)
                                forces 1; 1 drops the tile-count condition.                 */
+  int cuda_graph_steps;     /* time steps per CUDA-graph launch of lbm_step (0: none).  Small
+                               single-rank lattices (<= 2^20 cells) are launch-bound: the
+                               first lbm_step call captures 32 single steps from each storage
+                               parity into two graphs (re-captured after lbm_set_force), and
+                               every lbm_step(n) replays floor(n / 32) of them before plain
+                               launches of the rest; same kernels, bitwise equal.
+                               Environment LBM_CUDA_GRAPHS=0 (read per call) disables it.   */
 } lbm_info;
 
 /* Creates a context: validates admissibility, allocates the population grid(s) (two for

@@ -99,6 +99,7 @@ struct lbm_ctx {
   bool forced = false;
   const Ops *ops_plain = nullptr;  // the unforced kernels chosen at create
   bool tb_allowed = false;         // temporal blocking (two fused steps) eligible
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};  // captured step loops per parity (small lattices)
   double swe_g = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -169,6 +170,18 @@ void fill_params(lbm_ctx *c) {
   else fill_params_t<float>(c);
 }
 
+// CUDA-graph replay of the step loop for launch-bound (small) lattices
+constexpr int kGraphSteps = 32;                    // even: the storage parity is unchanged
+constexpr long long kGraphMaxCells = 1LL << 20;    // ~ < 50 us per step
+
+void drop_graphs(lbm_ctx *c) {
+  for (auto &gx : c->graph)
+    if (gx) {
+      cudaGraphExecDestroy(gx);
+      gx = nullptr;
+    }
+}
+
 // two fused pull steps available for this context and its current kernels
 bool use_temporal_blocking(const lbm_ctx *c) {
   if (!(c->tb_allowed && c->ops->pull2 && c->ops->tile_x > 0 && c->g.nx % c->ops->tile_x == 0 &&
@@ -180,10 +193,49 @@ bool use_temporal_blocking(const lbm_ctx *c) {
   return tiles >= 4 * 2 * 148 || (env && env[0] == '1');
 }
 
+// graph replay: small single-rank lattice on a capturable stream; LBM_CUDA_GRAPHS=0 disables
+bool use_graphs(const lbm_ctx *c) {
+  if (local_cells(c) > kGraphMaxCells || c->stream == nullptr || use_temporal_blocking(c)) return false;
+  const char *env = getenv("LBM_CUDA_GRAPHS");
+  return !(env && env[0] == '0');
+}
+
 // kernel of the next in-place step: AA odd/even, Esoteric Pull odd/even (state 0 -> odd)
-int inplace_pattern(const lbm_ctx *c) {
-  if (c->streaming == LBM_AA) return c->aa_state == 0 ? lbm::PAT_AA_ODD : lbm::PAT_AA_EVEN;
-  return c->aa_state == 0 ? lbm::PAT_ESO_ODD : lbm::PAT_ESO_EVEN;
+int inplace_pattern(const lbm_ctx *c, int state) {
+  if (c->streaming == LBM_AA) return state == 0 ? lbm::PAT_AA_ODD : lbm::PAT_AA_EVEN;
+  return state == 0 ? lbm::PAT_ESO_ODD : lbm::PAT_ESO_EVEN;
+}
+int inplace_pattern(const lbm_ctx *c) { return inplace_pattern(c, c->aa_state); }
+
+// Captures kGraphSteps single steps starting from each storage parity (pull: current grid
+// 0/1; in-place: state 0/1) into an executable graph.  Done once, on the first lbm_step call
+// (so a warm-up pays it), again after lbm_set_force; capture launches nothing.
+lbm_status ensure_graphs(lbm_ctx *c) {
+  const GridParams g = c->g;
+  for (int par = 0; par < 2; ++par) {
+    if (c->graph[par]) continue;
+    cudaGraph_t gr = nullptr;
+    LBM_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    int cur = par, st = par;
+    for (int k = 0; k < kGraphSteps; ++k) {
+      if (c->streaming != LBM_PULL) {
+        c->ops->aa(c->buf[0], g, c->params, c->swe_g, inplace_pattern(c, st), g.nzl, c->stream);
+        st ^= 1;
+      } else {
+        c->ops->pull(c->buf[cur], c->buf[1 - cur], g, c->params, c->swe_g, c->bb, g.nzl, c->stream);
+        cur ^= 1;
+      }
+    }
+    cudaError_t e = cudaStreamEndCapture(c->stream, &gr);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&c->graph[par], gr, 0);
+    if (gr) cudaGraphDestroy(gr);
+    if (e != cudaSuccess) {
+      c->graph[par] = nullptr;
+      return cuda_fail(c, e, "CUDA-graph capture of the step loop");
+    }
+  }
+  return LBM_OK;
 }
 
 // momentum correction of the canonical post-collision state: u = (j - F/2) / rho
@@ -452,6 +504,7 @@ lbm_status lbm_destroy(lbm_ctx *c) {
   if (!c) return LBM_EINVAL;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  drop_graphs(c);
   for (int k = 0; k < 2; ++k)
     if (c->buf[k]) cudaFree(c->buf[k]);
   if (c->staging) cudaFree(c->staging);
@@ -476,6 +529,7 @@ lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
   info->steps_done = c->steps;
   info->rate_specialization = c->rs;
   info->temporal_blocking = use_temporal_blocking(c) ? 2 : 1;
+  info->cuda_graph_steps = (c->nranks == 1 && use_graphs(c)) ? kGraphSteps : 0;
   return LBM_OK;
 }
 
@@ -512,6 +566,16 @@ lbm_status lbm_step(lbm_ctx *c, int n) {
   LBM_CUDA(c, cudaSetDevice(c->device));
   GridParams g = c->g;
   int t = 0;
+  // small lattices are launch-bound: replay a captured CUDA graph of kGraphSteps steps
+  if (use_graphs(c)) {
+    lbm_status st = ensure_graphs(c);
+    if (st != LBM_OK) return st;
+    const int par = (c->streaming == LBM_PULL) ? c->cur : c->aa_state;
+    for (; t + kGraphSteps <= n; t += kGraphSteps) {  // even step count: parity unchanged
+      LBM_CUDA(c, cudaGraphLaunch(c->graph[par], c->stream));
+      c->steps += kGraphSteps;
+    }
+  }
   if (use_temporal_blocking(c)) {  // pairs of steps fused in one sweep (k_pull2)
     for (; t + 2 <= n; t += 2) {
       c->ops->pull2(c->buf[c->cur], c->buf[1 - c->cur], g, c->params, c->swe_g, c->stream);
@@ -653,6 +717,7 @@ lbm_status lbm_set_force(lbm_ctx *c, const double *force) {
   for (int a = 0; a < 3; ++a) c->force[a] = force[a];
   c->forced = any;
   fill_params(c);
+  drop_graphs(c);  // the captured launches hold the old parameters by value
   return LBM_OK;
 }
 
