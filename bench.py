@@ -279,6 +279,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--backend", default=None, choices=["nccl", "gloo"],
                     help="torch.distributed backend for N > 1 (default: nccl with one GPU per rank)")
+    ap.add_argument("--halo", default="auto", choices=["auto", "peer", "exchange"],
+                    help="N > 1 halo path: peer = fused push into the neighbours' ghost planes over "
+                         "NVLink peer memory (pull streaming); exchange = torch.distributed P2P "
+                         "(NCCL); auto = peer when the streaming pattern allows it")
     ap.add_argument("--shape", type=int, nargs=3, default=None,
                     help="override the global lattice shape (profiling runs only)")
     args = ap.parse_args()
@@ -341,8 +345,20 @@ def main():
     u = np.ascontiguousarray(u[:d])
     lat.init_macroscopic(rho, u)
     runner = None
+    halo = None
     if n > 1:
-        runner = D.SlabRunner(lat, rank, n)
+        want_peer = args.halo == "peer" or (args.halo == "auto" and cfg["streaming"] == L.LBM_PULL)
+        if want_peer:
+            try:
+                runner = D.PeerRunner(lat, rank, n)
+                halo = "peer: fused boundary-plane push over NVLink peer memory (CUDA IPC), device flags"
+            except L.LbmError as ex:
+                if args.halo == "peer":
+                    raise
+                print(f"warning: fused halo push unavailable ({ex}); using the NCCL exchange", file=sys.stderr)
+        if runner is None:
+            runner = D.SlabRunner(lat, rank, n)
+            halo = f"exchange: torch.distributed P2P ({dist.get_backend()}) overlapped with the interior"
         runner.prime()
 
     def do_steps(k):
@@ -380,6 +396,8 @@ def main():
 
     ms = max_over_ranks(ms)
     if n > 1:
+        if isinstance(runner, D.PeerRunner):
+            runner.check()
         dist.barrier()
     lat.check_finite()
     total_cells = nx * ny * nz
@@ -391,7 +409,8 @@ def main():
     peak, peak_src = measured_peaks()
     bpc = bytes_per_cell(cfg)  # every population read once and written once per launch
     tb = lat.info().temporal_blocking if n == 1 else 1
-    launches_per_step = (1.0 / tb) if n == 1 else 3
+    # N > 1: interior + 2 boundary launches (+ wait and signal kernels of the fused push)
+    launches_per_step = (1.0 / tb) if n == 1 else (5 if isinstance(runner, D.PeerRunner) else 3)
     kernel_ms = ms_step * tb  # one launch covers tb steps on this stream
     achieved = bpc * cells_local / (kernel_ms * 1e-3) / 1e9
     kkey = f"{args.config}:{dtype_name(cfg)}"
@@ -402,7 +421,7 @@ def main():
                 "time_steps_per_launch": tb, "peak_source": peak_src,
                 "kernel": ("k_pull2 (two fused steps)" if tb == 2 else "k_pull/k_aa stream-collide") + f" ({kkey})"}
     if n > 1:
-        roofline["note"] = "N > 1: per-step time of boundary + interior launches with the halo exchange"
+        roofline["note"] = "N > 1: per-step time of boundary + interior launches with the halo " + halo.split(":")[0]
 
     # end-to-end through the C ABI with host buffers (pinned): init from host rho/u,
     # K steps, macroscopic fields back to the host
@@ -455,7 +474,8 @@ def main():
                        "rates": "rate set P (SURVEY.md 8(d))" if cfg["space"] != W.POPULATION else "omega = 1.6",
                        "l2": "inputs larger than L2 (population grids >> 126 MB)" if cells_local * bpc > 1e9
                        else "small grid: L2-resident", "parallelism": f"z-slab x{n}" if n > 1 else "single GPU",
-                       "kernel_regs": regs, "kernel_local_bytes": local},
+                       "kernel_regs": regs, "kernel_local_bytes": local,
+                       **({"halo": halo} if halo else {})},
             "roofline": roofline,
             "clocks": clocks,
             "e2e": e2e,
@@ -463,6 +483,8 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    if n > 1:
+        dist.barrier()  # no rank frees grids a neighbour still maps (fused push)
     lat.close()
     if n > 1:
         dist.destroy_process_group()

@@ -188,6 +188,40 @@ lbm_status lbm_get_halo(lbm_ctx *ctx, int which, lbm_halo *out);
 
 lbm_status lbm_sync(lbm_ctx *ctx);
 
+/* Fused halo push between slab contexts (PULL, nranks > 1).  Instead of a
+   separate exchange, the kernel of a step's two boundary planes stores the slab-crossing
+   populations (slab component -1 of plane 0, +1 of the last plane) straight into the
+   neighbours' ghost planes of the next grid, over NVLink peer memory (CUDA IPC) or, for
+   contexts of one process, plain device pointers; completion is signalled through
+   system-scope flags in the neighbours' memory, so no host or NCCL call sits between steps.
+   Collective protocol: every rank calls lbm_peer_export, the infos are exchanged (any host
+   transport), every rank calls lbm_peer_connect with its lower and upper neighbour's info
+   (periodic ring along the slab axis), all ranks pass a barrier, then lbm_peer_prime
+   (after every lbm_init_macroscopic / lbm_set_populations too), then lbm_step_peer(n) with
+   the same n on every rank (ranks must stay in lock-step; the grids swap identically).
+   The interior planes run on a second stream, overlapping the boundary planes and the
+   wait for the neighbours.  A wait that exceeds LBM_PEER_TIMEOUT_S seconds (environment,
+   default 60) gives up instead of hanging the GPU and is reported by lbm_peer_status. */
+typedef struct {
+  unsigned char grid_ipc[2][64]; /* cudaIpcMemHandle_t of population grids 0 and 1          */
+  unsigned char flags_ipc[64];   /* cudaIpcMemHandle_t of the completion flags              */
+  void *grid[2];                 /* device pointers (used for a peer in the same process)    */
+  void *flags;
+  long long pid;                 /* exporting process id                                      */
+  int device, rank, nranks, stencil, precision, nx, ny, nz;
+} lbm_peer_info;
+lbm_status lbm_peer_export(lbm_ctx *ctx, lbm_peer_info *out);
+/* Maps the neighbours' grids and flags; LBM_EINVAL if their lattice, stencil, precision or
+   ranks do not match this context's ring; LBM_EUNSUPPORTED for in-place streaming or one
+   rank; LBM_ECUDA if the memory cannot be mapped (no peer access). Resets the flags. */
+lbm_status lbm_peer_connect(lbm_ctx *ctx, const lbm_peer_info *lower, const lbm_peer_info *upper);
+/* Pushes the current grid's boundary planes into the neighbours' ghost planes. */
+lbm_status lbm_peer_prime(lbm_ctx *ctx);
+/* n time steps with the fused halo push (asynchronous on the context stream). */
+lbm_status lbm_step_peer(lbm_ctx *ctx, int n);
+/* *timed_out = 1 if a wait for a neighbour gave up (results invalid); synchronises. */
+lbm_status lbm_peer_status(lbm_ctx *ctx, int *timed_out);
+
 /* rho [cells], u [d][cells] of the canonical post-collision state (host, fp64; synchronises). */
 lbm_status lbm_get_macroscopic(lbm_ctx *ctx, double *rho, double *u);
 /* Canonical post-collision populations f*(x, t) in stored form, independent of the AA parity

@@ -30,7 +30,33 @@ struct GridParams {
   int zbegin;                // first local plane of this launch
   int wrapz;                 // single rank: periodic wrap along the slab axis by index
   int bcmask;                // bit (2 * axis + side): no-slip face (axis 0 x, 1 y, 2 slab)
+  // fused halo push (lbm_step_peer): ghost plane of the lower / upper neighbour's next grid
+  // (peer memory over NVLink, or a same-device context); null: no push
+  void *peer_lo = nullptr, *peer_hi = nullptr;
 };
+
+// Stores the slab-crossing populations of a boundary plane into the neighbours' ghost
+// planes: plane 0's downward (slab component -1) populations to the lower neighbour's top
+// ghost plane, plane nzl-1's upward ones to the upper neighbour's bottom ghost plane — the
+// values the neighbours' next pull step gathers (eq:LbStreaming across the cut).  The
+// system-scope fence orders them before the completion flag (k_peer_signal).
+template <class S, class real>
+__device__ __forceinline__ void peer_push(const GridParams &g, int zl, long long in_plane, const real *f) {
+  if (zl == 0 && g.peer_lo) {
+    real *p = static_cast<real *>(g.peer_lo) + in_plane;
+    sfor<S::Q>([&](auto i) {
+      if constexpr (S::mz(i) < 0) p[(long long)i * g.pop] = f[i];
+    });
+    __threadfence_system();
+  }
+  if (zl == g.nzl - 1 && g.peer_hi) {
+    real *p = static_cast<real *>(g.peer_hi) + in_plane;
+    sfor<S::Q>([&](auto i) {
+      if constexpr (S::mz(i) > 0) p[(long long)i * g.pop] = f[i];
+    });
+    __threadfence_system();
+  }
+}
 
 __device__ __forceinline__ int wrapi(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
 
@@ -40,7 +66,10 @@ __device__ __forceinline__ real ld_nc(const real *p) { return __ldg(p); }
 // ---------------------------------------------------------------------------
 // the fused stream–collide kernel (pull, optionally with half-way bounce-back)
 // ---------------------------------------------------------------------------
-template <class S, int SPACE, int REG, class real, bool BB, int RS = RS_GENERAL>
+// PEER: the boundary-plane variant of lbm_step_peer that also pushes the slab-crossing
+// populations into the neighbours' ghost planes (a separate instantiation: the bulk kernel
+// keeps its register budget).
+template <class S, int SPACE, int REG, class real, bool BB, int RS = RS_GENERAL, bool PEER = false>
 __global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, real *__restrict__ dst,
                                                    const GridParams g, const Rates<real> r, const real swe_g,
                                                    const Force<real> fr) {
@@ -86,6 +115,7 @@ __global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, 
   collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
 
   sfor<S::Q>([&](auto i) { dst[own + (long long)i * g.pop] = f[i]; });
+  if constexpr (PEER) peer_push<S>(g, zl, (long long)y * g.pitch + x, f);
 }
 
 // ---------------------------------------------------------------------------

@@ -13,6 +13,8 @@
 #include <cstring>
 #include <string>
 
+#include <unistd.h>  // getpid: same-process peers use plain device pointers
+
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for Nsight timelines
 
 #include "../../include/lbm.h"
@@ -107,6 +109,18 @@ struct lbm_ctx {
   void *staging = nullptr;
   size_t staging_bytes = 0;
   int *flag = nullptr;
+  // fused halo push between slab contexts (lbm_peer_*)
+  long long *peer_flags = nullptr;      // device [2]: phases completed by the lower / upper neighbour; [2] timeout
+  void *peer_ghost[2][2] = {};          // [grid][0 lower, 1 upper]: neighbour's ghost-plane base
+  long long *peer_remote[2] = {};       // lower neighbour's flags[1], upper neighbour's flags[0]
+  void *peer_mapped[6] = {};            // CUDA IPC mappings to close, keyed by (pid, exported pointer)
+  void *peer_raw[6] = {};
+  long long peer_pid[6] = {};
+  int n_mapped = 0;
+  long long peer_phase = 0;
+  bool peer_on = false;
+  cudaStream_t s_int = nullptr;         // interior planes of lbm_step_peer
+  cudaEvent_t ev_b = nullptr, ev_i = nullptr;
   std::string err;
 };
 
@@ -242,6 +256,53 @@ lbm_status ensure_graphs(lbm_ctx *c) {
 double3 post_shift(const lbm_ctx *c) {
   if (!c->forced) return make_double3(0, 0, 0);
   return make_double3(-0.5 * c->force[0], -0.5 * c->force[1], -0.5 * c->force[2]);
+}
+
+// ---- fused halo push: completion flags (system scope, NVLink peer memory) ----
+__device__ __forceinline__ long long ld_acquire_sys(const long long *p) {
+  long long v;
+  asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(long long *p, long long v) {
+  asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// one thread: wait until both neighbours completed phase >= target (flags[2]: timeout latch)
+__global__ void k_peer_wait(long long *flags, long long target, unsigned long long timeout_ns) {
+  if (ld_acquire_sys(flags + 2)) return;  // an earlier wait gave up: do not stall again
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_sys(flags) < target || ld_acquire_sys(flags + 1) < target) {
+    if (globaltimer() - t0 > timeout_ns) {
+      st_release_sys(flags + 2, 1);
+      return;
+    }
+    __nanosleep(256);
+  }
+}
+
+// one thread: publish 'phase' to both neighbours once this stream's earlier work is done
+__global__ void k_peer_signal(long long *lower, long long *upper, long long phase) {
+  __threadfence_system();
+  st_release_sys(lower, phase);
+  st_release_sys(upper, phase);
+}
+
+unsigned long long peer_timeout_ns() {
+  const char *env = getenv("LBM_PEER_TIMEOUT_S");
+  const double s = env ? atof(env) : 60.0;
+  return (unsigned long long)((s > 0 ? s : 60.0) * 1e9);
+}
+
+void peer_release(lbm_ctx *c) {
+  for (int k = 0; k < c->n_mapped; ++k) cudaIpcCloseMemHandle(c->peer_mapped[k]);
+  c->n_mapped = 0;
+  c->peer_on = false;
 }
 
 }  // namespace
@@ -505,6 +566,12 @@ lbm_status lbm_destroy(lbm_ctx *c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   drop_graphs(c);
+  peer_release(c);
+  if (c->s_int) cudaStreamSynchronize(c->s_int);
+  if (c->ev_b) cudaEventDestroy(c->ev_b);
+  if (c->ev_i) cudaEventDestroy(c->ev_i);
+  if (c->s_int) cudaStreamDestroy(c->s_int);
+  if (c->peer_flags) cudaFree(c->peer_flags);
   for (int k = 0; k < 2; ++k)
     if (c->buf[k]) cudaFree(c->buf[k]);
   if (c->staging) cudaFree(c->staging);
@@ -659,6 +726,185 @@ lbm_status lbm_sync(lbm_ctx *c) {
   if (!c) return LBM_EINVAL;
   LBM_CUDA(c, cudaSetDevice(c->device));
   LBM_CUDA(c, cudaStreamSynchronize(c->stream));
+  return LBM_OK;
+}
+
+lbm_status lbm_peer_export(lbm_ctx *c, lbm_peer_info *out) {
+  if (!c || !out) return LBM_EINVAL;
+  if (c->streaming != LBM_PULL) return fail(c, LBM_EUNSUPPORTED, "the fused halo push needs pull streaming");
+  if (c->nranks < 2) return fail(c, LBM_EUNSUPPORTED, "the fused halo push needs nranks > 1");
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  if (!c->peer_flags) {
+    LBM_CUDA(c, cudaMalloc(&c->peer_flags, 4 * sizeof(long long)));
+    LBM_CUDA(c, cudaMemset(c->peer_flags, 0, 4 * sizeof(long long)));
+  }
+  memset(out, 0, sizeof(*out));
+  for (int k = 0; k < 2; ++k) {
+    cudaIpcMemHandle_t h;
+    LBM_CUDA(c, cudaIpcGetMemHandle(&h, c->buf[k]));
+    memcpy(out->grid_ipc[k], &h, sizeof(h));
+    out->grid[k] = c->buf[k];
+  }
+  cudaIpcMemHandle_t h;
+  LBM_CUDA(c, cudaIpcGetMemHandle(&h, c->peer_flags));
+  memcpy(out->flags_ipc, &h, sizeof(h));
+  out->flags = c->peer_flags;
+  out->pid = (long long)getpid();
+  out->device = c->device;
+  out->rank = c->rank;
+  out->nranks = c->nranks;
+  out->stencil = c->stencil;
+  out->precision = c->prec;
+  out->nx = c->gnx;
+  out->ny = c->gny;
+  out->nz = c->gnz;
+  return LBM_OK;
+}
+
+lbm_status lbm_peer_connect(lbm_ctx *c, const lbm_peer_info *lo, const lbm_peer_info *hi) {
+  NvtxRange nvtx_("lbm_peer_connect");
+  if (!c || !lo || !hi) return LBM_EINVAL;
+  if (!c->peer_flags) return fail(c, LBM_EINVAL, "lbm_peer_export first");
+  const lbm_peer_info *nb[2] = {lo, hi};
+  const int want[2] = {(c->rank + c->nranks - 1) % c->nranks, (c->rank + 1) % c->nranks};
+  for (int k = 0; k < 2; ++k) {
+    const lbm_peer_info *p = nb[k];
+    if (p->nranks != c->nranks || p->rank != want[k] || p->stencil != c->stencil || p->precision != c->prec ||
+        p->nx != c->gnx || p->ny != c->gny || p->nz != c->gnz)
+      return fail(c, LBM_EINVAL, "peer info does not match this context's slab ring");
+  }
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  LBM_CUDA(c, cudaDeviceSynchronize());
+  peer_release(c);
+  const long long me = (long long)getpid();
+  // maps a peer allocation: same process -> its pointer; else CUDA IPC (one mapping per handle)
+  auto map = [&](const lbm_peer_info *p, const unsigned char *ipc, void *raw, void **out) -> lbm_status {
+    if (p->pid == me) {
+      if (p->device != c->device) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(p->device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (e != cudaSuccess) return cuda_fail(c, e, "cudaDeviceEnablePeerAccess");
+      }
+      *out = raw;
+      return LBM_OK;
+    }
+    for (int k = 0; k < c->n_mapped; ++k)  // the same neighbour on both sides (two ranks)
+      if (c->peer_pid[k] == p->pid && c->peer_raw[k] == raw) {
+        *out = c->peer_mapped[k];
+        return LBM_OK;
+      }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc, sizeof(h));
+    void *ptr = nullptr;
+    LBM_CUDA(c, cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    c->peer_pid[c->n_mapped] = p->pid;
+    c->peer_raw[c->n_mapped] = raw;
+    c->peer_mapped[c->n_mapped++] = ptr;
+    *out = ptr;
+    return LBM_OK;
+  };
+  void *g[2][2], *f[2];
+  for (int k = 0; k < 2; ++k) {
+    const lbm_peer_info *p = nb[k];
+    lbm_status s;
+    if ((s = map(p, p->grid_ipc[0], p->grid[0], &g[0][k])) != LBM_OK) return s;
+    if ((s = map(p, p->grid_ipc[1], p->grid[1], &g[1][k])) != LBM_OK) return s;
+    if ((s = map(p, p->flags_ipc, p->flags, &f[k])) != LBM_OK) return s;
+  }
+  const size_t top = (size_t)(c->g.nzl + 1) * c->g.plane * c->esize;  // ghost plane nzl + 1
+  for (int b = 0; b < 2; ++b) {
+    c->peer_ghost[b][0] = static_cast<char *>(g[b][0]) + top;  // lower's top ghost plane
+    c->peer_ghost[b][1] = g[b][1];                               // upper's bottom ghost plane
+  }
+  c->peer_remote[0] = static_cast<long long *>(f[0]) + 1;  // I am the lower's upper neighbour
+  c->peer_remote[1] = static_cast<long long *>(f[1]) + 0;
+  LBM_CUDA(c, cudaMemset(c->peer_flags, 0, 4 * sizeof(long long)));
+  if (!c->s_int) {
+    LBM_CUDA(c, cudaStreamCreateWithFlags(&c->s_int, cudaStreamNonBlocking));
+    LBM_CUDA(c, cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming));
+    LBM_CUDA(c, cudaEventCreateWithFlags(&c->ev_i, cudaEventDisableTiming));
+  }
+  LBM_CUDA(c, cudaDeviceSynchronize());
+  c->peer_phase = 0;
+  c->peer_on = true;
+  return LBM_OK;
+}
+
+lbm_status lbm_peer_prime(lbm_ctx *c) {
+  NvtxRange nvtx_("lbm_peer_prime");
+  if (!c) return LBM_EINVAL;
+  if (!c->peer_on) return fail(c, LBM_EINVAL, "lbm_peer_connect first");
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  lbm_layout lay;
+  lbm_status s = lbm_grid_layout((lbm_stencil)c->stencil, (lbm_precision)c->prec, c->gnx, c->gny, c->gnz,
+                                 c->nranks, &lay);
+  if (s != LBM_OK) return fail(c, s, "layout");
+  const size_t E = c->esize, bytes = lay.halo_elems * E;
+  const int b = c->cur;
+  const char *base = static_cast<const char *>(c->buf[b]);
+  const size_t top = (size_t)(c->g.nzl + 1) * c->g.plane * E;
+  // the ghost plane offsets of the receive blocks (recv_hi lies in plane nzl + 1, recv_lo in 0)
+  char *lo_dst = static_cast<char *>(c->peer_ghost[b][0]) - top + lay.recv_hi * E;
+  char *hi_dst = static_cast<char *>(c->peer_ghost[b][1]) + lay.recv_lo * E;
+  k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_phase, peer_timeout_ns());
+  LBM_CUDA(c, cudaMemcpyAsync(lo_dst, base + lay.send_lo * E, bytes, cudaMemcpyDefault, c->stream));
+  LBM_CUDA(c, cudaMemcpyAsync(hi_dst, base + lay.send_hi * E, bytes, cudaMemcpyDefault, c->stream));
+  k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_remote[0], c->peer_remote[1], c->peer_phase + 1);
+  c->peer_phase++;
+  return check_launch(c, "lbm_peer_prime");
+}
+
+lbm_status lbm_step_peer(lbm_ctx *c, int n) {
+  NvtxRange nvtx_("lbm_step_peer");
+  if (!c) return LBM_EINVAL;
+  if (n < 0) return fail(c, LBM_EINVAL, "negative step count");
+  if (!c->peer_on) return fail(c, LBM_EINVAL, "lbm_peer_connect first");
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  const unsigned long long tmo = peer_timeout_ns();
+  const int nzl = c->g.nzl;
+  LBM_CUDA(c, cudaEventRecord(c->ev_b, c->stream));
+  LBM_CUDA(c, cudaEventRecord(c->ev_i, c->stream));
+  for (int t = 0; t < n; ++t) {
+    const void *src = c->buf[c->cur];
+    void *dst = c->buf[1 - c->cur];
+    LBM_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_i, 0));  // interior of the previous step
+    LBM_CUDA(c, cudaStreamWaitEvent(c->s_int, c->ev_b, 0));   // boundary of the previous step
+    GridParams gi = c->g;
+    gi.zbegin = 1;
+    c->ops->pull(src, dst, gi, c->params, c->swe_g, c->bb, nzl - 2, c->s_int);
+    LBM_CUDA(c, cudaEventRecord(c->ev_i, c->s_int));
+    // boundary planes: wait for the neighbours' previous phase, push, signal
+    k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_phase, tmo);
+    GridParams gb = c->g;
+    gb.peer_lo = c->peer_ghost[1 - c->cur][0];
+    gb.peer_hi = c->peer_ghost[1 - c->cur][1];
+    gb.zbegin = 0;
+    c->ops->pull(src, dst, gb, c->params, c->swe_g, c->bb, 1, c->stream);
+    if (nzl > 1) {
+      gb.zbegin = nzl - 1;
+      c->ops->pull(src, dst, gb, c->params, c->swe_g, c->bb, 1, c->stream);
+    }
+    k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_remote[0], c->peer_remote[1], c->peer_phase + 1);
+    LBM_CUDA(c, cudaEventRecord(c->ev_b, c->stream));
+    c->peer_phase++;
+    c->cur ^= 1;
+    c->steps++;
+  }
+  LBM_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_i, 0));
+  return check_launch(c, "lbm_step_peer");
+}
+
+lbm_status lbm_peer_status(lbm_ctx *c, int *timed_out) {
+  if (!c || !timed_out) return LBM_EINVAL;
+  if (!c->peer_flags) {
+    *timed_out = 0;
+    return LBM_OK;
+  }
+  LBM_CUDA(c, cudaSetDevice(c->device));
+  LBM_CUDA(c, cudaStreamSynchronize(c->stream));
+  long long v = 0;
+  LBM_CUDA(c, cudaMemcpy(&v, c->peer_flags + 2, sizeof(v), cudaMemcpyDeviceToHost));
+  *timed_out = v != 0;
   return LBM_OK;
 }
 

@@ -202,6 +202,65 @@ class SlabRunner:
             self.lat.swap()
 
 
+def connect_local(lats):
+    """Fused halo push (lbm_peer_*) between the slab contexts of ONE process: plain device
+    pointers instead of CUDA IPC.  Call step_peer_local afterwards."""
+    infos = [l.peer_export() for l in lats]
+    n = len(lats)
+    for r, l in enumerate(lats):
+        lo, hi = neighbours(r, n)
+        l.peer_connect(infos[lo], infos[hi])
+    for l in lats:
+        l.sync()
+    for l in lats:
+        l.peer_prime()
+
+
+def step_peer_local(lats, n: int):
+    """n steps of every context of one process with the fused halo push.  The ranks'
+    launches are interleaved step by step (a context waits on the GPU for its neighbours)."""
+    for _ in range(n):
+        for l in lats:
+            l.step_peer(1)
+    for l in lats:
+        l.sync()
+        assert not l.peer_timed_out(), "a neighbour wait timed out"
+
+
+class PeerRunner:
+    """Multi-process time stepping with the fused halo push: the boundary-plane kernel
+    stores the slab-crossing populations straight into the neighbours' ghost planes
+    (NVLink peer memory through CUDA IPC; include/lbm.h lbm_peer_*), device-side
+    completion flags replace the per-step exchange call.  The host transport of the
+    torch.distributed group only carries the one-time handle exchange and barriers."""
+
+    def __init__(self, lat: "L.Lattice", rank: int, nranks: int, group=None):
+        import torch.distributed as dist
+
+        self.lat, self.rank, self.nranks, self.group = lat, rank, nranks, group
+        mine = lat.peer_export()
+        infos = [None] * nranks
+        dist.all_gather_object(infos, mine, group=group)
+        lo, hi = neighbours(rank, nranks)
+        lat.peer_connect(infos[lo], infos[hi])
+        lat.sync()
+        dist.barrier(group=group)
+
+    def prime(self):
+        import torch.distributed as dist
+
+        self.lat.sync()
+        dist.barrier(group=self.group)
+        self.lat.peer_prime()
+
+    def step(self, n: int = 1):
+        self.lat.step_peer(n)
+
+    def check(self):
+        if self.lat.peer_timed_out():
+            raise RuntimeError(f"rank {self.rank}: a wait for a neighbour's halo timed out")
+
+
 def gather_slabs(local_arrays, axis: int):
     """Concatenate per-rank host arrays along the slab axis (helper for tests)."""
     return np.concatenate(local_arrays, axis=axis)

@@ -67,6 +67,14 @@ class lbm_info(ctypes.Structure):
                 ("temporal_blocking", ctypes.c_int), ("cuda_graph_steps", ctypes.c_int)]
 
 
+class lbm_peer_info(ctypes.Structure):
+    _fields_ = [("grid_ipc", (ctypes.c_ubyte * 64) * 2), ("flags_ipc", ctypes.c_ubyte * 64),
+                ("grid", ctypes.c_void_p * 2), ("flags", ctypes.c_void_p), ("pid", ctypes.c_longlong),
+                ("device", ctypes.c_int), ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
+                ("stencil", ctypes.c_int), ("precision", ctypes.c_int), ("nx", ctypes.c_int),
+                ("ny", ctypes.c_int), ("nz", ctypes.c_int)]
+
+
 _dp = ctypes.POINTER(ctypes.c_double)
 _ip = ctypes.POINTER(ctypes.c_int)
 _vp = ctypes.c_void_p
@@ -84,6 +92,11 @@ SIGNATURES = [
     ("lbm_swap", ctypes.c_int, [_vp]),
     ("lbm_get_halo", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(lbm_halo)]),
     ("lbm_sync", ctypes.c_int, [_vp]),
+    ("lbm_peer_export", ctypes.c_int, [_vp, ctypes.POINTER(lbm_peer_info)]),
+    ("lbm_peer_connect", ctypes.c_int, [_vp, ctypes.POINTER(lbm_peer_info), ctypes.POINTER(lbm_peer_info)]),
+    ("lbm_peer_prime", ctypes.c_int, [_vp]),
+    ("lbm_step_peer", ctypes.c_int, [_vp, ctypes.c_int]),
+    ("lbm_peer_status", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int)]),
     ("lbm_get_macroscopic", ctypes.c_int, [_vp, _dp, _dp]),
     ("lbm_get_populations", ctypes.c_int, [_vp, _dp]),
     ("lbm_set_populations", ctypes.c_int, [_vp, _dp]),
@@ -251,6 +264,28 @@ class Lattice:
 
     def sync(self):
         _check(lib().lbm_sync(self._ctx), self._ctx)
+
+    # fused halo push between slab contexts (include/lbm.h lbm_peer_*)
+    def peer_export(self) -> bytes:
+        info = lbm_peer_info()
+        _check(lib().lbm_peer_export(self._ctx, ctypes.byref(info)), self._ctx)
+        return bytes(info)
+
+    def peer_connect(self, lower: bytes, upper: bytes):
+        lo = lbm_peer_info.from_buffer_copy(lower)
+        hi = lbm_peer_info.from_buffer_copy(upper)
+        _check(lib().lbm_peer_connect(self._ctx, ctypes.byref(lo), ctypes.byref(hi)), self._ctx)
+
+    def peer_prime(self):
+        _check(lib().lbm_peer_prime(self._ctx), self._ctx)
+
+    def step_peer(self, n=1):
+        _check(lib().lbm_step_peer(self._ctx, int(n)), self._ctx)
+
+    def peer_timed_out(self) -> bool:
+        v = ctypes.c_int(0)
+        _check(lib().lbm_peer_status(self._ctx, ctypes.byref(v)), self._ctx)
+        return bool(v.value)
 
     def get_macroscopic(self, out=None):
         z, y, x = self.local_shape

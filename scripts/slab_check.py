@@ -49,6 +49,8 @@ def fields(st, eq, shape, z0, nzl):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=12)
+    ap.add_argument("--halo", choices=["exchange", "peer"], default="exchange",
+                    help="exchange: SlabRunner (NCCL/gloo P2P); peer: PeerRunner (fused push over CUDA IPC)")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -67,17 +69,22 @@ def main():
         if "walls" in name:
             bc = [[0, 0], [0, 0], [L.LBM_BC_NOSLIP, L.LBM_BC_NOSLIP]]
         streaming = L.LBM_AA if name.endswith("AA") else L.LBM_PULL
+        if args.halo == "peer" and streaming != L.LBM_PULL:
+            continue  # the fused push is a pull-streaming path
         stream = torch.cuda.Stream()
         torch.cuda.set_stream(stream)
         lat = L.Lattice(st, space, eq, rates, shape, zero_centered=zc, bc=bc, swe_g=g, device=dev,
                         stream=stream.cuda_stream, rank=rank, nranks=world, streaming=streaming)
         r, u = fields(st, eq, shape, lat.offset, lat.extent)
         lat.init_macroscopic(np.ascontiguousarray(r), np.ascontiguousarray(u[:lat.d]))
-        runner = D.SlabRunner(lat, rank, world)
+        runner = (D.PeerRunner if args.halo == "peer" else D.SlabRunner)(lat, rank, world)
         runner.prime()
         runner.step(args.steps)
         torch.cuda.synchronize()
+        if args.halo == "peer":
+            runner.check()
         mine = lat.get_populations()
+        dist.barrier()  # no rank frees memory a neighbour still maps
         lat.close()
         parts = [None] * world
         dist.all_gather_object(parts, mine)
@@ -91,7 +98,7 @@ def main():
                 single = one.get_populations()
             same = np.array_equal(multi, single)
             ok &= same
-            print(f"[{backend} x{world}] {name} {shape}: {'PASS' if same else 'FAIL'} "
+            print(f"[{backend} x{world} {args.halo}] {name} {shape}: {'PASS' if same else 'FAIL'} "
                   f"(max |diff| {np.abs(multi - single).max():.3e})", flush=True)
         dist.barrier()
     dist.destroy_process_group()

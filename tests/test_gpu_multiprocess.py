@@ -28,10 +28,13 @@ def free_port():
 
 
 @pytest.mark.parametrize("nproc", [2, 3])
-def test_torchrun_slabs_bitwise(nproc):
+@pytest.mark.parametrize("halo", ["exchange", "peer"])
+def test_torchrun_slabs_bitwise(nproc, halo):
+    """halo=peer: the fused halo push across processes (CUDA IPC mappings of the
+    neighbours' grids and flags; processes sharing one GPU are time-sliced)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
-           os.path.join(ROOT, "scripts", "slab_check.py"), "--steps", "9"]
+           os.path.join(ROOT, "scripts", "slab_check.py"), "--steps", "9", "--halo", halo]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0

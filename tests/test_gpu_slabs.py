@@ -83,3 +83,83 @@ def test_aa_slabs_equal_single_rank_bitwise(st, space, eq, zc, nranks, steps):
         single = lat.get_populations()
     multi = run_slabs(st, space, eq, zc, rates, shape, f0, steps, nranks, streaming=L.LBM_AA)
     np.testing.assert_array_equal(multi, single)
+
+
+# ----------------------------------------------------------- fused halo push (lbm_peer_*)
+def run_slabs_peer(st, space, eq, zc, rates, shape, f0, steps, nranks, bc=None, reprime_at=None):
+    slab_axis = 2 if W.DIM_OF[st] == 2 else 1
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, bc=bc, rank=r, nranks=nranks)
+            for r in range(nranks)]
+
+    def load(f):
+        for lat in lats:
+            sl = [slice(None)] * 4
+            sl[slab_axis] = slice(lat.offset, lat.offset + lat.extent)
+            lat.set_populations(np.ascontiguousarray(f[tuple(sl)]))
+
+    load(f0)
+    D.connect_local(lats)
+    done = 0
+    if reprime_at is not None:  # run, reload a state mid-run, prime again, continue
+        D.step_peer_local(lats, reprime_at)
+        mid = np.concatenate([lat.get_populations() for lat in lats], axis=slab_axis)
+        load(mid)
+        for lat in lats:
+            lat.peer_prime()
+        done = reprime_at
+    D.step_peer_local(lats, steps - done)
+    out = np.concatenate([lat.get_populations() for lat in lats], axis=slab_axis)
+    for lat in lats:
+        lat.close()
+    return out
+
+
+@pytest.mark.parametrize("st,space,eq,zc,nranks,nz", [
+    (W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1, 2, 12),
+    (W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1, 4, 12),
+    (W.D3Q27, W.CENTRAL, W.EQ_DELTA, 1, 3, 6),     # two planes per slab: no interior
+    (W.D3Q19, W.RAW, W.EQ_DELTA, 1, 4, 4),         # one plane per slab
+    (W.D2Q9, W.CENTRAL, W.EQ_ABSOLUTE, 0, 4, 1),
+])
+def test_peer_push_equals_single_rank_bitwise(st, space, eq, zc, nranks, nz):
+    """Fused halo push: boundary kernels store into the neighbours' ghost planes, device
+    flags order the steps; equals the single-rank run bitwise, incl. a re-prime mid-run."""
+    shape = (20, 4 * nranks, 1) if st == W.D2Q9 else (20, 10, nz)
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc) as lat:
+        lat.set_populations(f0)
+        lat.step(13)
+        single = lat.get_populations()
+    multi = run_slabs_peer(st, space, eq, zc, rates, shape, f0, 13, nranks, reprime_at=5)
+    np.testing.assert_array_equal(multi, single)
+
+
+def test_peer_push_with_walls_matches_oracle():
+    st, space, eq, zc = W.D3Q27, W.RAW, W.EQ_DELTA, 1
+    shape = (16, 10, 16)
+    bc = [[0, 0], [L.LBM_BC_NOSLIP, L.LBM_BC_NOSLIP], [L.LBM_BC_NOSLIP, L.LBM_BC_NOSLIP]]
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape)
+    multi = run_slabs_peer(st, space, eq, zc, rates, shape, f0, 25, 4, bc=bc)
+    ref = oracle_run(st, space, eq, zc, rates, shape, f0, 25, bc=bc)
+    assert gate_error(st, multi, ref, zc) < F64_TOL
+
+
+def test_peer_rejects_mismatched_ring():
+    st, space, eq, zc = W.D3Q19, W.RAW, W.EQ_DELTA, 1
+    rates = W.rate_set_p(st)
+    a = L.Lattice(st, space, eq, rates, (16, 8, 8), rank=0, nranks=2)
+    b = L.Lattice(st, space, eq, rates, (16, 8, 8), rank=1, nranks=2)
+    c = L.Lattice(st, space, eq, rates, (16, 8, 16), rank=1, nranks=2)
+    ia, ib, ic = a.peer_export(), b.peer_export(), c.peer_export()
+    with pytest.raises(L.LbmError):
+        a.peer_connect(ic, ic)  # other lattice
+    with pytest.raises(L.LbmError):
+        a.peer_connect(ia, ia)  # wrong ranks
+    a.peer_connect(ib, ib)
+    with L.Lattice(st, space, eq, rates, (16, 8, 8), streaming=L.LBM_AA, rank=0, nranks=2) as d:
+        with pytest.raises(L.LbmError):
+            d.peer_export()
+    for x in (a, b, c):
+        x.close()
