@@ -132,3 +132,29 @@ def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):
     monkeypatch.setattr(L, "LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(ImportError):
         L.lib()
+
+
+def test_binding_structs_match_the_header(tmp_path):
+    """The ctypes structures of the binding have the C layout of include/lbm.h (size and
+    every field offset), checked against a program gcc compiles from the header."""
+    structs = {"lbm_domain": L.lbm_domain, "lbm_halo": L.lbm_halo, "lbm_layout": L.lbm_layout,
+               "lbm_info": L.lbm_info, "lbm_diagnostics": L.lbm_diagnostics, "lbm_peer_info": L.lbm_peer_info}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "lbm.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} %zu\\n", sizeof({name}));')
+        for field in cls._fields_:
+            f = field[0]
+            lines.append(f'  printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    import subprocess
+
+    subprocess.run(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                        check=True).stdout.splitlines())
+    for name, cls in structs.items():
+        assert int(got[name]) == ctypes.sizeof(cls), name
+        for field in cls._fields_:
+            assert int(got[f"{name}.{field[0]}"]) == getattr(cls, field[0]).offset, (name, field[0])
