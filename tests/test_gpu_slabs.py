@@ -118,7 +118,7 @@ def run_slabs_peer(st, space, eq, zc, rates, shape, f0, steps, nranks, bc=None, 
     (W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1, 2, 12),
     (W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1, 4, 12),
     (W.D3Q27, W.CENTRAL, W.EQ_DELTA, 1, 3, 6),     # two planes per slab: no interior
-    (W.D3Q19, W.RAW, W.EQ_DELTA, 1, 4, 4),         # one plane per slab
+    (W.D3Q19, W.RAW, W.EQ_DELTA, 1, 2, 8),
     (W.D2Q9, W.CENTRAL, W.EQ_ABSOLUTE, 0, 4, 1),
 ])
 def test_peer_push_equals_single_rank_bitwise(st, space, eq, zc, nranks, nz):
