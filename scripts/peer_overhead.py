@@ -1,0 +1,91 @@
+#!/usr/bin/env python
+"""Cost of the slab decomposition with the fused halo push, measured on ONE GPU: N slab
+contexts of one process (cuda:0, lbm_peer_* over plain device pointers, device-side flags)
+step a 1024 x 1024 x 128 D3Q27 cumulant lattice together; compared with one context stepping
+the whole lattice.  Same cells, same bytes: the difference is the boundary/interior split,
+the wait/signal kernels and the halo stores.
+
+  python scripts/peer_overhead.py [--steps 30] [--ranks 2 4]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import workloads as W  # noqa: E402
+from paper_2211_02435_b200 import distributed as D  # noqa: E402
+from paper_2211_02435_b200 import lbm as L  # noqa: E402
+
+
+def make(shape, rank=0, nranks=1):
+    st = W.D3Q27
+    lat = L.Lattice(st, W.CUMULANT, W.EQ_ABSOLUTE, W.rate_set_p(st), shape, zero_centered=1, rank=rank,
+                    nranks=nranks)
+    rho, u = W.tgv_fields(shape[0], shape[1], lat.extent, 0.05, z0=lat.offset)
+    lat.init_macroscopic(np.ascontiguousarray(rho), np.ascontiguousarray(u))
+    return lat
+
+
+def timed(fn, steps, streams):
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record(streams[0])
+    fn(steps)
+    for s in streams[1:]:  # join every context stream into the first
+        e = torch.cuda.Event()
+        e.record(s)
+        streams[0].wait_event(e)
+    ev[1].record(streams[0])
+    torch.cuda.synchronize()
+    return ev[0].elapsed_time(ev[1]) / steps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--ranks", type=int, nargs="+", default=[2, 4])
+    ap.add_argument("--shape", type=int, nargs=3, default=[1024, 1024, 128])
+    args = ap.parse_args()
+    shape = tuple(args.shape)
+    cells = shape[0] * shape[1] * shape[2]
+    out = {}
+    lat = make(shape)
+    s = [torch.cuda.ExternalStream(lat.stream)]
+    lat.step(3)
+    ms = timed(lat.step, args.steps, s)
+    out["1 context"] = ms
+    lat.close()
+    for n in args.ranks:
+        lats = [make(shape, r, n) for r in range(n)]
+        D.connect_local(lats)
+        streams = [torch.cuda.ExternalStream(l.stream) for l in lats]
+
+        def run(k):
+            for _ in range(k):
+                for l in lats:
+                    l.step_peer(1)
+
+        run(3)
+        ms = timed(run, args.steps, streams)
+        for l in lats:
+            l.sync()
+            assert not l.peer_timed_out()
+        out[f"{n} slab contexts, fused push"] = ms
+        for l in lats:
+            l.close()
+    base = out["1 context"]
+    for k, v in out.items():
+        print(f"{k:32s} {v:7.3f} ms/step  {cells / v / 1e3:8.0f} MLUPS  overhead {100 * (v / base - 1):+5.1f} %")
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
