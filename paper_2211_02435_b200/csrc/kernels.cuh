@@ -33,13 +33,14 @@ struct GridParams {
   // fused halo push (lbm_step_peer): ghost plane of the lower / upper neighbour's next grid
   // (peer memory over NVLink, or a same-device context); null: no push
   void *peer_lo = nullptr, *peer_hi = nullptr;
+  int peer_fence = 0;  // per-thread system-scope fence after the pushes (runtime.cu peer_fence)
 };
 
 // Stores the slab-crossing populations of a boundary plane into the neighbours' ghost
 // planes: plane 0's downward (slab component -1) populations to the lower neighbour's top
 // ghost plane, plane nzl-1's upward ones to the upper neighbour's bottom ghost plane — the
-// values the neighbours' next pull step gathers (eq:LbStreaming across the cut).  The
-// system-scope fence orders them before the completion flag (k_peer_signal).
+// values the neighbours' next pull step gathers (eq:LbStreaming across the cut).  They are
+// ordered before the completion flag by kernel completion + k_peer_signal's system fence.
 template <class S, class real>
 __device__ __forceinline__ void peer_push(const GridParams &g, int zl, long long in_plane, const real *f) {
   if (zl == 0 && g.peer_lo) {
@@ -47,14 +48,14 @@ __device__ __forceinline__ void peer_push(const GridParams &g, int zl, long long
     sfor<S::Q>([&](auto i) {
       if constexpr (S::mz(i) < 0) p[(long long)i * g.pop] = f[i];
     });
-    __threadfence_system();
+    if (g.peer_fence) __threadfence_system();
   }
   if (zl == g.nzl - 1 && g.peer_hi) {
     real *p = static_cast<real *>(g.peer_hi) + in_plane;
     sfor<S::Q>([&](auto i) {
       if constexpr (S::mz(i) > 0) p[(long long)i * g.pop] = f[i];
     });
-    __threadfence_system();
+    if (g.peer_fence) __threadfence_system();
   }
 }
 

@@ -71,8 +71,11 @@ struct OpsImpl {
                    int nplanes, cudaStream_t s) {
     if (nplanes <= 0) return;
     const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
-    if (g.peer_lo || g.peer_hi)  // boundary planes of lbm_step_peer (bounce-back variant: bcmask decides)
+    if ((g.peer_lo || g.peer_hi) && bb)  // boundary planes of lbm_step_peer
       k_pull<S, SPACE, REG, real, true, RS, true><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
+          static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
+    else if (g.peer_lo || g.peer_hi)
+      k_pull<S, SPACE, REG, real, false, RS, true><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
           static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
     else if (bb)
       k_pull<S, SPACE, REG, real, true, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(

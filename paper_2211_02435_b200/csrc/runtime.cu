@@ -299,6 +299,17 @@ unsigned long long peer_timeout_ns() {
   return (unsigned long long)((s > 0 ? s : 60.0) * 1e9);
 }
 
+// Per-thread system-scope fence after the halo stores: off by default.  The completion flag
+// is written by k_peer_signal, stream-ordered after the boundary kernel has COMPLETED; kernel
+// completion makes all of its writes visible at system scope (the property that lets the
+// host read zero-copy results after a stream synchronisation), and the signal thread fences
+// at system scope before its release store.  LBM_PEER_FENCE=1 adds the fence in the kernel
+// (+0.5 % per step, profiles/r1/peer_overhead.txt).
+int peer_fence() {
+  const char *env = getenv("LBM_PEER_FENCE");
+  return env && env[0] == '1';
+}
+
 void peer_release(lbm_ctx *c) {
   for (int k = 0; k < c->n_mapped; ++k) cudaIpcCloseMemHandle(c->peer_mapped[k]);
   c->n_mapped = 0;
@@ -878,6 +889,7 @@ lbm_status lbm_step_peer(lbm_ctx *c, int n) {
     GridParams gb = c->g;
     gb.peer_lo = c->peer_ghost[1 - c->cur][0];
     gb.peer_hi = c->peer_ghost[1 - c->cur][1];
+    gb.peer_fence = peer_fence();
     gb.zbegin = 0;
     c->ops->pull(src, dst, gb, c->params, c->swe_g, c->bb, 1, c->stream);
     if (nzl > 1) {

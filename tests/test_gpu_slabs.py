@@ -135,7 +135,9 @@ def test_peer_push_equals_single_rank_bitwise(st, space, eq, zc, nranks, nz):
     np.testing.assert_array_equal(multi, single)
 
 
-def test_peer_push_with_walls_matches_oracle():
+@pytest.mark.parametrize("fence", ["0", "1"])
+def test_peer_push_with_walls_matches_oracle(fence, monkeypatch):
+    monkeypatch.setenv("LBM_PEER_FENCE", fence)  # per-thread system fence after the pushes
     st, space, eq, zc = W.D3Q27, W.RAW, W.EQ_DELTA, 1
     shape = (16, 10, 16)
     bc = [[0, 0], [L.LBM_BC_NOSLIP, L.LBM_BC_NOSLIP], [L.LBM_BC_NOSLIP, L.LBM_BC_NOSLIP]]
