@@ -217,7 +217,13 @@ lbm_status lbm_peer_export(lbm_ctx *ctx, lbm_peer_info *out);
 lbm_status lbm_peer_connect(lbm_ctx *ctx, const lbm_peer_info *lower, const lbm_peer_info *upper);
 /* Pushes the current grid's boundary planes into the neighbours' ghost planes. */
 lbm_status lbm_peer_prime(lbm_ctx *ctx);
-/* n time steps with the fused halo push (asynchronous on the context stream). */
+/* n time steps with the fused halo push (asynchronous on the context stream).  The phase
+   counters live on the device, so the loop is a fixed launch sequence: n >= 32 replays
+   captured 32-step CUDA graphs (one per grid parity; LBM_CUDA_GRAPHS=0 disables).  Several
+   contexts driven from ONE host thread must be stepped in small interleaved chunks: a
+   context's stream waits on the GPU for its neighbours, and enqueuing many of its steps
+   first can fill the launch queue before the neighbours' work is enqueued (one process per
+   GPU, the deployment case, has no such coupling). */
 lbm_status lbm_step_peer(lbm_ctx *ctx, int n);
 /* *timed_out = 1 if a wait for a neighbour gave up (results invalid); synchronises. */
 lbm_status lbm_peer_status(lbm_ctx *ctx, int *timed_out);

@@ -117,7 +117,7 @@ struct lbm_ctx {
   void *peer_raw[6] = {};
   long long peer_pid[6] = {};
   int n_mapped = 0;
-  long long peer_phase = 0;
+  cudaGraphExec_t peer_graph[2] = {nullptr, nullptr};  // captured lbm_step_peer loops per grid parity
   bool peer_on = false;
   cudaStream_t s_int = nullptr;         // interior planes of lbm_step_peer
   cudaEvent_t ev_b = nullptr, ev_i = nullptr;
@@ -194,6 +194,16 @@ void drop_graphs(lbm_ctx *c) {
       cudaGraphExecDestroy(gx);
       gx = nullptr;
     }
+  for (auto &gx : c->peer_graph)
+    if (gx) {
+      cudaGraphExecDestroy(gx);
+      gx = nullptr;
+    }
+}
+
+bool graphs_enabled() {
+  const char *env = getenv("LBM_CUDA_GRAPHS");
+  return !(env && env[0] == '0');
 }
 
 // two fused pull steps available for this context and its current kernels
@@ -210,8 +220,7 @@ bool use_temporal_blocking(const lbm_ctx *c) {
 // graph replay: small single-rank lattice on a capturable stream; LBM_CUDA_GRAPHS=0 disables
 bool use_graphs(const lbm_ctx *c) {
   if (local_cells(c) > kGraphMaxCells || c->stream == nullptr || use_temporal_blocking(c)) return false;
-  const char *env = getenv("LBM_CUDA_GRAPHS");
-  return !(env && env[0] == '0');
+  return graphs_enabled();
 }
 
 // kernel of the next in-place step: AA odd/even, Esoteric Pull odd/even (state 0 -> odd)
@@ -273,9 +282,15 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// one thread: wait until both neighbours completed phase >= target (flags[2]: timeout latch)
-__global__ void k_peer_wait(long long *flags, long long target, unsigned long long timeout_ns) {
+// Completion flags of a context (device, 4 x int64): [0] phase completed by the lower
+// neighbour, [1] by the upper neighbour (both written remotely), [2] timeout latch, [3] this
+// context's own phase.  The phase lives on the device so that the step loop is a fixed
+// launch sequence (capturable in a CUDA graph).
+
+// one thread: wait until both neighbours completed this context's phase (flags[3])
+__global__ void k_peer_wait(long long *flags, unsigned long long timeout_ns) {
   if (ld_acquire_sys(flags + 2)) return;  // an earlier wait gave up: do not stall again
+  const long long target = flags[3];
   const unsigned long long t0 = globaltimer();
   while (ld_acquire_sys(flags) < target || ld_acquire_sys(flags + 1) < target) {
     if (globaltimer() - t0 > timeout_ns) {
@@ -286,8 +301,11 @@ __global__ void k_peer_wait(long long *flags, long long target, unsigned long lo
   }
 }
 
-// one thread: publish 'phase' to both neighbours once this stream's earlier work is done
-__global__ void k_peer_signal(long long *lower, long long *upper, long long phase) {
+// one thread: advance this context's phase and publish it to both neighbours, once this
+// stream's earlier work (the boundary planes and their halo stores) is complete
+__global__ void k_peer_signal(long long *flags, long long *lower, long long *upper) {
+  const long long phase = flags[3] + 1;
+  flags[3] = phase;
   __threadfence_system();
   st_release_sys(lower, phase);
   st_release_sys(upper, phase);
@@ -314,6 +332,43 @@ void peer_release(lbm_ctx *c) {
   for (int k = 0; k < c->n_mapped; ++k) cudaIpcCloseMemHandle(c->peer_mapped[k]);
   c->n_mapped = 0;
   c->peer_on = false;
+}
+
+// Enqueues n steps with the fused halo push starting from grid 'cur' (no context state
+// changes: also the body of the captured graphs).  Per step: the interior planes on s_int
+// after the previous step's boundary planes; on the context stream, after the previous
+// interior planes: wait for the neighbours' previous phase, the two boundary planes
+// (k_pull<PEER>: local stores + halo stores into the neighbours' next grid), signal.
+void enqueue_peer_steps(lbm_ctx *c, int n, int cur) {
+  const unsigned long long tmo = peer_timeout_ns();
+  const int nzl = c->g.nzl;
+  cudaEventRecord(c->ev_b, c->stream);
+  cudaEventRecord(c->ev_i, c->stream);
+  for (int t = 0; t < n; ++t) {
+    const void *src = c->buf[cur];
+    void *dst = c->buf[1 - cur];
+    cudaStreamWaitEvent(c->stream, c->ev_i, 0);  // interior of the previous step
+    cudaStreamWaitEvent(c->s_int, c->ev_b, 0);   // boundary of the previous step
+    GridParams gi = c->g;
+    gi.zbegin = 1;
+    c->ops->pull(src, dst, gi, c->params, c->swe_g, c->bb, nzl - 2, c->s_int);
+    cudaEventRecord(c->ev_i, c->s_int);
+    k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, tmo);
+    GridParams gb = c->g;
+    gb.peer_lo = c->peer_ghost[1 - cur][0];
+    gb.peer_hi = c->peer_ghost[1 - cur][1];
+    gb.peer_fence = peer_fence();
+    gb.zbegin = 0;
+    c->ops->pull(src, dst, gb, c->params, c->swe_g, c->bb, 1, c->stream);
+    if (nzl > 1) {
+      gb.zbegin = nzl - 1;
+      c->ops->pull(src, dst, gb, c->params, c->swe_g, c->bb, 1, c->stream);
+    }
+    k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_remote[0], c->peer_remote[1]);
+    cudaEventRecord(c->ev_b, c->stream);
+    cur ^= 1;
+  }
+  cudaStreamWaitEvent(c->stream, c->ev_i, 0);
 }
 
 }  // namespace
@@ -787,6 +842,7 @@ lbm_status lbm_peer_connect(lbm_ctx *c, const lbm_peer_info *lo, const lbm_peer_
   LBM_CUDA(c, cudaSetDevice(c->device));
   LBM_CUDA(c, cudaDeviceSynchronize());
   peer_release(c);
+  drop_graphs(c);  // captured peer loops hold the old neighbour pointers
   const long long me = (long long)getpid();
   // maps a peer allocation: same process -> its pointer; else CUDA IPC (one mapping per handle)
   auto map = [&](const lbm_peer_info *p, const unsigned char *ipc, void *raw, void **out) -> lbm_status {
@@ -836,7 +892,6 @@ lbm_status lbm_peer_connect(lbm_ctx *c, const lbm_peer_info *lo, const lbm_peer_
     LBM_CUDA(c, cudaEventCreateWithFlags(&c->ev_i, cudaEventDisableTiming));
   }
   LBM_CUDA(c, cudaDeviceSynchronize());
-  c->peer_phase = 0;
   c->peer_on = true;
   return LBM_OK;
 }
@@ -857,11 +912,10 @@ lbm_status lbm_peer_prime(lbm_ctx *c) {
   // the ghost plane offsets of the receive blocks (recv_hi lies in plane nzl + 1, recv_lo in 0)
   char *lo_dst = static_cast<char *>(c->peer_ghost[b][0]) - top + lay.recv_hi * E;
   char *hi_dst = static_cast<char *>(c->peer_ghost[b][1]) + lay.recv_lo * E;
-  k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_phase, peer_timeout_ns());
+  k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, peer_timeout_ns());
   LBM_CUDA(c, cudaMemcpyAsync(lo_dst, base + lay.send_lo * E, bytes, cudaMemcpyDefault, c->stream));
   LBM_CUDA(c, cudaMemcpyAsync(hi_dst, base + lay.send_hi * E, bytes, cudaMemcpyDefault, c->stream));
-  k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_remote[0], c->peer_remote[1], c->peer_phase + 1);
-  c->peer_phase++;
+  k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_remote[0], c->peer_remote[1]);
   return check_launch(c, "lbm_peer_prime");
 }
 
@@ -871,38 +925,32 @@ lbm_status lbm_step_peer(lbm_ctx *c, int n) {
   if (n < 0) return fail(c, LBM_EINVAL, "negative step count");
   if (!c->peer_on) return fail(c, LBM_EINVAL, "lbm_peer_connect first");
   LBM_CUDA(c, cudaSetDevice(c->device));
-  const unsigned long long tmo = peer_timeout_ns();
-  const int nzl = c->g.nzl;
-  LBM_CUDA(c, cudaEventRecord(c->ev_b, c->stream));
-  LBM_CUDA(c, cudaEventRecord(c->ev_i, c->stream));
-  for (int t = 0; t < n; ++t) {
-    const void *src = c->buf[c->cur];
-    void *dst = c->buf[1 - c->cur];
-    LBM_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_i, 0));  // interior of the previous step
-    LBM_CUDA(c, cudaStreamWaitEvent(c->s_int, c->ev_b, 0));   // boundary of the previous step
-    GridParams gi = c->g;
-    gi.zbegin = 1;
-    c->ops->pull(src, dst, gi, c->params, c->swe_g, c->bb, nzl - 2, c->s_int);
-    LBM_CUDA(c, cudaEventRecord(c->ev_i, c->s_int));
-    // boundary planes: wait for the neighbours' previous phase, push, signal
-    k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_phase, tmo);
-    GridParams gb = c->g;
-    gb.peer_lo = c->peer_ghost[1 - c->cur][0];
-    gb.peer_hi = c->peer_ghost[1 - c->cur][1];
-    gb.peer_fence = peer_fence();
-    gb.zbegin = 0;
-    c->ops->pull(src, dst, gb, c->params, c->swe_g, c->bb, 1, c->stream);
-    if (nzl > 1) {
-      gb.zbegin = nzl - 1;
-      c->ops->pull(src, dst, gb, c->params, c->swe_g, c->bb, 1, c->stream);
+  int t = 0;
+  if (n >= kGraphSteps && graphs_enabled()) {  // replay captured 32-step loops (same launches)
+    for (int par = 0; par < 2; ++par) {
+      if (c->peer_graph[par]) continue;
+      cudaGraph_t gr = nullptr;
+      LBM_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      enqueue_peer_steps(c, kGraphSteps, par);
+      cudaError_t e = cudaStreamEndCapture(c->stream, &gr);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&c->peer_graph[par], gr, 0);
+      if (gr) cudaGraphDestroy(gr);
+      if (e != cudaSuccess) {
+        c->peer_graph[par] = nullptr;
+        return cuda_fail(c, e, "CUDA-graph capture of the peer step loop");
+      }
     }
-    k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_remote[0], c->peer_remote[1], c->peer_phase + 1);
-    LBM_CUDA(c, cudaEventRecord(c->ev_b, c->stream));
-    c->peer_phase++;
-    c->cur ^= 1;
-    c->steps++;
+    for (; t + kGraphSteps <= n; t += kGraphSteps) {  // even: the grid parity is unchanged
+      LBM_CUDA(c, cudaGraphLaunch(c->peer_graph[c->cur], c->stream));
+      c->steps += kGraphSteps;
+    }
   }
-  LBM_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_i, 0));
+  if (t < n) {
+    enqueue_peer_steps(c, n - t, c->cur);
+    if ((n - t) & 1) c->cur ^= 1;
+    c->steps += n - t;
+  }
   return check_launch(c, "lbm_step_peer");
 }
 

@@ -53,14 +53,16 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--ranks", type=int, nargs="+", default=[2, 4])
     ap.add_argument("--shape", type=int, nargs=3, default=[1024, 1024, 128])
+    ap.add_argument("--chunk", type=int, default=64,
+                    help="steps per lbm_step_peer call (>= 32: captured CUDA graphs are replayed)")
     args = ap.parse_args()
     shape = tuple(args.shape)
     cells = shape[0] * shape[1] * shape[2]
     out = {}
     lat = make(shape)
     s = [torch.cuda.ExternalStream(lat.stream)]
-    lat.step(3)
-    ms = timed(lat.step, args.steps, s)
+    lat.step(args.chunk)
+    ms = timed(lambda k: [lat.step(min(args.chunk, k - i)) for i in range(0, k, args.chunk)], args.steps, s)
     out["1 context"] = ms
     lat.close()
     for n in args.ranks:
@@ -69,11 +71,13 @@ def main():
         streams = [torch.cuda.ExternalStream(l.stream) for l in lats]
 
         def run(k):
-            for _ in range(k):
+            while k > 0:
+                c = min(k, args.chunk)
                 for l in lats:
-                    l.step_peer(1)
+                    l.step_peer(c)
+                k -= c
 
-        run(3)
+        run(args.chunk)
         ms = timed(run, args.steps, streams)
         for l in lats:
             l.sync()

@@ -165,3 +165,96 @@ def test_peer_rejects_mismatched_ring():
             d.peer_export()
     for x in (a, b, c):
         x.close()
+
+
+# ----------------------------------------------------------- SURVEY.md 8(d) multi-rank parity runs
+def tgv_state(st, space, eq, zc, shape, lat):
+    rho, u = W.tgv_fields(shape[0], shape[1], shape[2], 0.05)
+    lat.init_macroscopic(np.ascontiguousarray(rho), np.ascontiguousarray(u[:lat.d]))
+    return lat.get_populations()
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+def test_c4_multirank_64cubed_bitwise(nranks):
+    """C4 (D3Q27 cumulant, zc + eq, fp64, pull) at 64^3, 100 steps, N = 2, 4, 8 slab ranks
+    (8-plane slabs at N = 8) with the fused halo push and with the exchange: both equal the
+    single-rank run bitwise (the single-rank run itself matches the oracle:
+    test_gpu_parity.py::test_config4_d3q27_cumulant)."""
+    st, space, eq, zc = W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1
+    shape = (64, 64, 64)
+    rates = W.rate_set_p(st)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc) as lat:
+        f0 = initial_state(st, space, eq, zc, shape)
+        lat.set_populations(f0)
+        lat.step(100)
+        single = lat.get_populations()
+    np.testing.assert_array_equal(run_slabs_peer(st, space, eq, zc, rates, shape, f0, 100, nranks), single)
+    np.testing.assert_array_equal(run_slabs(st, space, eq, zc, rates, shape, f0, 100, nranks), single)
+
+
+def test_c4_eight_slabs_256cubed_bitwise():
+    """The N = 8 decomposition of a 256^3 C4 lattice (32-plane slabs, fused halo push)
+    reproduces the single-rank run bitwise after 20 steps."""
+    st, space, eq, zc = W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1
+    shape = (256, 256, 256)
+    rates = W.rate_set_p(st)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc) as lat:
+        f0 = tgv_state(st, space, eq, zc, shape, lat)
+        lat.step(20)
+        single = lat.get_populations()
+    np.testing.assert_array_equal(run_slabs_peer(st, space, eq, zc, rates, shape, f0, 20, 8), single)
+
+
+def test_c5_eight_slabs_128squared():
+    """C5 (D2Q9 shallow water, CM, Zhou eq., absolute, fp64) at 128^2, dam radius 8, 100
+    steps: N = 8 y-slabs (fused halo push) equal the single-rank run bitwise, which matches
+    the oracle (cell-normalised metric, reading R12b)."""
+    st, space, eq, zc = W.D2Q9, W.CENTRAL, W.EQ_SWE, 0
+    shape = (128, 128, 1)
+    g, nu, om = W.swe_lattice_parameters()
+    rates = W.regularized_rates(st, om)
+    f0 = initial_state(st, space, eq, zc, shape, g=g, noise=0.0, dam=(8.0, 6.25, 1.25))
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, swe_g=g) as lat:
+        lat.set_populations(f0)
+        lat.step(100)
+        single = lat.get_populations()
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, swe_g=g, rank=r, nranks=8) for r in range(8)]
+    for lat in lats:
+        lat.set_populations(np.ascontiguousarray(f0[:, :, lat.offset:lat.offset + lat.extent]))
+    D.connect_local(lats)
+    D.step_peer_local(lats, 100)
+    multi = np.concatenate([lat.get_populations() for lat in lats], axis=2)
+    for lat in lats:
+        lat.close()
+    np.testing.assert_array_equal(multi, single)
+    ref = oracle_run(st, space, eq, zc, rates, shape, f0, 100, g=g)
+    assert gate_error(st, single, ref, zc, norm="cell") < F64_TOL
+
+
+@pytest.mark.parametrize("graphs", ["1", "0"])
+def test_peer_push_graph_replay_bitwise(graphs, monkeypatch):
+    """lbm_step_peer(n >= 32) replays captured 32-step graphs (device-side phase counters);
+    whole calls per context (not interleaved step by step) equal the single-rank run."""
+    monkeypatch.setenv("LBM_CUDA_GRAPHS", graphs)
+    st, space, eq, zc = W.D3Q19, W.CENTRAL, W.EQ_DELTA, 1
+    shape, nranks = (24, 10, 12), 3
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc) as lat:
+        lat.set_populations(f0)
+        lat.step(40 + 71)
+        single = lat.get_populations()
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, rank=r, nranks=nranks) for r in range(nranks)]
+    for lat in lats:
+        lat.set_populations(np.ascontiguousarray(f0[:, lat.offset:lat.offset + lat.extent]))
+    D.connect_local(lats)
+    for n in (40, 71):
+        for lat in lats:
+            lat.step_peer(n)
+    for lat in lats:
+        lat.sync()
+        assert not lat.peer_timed_out()
+    multi = np.concatenate([lat.get_populations() for lat in lats], axis=1)
+    for lat in lats:
+        lat.close()
+    np.testing.assert_array_equal(multi, single)
