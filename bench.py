@@ -49,22 +49,22 @@ CONFIGS = {
                       desc="D3Q27 cumulant TGV 1024^3 (strong scaling, N >= 2: 232 GB in AA), fp64, "
                            "zero-centered + absolute eq, AA in-place"),
     "c3": dict(stencil=W.D3Q27, space=W.CENTRAL, eq=W.EQ_ABSOLUTE, zc=1, prec=0, streaming=1,
-               shape=lambda n: (384, 384, 384), slab=2,
+               shape=lambda n: (384, 384, 384), slab=2, scaling="strong",
                desc="D3Q27 central-moment MRT TGV 384^3, fp64, zero-centered + absolute eq, AA in-place"),
     "c3eso": dict(stencil=W.D3Q27, space=W.CENTRAL, eq=W.EQ_ABSOLUTE, zc=1, prec=0, streaming=2,
-                  shape=lambda n: (384, 384, 384), slab=2,
+                  shape=lambda n: (384, 384, 384), slab=2, scaling="strong",
                   desc="D3Q27 central-moment MRT TGV 384^3, fp64, zero-centered + absolute eq, Esoteric Pull"),
     "c2_f64": dict(stencil=W.D3Q19, space=W.RAW, eq=W.EQ_DELTA, zc=1, prec=0, streaming=0,
-                   shape=lambda n: (256, 256, 256), slab=2,
+                   shape=lambda n: (256, 256, 256), slab=2, scaling="strong",
                    desc="D3Q19 raw-moment MRT TGV 256^3, fp64, zero-centered + delta eq, pull"),
     "c2_f32": dict(stencil=W.D3Q19, space=W.RAW, eq=W.EQ_DELTA, zc=1, prec=1, streaming=0,
-                   shape=lambda n: (256, 256, 256), slab=2,
+                   shape=lambda n: (256, 256, 256), slab=2, scaling="strong",
                    desc="D3Q19 raw-moment MRT TGV 256^3, fp32, zero-centered + delta eq, pull"),
     "c1": dict(stencil=W.D2Q9, space=W.POPULATION, eq=W.EQ_DELTA, zc=1, prec=0, streaming=0,
-               shape=lambda n: (64, 64, 1), slab=1,
+               shape=lambda n: (64, 64, 1), slab=1, scaling="strong",
                desc="D2Q9 BGK TGV 64x64, fp64, zero-centered + delta eq, pull"),
     "c5": dict(stencil=W.D2Q9, space=W.CENTRAL, eq=W.EQ_SWE, zc=0, prec=0, streaming=0,
-               shape=lambda n: (8192, 8192, 1), slab=1,
+               shape=lambda n: (8192, 8192, 1), slab=1, scaling="strong",
                desc="D2Q9 shallow-water CM LBM (Zhou eq.) dam break 8192^2, fp64, absolute, pull"),
 }
 
