@@ -280,9 +280,9 @@ def main():
     ap.add_argument("--backend", default=None, choices=["nccl", "gloo"],
                     help="torch.distributed backend for N > 1 (default: nccl with one GPU per rank)")
     ap.add_argument("--halo", default="auto", choices=["auto", "peer", "exchange"],
-                    help="N > 1 halo path: peer = fused push into the neighbours' ghost planes over "
-                         "NVLink peer memory (pull streaming); exchange = torch.distributed P2P "
-                         "(NCCL); auto = peer when the streaming pattern allows it")
+                    help="N > 1 halo path: peer = boundary kernels store into (pull) or access (AA) "
+                         "the neighbours' planes over NVLink peer memory; exchange = torch.distributed "
+                         "P2P (NCCL); auto = peer")
     ap.add_argument("--shape", type=int, nargs=3, default=None,
                     help="override the global lattice shape (profiling runs only)")
     args = ap.parse_args()
@@ -347,11 +347,14 @@ def main():
     runner = None
     halo = None
     if n > 1:
-        want_peer = args.halo == "peer" or (args.halo == "auto" and cfg["streaming"] == L.LBM_PULL)
+        want_peer = args.halo == "peer" or (args.halo == "auto" and cfg["streaming"] in (L.LBM_PULL, L.LBM_AA))
         if want_peer:
             try:
                 runner = D.PeerRunner(lat, rank, n)
-                halo = "peer: fused boundary-plane push over NVLink peer memory (CUDA IPC), device flags"
+                halo = ("peer: fused boundary-plane push over NVLink peer memory (CUDA IPC), device flags"
+                        if cfg["streaming"] == L.LBM_PULL else
+                        "peer: AA odd-step boundary kernels access the neighbours' planes over NVLink peer "
+                        "memory (CUDA IPC), device flags")
             except L.LbmError as ex:
                 if args.halo == "peer":
                     raise

@@ -124,7 +124,12 @@ __global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, 
 // ---------------------------------------------------------------------------
 // The odd kernel holds 27 gather and 27 scatter addresses across the collision; capping it
 // at 5 blocks/SM (96 registers, 4 B spill) beats 123 registers at 4 blocks (+3 %, B200).
-template <class S, int SPACE, int REG, class real, int PAT, int RS = RS_GENERAL>
+// PEER (odd pattern, boundary planes of lbm_step_peer): the slab-crossing accesses go straight
+// to the neighbours' boundary planes in peer memory (g.peer_lo: the lower neighbour's last
+// plane, g.peer_hi: the upper neighbour's first plane) instead of the ghost planes — the
+// AA odd step is race-free on the global lattice, so ranks need no exchange, only the
+// per-step completion flags.
+template <class S, int SPACE, int REG, class real, int PAT, int RS = RS_GENERAL, bool PEER = false>
 __global__ void __launch_bounds__(BLOCK_X, (PAT == PAT_AA_ODD ? 5 : 1))
     k_aa(real *mem, const GridParams g, const Rates<real> r, const real swe_g, const Force<real> fr) {
   const int x = blockIdx.x * BLOCK_X + threadIdx.x;
@@ -132,7 +137,28 @@ __global__ void __launch_bounds__(BLOCK_X, (PAT == PAT_AA_ODD ? 5 : 1))
   const int y = blockIdx.y;
   const int zl = g.zbegin + blockIdx.z;
   real f[S::Q];
-  if constexpr (PAT == PAT_AA_EVEN) {
+  if constexpr (PEER) {
+    static_assert(PAT == PAT_AA_ODD, "the peer variant is the odd AA step");
+    int xs[3], ys[3];
+    real *zb[3];
+#pragma unroll
+    for (int s = -1; s <= 1; ++s) {
+      xs[s + 1] = wrapi(x + s, g.nx);
+      ys[s + 1] = wrapi(y + s, g.ny) * g.pitch;
+      const int zv = zl + s;
+      zb[s + 1] = zv < 0 ? static_cast<real *>(g.peer_lo)
+                         : (zv >= g.nzl ? static_cast<real *>(g.peer_hi) : mem + (long long)(zv + 1) * g.plane);
+    }
+    sfor<S::Q>([&](auto i) {
+      constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+      f[i] = zb[1 - cz][(long long)S::opp(i) * g.pop + ys[1 - cy] + xs[1 - cx]];
+    });
+    collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
+    sfor<S::Q>([&](auto i) {
+      constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+      zb[1 + cz][(long long)i * g.pop + ys[1 + cy] + xs[1 + cx]] = f[i];
+    });
+  } else if constexpr (PAT == PAT_AA_EVEN) {
     const long long own = (long long)(zl + 1) * g.plane + (long long)y * g.pitch + x;
     // read-only path is safe in place: every slot is read, then written, by the same thread
     sfor<S::Q>([&](auto i) { f[i] = ld_nc(mem + own + (long long)i * g.pop); });

@@ -95,8 +95,12 @@ struct OpsImpl {
                                                                                           (real)swe_g, p.force);
         break;
       case PAT_AA_ODD:
-        k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,
-                                                                                         (real)swe_g, p.force);
+        if (g.peer_lo && g.peer_hi)  // boundary planes of lbm_step_peer
+          k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS, true><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
+              m, g, p.rates, (real)swe_g, p.force);
+        else
+          k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,
+                                                                                           (real)swe_g, p.force);
         break;
       case PAT_ESO_EVEN:
         k_eso<S, SPACE, REG, real, PAT_ESO_EVEN, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,

@@ -111,7 +111,10 @@ struct lbm_ctx {
   int *flag = nullptr;
   // fused halo push between slab contexts (lbm_peer_*)
   long long *peer_flags = nullptr;      // device [2]: phases completed by the lower / upper neighbour; [2] timeout
-  void *peer_ghost[2][2] = {};          // [grid][0 lower, 1 upper]: neighbour's ghost-plane base
+  void *peer_ghost[2][2] = {};          // [grid][0 lower, 1 upper]: the plane the boundary kernels
+                                        // address in the neighbour (pull: its ghost plane of the
+                                        // next grid; AA: its adjacent boundary plane)
+  void *peer_base[2][2] = {};           // [grid][side]: the neighbours' grid bases
   long long *peer_remote[2] = {};       // lower neighbour's flags[1], upper neighbour's flags[0]
   void *peer_mapped[6] = {};            // CUDA IPC mappings to close, keyed by (pid, exported pointer)
   void *peer_raw[6] = {};
@@ -339,36 +342,67 @@ void peer_release(lbm_ctx *c) {
 // after the previous step's boundary planes; on the context stream, after the previous
 // interior planes: wait for the neighbours' previous phase, the two boundary planes
 // (k_pull<PEER>: local stores + halo stores into the neighbours' next grid), signal.
+int pull_parity(const lbm_ctx *c) { return c->streaming == LBM_PULL ? c->cur : c->aa_state; }
+
 void enqueue_peer_steps(lbm_ctx *c, int n, int cur) {
   const unsigned long long tmo = peer_timeout_ns();
   const int nzl = c->g.nzl;
+  const bool pull = c->streaming == LBM_PULL;
   cudaEventRecord(c->ev_b, c->stream);
   cudaEventRecord(c->ev_i, c->stream);
   for (int t = 0; t < n; ++t) {
-    const void *src = c->buf[cur];
-    void *dst = c->buf[1 - cur];
+    // pull: cur = current grid; in place (AA): cur = state (0: the odd kernel runs)
+    const int pat = pull ? 0 : inplace_pattern(c, cur);
+    auto launch = [&](GridParams g, int z0, int np, cudaStream_t s) {
+      g.zbegin = z0;
+      if (pull)
+        c->ops->pull(c->buf[cur], c->buf[1 - cur], g, c->params, c->swe_g, c->bb, np, s);
+      else
+        c->ops->aa(c->buf[0], g, c->params, c->swe_g, pat, np, s);
+    };
     cudaStreamWaitEvent(c->stream, c->ev_i, 0);  // interior of the previous step
     cudaStreamWaitEvent(c->s_int, c->ev_b, 0);   // boundary of the previous step
-    GridParams gi = c->g;
-    gi.zbegin = 1;
-    c->ops->pull(src, dst, gi, c->params, c->swe_g, c->bb, nzl - 2, c->s_int);
+    launch(c->g, 1, nzl - 2, c->s_int);
     cudaEventRecord(c->ev_i, c->s_int);
     k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, tmo);
     GridParams gb = c->g;
-    gb.peer_lo = c->peer_ghost[1 - cur][0];
-    gb.peer_hi = c->peer_ghost[1 - cur][1];
-    gb.peer_fence = peer_fence();
-    gb.zbegin = 0;
-    c->ops->pull(src, dst, gb, c->params, c->swe_g, c->bb, 1, c->stream);
-    if (nzl > 1) {
-      gb.zbegin = nzl - 1;
-      c->ops->pull(src, dst, gb, c->params, c->swe_g, c->bb, 1, c->stream);
+    if (pull || pat == lbm::PAT_AA_ODD) {  // the even AA step touches only its own cells
+      const int b = pull ? 1 - cur : 0;
+      gb.peer_lo = c->peer_ghost[b][0];
+      gb.peer_hi = c->peer_ghost[b][1];
+      gb.peer_fence = peer_fence();
     }
+    launch(gb, 0, 1, c->stream);
+    if (nzl > 1) launch(gb, nzl - 1, 1, c->stream);
     k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_remote[0], c->peer_remote[1]);
     cudaEventRecord(c->ev_b, c->stream);
     cur ^= 1;
   }
   cudaStreamWaitEvent(c->stream, c->ev_i, 0);
+}
+
+// In-place (AA) peer mode after an odd step (state B): the canonical post-collision values of
+// this slab's boundary cells that cross the cut were written straight into the neighbours'
+// boundary planes; copy them back into the ghost planes, where the canonical readers
+// (kernels.cuh Canon) look for them.  Stream-ordered after this rank's last step; the
+// neighbours must not have started their next step (ranks read in lock-step).
+lbm_status peer_refresh(lbm_ctx *c) {
+  if (!c->peer_on || c->streaming == LBM_PULL || c->aa_state != 1) return LBM_OK;
+  lbm_layout lay;
+  lbm_status s = lbm_grid_layout((lbm_stencil)c->stencil, (lbm_precision)c->prec, c->gnx, c->gny, c->gnz,
+                                 c->nranks, &lay);
+  if (s != LBM_OK) return fail(c, s, "layout");
+  const size_t E = c->esize, bytes = lay.halo_elems * E;
+  char *mine = static_cast<char *>(c->buf[0]);
+  const char *lo = static_cast<const char *>(c->peer_base[0][0]);
+  const char *hi = static_cast<const char *>(c->peer_base[0][1]);
+  // ghost plane 0 <- the lower neighbour's last plane (slab component -1 block); ghost plane
+  // nzl + 1 <- the upper neighbour's first plane (+1 block): the "post" blocks of lbm_get_halo
+  LBM_CUDA(c, cudaMemcpyAsync(mine + lay.aa_post_send_lo * E, lo + lay.aa_post_recv_hi * E, bytes,
+                              cudaMemcpyDefault, c->stream));
+  LBM_CUDA(c, cudaMemcpyAsync(mine + lay.aa_post_send_hi * E, hi + lay.aa_post_recv_lo * E, bytes,
+                              cudaMemcpyDefault, c->stream));
+  return LBM_OK;
 }
 
 }  // namespace
@@ -797,7 +831,7 @@ lbm_status lbm_sync(lbm_ctx *c) {
 
 lbm_status lbm_peer_export(lbm_ctx *c, lbm_peer_info *out) {
   if (!c || !out) return LBM_EINVAL;
-  if (c->streaming != LBM_PULL) return fail(c, LBM_EUNSUPPORTED, "the fused halo push needs pull streaming");
+  if (c->streaming == LBM_ESOTERIC_PULL) return fail(c, LBM_EUNSUPPORTED, "Esoteric Pull is single-rank");
   if (c->nranks < 2) return fail(c, LBM_EUNSUPPORTED, "the fused halo push needs nranks > 1");
   LBM_CUDA(c, cudaSetDevice(c->device));
   if (!c->peer_flags) {
@@ -806,6 +840,7 @@ lbm_status lbm_peer_export(lbm_ctx *c, lbm_peer_info *out) {
   }
   memset(out, 0, sizeof(*out));
   for (int k = 0; k < 2; ++k) {
+    if (!c->buf[k]) continue;  // in place (AA): one grid
     cudaIpcMemHandle_t h;
     LBM_CUDA(c, cudaIpcGetMemHandle(&h, c->buf[k]));
     memcpy(out->grid_ipc[k], &h, sizeof(h));
@@ -875,13 +910,20 @@ lbm_status lbm_peer_connect(lbm_ctx *c, const lbm_peer_info *lo, const lbm_peer_
     const lbm_peer_info *p = nb[k];
     lbm_status s;
     if ((s = map(p, p->grid_ipc[0], p->grid[0], &g[0][k])) != LBM_OK) return s;
-    if ((s = map(p, p->grid_ipc[1], p->grid[1], &g[1][k])) != LBM_OK) return s;
+    g[1][k] = nullptr;
+    if (p->grid[1] && (s = map(p, p->grid_ipc[1], p->grid[1], &g[1][k])) != LBM_OK) return s;
     if ((s = map(p, p->flags_ipc, p->flags, &f[k])) != LBM_OK) return s;
   }
-  const size_t top = (size_t)(c->g.nzl + 1) * c->g.plane * c->esize;  // ghost plane nzl + 1
+  const size_t P = c->g.plane * c->esize, nzl = (size_t)c->g.nzl;
   for (int b = 0; b < 2; ++b) {
-    c->peer_ghost[b][0] = static_cast<char *>(g[b][0]) + top;  // lower's top ghost plane
-    c->peer_ghost[b][1] = g[b][1];                               // upper's bottom ghost plane
+    for (int k = 0; k < 2; ++k) c->peer_base[b][k] = g[b][k];
+    if (c->streaming == LBM_PULL) {
+      c->peer_ghost[b][0] = static_cast<char *>(g[b][0]) + (nzl + 1) * P;  // lower's top ghost plane
+      c->peer_ghost[b][1] = g[b][1];                                        // upper's bottom ghost plane
+    } else if (b == 0) {
+      c->peer_ghost[0][0] = static_cast<char *>(g[0][0]) + nzl * P;  // AA: lower's last plane
+      c->peer_ghost[0][1] = static_cast<char *>(g[0][1]) + P;        // AA: upper's first plane
+    }
   }
   c->peer_remote[0] = static_cast<long long *>(f[0]) + 1;  // I am the lower's upper neighbour
   c->peer_remote[1] = static_cast<long long *>(f[1]) + 0;
@@ -906,6 +948,11 @@ lbm_status lbm_peer_prime(lbm_ctx *c) {
                                  c->nranks, &lay);
   if (s != LBM_OK) return fail(c, s, "layout");
   const size_t E = c->esize, bytes = lay.halo_elems * E;
+  if (c->streaming != LBM_PULL) {  // AA: no ghost data; the handshake orders the neighbours' init
+    k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, peer_timeout_ns());
+    k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_remote[0], c->peer_remote[1]);
+    return check_launch(c, "lbm_peer_prime");
+  }
   const int b = c->cur;
   const char *base = static_cast<const char *>(c->buf[b]);
   const size_t top = (size_t)(c->g.nzl + 1) * c->g.plane * E;
@@ -931,7 +978,7 @@ lbm_status lbm_step_peer(lbm_ctx *c, int n) {
       if (c->peer_graph[par]) continue;
       cudaGraph_t gr = nullptr;
       LBM_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-      enqueue_peer_steps(c, kGraphSteps, par);
+      enqueue_peer_steps(c, kGraphSteps, par);  // par: pull grid / AA state
       cudaError_t e = cudaStreamEndCapture(c->stream, &gr);
       if (e == cudaSuccess) e = cudaGetLastError();
       if (e == cudaSuccess) e = cudaGraphInstantiate(&c->peer_graph[par], gr, 0);
@@ -941,14 +988,18 @@ lbm_status lbm_step_peer(lbm_ctx *c, int n) {
         return cuda_fail(c, e, "CUDA-graph capture of the peer step loop");
       }
     }
-    for (; t + kGraphSteps <= n; t += kGraphSteps) {  // even: the grid parity is unchanged
-      LBM_CUDA(c, cudaGraphLaunch(c->peer_graph[c->cur], c->stream));
+    const int par = pull_parity(c);
+    for (; t + kGraphSteps <= n; t += kGraphSteps) {  // even: the parity is unchanged
+      LBM_CUDA(c, cudaGraphLaunch(c->peer_graph[par], c->stream));
       c->steps += kGraphSteps;
     }
   }
   if (t < n) {
-    enqueue_peer_steps(c, n - t, c->cur);
-    if ((n - t) & 1) c->cur ^= 1;
+    enqueue_peer_steps(c, n - t, pull_parity(c));
+    if ((n - t) & 1) {
+      if (c->streaming == LBM_PULL) c->cur ^= 1;
+      else c->aa_state ^= 1;
+    }
     c->steps += n - t;
   }
   return check_launch(c, "lbm_step_peer");
@@ -972,6 +1023,7 @@ lbm_status lbm_get_macroscopic(lbm_ctx *c, double *rho, double *u) {
   NvtxRange nvtx_("lbm_get_macroscopic");
   if (!c || !rho || !u) return fail(c, LBM_EINVAL, "null argument");
   LBM_CUDA(c, cudaSetDevice(c->device));
+  if (lbm_status ps = peer_refresh(c); ps != LBM_OK) return ps;
   const long long n = local_cells(c);
   lbm_status s = ensure_staging(c, (size_t)n * 4 * sizeof(double));
   if (s != LBM_OK) return s;
@@ -991,6 +1043,7 @@ lbm_status lbm_get_populations(lbm_ctx *c, double *f) {
   NvtxRange nvtx_("lbm_get_populations");
   if (!c || !f) return fail(c, LBM_EINVAL, "null argument");
   LBM_CUDA(c, cudaSetDevice(c->device));
+  if (lbm_status ps = peer_refresh(c); ps != LBM_OK) return ps;
   const long long n = local_cells(c);
   const size_t bytes = (size_t)n * c->q * sizeof(double);
   lbm_status s = ensure_staging(c, bytes);
@@ -1031,6 +1084,7 @@ lbm_status lbm_get_diagnostics(lbm_ctx *c, lbm_diagnostics *out) {
   NvtxRange nvtx_("lbm_get_diagnostics");
   if (!c || !out) return fail(c, LBM_EINVAL, "null argument");
   LBM_CUDA(c, cudaSetDevice(c->device));
+  if (lbm_status ps = peer_refresh(c); ps != LBM_OK) return ps;
   const size_t pbytes = (size_t)5 * lbm::DIAG_GRID * sizeof(double);
   lbm_status s = ensure_staging(c, pbytes + 5 * sizeof(double));
   if (s != LBM_OK) return s;
@@ -1058,6 +1112,7 @@ lbm_status lbm_get_cells(lbm_ctx *c, const long long *cells, long long n, double
   for (long long k = 0; k < n; ++k)
     if (cells[k] < 0 || cells[k] >= ncell) return fail(c, LBM_EINVAL, "cell index out of range");
   LBM_CUDA(c, cudaSetDevice(c->device));
+  if (lbm_status ps = peer_refresh(c); ps != LBM_OK) return ps;
   const size_t ibytes = (size_t)n * sizeof(long long), obytes = (size_t)n * c->q * sizeof(double);
   lbm_status s = ensure_staging(c, ibytes + obytes + 256);
   if (s != LBM_OK) return s;

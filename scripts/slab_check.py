@@ -69,8 +69,6 @@ def main():
         if "walls" in name:
             bc = [[0, 0], [0, 0], [L.LBM_BC_NOSLIP, L.LBM_BC_NOSLIP]]
         streaming = L.LBM_AA if name.endswith("AA") else L.LBM_PULL
-        if args.halo == "peer" and streaming != L.LBM_PULL:
-            continue  # the fused push is a pull-streaming path
         stream = torch.cuda.Stream()
         torch.cuda.set_stream(stream)
         lat = L.Lattice(st, space, eq, rates, shape, zero_centered=zc, bc=bc, swe_g=g, device=dev,

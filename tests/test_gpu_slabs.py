@@ -86,10 +86,11 @@ def test_aa_slabs_equal_single_rank_bitwise(st, space, eq, zc, nranks, steps):
 
 
 # ----------------------------------------------------------- fused halo push (lbm_peer_*)
-def run_slabs_peer(st, space, eq, zc, rates, shape, f0, steps, nranks, bc=None, reprime_at=None):
+def run_slabs_peer(st, space, eq, zc, rates, shape, f0, steps, nranks, bc=None, reprime_at=None,
+                   streaming=L.LBM_PULL):
     slab_axis = 2 if W.DIM_OF[st] == 2 else 1
-    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, bc=bc, rank=r, nranks=nranks)
-            for r in range(nranks)]
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, bc=bc, rank=r, nranks=nranks,
+                      streaming=streaming) for r in range(nranks)]
 
     def load(f):
         for lat in lats:
@@ -160,7 +161,7 @@ def test_peer_rejects_mismatched_ring():
     with pytest.raises(L.LbmError):
         a.peer_connect(ia, ia)  # wrong ranks
     a.peer_connect(ib, ib)
-    with L.Lattice(st, space, eq, rates, (16, 8, 8), streaming=L.LBM_AA, rank=0, nranks=2) as d:
+    with L.Lattice(st, space, eq, rates, (16, 8, 8)) as d:  # one rank: nothing to connect
         with pytest.raises(L.LbmError):
             d.peer_export()
     for x in (a, b, c):
@@ -258,3 +259,60 @@ def test_peer_push_graph_replay_bitwise(graphs, monkeypatch):
     for lat in lats:
         lat.close()
     np.testing.assert_array_equal(multi, single)
+
+
+@pytest.mark.parametrize("st,space,eq,zc,nranks", [
+    (W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1, 2),
+    (W.D3Q27, W.CENTRAL, W.EQ_ABSOLUTE, 1, 3),
+    (W.D3Q19, W.RAW, W.EQ_DELTA, 1, 4),
+    (W.D2Q9, W.CUMULANT, W.EQ_ABSOLUTE, 1, 4),
+])
+@pytest.mark.parametrize("steps,reprime", [(7, None), (8, None), (9, 4), (10, 3)])
+def test_peer_aa_equals_single_rank_bitwise(st, space, eq, zc, nranks, steps, reprime):
+    """Multi-rank AA with the fused peer path: the odd step's boundary kernels access the
+    neighbours' boundary planes directly (no ghost exchange); the canonical state read at
+    either parity (odd counts: refreshed ghost planes), incl. a reload + re-prime at both
+    parities, equals the single-rank run bitwise."""
+    shape = (20, 12, 1) if st == W.D2Q9 else (20, 10, 12)
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc) as lat:
+        lat.set_populations(f0)
+        lat.step(steps)
+        single = lat.get_populations()
+    multi = run_slabs_peer(st, space, eq, zc, rates, shape, f0, steps, nranks, reprime_at=reprime,
+                           streaming=L.LBM_AA)
+    np.testing.assert_array_equal(multi, single)
+
+
+def test_peer_aa_graph_replay_and_macroscopic():
+    """AA peer loop replayed from captured graphs (whole calls per context), then the
+    macroscopic fields and the diagnostics at the odd parity match the single-rank run."""
+    st, space, eq, zc = W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1
+    shape, nranks = (24, 10, 12), 3
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, streaming=L.LBM_AA) as lat:
+        lat.set_populations(f0)
+        lat.step(33 + 32)
+        rho1, u1 = lat.get_macroscopic()
+        f1 = lat.get_populations()
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, rank=r, nranks=nranks, streaming=L.LBM_AA)
+            for r in range(nranks)]
+    for lat in lats:
+        lat.set_populations(np.ascontiguousarray(f0[:, lat.offset:lat.offset + lat.extent]))
+    D.connect_local(lats)
+    for n in (33, 32):
+        for lat in lats:
+            lat.step_peer(n)
+    for lat in lats:
+        lat.sync()
+        assert not lat.peer_timed_out()
+    rho = np.concatenate([lat.get_macroscopic()[0] for lat in lats], axis=0)
+    u = np.concatenate([lat.get_macroscopic()[1] for lat in lats], axis=1)
+    f = np.concatenate([lat.get_populations() for lat in lats], axis=1)
+    for lat in lats:
+        lat.close()
+    np.testing.assert_array_equal(f, f1)
+    np.testing.assert_array_equal(rho, rho1)
+    np.testing.assert_array_equal(u, u1)
