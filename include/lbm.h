@@ -188,12 +188,16 @@ lbm_status lbm_get_halo(lbm_ctx *ctx, int which, lbm_halo *out);
 
 lbm_status lbm_sync(lbm_ctx *ctx);
 
-/* Fused halo push between slab contexts (PULL, nranks > 1).  Instead of a
-   separate exchange, the kernel of a step's two boundary planes stores the slab-crossing
-   populations (slab component -1 of plane 0, +1 of the last plane) straight into the
-   neighbours' ghost planes of the next grid, over NVLink peer memory (CUDA IPC) or, for
-   contexts of one process, plain device pointers; completion is signalled through
-   system-scope flags in the neighbours' memory, so no host or NCCL call sits between steps.
+/* Fused halo exchange between slab contexts (nranks > 1) over NVLink peer
+   memory (CUDA IPC) or, for contexts of one process, plain device pointers.
+   PULL: the kernel of a step's two boundary planes also stores the slab-crossing populations
+   (slab component -1 of plane 0, +1 of the last plane) straight into the neighbours' ghost
+   planes of the next grid.  AA: the odd step's boundary kernels read and write the
+   neighbours' adjacent boundary planes directly (the odd step is race-free on the global
+   lattice, so no ghost data moves at all); the even step is local.  Completion is signalled
+   through system-scope flags in the neighbours' memory, so no host or NCCL call sits between
+   steps.  Canonical reads after an odd AA step first copy the crossing values back into the
+   ghost planes (neighbours must not have started their next step).
    Collective protocol: every rank calls lbm_peer_export, the infos are exchanged (any host
    transport), every rank calls lbm_peer_connect with its lower and upper neighbour's info
    (periodic ring along the slab axis), all ranks pass a barrier, then lbm_peer_prime
@@ -212,10 +216,11 @@ typedef struct {
 } lbm_peer_info;
 lbm_status lbm_peer_export(lbm_ctx *ctx, lbm_peer_info *out);
 /* Maps the neighbours' grids and flags; LBM_EINVAL if their lattice, stencil, precision or
-   ranks do not match this context's ring; LBM_EUNSUPPORTED for in-place streaming or one
-   rank; LBM_ECUDA if the memory cannot be mapped (no peer access). Resets the flags. */
+   ranks do not match this context's ring; LBM_EUNSUPPORTED for Esoteric Pull or one rank
+   (at export); LBM_ECUDA if the memory cannot be mapped (no peer access). Resets the flags. */
 lbm_status lbm_peer_connect(lbm_ctx *ctx, const lbm_peer_info *lower, const lbm_peer_info *upper);
-/* Pushes the current grid's boundary planes into the neighbours' ghost planes. */
+/* PULL: pushes the current grid's boundary planes into the neighbours' ghost planes; AA:
+   only the handshake (orders the neighbours' initialisation before the first step). */
 lbm_status lbm_peer_prime(lbm_ctx *ctx);
 /* n time steps with the fused halo push (asynchronous on the context stream).  The phase
    counters live on the device, so the loop is a fixed launch sequence: n >= 32 replays
