@@ -132,3 +132,63 @@ def test_halo_blocks_are_the_crossing_populations():
         assert (lay.aa_pre_send_hi // lay.plane, lay.aa_pre_send_hi % lay.plane) == (top, down[0] * lay.pop)
         assert (lay.aa_post_send_lo, lay.aa_post_send_hi) == (lay.aa_pre_recv_lo, lay.aa_pre_recv_hi)
         assert (lay.aa_post_recv_lo, lay.aa_post_recv_hi) == (lay.aa_pre_send_lo, lay.aa_pre_send_hi)
+
+
+class _FakePeerLattice:
+    """Stands in for a Lattice in PeerRunner's host protocol (no device): records the
+    calls and the neighbour infos it was connected with."""
+
+    def __init__(self, rank, nranks):
+        self.rank, self.nranks, self.calls = rank, nranks, []
+
+    def peer_export(self):
+        info = L.lbm_peer_info()
+        info.rank, info.nranks, info.pid = self.rank, self.nranks, os.getpid()
+        self.calls.append("export")
+        return bytes(info)
+
+    def peer_connect(self, lower, upper):
+        lo = L.lbm_peer_info.from_buffer_copy(lower)
+        hi = L.lbm_peer_info.from_buffer_copy(upper)
+        self.calls.append(("connect", lo.rank, hi.rank))
+
+    def sync(self):
+        self.calls.append("sync")
+
+    def peer_prime(self):
+        self.calls.append("prime")
+
+    def step_peer(self, n):
+        self.calls.append(("step", n))
+
+    def peer_timed_out(self):
+        return False
+
+
+def _peer_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lat = _FakePeerLattice(rank, world)
+        runner = D.PeerRunner(lat, rank, world)
+        runner.prime()
+        runner.step(7)
+        runner.check()
+        out[rank] = lat.calls
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_runner_host_protocol(world):
+    """PeerRunner (the fused-halo driver) on gloo: every rank exports, gathers all infos,
+    connects to its periodic lower / upper neighbours, synchronises before the barrier,
+    primes, then steps with one library call."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_peer_worker, args=(world, free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        calls = out[r]
+        lo, hi = (r - 1) % world, (r + 1) % world
+        assert calls == ["export", ("connect", lo, hi), "sync", "sync", "prime", ("step", 7)], calls
