@@ -96,7 +96,7 @@ typedef struct {
   int nx, ny, nz;  /* GLOBAL lattice extents; D2Q9: nz = 1 (the slab axis is then y)        */
   int bc[3][2];    /* [axis][low, high] lbm_bc; periodic must be set on both faces of an axis */
   int precision;   /* lbm_precision (storage and arithmetic precision)                        */
-  int streaming;   /* lbm_streaming; LBM_AA needs nranks == 1 and all faces periodic          */
+  int streaming;   /* lbm_streaming; in place: all faces periodic (Esoteric Pull: one rank)   */
   double swe_g;    /* lattice gravity g (LBM_EQ_SWE only)                                     */
   int device;      /* CUDA device ordinal                                                     */
   void *stream;    /* cudaStream_t to enqueue on, or NULL: the library creates its own        */
