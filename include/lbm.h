@@ -141,10 +141,11 @@ typedef struct {
                                variable LBM_RATE_SPECIALIZATION=0 to force 0.            */
   int temporal_blocking;    /* time steps per sweep of lbm_step: 2 when pairs of steps are
                                fused (D3Q19 fp64, pull, single rank, periodic, nx % 16 == 0,
-                               ny % 8 == 0, >= 1184 16x8 tile columns; the intermediate step
-                               stays in shared memory; same arithmetic, bitwise equal), else
-                               1.  Environment LBM_TEMPORAL_BLOCKING: 0 (read at create)
-                               forces 1; 1 drops the tile-count condition.                 */
+                               ny % 8 == 0, >= 1184 CTAs = 16x8 tile columns x slab chunks of
+                               >= 32 planes; the intermediate step stays in shared memory;
+                               same arithmetic, bitwise equal), else 1.  Environment
+                               LBM_TEMPORAL_BLOCKING: 0 (read at create) forces 1; 1 drops
+                               the CTA-count condition.                                    */
   int cuda_graph_steps;     /* time steps per CUDA-graph launch of lbm_step (0: none).  Small
                                single-rank lattices (<= 2^20 cells) are launch-bound: the
                                first lbm_step call captures 32 single steps from each storage

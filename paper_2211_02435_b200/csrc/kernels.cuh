@@ -450,7 +450,10 @@ __global__ void __launch_bounds__(Tile2<TX, TY>::THREADS, 1)
   const bool act2 = t < TX * TY;
   const int ix = t % TX, iy = t / TX;
   const int n = g.nzl;
-  for (int k = -1; k <= n; ++k) {
+  // blockIdx.z: chunk [p0, p1) of the output planes (more CTAs for short slabs); each chunk
+  // recomputes the two step-(t+1) planes at its ends
+  const int p0 = (int)((long long)n * blockIdx.z / gridDim.z), p1 = (int)((long long)n * (blockIdx.z + 1) / gridDim.z);
+  for (int k = p0 - 1; k <= p1; ++k) {
     if (act1) {
       const int zc = wrapi(k, n);
       long long zo[3];
@@ -462,11 +465,11 @@ __global__ void __launch_bounds__(Tile2<TX, TY>::THREADS, 1)
         f[i] = ld_nc(src + zo[1 - cz] + (long long)i * g.pop + ys[1 - cy] + xs[1 - cx]);
       });
       collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
-      real *slot = ring + (size_t)((k + 3) % 3) * S::Q * T::HW;
+      real *slot = ring + (size_t)((k + 3) % 3) * S::Q * T::HW;  // k >= -1
       sfor<S::Q>([&](auto i) { slot[i * T::HW + t] = f[i]; });
     }
     __syncthreads();
-    if (k >= 1 && act2) {
+    if (k >= p0 + 1 && act2) {
       const int p = k - 1;  // plane of step t+2
       real f[S::Q];
       sfor<S::Q>([&](auto i) {

@@ -44,7 +44,7 @@ struct Ops {
   void (*attributes)(int *regs, int *local_bytes);
   // two fused pull steps (temporal blocking; 3D, single rank, periodic); tile TX x TY
   // (0 x 0: not provided).  Requires nx % TX == 0 and ny % TY == 0.
-  void (*pull2)(const void *src, void *dst, const GridParams &g, const void *params, double swe_g,
+  void (*pull2)(const void *src, void *dst, const GridParams &g, const void *params, double swe_g, int zchunks,
                 cudaStream_t s);
   int tile_x, tile_y;
 };
@@ -153,7 +153,7 @@ struct OpsImpl {
     k_diag_final<double><<<1, DIAG_BLOCK, 0, s>>>(partial, out);
   }
   static void pull2(const void *src, void *dst, const GridParams &g, const void *params, double swe_g,
-                    cudaStream_t s) {
+                    int zchunks, cudaStream_t s) {
     constexpr int TX = TbTile<S, real>::TX, TY = TbTile<S, real>::TY;
     if constexpr (S::D == 3 && TX > 0) {
       using T = Tile2<TX, TY>;
@@ -165,7 +165,7 @@ struct OpsImpl {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
       }
-      kern<<<dim3((unsigned)(g.nx / TX), (unsigned)(g.ny / TY), 1), T::THREADS, smem, s>>>(
+      kern<<<dim3((unsigned)(g.nx / TX), (unsigned)(g.ny / TY), (unsigned)zchunks), T::THREADS, smem, s>>>(
           static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
     }
   }

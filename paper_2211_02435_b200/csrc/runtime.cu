@@ -210,14 +210,35 @@ bool graphs_enabled() {
 }
 
 // two fused pull steps available for this context and its current kernels
+// Temporal blocking: CTAs (tile columns x slab chunks) for >= 4 waves (148 SMs x 2 CTAs),
+// slab chunks of >= 32 planes (each chunk recomputes two step-(t+1) planes).
+constexpr long long kTbMinCtas = 4 * 2 * 148;
+constexpr int kTbMinChunkPlanes = 32;
+
+long long tb_tiles(const lbm_ctx *c) {
+  return (long long)(c->g.nx / c->ops->tile_x) * (c->g.ny / c->ops->tile_y);
+}
+
+int tb_zchunks(const lbm_ctx *c) {
+  const int n = c->g.nzl;
+  if (const char *e = getenv("LBM_TB_ZCHUNKS")) {  // test hook
+    const int k = atoi(e);
+    return k < 1 ? 1 : (k > n ? n : k);
+  }
+  const long long tiles = tb_tiles(c);
+  const long long need = (kTbMinCtas + tiles - 1) / tiles;
+  const int maxch = n / kTbMinChunkPlanes > 1 ? n / kTbMinChunkPlanes : 1;
+  return (int)(need < maxch ? need : maxch);
+}
+
 bool use_temporal_blocking(const lbm_ctx *c) {
   if (!(c->tb_allowed && c->ops->pull2 && c->ops->tile_x > 0 && c->g.nx % c->ops->tile_x == 0 &&
         c->g.ny % c->ops->tile_y == 0))
     return false;
-  // >= 4 waves of tile columns (148 SMs x 2 CTAs): fewer leave the fused sweep tail-bound
-  const long long tiles = (long long)(c->g.nx / c->ops->tile_x) * (c->g.ny / c->ops->tile_y);
   const char *env = getenv("LBM_TEMPORAL_BLOCKING");
-  return tiles >= 4 * 2 * 148 || (env && env[0] == '1');
+  if (env && env[0] == '1') return true;
+  // fewer CTAs than 4 waves leave the fused sweep tail-bound
+  return tb_tiles(c) * tb_zchunks(c) >= kTbMinCtas;
 }
 
 // graph replay: small single-rank lattice on a capturable stream; LBM_CUDA_GRAPHS=0 disables
@@ -745,7 +766,7 @@ lbm_status lbm_step(lbm_ctx *c, int n) {
   }
   if (use_temporal_blocking(c)) {  // pairs of steps fused in one sweep (k_pull2)
     for (; t + 2 <= n; t += 2) {
-      c->ops->pull2(c->buf[c->cur], c->buf[1 - c->cur], g, c->params, c->swe_g, c->stream);
+      c->ops->pull2(c->buf[c->cur], c->buf[1 - c->cur], g, c->params, c->swe_g, tb_zchunks(c), c->stream);
       c->cur ^= 1;
       c->steps += 2;
     }
