@@ -35,7 +35,10 @@
  *   * streaming: two-grid pull, f_i(x, t+1) = f*_i(x - xi_i, t)
  *     (eq:LbStreaming PAPER.md:223-224, pull pattern PAPER.md:857-859),
  *     periodic faces, or half-way bounce-back on no-slip faces (not in the
- *     paper; reading R18).
+ *     paper; reading R18);
+ *   * body force (source q^F of eq:MrtUpdateGeneral):
+ *     Guo's F^G with q^F = (I - S/2) T(F^G) for the linear spaces (reading R23),
+ *     F on the first-order cumulants only for the cumulant space (reading R26).
  *
  * Templated on the real type: the long double (x87 80-bit) instantiation is
  * the parity reference, the double instantiation is the timed CPU baseline.
@@ -559,8 +562,8 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
   R FG[27], qF[27];
   for (int i = 0; i < q; ++i) FG[i] = 0;
   if (m.forced) {
-    if (m.space == SP_CUMULANT || m.eq == EQ_SWE) return false;  // not provided (reading R23)
-    guo_force(m, u, FG);
+    if (m.eq == EQ_SWE) return false;             // not provided (reading R23)
+    if (m.space != SP_CUMULANT) guo_force(m, u, FG);  // cumulants: reading R26 below
   }
 
   if (m.space == SP_POPULATION) {
@@ -650,11 +653,14 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
     const int *e = m.mono[k].data();
     if (e[0] + e[1] + e[2] >= 2) Cs.c[sidx(e)] = Cstar_mono[k];
   }
-  // conserved first-order entries pass through unchanged
+  // conserved first-order entries pass through unchanged.  With a body
+  // force (reading R26) the source q^F is F on the first-order cumulants and zero on every
+  // cumulant of order >= 2: with u = (j + F/2)/rho the first-order entry is kappa_100 = -F_x/2
+  // and becomes kappa*_100 = kappa_100 + F_x, the momentum gains F.
   const int e100[3] = {1, 0, 0}, e010[3] = {0, 1, 0}, e001[3] = {0, 0, 1};
-  Cs.c[sidx(e100)] = C.c[sidx(e100)];
-  Cs.c[sidx(e010)] = C.c[sidx(e010)];
-  Cs.c[sidx(e001)] = C.c[sidx(e001)];
+  Cs.c[sidx(e100)] = C.c[sidx(e100)] + m.F[0];
+  Cs.c[sidx(e010)] = C.c[sidx(e010)] + m.F[1];
+  Cs.c[sidx(e001)] = C.c[sidx(e001)] + m.F[2];
   R ks27[27];
   central_from_cumulants(Cs, rho, ks27);
   for (int p = 0; p < q; ++p) {

@@ -25,7 +25,8 @@ MUTANTS = [
     ("series log: wrong sign", "R sgn = (n % 2 == 1) ? R(1) : R(-1);", "R sgn = R(1);"),
     # EQUIVALENT mutant, expected to survive: S^6 reaches degree <= 6 only through six first-order
     # factors, and the oracle takes the log of the CENTRAL moment series, whose first-order
-    # coefficients vanish (kappa_100 = 0) - the n = 6 term is identically zero in every use.
+    # coefficients vanish (kappa_100 = 0) - the n = 6 term is identically zero in every unforced
+    # use; with a body force (R26) kappa_100 = -F/2 and the term is O((F/2 rho)^6) ~ 1e-24.
     ("series log: stop at n = 5 [equivalent]", "for (int n = 1; n <= 6; ++n) {\n    R sgn",
      "for (int n = 1; n <= 5; ++n) {\n    R sgn"),
     ("series exp: drop 1/n!", "for (int k = 0; k < 27; ++k) acc.c[k] += pw.c[k] / fact;",
@@ -51,6 +52,11 @@ MUTANTS = [
      "const R cs2 = (m.eq == EQ_SWE) ? m.g * rho : R(CS2);\n  for"),
     ("velocity: u = j (no division by rho)", "u[a] = (j[a] + R(half) * m.F[a] / R(2)) / rho;",
      "u[a] = (j[a] + R(half) * m.F[a] / R(2));"),
+    ("cumulant force: F/2 instead of F on the first-order cumulants (R26)",
+     "Cs.c[sidx(e100)] = C.c[sidx(e100)] + m.F[0];", "Cs.c[sidx(e100)] = C.c[sidx(e100)] + m.F[0] / R(2);"),
+    ("cumulant force: source also on the cumulants of order >= 2 (R26)",
+     "Cstar_poly[p] = Cpoly[p] + m.omega[p] * (ceq - Cpoly[p]);",
+     "Cstar_poly[p] = Cpoly[p] + m.omega[p] * (ceq - Cpoly[p]) + m.F[0];"),
     ("stencil order: swap (1,1) and (-1,-1) in-plane", "{1, 1}, {-1, -1}, {1, -1}, {-1, 1}};",
      "{-1, -1}, {1, 1}, {1, -1}, {-1, 1}};"),
 ]

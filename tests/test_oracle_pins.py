@@ -506,9 +506,9 @@ FORCE = np.array([2e-4, -1e-4, 3e-4])
 
 
 @pytest.mark.parametrize("st", STENCILS)
-@pytest.mark.parametrize("space", [W.POPULATION, W.RAW, W.CENTRAL])
+@pytest.mark.parametrize("space", [W.POPULATION, W.RAW, W.CENTRAL, W.CUMULANT])
 def test_force_momentum_and_paper_example(st, space):
-    """Body force (reading R23): per cell the mass is unchanged and the momentum gains F;
+    """Body force (readings R23, R26): per cell the mass is unchanged and the momentum gains F;
     written as the paper's worked example: with u = (j + F/2)/rho the
     post-collision first-order raw moment is m*_{10|0} = rho u_x + F_x / 2."""
     xi, opp, w, M, Minv = oracle.tables(st)
@@ -524,12 +524,46 @@ def test_force_momentum_and_paper_example(st, space):
         fo_abs = fo + w if zc else fo
         np.testing.assert_allclose(fo_abs.sum(1), rho, atol=1e-15)
         np.testing.assert_allclose(fo_abs @ xi, rho[:, None] * u + F / 2, atol=1e-16)
-    with pytest.raises(RuntimeError):
-        oracle.collide(st, W.CUMULANT, W.EQ_ABSOLUTE, 1, rates_for(st, W.CUMULANT), fa - w, force=F)
+
+
+def test_force_shallow_water_unsupported():
+    """No force model for the shallow-water methods (reading R23)."""
+    xi, opp, w, M, Minv = oracle.tables(W.D2Q9)
+    f = np.tile(2.0 * w, (3, 1))
+    for space in (W.CENTRAL, W.CUMULANT):
+        with pytest.raises(RuntimeError):
+            oracle.collide(W.D2Q9, space, W.EQ_SWE, 0, W.rate_set_p(W.D2Q9), f, g=0.0613125,
+                           force=[1e-4, 0, 0])
+
+
+@pytest.mark.parametrize("st", [W.D2Q9, W.D3Q27])
+def test_cumulant_force_is_first_order_only(st):
+    """Reading R26: the cumulant source q^F is F on the first-order cumulants and zero on every
+    cumulant of order >= 2.  Cumulants of order >= 2 do not depend on the frame (PAPER.md:411,
+    eq:CumulantAndCentralMomentGenFuncs), so the forced and the unforced collision of the same
+    cell leave IDENTICAL cumulants of order >= 2 (computed from the outputs by the pinned
+    generating-function transform) and differ in momentum by exactly F.  Full stencils only:
+    there the populations determine all 3^d monomial cumulants."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    F = FORCE.copy()
+    if W.DIM_OF[st] == 2:
+        F[2] = 0
+    fa = random_cells(st, 12)
+    rates = W.rates_random(st, seed=5)
+    plain = oracle.collide(st, W.CUMULANT, W.EQ_ABSOLUTE, 0, rates, fa)
+    forced = oracle.collide(st, W.CUMULANT, W.EQ_ABSOLUTE, 0, rates, fa, force=F)
+    _, c_plain, _, _ = oracle.central_and_cumulants(st, plain)
+    _, c_forced, _, _ = oracle.central_and_cumulants(st, forced)
+    order = np.array([k % 3 + (k // 3) % 3 + k // 9 for k in range(27)])
+    hi = order >= 2
+    np.testing.assert_allclose(c_forced[:, hi], c_plain[:, hi], atol=1e-15)
+    assert np.abs(c_forced[:, hi] - c_plain[:, hi]).max() < 1e-3 * np.abs(F).max()
+    np.testing.assert_allclose(forced @ xi - plain @ xi, np.tile(F, (len(fa), 1)), atol=1e-16)
+    np.testing.assert_allclose(forced.sum(1), plain.sum(1), atol=1e-15)
 
 
 @pytest.mark.parametrize("st", STENCILS)
-@pytest.mark.parametrize("space", [W.POPULATION, W.RAW, W.CENTRAL])
+@pytest.mark.parametrize("space", [W.POPULATION, W.RAW, W.CENTRAL, W.CUMULANT])
 def test_force_isotropy(st, space):
     """Rotating the cell and the force together commutes with the forced collision."""
     xi, opp, w, M, Minv = oracle.tables(st)
@@ -538,17 +572,18 @@ def test_force_isotropy(st, space):
         F[2] = 0
     fa = random_cells(st, 8)
     rates = np.array([1.3]) if space == W.POPULATION else W.rate_set_p(st)
-    out = oracle.collide(st, space, W.EQ_DELTA, 1, rates, fa - w, force=F)
+    eq = W.EQ_ABSOLUTE if space == W.CUMULANT else W.EQ_DELTA
+    out = oracle.collide(st, space, eq, 1, rates, fa - w, force=F)
     for P in symmetry_generators(W.DIM_OF[st]):
         img = xi @ P.T
         perm = [int(np.flatnonzero((xi == img[i]).all(1))[0]) for i in range(len(w))]
         rot_in = np.empty_like(fa)
         rot_in[:, perm] = fa - w
-        rot_out = oracle.collide(st, space, W.EQ_DELTA, 1, rates, rot_in, force=P @ F)
+        rot_out = oracle.collide(st, space, eq, 1, rates, rot_in, force=P @ F)
         np.testing.assert_allclose(rot_out[:, perm], out, atol=2e-16)
 
 
-@pytest.mark.parametrize("space,nu", [(W.POPULATION, 1 / 6), (W.RAW, 0.1), (W.CENTRAL, 0.05)])
+@pytest.mark.parametrize("space,nu", [(W.POPULATION, 1 / 6), (W.RAW, 0.1), (W.CENTRAL, 0.05), (W.CUMULANT, 0.08)])
 def test_poiseuille_flow(space, nu):
     """Force-driven channel between half-way bounce-back walls (readings R18, R23): the steady
     profile is u_x(y) = F / (2 nu) (y + 1/2)(H - 1/2 - y) (walls half a node outside)."""
@@ -556,7 +591,8 @@ def test_poiseuille_flow(space, nu):
     om = W.omega_from_nu(nu)
     rates = [om] if space == W.POPULATION else W.regularized_rates(st, om)
     bc = [[W.PERIODIC, W.PERIODIC], [W.NOSLIP, W.NOSLIP], [W.PERIODIC, W.PERIODIC]]
-    sim = oracle.Sim(st, space, W.EQ_DELTA, 1, rates, (nx, ny, 1), bc=bc)
+    eq = W.EQ_ABSOLUTE if space == W.CUMULANT else W.EQ_DELTA
+    sim = oracle.Sim(st, space, eq, 1, rates, (nx, ny, 1), bc=bc)
     sim.set(np.zeros((9, 1, ny, nx)))
     sim.set_force([Fx, 0, 0])
     sim.step(int(8 * ny * ny / nu))
