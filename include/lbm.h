@@ -244,8 +244,10 @@ lbm_status lbm_get_populations(lbm_ctx *ctx, double *f);
    (reading R23): u = (j + F/2) / rho and q^F = (I - S/2) T(F^G) with
    F^G_i = w_i [3 xi.F + 9 (xi.u)(xi.F) - 3 u.F]; the momentum gains F per step (kappa_100 = -F/2
    before, +F/2 after the collision).  Velocities reported for the
-   post-collision state are (j - F/2) / rho.  LBM_EUNSUPPORTED for cumulant and shallow-water
-   methods.  A zero force restores the unforced kernels. */
+   post-collision state are (j - F/2) / rho.  Cumulant methods (reading R26): q^F is F on the
+   first-order cumulants and zero on all cumulants of order >= 2 (no T(F^G) exists for the
+   nonlinear transform; Guo's source has no second-order central moments).
+   LBM_EUNSUPPORTED for the shallow-water methods.  A zero force restores the unforced kernels. */
 lbm_status lbm_set_force(lbm_ctx *ctx, const double *force);
 /* Global sums over this rank's slab of the canonical state, on the device in fp64 with a
    fixed (deterministic) summation order: mass = sum rho, momentum = sum rho u (physical

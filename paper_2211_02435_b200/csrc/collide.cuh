@@ -725,8 +725,14 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
   constexpr bool zc = (REG != REG_ABS);
   constexpr int NC = S::NC;
   constexpr bool FORCED = (RS & RS_FORCE) != 0;
-  static_assert(!FORCED || SPACE == SPACE_POPULATION || SPACE == SPACE_RAW || SPACE == SPACE_CENTRAL,
-                "forcing is provided for population, raw and central-moment collisions");
+  static_assert(!FORCED || SPACE == SPACE_POPULATION || SPACE == SPACE_RAW || SPACE == SPACE_CENTRAL ||
+                    SPACE == SPACE_CUMULANT,
+                "forcing is provided for population, raw-moment, central-moment and cumulant collisions");
+  // cumulants (reading R26): the source is F on the first-order cumulants only.  Cumulants of
+  // order >= 2 do not depend on the frame, so the forward transform is taken
+  // about u0 = j / rho (kappa_100 = 0) instead of the shifted u = (j + F/2)/rho
+  // (kappa_100 = -F_x/2), and the backward one about the post-collision mean (j + F)/rho.
+  constexpr bool SHIFT_U = FORCED && SPACE != SPACE_CUMULANT;
   constexpr int RSR = RS & 3;  // rate specialisation proper
   real c[NC];
   sfor<NC>([&](auto k) { c[k] = real(0); });
@@ -798,7 +804,7 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
     real jz = real(0);
     if constexpr (S::D == 3) jz = c[E(0, 0, 1)];
     real ux = jx * inv, uy = jy * inv, uz = jz * inv;
-    if constexpr (FORCED) {  // u = (j + F/2) / rho
+    if constexpr (SHIFT_U) {  // u = (j + F/2) / rho
       ux = fma(real(0.5) * fr.F[0], inv, ux);
       uy = fma(real(0.5) * fr.F[1], inv, uy);
       uz = fma(real(0.5) * fr.F[2], inv, uz);
@@ -837,9 +843,9 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
         // collapse conserved central moments: kappa_000 = rho, kappa_100 = -F_x/2 (= 0 without a
         // force)
         c[0] = rho;
-        c[E(1, 0, 0)] = FORCED ? real(-0.5) * fr.F[0] : real(0);
-        c[E(0, 1, 0)] = FORCED ? real(-0.5) * fr.F[1] : real(0);
-        if constexpr (S::D == 3) c[E(0, 0, 1)] = FORCED ? real(-0.5) * fr.F[2] : real(0);
+        c[E(1, 0, 0)] = SHIFT_U ? real(-0.5) * fr.F[0] : real(0);
+        c[E(0, 1, 0)] = SHIFT_U ? real(-0.5) * fr.F[1] : real(0);
+        if constexpr (S::D == 3) c[E(0, 0, 1)] = SHIFT_U ? real(-0.5) * fr.F[2] : real(0);
       }
       if constexpr (SPACE == SPACE_CENTRAL) {
         if constexpr (REG == REG_DELTA) {
@@ -880,6 +886,11 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
         EqCumulant<real> eq{rho * cs2};
         if constexpr (S::D == 3) relax_basis3<S, RSR>(c, eq, r); else relax_basis2<RSR>(c, eq, r);
         if constexpr (S::D == 3) cumulant_to_central3<S>(c, inv); else cumulant_to_central2(c, inv);
+        if constexpr (FORCED) {  // C*_100 = C_100 + F_x: the post-collision mean is (j + F)/rho
+          ux = fma(fr.F[0], inv, ux);
+          uy = fma(fr.F[1], inv, uy);
+          uz = fma(fr.F[2], inv, uz);
+        }
       }
       // ---- central -> raw
       if constexpr (S::D == 3) bin_bwd3(c, ux, uy, uz); else bin_bwd2(c, ux, uy);

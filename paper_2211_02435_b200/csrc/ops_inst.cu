@@ -24,8 +24,8 @@ constexpr int SP = LBM_SPACE;
 namespace lbm {
 template <class St_, int SP_, int REG_, class Re_>
 const Ops *with_rs(int rs) {
-  // body force (Guo, reading R23): population, raw and central-moment collisions
-  if constexpr (SP_ == SPACE_POPULATION || SP_ == SPACE_RAW || SP_ == SPACE_CENTRAL) {
+  // body force (Guo, reading R23; cumulants: reading R26): all but the shallow-water methods
+  if constexpr (SP_ == SPACE_POPULATION || SP_ == SPACE_RAW || SP_ == SPACE_CENTRAL || SP_ == SPACE_CUMULANT) {
     if (rs == (RS_GENERAL | RS_FORCE)) return &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL | RS_FORCE>::table;
   }
   if (rs & RS_FORCE) return nullptr;

@@ -1085,9 +1085,11 @@ lbm_status lbm_set_force(lbm_ctx *c, const double *force) {
   if (c->d == 2 && force[2] != 0.0) return fail(c, LBM_EINVAL, "a D2Q9 force has no z component");
   const bool any = force[0] != 0.0 || force[1] != 0.0 || force[2] != 0.0;
   if (any) {
-    if (!(c->kspace == LBM_SPACE_POPULATION || c->kspace == LBM_SPACE_RAW || c->kspace == LBM_SPACE_CENTRAL))
+    if (!(c->kspace == LBM_SPACE_POPULATION || c->kspace == LBM_SPACE_RAW || c->kspace == LBM_SPACE_CENTRAL ||
+          c->kspace == LBM_SPACE_CUMULANT))
       return fail(c, LBM_EUNSUPPORTED,
-                  "a body force is provided for population, raw- and central-moment collisions (reading R23)");
+                  "a body force is provided for population, raw-moment, central-moment and cumulant collisions "
+                  "(readings R23, R26), not for shallow water");
     const Ops *f = find_ops(c->stencil, c->prec, c->kspace, c->regime, lbm::RS_GENERAL | lbm::RS_FORCE);
     if (!f) return fail(c, LBM_EUNSUPPORTED, "no forced kernel instantiated for this combination");
     c->ops = f;
