@@ -56,6 +56,10 @@ def lib():
         L.oracle_collide_forced.argtypes = [ctypes.c_int] * 4 + [dp, ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                                                  dp, dp, dp, ctypes.c_longlong]
         L.oracle_sim_set_force.argtypes = [ctypes.c_void_p, dp]
+        L.oracle_collide_forced_model.argtypes = [ctypes.c_int] * 4 + [dp, ctypes.c_int, ctypes.c_double,
+                                                                       ctypes.c_int, dp, ctypes.c_int, dp, dp,
+                                                                       ctypes.c_longlong]
+        L.oracle_sim_set_force_model.argtypes = [ctypes.c_void_p, ctypes.c_int]
         L.oracle_max_threads.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         _LIB = L
@@ -87,16 +91,19 @@ def tables(stencil: int):
             M[: n * n].reshape(n, n).copy(), Minv[: n * n].reshape(n, n).copy())
 
 
-def collide(stencil, space, eq, zc, rates, f_in, g=0.0, prec=LONG_DOUBLE, force=None):
+GUO, HE = 0, 1  # force models (readings R23, R27)
+
+
+def collide(stencil, space, eq, zc, rates, f_in, g=0.0, prec=LONG_DOUBLE, force=None, force_model=GUO):
     """Collision of independent cells; f_in [n, q] in stored form; optional uniform body
-    force density force[3] (Guo forcing, reading R23)."""
+    force density force[3] (Guo forcing, reading R23, or He forcing, reading R27)."""
     f_in = np.ascontiguousarray(f_in, dtype=np.float64)
     out = np.empty_like(f_in)
     r = np.ascontiguousarray(rates, dtype=np.float64).reshape(-1)
     if force is not None:
         F = np.ascontiguousarray(np.asarray(force, dtype=np.float64).reshape(3))
-        rc = lib().oracle_collide_forced(stencil, space, eq, int(zc), _dp(r), r.size, float(g), prec, _dp(F),
-                                         _dp(f_in), _dp(out), f_in.shape[0])
+        rc = lib().oracle_collide_forced_model(stencil, space, eq, int(zc), _dp(r), r.size, float(g), prec,
+                                               _dp(F), int(force_model), _dp(f_in), _dp(out), f_in.shape[0])
     else:
         rc = lib().oracle_collide(stencil, space, eq, int(zc), _dp(r), r.size, float(g), prec, _dp(f_in),
                                   _dp(out), f_in.shape[0])
@@ -163,9 +170,11 @@ class Sim:
     def step(self, n=1):
         lib().oracle_sim_step(self._h, int(n))
 
-    def set_force(self, force):
+    def set_force(self, force, force_model=GUO):
         F = np.ascontiguousarray(np.asarray(force, dtype=np.float64).reshape(3))
         lib().oracle_sim_set_force(self._h, _dp(F))
+        if lib().oracle_sim_set_force_model(self._h, int(force_model)) != 0:
+            raise ValueError("unknown force model")
 
     def macroscopic(self):
         q, nz, ny, nx = self.shape

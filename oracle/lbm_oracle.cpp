@@ -37,7 +37,8 @@
  *     periodic faces, or half-way bounce-back on no-slip faces (not in the
  *     paper; reading R18);
  *   * body force (source q^F of eq:MrtUpdateGeneral):
- *     Guo's F^G with q^F = (I - S/2) T(F^G) for the linear spaces (reading R23),
+ *     Guo's F^G (reading R23) or He's F^He = f_eq (xi - u).F / (rho c_s^2) (reading R27)
+ *     with q^F = (I - S/2) T(F) for the linear spaces,
  *     F on the first-order cumulants only for the cumulant space (reading R26).
  *
  * Templated on the real type: the long double (x87 80-bit) instantiation is
@@ -308,6 +309,7 @@ template <class R> struct Method {
   R g = 0;  // SWE lattice gravity
   R F[3] = {0, 0, 0};  // uniform body force density (lattice units)
   bool forced = false;
+  int force_model = 0;  // 0: Guo (reading R23), 1: He (reading R27)
   std::vector<std::array<int, 3>> xi;
   std::vector<int> opp;
   std::vector<Poly> basis;
@@ -454,6 +456,23 @@ template <class R> static void guo_force(const Method<R> &m, const R u[3], R *FG
   }
 }
 
+template <class R> static bool equilibrium_cell(const Method<R> &m, R rho, const R u[3], R *f);
+
+/* He's force term F^He_i = f_eq_i(rho, u) (xi_i - u).F / (rho c_s^2) (He, Shan, Doolen 1998,  */
+/* cited at PAPER.md:214, 539; reading R27) with f_eq the method's own equilibrium            */
+/* (absolute populations); the source is q^F = (I - S/2) T(F^He) like Guo's.                   */
+template <class R> static bool he_force(const Method<R> &m, R rho, const R u[3], R *FG) {
+  R feq[27];
+  if (!equilibrium_cell(m, rho, u, feq)) return false;
+  for (int i = 0; i < m.q; ++i) {
+    R cF = 0;
+    for (int a = 0; a < 3; ++a) cF += (R(m.xi[i][a]) - u[a]) * m.F[a];
+    R fa = m.zc ? feq[i] + m.w[i] : feq[i];
+    FG[i] = fa * cF / (rho * R(CS2));
+  }
+  return true;
+}
+
 /* K(u)[p][i] = p(xi_i - u) */
 template <class R> static void central_matrix(const Method<R> &m, const R u[3], R *K) {
   int q = m.q;
@@ -563,7 +582,13 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
   for (int i = 0; i < q; ++i) FG[i] = 0;
   if (m.forced) {
     if (m.eq == EQ_SWE) return false;             // not provided (reading R23)
-    if (m.space != SP_CUMULANT) guo_force(m, u, FG);  // cumulants: reading R26 below
+    if (m.space != SP_CUMULANT) {  // cumulants: reading R26 below (the same for both models)
+      if (m.force_model == 1) {
+        if (!he_force(m, rho, u, FG)) return false;
+      } else {
+        guo_force(m, u, FG);
+      }
+    }
   }
 
   if (m.space == SP_POPULATION) {
@@ -809,12 +834,13 @@ int oracle_weights_ld(int stencil, long double *w) {
 namespace {
 template <class R>
 int collide_cells(int stencil, int space, int eq, int zc, const double *rates, int nrates, double g,
-                  const double *force, const double *fin, double *fout, long long n) {
+                  const double *force, const double *fin, double *fout, long long n, int force_model = 0) {
   Method<R> m;
   if (!build_method(m, stencil, space, eq, zc, rates, nrates, g)) return -1;
   if (force) {
     for (int a = 0; a < 3; ++a) m.F[a] = R(force[a]);
     m.forced = true;
+    m.force_model = force_model;
   }
   int bad = 0;
 #pragma omp parallel for reduction(+ : bad)
@@ -845,6 +871,16 @@ int oracle_collide_forced(int stencil, int space, int eq, int zc, const double *
   if (prec == 1)
     return collide_cells<long double>(stencil, space, eq, zc, rates, nrates, g, force, fin, fout, n);
   return collide_cells<double>(stencil, space, eq, zc, rates, nrates, g, force, fin, fout, n);
+}
+
+/* the same with the force model chosen: 0 Guo (reading R23), 1 He (reading R27) */
+int oracle_collide_forced_model(int stencil, int space, int eq, int zc, const double *rates, int nrates,
+                                double g, int prec, const double *force, int model, const double *fin,
+                                double *fout, long long n) {
+  if (model != 0 && model != 1) return -1;
+  if (prec == 1)
+    return collide_cells<long double>(stencil, space, eq, zc, rates, nrates, g, force, fin, fout, n, model);
+  return collide_cells<double>(stencil, space, eq, zc, rates, nrates, g, force, fin, fout, n, model);
 }
 
 /* equilibrium populations at given (rho, u[d]) per cell: f [n][q] stored form */
@@ -1011,6 +1047,17 @@ int oracle_sim_set_force(void *h, const double *force) {
     doit((Sim<long double> *)as->p);
   else
     doit((Sim<double> *)as->p);
+  return 0;
+}
+
+/* force model of the following steps: 0 Guo (reading R23), 1 He (reading R27) */
+int oracle_sim_set_force_model(void *h, int model) {
+  if (model != 0 && model != 1) return -1;
+  AnySim *as = (AnySim *)h;
+  if (as->prec == 1)
+    ((Sim<long double> *)as->p)->m.force_model = model;
+  else
+    ((Sim<double> *)as->p)->m.force_model = model;
   return 0;
 }
 

@@ -505,11 +505,12 @@ def test_tgv_energy_decay(space, eq, zc, nu):
 FORCE = np.array([2e-4, -1e-4, 3e-4])
 
 
+@pytest.mark.parametrize("model", [oracle.GUO, oracle.HE])
 @pytest.mark.parametrize("st", STENCILS)
 @pytest.mark.parametrize("space", [W.POPULATION, W.RAW, W.CENTRAL, W.CUMULANT])
-def test_force_momentum_and_paper_example(st, space):
-    """Body force (readings R23, R26): per cell the mass is unchanged and the momentum gains F;
-    written as the paper's worked example: with u = (j + F/2)/rho the
+def test_force_momentum_and_paper_example(st, space, model):
+    """Body force (readings R23, R26, R27): per cell the mass is unchanged and the momentum gains
+    F; written as the paper's worked example: with u = (j + F/2)/rho the
     post-collision first-order raw moment is m*_{10|0} = rho u_x + F_x / 2."""
     xi, opp, w, M, Minv = oracle.tables(st)
     F = FORCE.copy()
@@ -520,10 +521,77 @@ def test_force_momentum_and_paper_example(st, space):
     u = (fa @ xi + F / 2) / rho[:, None]  # pre-collision velocity with the half-force shift
     for eq, zc in admissible(space):
         fin = fa - w if zc else fa
-        fo = oracle.collide(st, space, eq, zc, rates_for(st, space), fin, force=F)
+        fo = oracle.collide(st, space, eq, zc, rates_for(st, space), fin, force=F, force_model=model)
         fo_abs = fo + w if zc else fo
         np.testing.assert_allclose(fo_abs.sum(1), rho, atol=1e-15)
         np.testing.assert_allclose(fo_abs @ xi, rho[:, None] * u + F / 2, atol=1e-16)
+
+
+def cells_with_velocity(st, n, u_dir, speed, F, seed=11, amp=2e-2):
+    """Absolute populations with the SHIFTED velocity (j + F/2)/rho = speed * u_dir exactly:
+    random non-equilibrium noise, then the momentum corrected along a zero-mass direction."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    rng = np.random.default_rng(seed)
+    rho = 1.0 + rng.uniform(-0.03, 0.03, n)
+    u = np.tile(speed * np.asarray(u_dir, float), (n, 1))
+    f = textbook_feq(st, rho, u) + amp * w * rng.uniform(-1, 1, (n, len(w)))
+    d = W.DIM_OF[st]
+    for _ in range(2):  # set sum f = rho and sum f xi = rho u - F/2 with w-weighted corrections
+        f += w * (rho - f.sum(1))[:, None]
+        dj = rho[:, None] * u - F / 2 - f @ xi
+        f += 3.0 * w * (dj[:, :d] @ xi[:, :d].T)
+    return f
+
+
+@pytest.mark.parametrize("st,space", [(W.D2Q9, W.POPULATION), (W.D3Q19, W.RAW), (W.D3Q27, W.CENTRAL),
+                                      (W.D2Q9, W.CENTRAL)])
+def test_he_force_equals_guo_at_rest(st, space):
+    """Reading R27: at u = 0 He's term f_eq (xi - u).F/(rho c_s^2) is rho w_i 3 xi.F / rho, which
+    is Guo's w_i [3 xi.F + 9 (xi.u)(xi.F) - 3 u.F] at u = 0 — the two forced collisions agree."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    F = FORCE.copy()
+    if W.DIM_OF[st] == 2:
+        F[2] = 0
+    fa = cells_with_velocity(st, 10, [1, 0, 0], 0.0, F)
+    np.testing.assert_allclose((fa @ xi + F / 2), 0, atol=1e-15)
+    rates = rates_for(st, space)
+    for eq, zc in admissible(space):
+        fin = fa - w if zc else fa
+        g = oracle.collide(st, space, eq, zc, rates, fin, force=F, force_model=oracle.GUO)
+        h = oracle.collide(st, space, eq, zc, rates, fin, force=F, force_model=oracle.HE)
+        np.testing.assert_allclose(h, g, atol=2e-17)
+
+
+@pytest.mark.parametrize("st,space", [(W.D2Q9, W.POPULATION), (W.D3Q27, W.RAW), (W.D3Q27, W.CENTRAL)])
+def test_he_minus_guo_is_second_order_in_u(st, space):
+    """Reading R27: He's and Guo's terms agree to first order in u (both carry the (xi.u)(xi.F)
+    term of the second-order expansion), so the forced collisions differ by O(u^2 F): halving u
+    quarters the difference.  A wrong sign or a missing (xi - u) shift breaks the ratio."""
+    F = FORCE.copy()
+    if W.DIM_OF[st] == 2:
+        F[2] = 0
+    xi, opp, w, M, Minv = oracle.tables(st)
+    rates = rates_for(st, space)
+    diffs = []
+    for speed in (0.04, 0.02, 0.01):
+        fa = cells_with_velocity(st, 6, [0.6, -0.8, 0.0] if W.DIM_OF[st] == 2 else [0.48, -0.64, 0.6], speed, F)
+        g = oracle.collide(st, space, W.EQ_ABSOLUTE, 0, rates, fa, force=F, force_model=oracle.GUO)
+        h = oracle.collide(st, space, W.EQ_ABSOLUTE, 0, rates, fa, force=F, force_model=oracle.HE)
+        diffs.append(np.abs(h - g).max())
+    assert diffs[0] > 1e-3 * 0.04 ** 2 * np.abs(F).max()  # the models are not identical
+    for a, b in zip(diffs, diffs[1:]):
+        assert 3.6 < a / b < 4.4, diffs
+
+
+def test_force_cumulant_models_coincide():
+    """Reading R26/R27: for the cumulant methods both models give the first-order source F."""
+    st = W.D3Q27
+    xi, opp, w, M, Minv = oracle.tables(st)
+    fa = random_cells(st, 6)
+    rates = rates_for(st, W.CUMULANT)
+    g = oracle.collide(st, W.CUMULANT, W.EQ_ABSOLUTE, 1, rates, fa - w, force=FORCE, force_model=oracle.GUO)
+    h = oracle.collide(st, W.CUMULANT, W.EQ_ABSOLUTE, 1, rates, fa - w, force=FORCE, force_model=oracle.HE)
+    np.testing.assert_array_equal(g, h)
 
 
 def test_force_shallow_water_unsupported():
@@ -562,9 +630,10 @@ def test_cumulant_force_is_first_order_only(st):
     np.testing.assert_allclose(forced.sum(1), plain.sum(1), atol=1e-15)
 
 
+@pytest.mark.parametrize("model", [oracle.GUO, oracle.HE])
 @pytest.mark.parametrize("st", STENCILS)
 @pytest.mark.parametrize("space", [W.POPULATION, W.RAW, W.CENTRAL, W.CUMULANT])
-def test_force_isotropy(st, space):
+def test_force_isotropy(st, space, model):
     """Rotating the cell and the force together commutes with the forced collision."""
     xi, opp, w, M, Minv = oracle.tables(st)
     F = FORCE.copy()
@@ -573,18 +642,20 @@ def test_force_isotropy(st, space):
     fa = random_cells(st, 8)
     rates = np.array([1.3]) if space == W.POPULATION else W.rate_set_p(st)
     eq = W.EQ_ABSOLUTE if space == W.CUMULANT else W.EQ_DELTA
-    out = oracle.collide(st, space, eq, 1, rates, fa - w, force=F)
+    out = oracle.collide(st, space, eq, 1, rates, fa - w, force=F, force_model=model)
     for P in symmetry_generators(W.DIM_OF[st]):
         img = xi @ P.T
         perm = [int(np.flatnonzero((xi == img[i]).all(1))[0]) for i in range(len(w))]
         rot_in = np.empty_like(fa)
         rot_in[:, perm] = fa - w
-        rot_out = oracle.collide(st, space, eq, 1, rates, rot_in, force=P @ F)
+        rot_out = oracle.collide(st, space, eq, 1, rates, rot_in, force=P @ F, force_model=model)
         np.testing.assert_allclose(rot_out[:, perm], out, atol=2e-16)
 
 
-@pytest.mark.parametrize("space,nu", [(W.POPULATION, 1 / 6), (W.RAW, 0.1), (W.CENTRAL, 0.05), (W.CUMULANT, 0.08)])
-def test_poiseuille_flow(space, nu):
+@pytest.mark.parametrize("space,nu,model", [(W.POPULATION, 1 / 6, oracle.GUO), (W.RAW, 0.1, oracle.GUO),
+                                            (W.CENTRAL, 0.05, oracle.GUO), (W.CUMULANT, 0.08, oracle.GUO),
+                                            (W.POPULATION, 0.1, oracle.HE), (W.CENTRAL, 0.05, oracle.HE)])
+def test_poiseuille_flow(space, nu, model):
     """Force-driven channel between half-way bounce-back walls (readings R18, R23): the steady
     profile is u_x(y) = F / (2 nu) (y + 1/2)(H - 1/2 - y) (walls half a node outside)."""
     st, nx, ny, Fx = W.D2Q9, 4, 24, 1e-6
@@ -594,7 +665,7 @@ def test_poiseuille_flow(space, nu):
     eq = W.EQ_ABSOLUTE if space == W.CUMULANT else W.EQ_DELTA
     sim = oracle.Sim(st, space, eq, 1, rates, (nx, ny, 1), bc=bc)
     sim.set(np.zeros((9, 1, ny, nx)))
-    sim.set_force([Fx, 0, 0])
+    sim.set_force([Fx, 0, 0], force_model=model)
     sim.step(int(8 * ny * ny / nu))
     r, u = sim.macroscopic()
     y = np.arange(ny)
