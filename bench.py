@@ -54,6 +54,9 @@ CONFIGS = {
     "c3eso": dict(stencil=W.D3Q27, space=W.CENTRAL, eq=W.EQ_ABSOLUTE, zc=1, prec=0, streaming=2,
                   shape=lambda n: (384, 384, 384), slab=2, scaling="strong",
                   desc="D3Q27 central-moment MRT TGV 384^3, fp64, zero-centered + absolute eq, Esoteric Pull"),
+    "c3twist": dict(stencil=W.D3Q27, space=W.CENTRAL, eq=W.EQ_ABSOLUTE, zc=1, prec=0, streaming=3,
+                    shape=lambda n: (384, 384, 384), slab=2, scaling="strong",
+                    desc="D3Q27 central-moment MRT TGV 384^3, fp64, zero-centered + absolute eq, Esoteric Twist"),
     "c2_f64": dict(stencil=W.D3Q19, space=W.RAW, eq=W.EQ_DELTA, zc=1, prec=0, streaming=0,
                    shape=lambda n: (256, 256, 256), slab=2, scaling="strong",
                    desc="D3Q19 raw-moment MRT TGV 256^3, fp64, zero-centered + delta eq, pull"),

@@ -86,9 +86,11 @@ typedef enum {
                           PAPER.md:1023-1026)                                                          */
 } lbm_equilibrium;
 typedef enum { LBM_FP64 = 0, LBM_FP32 = 1 } lbm_precision;
-/* Streaming patterns: two-grid pull; in place: AA (Bailey 2009; single or
-   several ranks, periodic) and Esoteric Pull (Lehmann 2022; single rank, periodic). */
-typedef enum { LBM_PULL = 0, LBM_AA = 1, LBM_ESOTERIC_PULL = 2 } lbm_streaming;
+/* Streaming patterns: two-grid pull; in place: AA (Bailey 2009; several
+   ranks with periodic faces, or one rank with periodic and/or no-slip faces), Esoteric Pull (Lehmann 2022; single rank, periodic) and Esoteric
+   Twist (Geier & Schoenherr 2017, reading R28: every cell touches only its positive octant
+   x + {0,1}^d; single rank, periodic).  All three in-place patterns move the same bytes. */
+typedef enum { LBM_PULL = 0, LBM_AA = 1, LBM_ESOTERIC_PULL = 2, LBM_ESOTERIC_TWIST = 3 } lbm_streaming;
 typedef enum { LBM_BC_PERIODIC = 0, LBM_BC_NOSLIP = 1 } lbm_bc;
 typedef enum { LBM_REGION_ALL = 0, LBM_REGION_BOUNDARY = 1, LBM_REGION_INTERIOR = 2 } lbm_region;
 
@@ -96,7 +98,7 @@ typedef struct {
   int nx, ny, nz;  /* GLOBAL lattice extents; D2Q9: nz = 1 (the slab axis is then y)        */
   int bc[3][2];    /* [axis][low, high] lbm_bc; periodic must be set on both faces of an axis */
   int precision;   /* lbm_precision (storage and arithmetic precision)                        */
-  int streaming;   /* lbm_streaming; in place: all faces periodic (Esoteric Pull: one rank)   */
+  int streaming;   /* lbm_streaming; Esoteric: one rank, periodic; AA + no-slip: one rank     */
   double swe_g;    /* lattice gravity g (LBM_EQ_SWE only)                                     */
   int device;      /* CUDA device ordinal                                                     */
   void *stream;    /* cudaStream_t to enqueue on, or NULL: the library creates its own        */
@@ -217,7 +219,7 @@ typedef struct {
 } lbm_peer_info;
 lbm_status lbm_peer_export(lbm_ctx *ctx, lbm_peer_info *out);
 /* Maps the neighbours' grids and flags; LBM_EINVAL if their lattice, stencil, precision or
-   ranks do not match this context's ring; LBM_EUNSUPPORTED for Esoteric Pull or one rank
+   ranks do not match this context's ring; LBM_EUNSUPPORTED for Esoteric Pull / Twist or one rank
    (at export); LBM_ECUDA if the memory cannot be mapped (no peer access). Resets the flags. */
 lbm_status lbm_peer_connect(lbm_ctx *ctx, const lbm_peer_info *lower, const lbm_peer_info *upper);
 /* PULL: pushes the current grid's boundary planes into the neighbours' ghost planes; AA:
@@ -249,6 +251,14 @@ lbm_status lbm_get_populations(lbm_ctx *ctx, double *f);
    nonlinear transform; Guo's source has no second-order central moments).
    LBM_EUNSUPPORTED for the shallow-water methods.  A zero force restores the unforced kernels. */
 lbm_status lbm_set_force(lbm_ctx *ctx, const double *force);
+/* Force model of the source term (PAPER.md:538-539 names Guo and He):
+   LBM_FORCE_GUO (default, reading R23) or LBM_FORCE_HE (reading R27): F^He_i = f_eq_i(rho, u)
+   (xi_i - u).F / (rho c_s^2) with the method's own equilibrium at u = (j + F/2)/rho and the same
+   q^F = (I - S/2) T(F^He).  For cumulant methods both give the first-order source of R26.
+   Takes effect for the current force (re-selects the kernels) and later lbm_set_force calls.
+   LBM_EINVAL for an unknown model. */
+typedef enum { LBM_FORCE_GUO = 0, LBM_FORCE_HE = 1 } lbm_force_model;
+lbm_status lbm_set_force_model(lbm_ctx *ctx, lbm_force_model model);
 /* Global sums over this rank's slab of the canonical state, on the device in fp64 with a
    fixed (deterministic) summation order: mass = sum rho, momentum = sum rho u (physical
    x, y, z; 2D: z = 0), kinetic energy = sum rho |u|^2 / 2 (lattice-node form of

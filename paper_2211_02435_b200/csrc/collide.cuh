@@ -683,7 +683,7 @@ __device__ __forceinline__ void add_background(real (&c)[NC], real sgn) {
 // F^G_i = w_i [3 xi.F + 9 (xi.u)(xi.F) - 3 u.F] is added after relaxation.  The momentum
 // gains exactly F (kappa_100: -F/2 before, +F/2 after).
 // --------------------------------------------------------------------------
-enum { RS_FORCE = 4 };  // flag bit of the RS template parameter
+enum { RS_FORCE = 4, RS_FORCE_HE = 8 };  // flag bits of the RS template parameter (Guo / He)
 
 template <class real>
 struct Force {
@@ -719,12 +719,43 @@ __device__ __forceinline__ void guo_cube(real (&s)[NC], const Force<real> &fr, r
   });
 }
 
+template <class S, int SPACE, int REG, class real>
+__device__ __forceinline__ void equilibrium(real (&f)[S::Q], real rho, real ux, real uy, real uz, real swe_g);
+
+// He's force term F^He_i = f_eq_i(rho, u) (xi_i - u).F / (rho c_s^2) (He, Shan, Doolen 1998,
+// PAPER.md:214, 539; reading R27) with the method's own absolute equilibrium at the shifted u,
+// in the cube layout like guo_cube.
+template <class S, int SPACE, class real, int NC>
+__device__ __forceinline__ void he_cube(real (&s)[NC], const Force<real> &fr, real rho, real inv, real ux,
+                                        real uy, real uz) {
+  real fe[S::Q];
+  equilibrium<S, (SPACE == SPACE_CENTRAL ? SPACE_CENTRAL : SPACE_RAW), REG_ABS, real>(fe, rho, ux, uy, uz,
+                                                                                       real(0));
+  const real uF = fma(uz, fr.F[2], fma(uy, fr.F[1], ux * fr.F[0]));
+  const real k = real(3) * inv;  // 1 / (rho c_s^2)
+  sfor<NC>([&](auto e) { s[e] = real(0); });
+  sfor<S::Q>([&](auto i) {
+    constexpr int vx = S::vx(i), vy = S::vy(i), vz = S::vz(i);
+    const real xF = signed_add<vz>(signed_add<vy>(signed_add<vx>(real(0), fr.F[0]), fr.F[1]), fr.F[2]);
+    s[S::pos(i)] = fe[i] * ((xF - uF) * k);
+  });
+}
+
+template <class S, int SPACE, int RS, class real, int NC>
+__device__ __forceinline__ void force_cube(real (&s)[NC], const Force<real> &fr, real rho, real inv, real ux,
+                                           real uy, real uz) {
+  if constexpr ((RS & RS_FORCE_HE) != 0) he_cube<S, SPACE>(s, fr, rho, inv, ux, uy, uz);
+  else guo_cube<S>(s, fr, ux, uy, uz);
+}
+
 template <class S, int SPACE, int REG, class real, int RS = RS_GENERAL>
 __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, real swe_g,
                                         const Force<real> &fr) {
   constexpr bool zc = (REG != REG_ABS);
   constexpr int NC = S::NC;
-  constexpr bool FORCED = (RS & RS_FORCE) != 0;
+  constexpr bool FORCED = (RS & (RS_FORCE | RS_FORCE_HE)) != 0;
+  static_assert(!(RS & RS_FORCE_HE) || SPACE == SPACE_POPULATION || SPACE == SPACE_RAW || SPACE == SPACE_CENTRAL,
+                "He forcing: population, raw- and central-moment collisions (cumulants: R26 = Guo)");
   static_assert(!FORCED || SPACE == SPACE_POPULATION || SPACE == SPACE_RAW || SPACE == SPACE_CENTRAL ||
                     SPACE == SPACE_CUMULANT,
                 "forcing is provided for population, raw-moment, central-moment and cumulant collisions");
@@ -788,7 +819,7 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
     }
     if constexpr (FORCED) {  // + (1 - w/2) F^G_i
       real s[NC];
-      guo_cube<S>(s, fr, ux, uy, uz);
+      force_cube<S, SPACE, RS>(s, fr, rho, inv, ux, uy, uz);
       const real a = real(1) - fr.half.w[0];
       sfor<S::Q>([&](auto i) { f[i] = fma(a, s[S::pos(i)], f[i]); });
     }
@@ -816,7 +847,7 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
     // source term q^F = (I - S/2) T(F^G) added after relaxation (FORCED only)
     auto add_force = [&](auto central) {
       real s[NC];
-      guo_cube<S>(s, fr, ux, uy, uz);
+      force_cube<S, SPACE, RS>(s, fr, rho, inv, ux, uy, uz);
       if constexpr (S::D == 3) fwd_raw3<S>(s); else fwd_raw2(s);
       if constexpr (decltype(central)::value) {
         if constexpr (S::D == 3) bin_fwd3(s, ux, uy, uz); else bin_fwd2(s, ux, uy);

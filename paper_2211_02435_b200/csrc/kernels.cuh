@@ -120,8 +120,29 @@ __global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, 
 }
 
 // ---------------------------------------------------------------------------
-// AA pattern (single rank, periodic): in-place
+// AA pattern: in-place.  BB (single rank): half-way bounce-back on the no-slip faces of
+// g.bcmask (reading R18).  The odd step reads f_i(x) = f*_opp(x) from mem(x, i) when x - xi_i
+// is beyond a wall, and writes f*_i(x) to mem(x, opp i) when x + xi_i is — the slot the next
+// (even) step reads as the bounced f_opp(x).  Both slots belong to cell x alone (no other cell
+// maps onto them), so the update stays race-free; the even step needs no change.
 // ---------------------------------------------------------------------------
+template <class S>
+struct Walls {
+  bool x[3], y[3], z[3];  // offset s = -1, 0, +1 (index s + 1) lies beyond a no-slip face
+  __device__ __forceinline__ Walls(const GridParams &g, int x0, int y0, int zl) {
+#pragma unroll
+    for (int s = -1; s <= 1; ++s) {
+      const int xv = x0 + s, yv = y0 + s, zgv = g.z0 + zl + s;
+      x[s + 1] = (xv < 0 && (g.bcmask & 1)) || (xv >= g.nx && (g.bcmask & 2));
+      y[s + 1] = (yv < 0 && (g.bcmask & 4)) || (yv >= g.ny && (g.bcmask & 8));
+      z[s + 1] = (zgv < 0 && (g.bcmask & 16)) || (zgv >= g.nzg && (g.bcmask & 32));
+    }
+  }
+  // the neighbour x + (cx, cy, cz) lies beyond a wall (crossing any wall axis bounces)
+  __device__ __forceinline__ bool beyond(int cx, int cy, int cz) const {
+    return x[1 + cx] || y[1 + cy] || z[1 + cz];
+  }
+};
 // The odd kernel holds 27 gather and 27 scatter addresses across the collision; capping it
 // at 5 blocks/SM (96 registers, 4 B spill) beats 123 registers at 4 blocks (+3 %, B200).
 // PEER (odd pattern, boundary planes of lbm_step_peer): the slab-crossing accesses go straight
@@ -129,7 +150,7 @@ __global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, 
 // plane, g.peer_hi: the upper neighbour's first plane) instead of the ghost planes — the
 // AA odd step is race-free on the global lattice, so ranks need no exchange, only the
 // per-step completion flags.
-template <class S, int SPACE, int REG, class real, int PAT, int RS = RS_GENERAL, bool PEER = false>
+template <class S, int SPACE, int REG, class real, int PAT, int RS = RS_GENERAL, bool PEER = false, bool BB = false>
 __global__ void __launch_bounds__(BLOCK_X, (PAT == PAT_AA_ODD ? 5 : 1))
     k_aa(real *mem, const GridParams g, const Rates<real> r, const real swe_g, const Force<real> fr) {
   const int x = blockIdx.x * BLOCK_X + threadIdx.x;
@@ -175,17 +196,35 @@ __global__ void __launch_bounds__(BLOCK_X, (PAT == PAT_AA_ODD ? 5 : 1))
       // and returned after the odd step, distributed.py)
       zo[s + 1] = (long long)((g.wrapz ? wrapi(zl + s, g.nzl) : zl + s) + 1) * g.plane;
     }
-    // read f_i(x) = mem(x - xi_i, opp i)
-    sfor<S::Q>([&](auto i) {
-      constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
-      f[i] = ld_nc(mem + zo[1 - cz] + (long long)S::opp(i) * g.pop + ys[1 - cy] + xs[1 - cx]);
-    });
-    collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
-    // write f*_i(x) to mem(x + xi_i, i)
-    sfor<S::Q>([&](auto i) {
-      constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
-      mem[zo[1 + cz] + (long long)i * g.pop + ys[1 + cy] + xs[1 + cx]] = f[i];
-    });
+    if constexpr (BB) {
+      const Walls<S> w(g, x, y, zl);
+      const long long own = (long long)(zl + 1) * g.plane + (long long)y * g.pitch + x;
+      // read f_i(x) = mem(x - xi_i, opp i), or f*_opp(x) = mem(x, i) from beyond a wall
+      sfor<S::Q>([&](auto i) {
+        constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+        const long long a = zo[1 - cz] + (long long)S::opp(i) * g.pop + ys[1 - cy] + xs[1 - cx];
+        f[i] = ld_nc(mem + (w.beyond(-cx, -cy, -cz) ? own + (long long)i * g.pop : a));
+      });
+      collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
+      // write f*_i(x) to mem(x + xi_i, i), or to mem(x, opp i) towards a wall
+      sfor<S::Q>([&](auto i) {
+        constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+        const long long a = zo[1 + cz] + (long long)i * g.pop + ys[1 + cy] + xs[1 + cx];
+        mem[w.beyond(cx, cy, cz) ? own + (long long)S::opp(i) * g.pop : a] = f[i];
+      });
+    } else {
+      // read f_i(x) = mem(x - xi_i, opp i)
+      sfor<S::Q>([&](auto i) {
+        constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+        f[i] = ld_nc(mem + zo[1 - cz] + (long long)S::opp(i) * g.pop + ys[1 - cy] + xs[1 - cx]);
+      });
+      collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
+      // write f*_i(x) to mem(x + xi_i, i)
+      sfor<S::Q>([&](auto i) {
+        constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+        mem[zo[1 + cz] + (long long)i * g.pop + ys[1 + cy] + xs[1 + cx]] = f[i];
+      });
+    }
   }
 }
 
@@ -247,9 +286,48 @@ __global__ void __launch_bounds__(BLOCK_X)
 }
 
 // ---------------------------------------------------------------------------
+// Esoteric Twist (Geier & Schoenherr 2017, cited at PAPER.md:861; reading R28; single rank,
+// periodic): in place, every cell touches only the 2^d cells of its positive octant
+// x + o, o in {0, 1}^d.  With o+(i) = max(xi_i, 0) and o-(i) = max(-xi_i, 0) per axis:
+//   TW0 (state T0 -> T1): f_i = mem(x + o-(i), i)      -> collide -> mem(x + o+(i), opp i)
+//   TW1 (state T1 -> T0): f_i = mem(x + o-(i), opp i)  -> collide -> mem(x + o+(i), i)
+// (state T0: f*_i(x) at mem(x + o+(i), i); T1: at mem(x + o+(i), opp i).  The slots a cell
+// reads are the slots it writes, o+(opp i) = o-(i): race-free in place.  x - xi_i + o+(i) =
+// x + o-(i) makes the reads the pulls of eq:LbStreaming.)
+// ---------------------------------------------------------------------------
+enum { PAT_TW0 = 5, PAT_TW1 = 6 };
+
+template <class S, int SPACE, int REG, class real, int PAT, int RS = RS_GENERAL>
+__global__ void __launch_bounds__(BLOCK_X)
+    k_twist(real *mem, const GridParams g, const Rates<real> r, const real swe_g, const Force<real> fr) {
+  const int x = blockIdx.x * BLOCK_X + threadIdx.x;
+  if (x >= g.nx) return;
+  const int y = blockIdx.y;
+  const int zl = g.zbegin + blockIdx.z;
+  constexpr bool t0 = (PAT == PAT_TW0);
+  // offsets 0 / +1 of the octant along each axis
+  const int xs[2] = {x, wrapi(x + 1, g.nx)};
+  const long long ys[2] = {(long long)y * g.pitch, (long long)wrapi(y + 1, g.ny) * g.pitch};
+  const long long zo[2] = {(long long)(zl + 1) * g.plane, (long long)(wrapi(zl + 1, g.nzl) + 1) * g.plane};
+  real f[S::Q];
+  sfor<S::Q>([&](auto i) {
+    constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+    constexpr int slot = t0 ? int(i) : S::opp(i);
+    f[i] = ld_nc(mem + zo[cz < 0] + (long long)slot * g.pop + ys[cy < 0] + xs[cx < 0]);
+  });
+  collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
+  sfor<S::Q>([&](auto i) {
+    constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+    constexpr int slot = t0 ? S::opp(i) : int(i);
+    mem[zo[cz > 0] + (long long)slot * g.pop + ys[cy > 0] + xs[cx > 0]] = f[i];
+  });
+}
+
+// ---------------------------------------------------------------------------
 // helpers: init from macroscopic fields, canonical get/set, macroscopic moments,
 // collision-only test kernel, finiteness probe.  'pat' = lbm_streaming (0 pull, 1 AA,
-// 2 Esoteric Pull); 'state' for AA: 0 = A, 1 = B; for Esoteric Pull: 0 = E, 1 = O.
+// 2 Esoteric Pull, 3 Esoteric Twist); 'state' for AA: 0 = A, 1 = B; for Esoteric Pull:
+// 0 = E, 1 = O; for Esoteric Twist: 0 = T0, 1 = T1.
 // ---------------------------------------------------------------------------
 template <class S>
 struct Canon {
@@ -258,10 +336,23 @@ struct Canon {
   __device__ static __forceinline__ long long at(const GridParams &g, int x, int y, int zl, int pat, int state) {
     const long long own = (long long)(zl + 1) * g.plane + (long long)y * g.pitch + x;
     if (pat == 0) return own + (long long)i * g.pop;
+    if (pat == 3) {  // Esoteric Twist: mem(x + o+(i), i) in state T0, slot opp i in T1
+      constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+      const int xx = cx > 0 ? wrapi(x + 1, g.nx) : x, yy = cy > 0 ? wrapi(y + 1, g.ny) : y;
+      const int zz = cz > 0 ? wrapi(zl + 1, g.nzl) : zl;
+      return (long long)(zz + 1) * g.plane + (long long)yy * g.pitch + xx +
+             (long long)(state == 0 ? int(i) : S::opp(i)) * g.pop;
+    }
     const int xx = wrapi(x + S::mx(i), g.nx), yy = wrapi(y + S::my(i), g.ny);
     const int zz = g.wrapz ? wrapi(zl + S::mz(i), g.nzl) : zl + S::mz(i);  // multi-rank: ghost plane
     const long long nb = (long long)(zz + 1) * g.plane + (long long)yy * g.pitch + xx;  // cell x + xi_i
-    if (pat == 1) return state == 0 ? own + (long long)S::opp(i) * g.pop : nb + (long long)i * g.pop;
+    if (pat == 1) {
+      if (state == 0) return own + (long long)S::opp(i) * g.pop;
+      // state B with walls (single rank): populations headed beyond a wall sit in mem(x, opp i)
+      if (g.bcmask && Walls<S>(g, x, y, zl).beyond(S::mx(i), S::my(i), S::mz(i)))
+        return own + (long long)S::opp(i) * g.pop;
+      return nb + (long long)i * g.pop;
+    }
     if constexpr (i == 0) return own;
     const int slot = state == 0 ? i : S::opp(i);
     return (first_of_pair<S>(i) ? nb : own) + (long long)slot * g.pop;

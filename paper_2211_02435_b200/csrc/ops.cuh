@@ -22,7 +22,8 @@ struct Ops {
   // pull stream–collide of planes [zbegin, zbegin + nplanes) from src into dst
   void (*pull)(const void *src, void *dst, const GridParams &g, const void *params, double swe_g, int bb,
                int nplanes, cudaStream_t s);
-  // in-place step (PAT_AA_EVEN / PAT_AA_ODD / PAT_ESO_EVEN / PAT_ESO_ODD), planes [zbegin, zbegin + nplanes)
+  // in-place step (PAT_AA_EVEN / PAT_AA_ODD / PAT_ESO_EVEN / PAT_ESO_ODD / PAT_TW0 / PAT_TW1),
+  // planes [zbegin, zbegin + nplanes)
   void (*aa)(void *mem, const GridParams &g, const void *params, double swe_g, int pattern, int nplanes,
              cudaStream_t s);
   void (*init)(void *mem, const GridParams &g, int aa, const double *rho, const double *u, double swe_g,
@@ -98,6 +99,9 @@ struct OpsImpl {
         if (g.peer_lo && g.peer_hi)  // boundary planes of lbm_step_peer
           k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS, true><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
               m, g, p.rates, (real)swe_g, p.force);
+        else if (g.bcmask)  // no-slip faces (single rank): half-way bounce-back
+          k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS, false, true><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(
+              m, g, p.rates, (real)swe_g, p.force);
         else
           k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,
                                                                                            (real)swe_g, p.force);
@@ -105,6 +109,14 @@ struct OpsImpl {
       case PAT_ESO_EVEN:
         k_eso<S, SPACE, REG, real, PAT_ESO_EVEN, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,
                                                                                             (real)swe_g, p.force);
+        break;
+      case PAT_TW0:
+        k_twist<S, SPACE, REG, real, PAT_TW0, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,
+                                                                                         (real)swe_g, p.force);
+        break;
+      case PAT_TW1:
+        k_twist<S, SPACE, REG, real, PAT_TW1, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,
+                                                                                         (real)swe_g, p.force);
         break;
       default:
         k_eso<S, SPACE, REG, real, PAT_ESO_ODD, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,

@@ -1,15 +1,16 @@
-// ops_inst.cu — instantiates the kernels of one (stencil, precision, space)
-// triple.  Compiled once per triple with
-//   -DLBM_STENCIL=D3Q27 -DLBM_REAL=double -DLBM_PREC=f64 -DLBM_SPACE=CUMULANT
-// and exports  const lbm::Ops *lbm_ops_<stencil>_<prec>_<space>(int regime).
+// ops_inst.cu — instantiates the kernels of one (stencil, precision, space, regime)
+// quadruple.  Compiled once per quadruple (so the heavy instantiations compile in parallel) with
+//   -DLBM_STENCIL=D3Q27 -DLBM_REAL=double -DLBM_PREC=f64 -DLBM_SPACE=CUMULANT -DLBM_REGIME=2
+// and exports  const lbm::Ops *lbm_ops_<stencil>_<prec>_<space>_r<regime>(int rs)
+// (nullptr for inadmissible combinations and kernel variants that are not instantiated).
 #include "ops.cuh"
 
-#ifndef LBM_STENCIL
-#error "define LBM_STENCIL, LBM_REAL, LBM_PREC, LBM_SPACE"
+#if !defined(LBM_STENCIL) || !defined(LBM_REGIME)
+#error "define LBM_STENCIL, LBM_REAL, LBM_PREC, LBM_SPACE, LBM_REGIME"
 #endif
 
-#define LBM_NAME2(st, pr, sp) lbm_ops_##st##_##pr##_##sp
-#define LBM_NAME(st, pr, sp) LBM_NAME2(st, pr, sp)
+#define LBM_NAME2(st, pr, sp, rg) lbm_ops_##st##_##pr##_##sp##_r##rg
+#define LBM_NAME(st, pr, sp, rg) LBM_NAME2(st, pr, sp, rg)
 
 namespace lbm {
 namespace {
@@ -28,7 +29,11 @@ const Ops *with_rs(int rs) {
   if constexpr (SP_ == SPACE_POPULATION || SP_ == SPACE_RAW || SP_ == SPACE_CENTRAL || SP_ == SPACE_CUMULANT) {
     if (rs == (RS_GENERAL | RS_FORCE)) return &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL | RS_FORCE>::table;
   }
-  if (rs & RS_FORCE) return nullptr;
+  // He forcing (reading R27): the linear spaces (for cumulants R26 makes He and Guo coincide)
+  if constexpr (SP_ == SPACE_POPULATION || SP_ == SPACE_RAW || SP_ == SPACE_CENTRAL) {
+    if (rs == (RS_GENERAL | RS_FORCE_HE)) return &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL | RS_FORCE_HE>::table;
+  }
+  if (rs & (RS_FORCE | RS_FORCE_HE)) return nullptr;
   if constexpr (SP_ == SPACE_POPULATION) {
     return rs == RS_GENERAL ? &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL>::table : nullptr;
   } else {
@@ -43,31 +48,19 @@ const Ops *with_rs(int rs) {
   }
 }
 
-template <class St_, class Re_, int SP_>
-const Ops *select_ops(int regime, int rs) {
+template <class St_, class Re_, int SP_, int REG_>
+const Ops *select_ops(int rs) {
   if constexpr (SP_ == SPACE_SWE || SP_ == SPACE_SWE_K) {
-    if constexpr (St_::Q == 9) {
-      if (regime == REG_ABS) return with_rs<St_, SP_, REG_ABS, Re_>(rs);
-    }
+    if constexpr (St_::Q == 9 && REG_ == REG_ABS) return with_rs<St_, SP_, REG_, Re_>(rs);
     return nullptr;
-  } else if constexpr (SP_ == SPACE_CUMULANT) {
-    // cumulants admit no delta equilibrium
-    switch (regime) {
-      case REG_ABS: return with_rs<St_, SP_, REG_ABS, Re_>(rs);
-      case REG_ZC_ABS: return with_rs<St_, SP_, REG_ZC_ABS, Re_>(rs);
-      default: return nullptr;
-    }
+  } else if constexpr (SP_ == SPACE_CUMULANT && REG_ == REG_DELTA) {
+    return nullptr;  // cumulants admit no delta equilibrium
   } else {
-    switch (regime) {
-      case REG_ABS: return with_rs<St_, SP_, REG_ABS, Re_>(rs);
-      case REG_DELTA: return with_rs<St_, SP_, REG_DELTA, Re_>(rs);
-      case REG_ZC_ABS: return with_rs<St_, SP_, REG_ZC_ABS, Re_>(rs);
-      default: return nullptr;
-    }
+    return with_rs<St_, SP_, REG_, Re_>(rs);
   }
 }
 }  // namespace lbm
 
-extern "C" const lbm::Ops *LBM_NAME(LBM_STENCIL, LBM_PREC, LBM_SPACE)(int regime, int rs) {
-  return lbm::select_ops<lbm::St, lbm::Re, lbm::SP>(regime, rs);
+extern "C" const lbm::Ops *LBM_NAME(LBM_STENCIL, LBM_PREC, LBM_SPACE, LBM_REGIME)(int rs) {
+  return lbm::select_ops<lbm::St, lbm::Re, lbm::SP, LBM_REGIME>(rs);
 }

@@ -30,7 +30,19 @@ struct NvtxRange {  // scoped NVTX range around the C-ABI entry points (tracing)
 using lbm::GridParams;
 using lbm::Ops;
 
-#define LBM_DECL_OPS(st, pr, sp) extern "C" const Ops *lbm_ops_##st##_##pr##_##sp(int regime, int rs);
+// one exported table getter per (stencil, precision, space, regime) translation unit
+#define LBM_DECL_OPS(st, pr, sp)                                                     \
+  extern "C" const Ops *lbm_ops_##st##_##pr##_##sp##_r0(int rs);                      \
+  extern "C" const Ops *lbm_ops_##st##_##pr##_##sp##_r1(int rs);                      \
+  extern "C" const Ops *lbm_ops_##st##_##pr##_##sp##_r2(int rs);                      \
+  static const Ops *lbm_ops_##st##_##pr##_##sp(int regime, int rs) {                  \
+    switch (regime) {                                                                 \
+      case 0: return lbm_ops_##st##_##pr##_##sp##_r0(rs);                             \
+      case 1: return lbm_ops_##st##_##pr##_##sp##_r1(rs);                             \
+      case 2: return lbm_ops_##st##_##pr##_##sp##_r2(rs);                             \
+      default: return nullptr;                                                        \
+    }                                                                                 \
+  }
 #define LBM_DECL_ALL(st, pr)          \
   LBM_DECL_OPS(st, pr, POPULATION)    \
   LBM_DECL_OPS(st, pr, RAW)           \
@@ -99,6 +111,7 @@ struct lbm_ctx {
   double rates_d[27] = {0};
   double force[3] = {0, 0, 0};
   bool forced = false;
+  int force_model = LBM_FORCE_GUO;
   const Ops *ops_plain = nullptr;  // the unforced kernels chosen at create
   bool tb_allowed = false;         // temporal blocking (two fused steps) eligible
   cudaGraphExec_t graph[2] = {nullptr, nullptr};  // captured step loops per parity (small lattices)
@@ -250,6 +263,7 @@ bool use_graphs(const lbm_ctx *c) {
 // kernel of the next in-place step: AA odd/even, Esoteric Pull odd/even (state 0 -> odd)
 int inplace_pattern(const lbm_ctx *c, int state) {
   if (c->streaming == LBM_AA) return state == 0 ? lbm::PAT_AA_ODD : lbm::PAT_AA_EVEN;
+  if (c->streaming == LBM_ESOTERIC_TWIST) return state == 0 ? lbm::PAT_TW0 : lbm::PAT_TW1;
   return state == 0 ? lbm::PAT_ESO_ODD : lbm::PAT_ESO_EVEN;
 }
 int inplace_pattern(const lbm_ctx *c) { return inplace_pattern(c, c->aa_state); }
@@ -557,7 +571,8 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
       return fail(nullptr, LBM_EINVAL, "periodic must be set on both faces of an axis");
   }
   if (D.precision != LBM_FP64 && D.precision != LBM_FP32) return fail(nullptr, LBM_EINVAL, "unknown precision");
-  if (D.streaming != LBM_PULL && D.streaming != LBM_AA && D.streaming != LBM_ESOTERIC_PULL)
+  if (D.streaming != LBM_PULL && D.streaming != LBM_AA && D.streaming != LBM_ESOTERIC_PULL &&
+      D.streaming != LBM_ESOTERIC_TWIST)
     return fail(nullptr, LBM_EINVAL, "unknown streaming");
   if (D.nranks < 1 || D.rank < 0 || D.rank >= D.nranks) return fail(nullptr, LBM_EINVAL, "bad rank/nranks");
   const int slab_extent = two_d ? D.ny : D.nz;
@@ -566,10 +581,11 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   if (slab_extent / D.nranks < 2) return fail(nullptr, LBM_EINVAL, "slabs need at least 2 planes");
   bool any_wall = false;
   for (int a = 0; a < 3; ++a) any_wall |= (D.bc[a][0] == LBM_BC_NOSLIP);
-  if (D.streaming == LBM_AA && any_wall)
-    return fail(nullptr, LBM_EUNSUPPORTED, "AA streaming is provided for periodic faces");
-  if (D.streaming == LBM_ESOTERIC_PULL && (any_wall || D.nranks > 1))
-    return fail(nullptr, LBM_EUNSUPPORTED, "Esoteric Pull is provided for a single rank with periodic faces");
+  if (D.streaming == LBM_AA && any_wall && D.nranks > 1)
+    return fail(nullptr, LBM_EUNSUPPORTED, "AA streaming with no-slip faces is provided for a single rank");
+  if ((D.streaming == LBM_ESOTERIC_PULL || D.streaming == LBM_ESOTERIC_TWIST) && (any_wall || D.nranks > 1))
+    return fail(nullptr, LBM_EUNSUPPORTED,
+                "Esoteric Pull / Twist are provided for a single rank with periodic faces");
 
   int regime = lbm::REG_ABS;
   if (zc) regime = (equilibrium == LBM_EQ_DELTA) ? lbm::REG_DELTA : lbm::REG_ZC_ABS;
@@ -822,7 +838,8 @@ lbm_status lbm_swap(lbm_ctx *c) {
 
 lbm_status lbm_get_halo(lbm_ctx *c, int which, lbm_halo *out) {
   if (!c || !out) return LBM_EINVAL;
-  if (c->streaming == LBM_ESOTERIC_PULL) return fail(c, LBM_EUNSUPPORTED, "Esoteric Pull is single-rank");
+  if (c->streaming == LBM_ESOTERIC_PULL || c->streaming == LBM_ESOTERIC_TWIST)
+    return fail(c, LBM_EUNSUPPORTED, "Esoteric Pull / Twist are single-rank");
   char *base = static_cast<char *>(grid_ptr(c, which));
   lbm_layout lay;
   lbm_status s = lbm_grid_layout((lbm_stencil)c->stencil, (lbm_precision)c->prec, c->gnx, c->gny, c->gnz,
@@ -852,7 +869,8 @@ lbm_status lbm_sync(lbm_ctx *c) {
 
 lbm_status lbm_peer_export(lbm_ctx *c, lbm_peer_info *out) {
   if (!c || !out) return LBM_EINVAL;
-  if (c->streaming == LBM_ESOTERIC_PULL) return fail(c, LBM_EUNSUPPORTED, "Esoteric Pull is single-rank");
+  if (c->streaming == LBM_ESOTERIC_PULL || c->streaming == LBM_ESOTERIC_TWIST)
+    return fail(c, LBM_EUNSUPPORTED, "Esoteric Pull / Twist are single-rank");
   if (c->nranks < 2) return fail(c, LBM_EUNSUPPORTED, "the fused halo push needs nranks > 1");
   LBM_CUDA(c, cudaSetDevice(c->device));
   if (!c->peer_flags) {
@@ -1090,7 +1108,10 @@ lbm_status lbm_set_force(lbm_ctx *c, const double *force) {
       return fail(c, LBM_EUNSUPPORTED,
                   "a body force is provided for population, raw-moment, central-moment and cumulant collisions "
                   "(readings R23, R26), not for shallow water");
-    const Ops *f = find_ops(c->stencil, c->prec, c->kspace, c->regime, lbm::RS_GENERAL | lbm::RS_FORCE);
+    // He and Guo coincide for the cumulant methods (readings R26, R27): one kernel
+    const bool he = c->force_model == LBM_FORCE_HE && c->kspace != LBM_SPACE_CUMULANT;
+    const Ops *f = find_ops(c->stencil, c->prec, c->kspace, c->regime,
+                            lbm::RS_GENERAL | (he ? lbm::RS_FORCE_HE : lbm::RS_FORCE));
     if (!f) return fail(c, LBM_EUNSUPPORTED, "no forced kernel instantiated for this combination");
     c->ops = f;
   } else {
@@ -1101,6 +1122,17 @@ lbm_status lbm_set_force(lbm_ctx *c, const double *force) {
   fill_params(c);
   drop_graphs(c);  // the captured launches hold the old parameters by value
   return LBM_OK;
+}
+
+lbm_status lbm_set_force_model(lbm_ctx *c, lbm_force_model model) {
+  if (!c) return fail(c, LBM_EINVAL, "null argument");
+  if (model != LBM_FORCE_GUO && model != LBM_FORCE_HE) return fail(c, LBM_EINVAL, "unknown force model");
+  const int old = c->force_model;
+  c->force_model = model;
+  if (!c->forced) return LBM_OK;
+  const lbm_status s = lbm_set_force(c, c->force);  // re-selects the forced kernels
+  if (s != LBM_OK) c->force_model = old;
+  return s;
 }
 
 lbm_status lbm_get_diagnostics(lbm_ctx *c, lbm_diagnostics *out) {

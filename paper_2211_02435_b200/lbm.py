@@ -20,8 +20,9 @@ LBM_D2Q9, LBM_D3Q19, LBM_D3Q27 = 0, 1, 2
 LBM_SPACE_POPULATION, LBM_SPACE_RAW, LBM_SPACE_CENTRAL, LBM_SPACE_CUMULANT = 0, 1, 2, 3
 LBM_EQ_ABSOLUTE, LBM_EQ_DELTA, LBM_EQ_SWE = 0, 1, 2
 LBM_FP64, LBM_FP32 = 0, 1
-LBM_PULL, LBM_AA, LBM_ESOTERIC_PULL = 0, 1, 2
+LBM_PULL, LBM_AA, LBM_ESOTERIC_PULL, LBM_ESOTERIC_TWIST = 0, 1, 2, 3
 LBM_BC_PERIODIC, LBM_BC_NOSLIP = 0, 1
+LBM_FORCE_GUO, LBM_FORCE_HE = 0, 1
 LBM_REGION_ALL, LBM_REGION_BOUNDARY, LBM_REGION_INTERIOR = 0, 1, 2
 
 Q_OF = {LBM_D2Q9: 9, LBM_D3Q19: 19, LBM_D3Q27: 27}
@@ -103,6 +104,7 @@ SIGNATURES = [
     ("lbm_get_cells", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_longlong), ctypes.c_longlong, _dp]),
     ("lbm_get_diagnostics", ctypes.c_int, [_vp, ctypes.POINTER(lbm_diagnostics)]),
     ("lbm_set_force", ctypes.c_int, [_vp, _dp]),
+    ("lbm_set_force_model", ctypes.c_int, [_vp, ctypes.c_int]),
     ("lbm_check_finite", ctypes.c_int, [_vp]),
     ("lbm_test_collide", ctypes.c_int, [_vp, _dp, _dp, ctypes.c_longlong]),
     ("lbm_stencil_info", ctypes.c_int, [ctypes.c_int, _ip, _ip, _ip]),
@@ -299,8 +301,11 @@ class Lattice:
         _check(lib().lbm_get_populations(self._ctx, _d(f)), self._ctx)
         return f
 
-    def set_force(self, force):
-        """Uniform body force density (Guo forcing, include/lbm.h lbm_set_force)."""
+    def set_force(self, force, model=None):
+        """Uniform body force density (include/lbm.h lbm_set_force); model: LBM_FORCE_GUO or
+        LBM_FORCE_HE (lbm_set_force_model), None keeps the current one (default Guo)."""
+        if model is not None:
+            _check(lib().lbm_set_force_model(self._ctx, int(model)), self._ctx)
         F = np.ascontiguousarray(np.asarray(force, dtype=np.float64).reshape(-1))
         F = np.concatenate([F, np.zeros(3 - F.size)]) if F.size < 3 else F
         _check(lib().lbm_set_force(self._ctx, _d(np.ascontiguousarray(F))), self._ctx)

@@ -57,6 +57,10 @@ MUTANTS = [
     ("cumulant force: source also on the cumulants of order >= 2 (R26)",
      "Cstar_poly[p] = Cpoly[p] + m.omega[p] * (ceq - Cpoly[p]);",
      "Cstar_poly[p] = Cpoly[p] + m.omega[p] * (ceq - Cpoly[p]) + m.F[0];"),
+    ("He force: (xi + u) instead of (xi - u) (R27)", "cF += (R(m.xi[i][a]) - u[a]) * m.F[a];",
+     "cF += (R(m.xi[i][a]) + u[a]) * m.F[a];"),
+    ("He force: equilibrium without the background for zero-centered storage (R27)",
+     "R fa = m.zc ? feq[i] + m.w[i] : feq[i];", "R fa = feq[i];"),
     ("stencil order: swap (1,1) and (-1,-1) in-plane", "{1, 1}, {-1, -1}, {1, -1}, {-1, 1}};",
      "{-1, -1}, {1, 1}, {1, -1}, {-1, 1}};"),
 ]

@@ -100,8 +100,16 @@ def test_admissibility_errors():
     assert st == L.LBM_EUNSUPPORTED
     st, _ = create_status(streaming=L.LBM_ESOTERIC_PULL, bc=[[0, 0], [1, 1], [0, 0]])
     assert st == L.LBM_EUNSUPPORTED
-    st, _ = create_status(streaming=L.LBM_AA, bc=[[1, 1], [0, 0], [0, 0]])
+    st, _ = create_status(streaming=L.LBM_ESOTERIC_TWIST, nranks=2, rank=0)
     assert st == L.LBM_EUNSUPPORTED
+    st, _ = create_status(streaming=L.LBM_ESOTERIC_TWIST, bc=[[1, 1], [0, 0], [0, 0]])
+    assert st == L.LBM_EUNSUPPORTED
+    st, _ = create_status(streaming=4)
+    assert st == L.LBM_EINVAL
+    st, _ = create_status(streaming=L.LBM_AA, bc=[[1, 1], [0, 0], [0, 0]], nranks=2, rank=0)
+    assert st == L.LBM_EUNSUPPORTED
+    st, _ = create_status(streaming=L.LBM_AA, bc=[[1, 1], [0, 0], [0, 0]])
+    assert st != L.LBM_EUNSUPPORTED  # AA with walls on one rank passes validation
 
 
 def test_argument_errors():

@@ -27,6 +27,7 @@ CONFIGS = {
     "c3": (W.D3Q27, W.CENTRAL, W.EQ_ABSOLUTE, 1, L.LBM_FP64, L.LBM_AA, (384, 384, 384), 3),
     "c3_even": (W.D3Q27, W.CENTRAL, W.EQ_ABSOLUTE, 1, L.LBM_FP64, L.LBM_AA, (384, 384, 384), 4),
     "c3_esoteric": (W.D3Q27, W.CENTRAL, W.EQ_ABSOLUTE, 1, L.LBM_FP64, L.LBM_ESOTERIC_PULL, (384, 384, 384), 3),
+    "c3_twist": (W.D3Q27, W.CENTRAL, W.EQ_ABSOLUTE, 1, L.LBM_FP64, L.LBM_ESOTERIC_TWIST, (384, 384, 384), 4),
     "c4_aa": (W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1, L.LBM_FP64, L.LBM_AA, (1024, 1024, 128), 3),
     "c2_f64": (W.D3Q19, W.RAW, W.EQ_DELTA, 1, L.LBM_FP64, L.LBM_PULL, (256, 256, 256), 3),
     "c2_f32": (W.D3Q19, W.RAW, W.EQ_DELTA, 1, L.LBM_FP32, L.LBM_PULL, (256, 256, 256), 3),
