@@ -415,8 +415,11 @@ def main():
     peak, peak_src = measured_peaks()
     bpc = bytes_per_cell(cfg)  # every population read once and written once per launch
     tb = lat.info().temporal_blocking if n == 1 else 1
+    resident = lat.info().resident_cluster if n == 1 else 0
     # N > 1: interior + 2 boundary launches (+ wait and signal kernels of the fused push)
     launches_per_step = (1.0 / tb) if n == 1 else (5 if isinstance(runner, D.PeerRunner) else 3)
+    if resident:  # one cluster launch runs all K steps of lbm_step(K)
+        launches_per_step = 1.0 / args.steps
     kernel_ms = ms_step * tb  # one launch covers tb steps on this stream
     achieved = bpc * cells_local / (kernel_ms * 1e-3) / 1e9
     kkey = f"{args.config}:{dtype_name(cfg)}"
@@ -428,6 +431,11 @@ def main():
                 "kernel": ("k_pull2 (two fused steps)" if tb == 2 else "k_pull/k_aa stream-collide") + f" ({kkey})"}
     if n > 1:
         roofline["note"] = "N > 1: per-step time of boundary + interior launches with the halo " + halo.split(":")[0]
+    if resident:
+        roofline["kernel"] = f"k_resident2 (cluster of {resident} CTAs, lattice in shared memory) ({kkey})"
+        roofline["note"] = ("cluster-resident loop: HBM is touched once per launch, a step is bound by the "
+                            "collision latency, a DSMEM store and one cluster barrier; achieved = the "
+                            "algorithmic bytes a step would move / step time, for comparison only")
 
     # end-to-end through the C ABI with host buffers (pinned): init from host rho/u,
     # K steps, macroscopic fields back to the host

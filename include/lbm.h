@@ -155,6 +155,15 @@ typedef struct {
                                every lbm_step(n) replays floor(n / 32) of them before plain
                                launches of the rest; same kernels, bitwise equal.
                                Environment LBM_CUDA_GRAPHS=0 (read per call) disables it.   */
+  int resident_cluster;     /* CTAs of the thread-block cluster that runs ALL n steps of an
+                               lbm_step(n) in one launch with the lattice resident in shared
+                               memory (2D, pull, single rank; the rows of each CTA plus two
+                               ghost rows of both grids must fit its shared memory, <= 512
+                               cells per CTA, i.e. lattices up to 8192 cells; halo rows
+                               cross via distributed shared memory, one cluster barrier per
+                               step; same collision code, bitwise equal); 0: not used.
+                               Environment LBM_RESIDENT=0 disables it, LBM_RESIDENT_CLUSTER=k
+                               caps the cluster size (both read per call).                 */
 } lbm_info;
 
 /* Creates a context: validates admissibility, allocates the population grid(s) (two for

@@ -5,6 +5,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace lbm {
@@ -48,7 +50,17 @@ struct Ops {
   void (*pull2)(const void *src, void *dst, const GridParams &g, const void *params, double swe_g, int zchunks,
                 cudaStream_t s);
   int tile_x, tile_y;
+  // n pull steps of a small 2D lattice in one launch of a `cluster`-CTA thread-block cluster
+  // with the lattice resident in shared memory (k_resident2); returns the launch's cudaError_t
+  // (nullptr for 3D stencils)
+  int (*resident)(const void *src, void *dst, const GridParams &g, const void *params, double swe_g, int bb,
+                  int nsteps, int cluster, cudaStream_t s);
 };
+
+// shared memory of k_resident2: two grids [Q][R + 2][nx]
+inline size_t resident_smem(int q, int nx, int rows, int esize) {
+  return (size_t)2 * q * (size_t)(rows + 2) * nx * esize;
+}
 
 // Temporal-blocking tile of k_pull2 (scripts/tb_variants.cu on B200,
 // profiles/r1/tb_variants.txt): D3Q19 fp64 16 x 8 (2 CTAs/SM; -17 % time per 2 steps on a
@@ -181,6 +193,40 @@ struct OpsImpl {
           static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
     }
   }
+  template <bool BB>
+  static cudaError_t launch_resident(const real *src, real *dst, const GridParams &g, const MethodParams<real> &p,
+                                     double swe_g, int nsteps, int cluster, cudaStream_t s) {
+    auto kern = k_resident2<S, SPACE, REG, real, RS, BB>;
+    const int rows = g.nzl / cluster;
+    const size_t smem = resident_smem(S::Q, g.nx, rows, (int)sizeof(real));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess && cluster > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)cluster, 1, 1);
+    cfg.blockDim = dim3((unsigned)std::min(1024, (rows * g.nx + 31) / 32 * 32), 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, src, dst, g, nsteps, p.rates, (real)swe_g, p.force);
+  }
+  static int resident(const void *src, void *dst, const GridParams &g, const void *params, double swe_g, int bb,
+                      int nsteps, int cluster, cudaStream_t s) {
+    if constexpr (S::D == 2) {
+      const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
+      const real *a = static_cast<const real *>(src);
+      real *b = static_cast<real *>(dst);
+      return (int)(bb ? launch_resident<true>(a, b, g, p, swe_g, nsteps, cluster, s)
+                      : launch_resident<false>(a, b, g, p, swe_g, nsteps, cluster, s));
+    }
+    return (int)cudaErrorNotSupported;
+  }
   static void attributes(int *regs, int *local_bytes) {
     cudaFuncAttributes a{};
     if (cudaFuncGetAttributes(&a, k_pull<S, SPACE, REG, real, false, RS>) == cudaSuccess) {
@@ -196,7 +242,8 @@ struct OpsImpl {
                              &attributes,
                              (S::D == 3 && TbTile<S, real>::TX > 0) ? &pull2 : nullptr,
                              TbTile<S, real>::TX,
-                             TbTile<S, real>::TY};
+                             TbTile<S, real>::TY,
+                             S::D == 2 ? &resident : nullptr};
 };
 
 }  // namespace lbm

@@ -112,6 +112,8 @@ struct lbm_ctx {
   double force[3] = {0, 0, 0};
   bool forced = false;
   int force_model = LBM_FORCE_GUO;
+  bool resident_failed = false;  // the cluster-resident launch was refused once: do not retry
+  int last_cluster = 0;
   const Ops *ops_plain = nullptr;  // the unforced kernels chosen at create
   bool tb_allowed = false;         // temporal blocking (two fused steps) eligible
   cudaGraphExec_t graph[2] = {nullptr, nullptr};  // captured step loops per parity (small lattices)
@@ -252,6 +254,36 @@ bool use_temporal_blocking(const lbm_ctx *c) {
   if (env && env[0] == '1') return true;
   // fewer CTAs than 4 waves leave the fused sweep tail-bound
   return tb_tiles(c) * tb_zchunks(c) >= kTbMinCtas;
+}
+
+// cluster-resident loop (k_resident2): small single-rank 2D pull lattices; returns the CTAs
+// per cluster (0: not used).  The largest cluster (<= 16 CTAs, one per SM) whose CTAs hold
+// their rows + 2 ghost rows of both grids in shared memory and at most kResidentMaxCellsPerCta
+// cells: a step is latency-bound (collision chain + DSMEM store + cluster barrier, ~1.1 us at
+// 256 cells per CTA); beyond 512 cells per CTA the CUDA-graph replay of plain launches, whose
+// steps spread over all SMs, is as fast (B200: 128^2 at 16 CTAs 8.6 vs 9.1 GLUPS).
+// LBM_RESIDENT=0 disables, LBM_RESIDENT_CLUSTER=k caps the cluster size (read per call).
+constexpr int kResidentMaxCellsPerCta = 512;
+int resident_cluster(const lbm_ctx *c) {
+  if (!c->ops->resident || c->resident_failed || c->nranks > 1 || c->streaming != LBM_PULL) return 0;
+  const char *env = getenv("LBM_RESIDENT");
+  if (env && env[0] == '0') return 0;
+  int cap = 16;
+  if (const char *ce = getenv("LBM_RESIDENT_CLUSTER")) cap = std::max(1, atoi(ce));
+  int optin = 0;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int ny = c->g.nzl, nx = c->g.nx;
+  for (int C = 16; C >= 1; C /= 2) {
+    if (C > cap || ny % C != 0) continue;
+    const int rows = ny / C;
+    if (lbm::resident_smem(c->q, nx, rows, c->esize) <= (size_t)optin && rows * nx <= kResidentMaxCellsPerCta)
+      return C;
+    return 0;  // fewer CTAs only hold more rows each
+  }
+  return 0;
 }
 
 // graph replay: small single-rank lattice on a capturable stream; LBM_CUDA_GRAPHS=0 disables
@@ -733,7 +765,8 @@ lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
   info->steps_done = c->steps;
   info->rate_specialization = c->rs;
   info->temporal_blocking = use_temporal_blocking(c) ? 2 : 1;
-  info->cuda_graph_steps = (c->nranks == 1 && use_graphs(c)) ? kGraphSteps : 0;
+  info->resident_cluster = resident_cluster(c);
+  info->cuda_graph_steps = (c->nranks == 1 && !info->resident_cluster && use_graphs(c)) ? kGraphSteps : 0;
   return LBM_OK;
 }
 
@@ -770,6 +803,21 @@ lbm_status lbm_step(lbm_ctx *c, int n) {
   LBM_CUDA(c, cudaSetDevice(c->device));
   GridParams g = c->g;
   int t = 0;
+  // small 2D lattices: all n steps in one cluster-resident launch (falls back to the plain
+  // path for good if the cluster cannot be launched on this device)
+  if (const int C = n > 0 ? resident_cluster(c) : 0) {
+    const int dst = c->cur ^ (n & 1);
+    const cudaError_t e = (cudaError_t)c->ops->resident(c->buf[c->cur], c->buf[dst], g, c->params, c->swe_g,
+                                                         c->bb, n, C, c->stream);
+    if (e == cudaSuccess) {
+      c->cur = dst;
+      c->steps += n;
+      c->last_cluster = C;
+      return check_launch(c, "k_resident2");
+    }
+    cudaGetLastError();
+    c->resident_failed = true;
+  }
   // small lattices are launch-bound: replay a captured CUDA graph of kGraphSteps steps
   if (use_graphs(c)) {
     lbm_status st = ensure_graphs(c);

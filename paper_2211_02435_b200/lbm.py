@@ -65,7 +65,8 @@ class lbm_info(ctypes.Structure):
                 ("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int), ("pitch", ctypes.c_size_t),
                 ("bytes_per_element", ctypes.c_size_t), ("device_bytes", ctypes.c_size_t),
                 ("steps_done", ctypes.c_longlong), ("rate_specialization", ctypes.c_int),
-                ("temporal_blocking", ctypes.c_int), ("cuda_graph_steps", ctypes.c_int)]
+                ("temporal_blocking", ctypes.c_int), ("cuda_graph_steps", ctypes.c_int),
+                ("resident_cluster", ctypes.c_int)]
 
 
 class lbm_peer_info(ctypes.Structure):
