@@ -142,10 +142,11 @@ typedef struct {
                                one become compile-time constants; set the environment
                                variable LBM_RATE_SPECIALIZATION=0 to force 0.            */
   int temporal_blocking;    /* time steps per sweep of lbm_step: 2 when pairs of steps are
-                               fused (D3Q19 fp64, pull, single rank, periodic, nx % 16 == 0,
-                               ny % 8 == 0, >= 1184 CTAs = 16x8 tile columns x slab chunks of
-                               >= 32 planes; the intermediate step stays in shared memory;
-                               same arithmetic, bitwise equal), else 1.  Environment
+                               fused (pull, single rank, periodic; D3Q19 fp64 with nx % 16 == 0,
+                               ny % 8 == 0 (16x8 tiles), or D2Q9 with nx % 256 == 0 (256-cell
+                               strips); >= 1184 CTAs = tiles x slab chunks of >= 32 planes;
+                               the intermediate step stays in shared memory; same
+                               arithmetic, bitwise equal), else 1.  Environment
                                LBM_TEMPORAL_BLOCKING: 0 (read at create) forces 1; 1 drops
                                the CTA-count condition.                                    */
   int cuda_graph_steps;     /* time steps per CUDA-graph launch of lbm_step (0: none).  Small

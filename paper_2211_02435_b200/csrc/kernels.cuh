@@ -658,6 +658,78 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Temporal blocking for 2D lattices: the same two-step sweep as k_pull2 with a 1D tile.
+// A CTA owns TX consecutive cells of a row and sweeps the slab axis (physical y): at row k
+// it computes step t+1 on the TX + 2 cells of the halo-extended strip into a 3-row ring,
+// then step t+2 on row k-1 of the strip interior from the ring.  The step-t loads of row
+// k+1 are issued before the collisions of row k (software pipelining: the HBM latency hides
+// under the arithmetic of two collisions).  Same collide() as k_pull: bitwise equal.
+// ---------------------------------------------------------------------------
+template <int TX>
+struct Tile1 {
+  static constexpr int HW = TX + 2;
+  static constexpr int THREADS = (HW + 31) / 32 * 32;
+};
+
+template <class S, int SPACE, int REG, class real, int RS, int TX, int MINB = 1, bool PF = true>
+__global__ void __launch_bounds__(Tile1<TX>::THREADS, MINB)
+    k_pull2_2d(const real *__restrict__ src, real *__restrict__ dst, const GridParams g, const Rates<real> r,
+               const real swe_g, const Force<real> fr) {
+  static_assert(S::D == 2, "2D temporal blocking");
+  using T = Tile1<TX>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  real *ring = reinterpret_cast<real *>(smem_raw);  // [3][Q][HW]
+  const int t = threadIdx.x;
+  const int x0 = blockIdx.x * TX;
+  const bool act1 = t < T::HW;
+  const int gx = wrapi(x0 - 1 + t, g.nx);
+  const int xs[3] = {wrapi(gx - 1, g.nx), gx, wrapi(gx + 1, g.nx)};
+  const int n = g.nzl;
+  const int p0 = (int)((long long)n * blockIdx.y / gridDim.y);
+  const int p1 = (int)((long long)n * (blockIdx.y + 1) / gridDim.y);
+  // step-t populations of the halo-extended strip at row k (pull: row k - xi_y)
+  auto load = [&](int k, real (&f)[S::Q]) {
+    const int zc = wrapi(k, n);
+    const long long zo[3] = {(long long)(wrapi(zc - 1, n) + 1) * g.plane, (long long)(zc + 1) * g.plane,
+                             (long long)(wrapi(zc + 1, n) + 1) * g.plane};
+    sfor<S::Q>([&](auto i) {
+      constexpr int cx = S::mx(i), cz = S::mz(i);
+      f[i] = ld_nc(src + zo[1 - cz] + (long long)i * g.pop + xs[1 - cx]);
+    });
+  };
+  real fn[S::Q];
+  if (PF && act1) load(p0 - 1, fn);
+  for (int k = p0 - 1; k <= p1; ++k) {
+    if (act1) {
+      real f[S::Q];
+      if constexpr (PF) {
+        sfor<S::Q>([&](auto i) { f[i] = fn[i]; });
+        if (k < p1) load(k + 1, fn);  // in flight during the two collisions below
+      } else {
+        load(k, f);
+      }
+      collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
+      real *slot = ring + (size_t)((k + 3) % 3) * S::Q * T::HW;  // k >= -1
+      sfor<S::Q>([&](auto i) { slot[i * T::HW + t] = f[i]; });
+    }
+    __syncthreads();
+    if (k >= p0 + 1 && t < TX) {
+      const int p = k - 1;  // row of step t+2
+      real f[S::Q];
+      sfor<S::Q>([&](auto i) {
+        constexpr int cx = S::mx(i), cz = S::mz(i);
+        const real *slot = ring + (size_t)((p - cz + 3) % 3) * S::Q * T::HW;
+        f[i] = slot[i * T::HW + (t + 1 - cx)];
+      });
+      collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
+      const long long own = (long long)(p + 1) * g.plane + (x0 + t);
+      sfor<S::Q>([&](auto i) { dst[own + (long long)i * g.pop] = f[i]; });
+    }
+    __syncthreads();
+  }
+}
+
 // canonical populations of selected cells (local linear index x + nx (y + ny z))
 template <class S, class real>
 __global__ void k_get_cells(const real *mem, const GridParams g, int aa, int state, const long long *__restrict__ idx,

@@ -69,9 +69,12 @@ inline size_t resident_smem(int q, int nx, int rows, int esize) {
 // latency (+55 % time at best).  The runtime also requires >= 4 waves of tiles.
 template <class S, class real>
 struct TbTile {
-  static constexpr bool on = (S::Q == 19) && sizeof(real) == 8;
-  static constexpr int TX = on ? 16 : 0;
-  static constexpr int TY = on ? 8 : 0;
+  // 2D (D2Q9, k_pull2_2d): 256-cell strips, 3-row ring of 3 x 9 x 258 values (55.7 KB fp64:
+  // 4 CTAs/SM); 3D: D3Q19 fp64 only (see above)
+  static constexpr bool on3 = (S::Q == 19) && sizeof(real) == 8;
+  static constexpr bool on = on3 || S::D == 2;
+  static constexpr int TX = S::D == 2 ? 256 : (on3 ? 16 : 0);
+  static constexpr int TY = S::D == 2 ? 1 : (on3 ? 8 : 0);
 };
 
 inline dim3 cell_grid(const GridParams &g, int nplanes) {
@@ -191,6 +194,21 @@ struct OpsImpl {
       }
       kern<<<dim3((unsigned)(g.nx / TX), (unsigned)(g.ny / TY), (unsigned)zchunks), T::THREADS, smem, s>>>(
           static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
+    } else if constexpr (S::D == 2) {
+      using T = Tile1<TX>;
+      const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
+      const size_t smem = (size_t)3 * S::Q * T::HW * sizeof(real);
+      // scripts/tb2d_variants.cu on B200 (profiles/r1/tb2d_variants.txt): >= 2 CTAs/SM with the
+      // next row's loads prefetched; SRT (light collision): 3 CTAs/SM without the prefetch
+      constexpr bool srt = SPACE == SPACE_POPULATION;
+      auto kern = k_pull2_2d<S, SPACE, REG, real, RS, TX, srt ? 3 : 2, !srt>;
+      static bool configured = false;
+      if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+      }
+      kern<<<dim3((unsigned)(g.nx / TX), (unsigned)zchunks, 1), T::THREADS, smem, s>>>(
+          static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
     }
   }
   template <bool BB>
@@ -240,7 +258,7 @@ struct OpsImpl {
   static constexpr Ops table{S::Q,      S::D,  &pull,         &aa,           &init,      &get_pop,
                              &set_pop, &macro, &test_collide, &check_finite, &get_cells, &diagnostics,
                              &attributes,
-                             (S::D == 3 && TbTile<S, real>::TX > 0) ? &pull2 : nullptr,
+                             (TbTile<S, real>::TX > 0) ? &pull2 : nullptr,
                              TbTile<S, real>::TX,
                              TbTile<S, real>::TY,
                              S::D == 2 ? &resident : nullptr};
