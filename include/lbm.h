@@ -145,8 +145,9 @@ typedef struct {
                                fused (pull, single rank, periodic; D3Q19 fp64 with nx % 16 == 0,
                                ny % 8 == 0 (16x8 tiles), or D2Q9 with nx % 256 == 0 (256-cell
                                strips); >= 1184 CTAs = tiles x slab chunks of >= 32 planes;
-                               the intermediate step stays in shared memory; same
-                               arithmetic, bitwise equal), else 1.  Environment
+                               the intermediate step stays in shared memory; the same
+                               collision code, equal to single steps up to FMA contraction
+                               by the compiler, i.e. to rounding), else 1.  Environment
                                LBM_TEMPORAL_BLOCKING: 0 (read at create) forces 1; 1 drops
                                the CTA-count condition.                                    */
   int cuda_graph_steps;     /* time steps per CUDA-graph launch of lbm_step (0: none).  Small

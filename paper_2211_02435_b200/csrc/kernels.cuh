@@ -520,8 +520,8 @@ struct Tile2 {
   static constexpr int THREADS = (HW + 31) / 32 * 32;
 };
 
-template <class S, int SPACE, int REG, class real, int RS, int TX, int TY>
-__global__ void __launch_bounds__(Tile2<TX, TY>::THREADS, 1)
+template <class S, int SPACE, int REG, class real, int RS, int TX, int TY, int MINB = 1, bool PF = false>
+__global__ void __launch_bounds__(Tile2<TX, TY>::THREADS, MINB)
     k_pull2(const real *__restrict__ src, real *__restrict__ dst, const GridParams g, const Rates<real> r,
             const real swe_g, const Force<real> fr) {
   using T = Tile2<TX, TY>;
@@ -546,17 +546,30 @@ __global__ void __launch_bounds__(Tile2<TX, TY>::THREADS, 1)
   // blockIdx.z: chunk [p0, p1) of the output planes (more CTAs for short slabs); each chunk
   // recomputes the two step-(t+1) planes at its ends
   const int p0 = (int)((long long)n * blockIdx.z / gridDim.z), p1 = (int)((long long)n * (blockIdx.z + 1) / gridDim.z);
+  // step-t populations of the halo-extended tile at plane k (pull: plane k - xi_z)
+  auto load = [&](int k, real (&f)[S::Q]) {
+    const int zc = wrapi(k, n);
+    long long zo[3];
+#pragma unroll
+    for (int s = -1; s <= 1; ++s) zo[s + 1] = (long long)(wrapi(zc + s, n) + 1) * g.plane;
+    sfor<S::Q>([&](auto i) {
+      constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+      f[i] = ld_nc(src + zo[1 - cz] + (long long)i * g.pop + ys[1 - cy] + xs[1 - cx]);
+    });
+  };
+  real fn[PF ? S::Q : 1];
+  if constexpr (PF) {
+    if (act1) load(p0 - 1, fn);
+  }
   for (int k = p0 - 1; k <= p1; ++k) {
     if (act1) {
-      const int zc = wrapi(k, n);
-      long long zo[3];
-#pragma unroll
-      for (int s = -1; s <= 1; ++s) zo[s + 1] = (long long)(wrapi(zc + s, n) + 1) * g.plane;
       real f[S::Q];
-      sfor<S::Q>([&](auto i) {
-        constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
-        f[i] = ld_nc(src + zo[1 - cz] + (long long)i * g.pop + ys[1 - cy] + xs[1 - cx]);
-      });
+      if constexpr (PF) {  // the next plane's loads fly during the collisions below
+        sfor<S::Q>([&](auto i) { f[i] = fn[i]; });
+        if (k < p1) load(k + 1, fn);
+      } else {
+        load(k, f);
+      }
       collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
       real *slot = ring + (size_t)((k + 3) % 3) * S::Q * T::HW;  // k >= -1
       sfor<S::Q>([&](auto i) { slot[i * T::HW + t] = f[i]; });

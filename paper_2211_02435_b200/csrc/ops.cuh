@@ -62,19 +62,26 @@ inline size_t resident_smem(int q, int nx, int rows, int esize) {
   return (size_t)2 * q * (size_t)(rows + 2) * nx * esize;
 }
 
-// Temporal-blocking tile of k_pull2 (scripts/tb_variants.cu on B200,
-// profiles/r1/tb_variants.txt): D3Q19 fp64 16 x 8 (2 CTAs/SM; -17 % time per 2 steps on a
-// 1024^2 x 128 lattice).  Not used for fp32 (+-5 %, worse on 256^3) nor D3Q27 — 27 fp64
-// populations per cell leave shared memory for too few warps to hide the fp64 collision
-// latency (+55 % time at best).  The runtime also requires >= 4 waves of tiles.
-template <class S, class real>
+// Temporal-blocking tile of k_pull2 / k_pull2_2d, measured on B200 (scripts/tb_variants.cu,
+// scripts/tb2d_variants.cu; profiles/r1/tb_variants*.txt, tb2d_variants.txt), 1024^2 x 128 and
+// 8192^2, time per 2 steps against two single k_pull steps:
+//   D3Q19 fp64: 16 x 8, 2 CTAs/SM, next plane's loads prefetched: raw 9.3 vs 12.2 ms,
+//               cumulant 10.3 vs 12.2 ms;
+//   D3Q19 fp32: 16 x 8, 3 CTAs/SM, prefetched: 4.96 vs 6.16 ms;
+//   D3Q27 fp64 raw / SRT: 16 x 8, 1 CTA/SM, prefetched: raw 14.0 vs 17.3 ms;
+//   D3Q27 central: 17.1 vs 17.4 (not used), cumulant: 20.4 vs 17.4 (not used) — 27 fp64
+//               populations per halo cell leave shared memory for too few warps to hide the
+//               heavier collisions;
+//   D2Q9: 256-cell strips (k_pull2_2d), 2-3 CTAs/SM.
+// The runtime also requires >= 4 waves of CTAs.
+template <class S, class real, int SPACE>
 struct TbTile {
-  // 2D (D2Q9, k_pull2_2d): 256-cell strips, 3-row ring of 3 x 9 x 258 values (55.7 KB fp64:
-  // 4 CTAs/SM); 3D: D3Q19 fp64 only (see above)
-  static constexpr bool on3 = (S::Q == 19) && sizeof(real) == 8;
+  static constexpr bool f64 = sizeof(real) == 8;
+  static constexpr bool on3 = (S::Q == 19) || (S::Q == 27 && f64 && (SPACE == SPACE_RAW || SPACE == SPACE_POPULATION));
   static constexpr bool on = on3 || S::D == 2;
   static constexpr int TX = S::D == 2 ? 256 : (on3 ? 16 : 0);
   static constexpr int TY = S::D == 2 ? 1 : (on3 ? 8 : 0);
+  static constexpr int MINB = S::Q == 27 ? 1 : (f64 ? 2 : 3);  // 3D: CTAs per SM
 };
 
 inline dim3 cell_grid(const GridParams &g, int nplanes) {
@@ -181,12 +188,13 @@ struct OpsImpl {
   }
   static void pull2(const void *src, void *dst, const GridParams &g, const void *params, double swe_g,
                     int zchunks, cudaStream_t s) {
-    constexpr int TX = TbTile<S, real>::TX, TY = TbTile<S, real>::TY;
+    using TT = TbTile<S, real, SPACE>;
+    constexpr int TX = TT::TX, TY = TT::TY;
     if constexpr (S::D == 3 && TX > 0) {
       using T = Tile2<TX, TY>;
       const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
       const size_t smem = (size_t)3 * S::Q * T::HW * sizeof(real);
-      auto kern = k_pull2<S, SPACE, REG, real, RS, TX, TY>;
+      auto kern = k_pull2<S, SPACE, REG, real, RS, TX, TY, TT::MINB, true>;
       static bool configured = false;  // opt in to > 48 KB of dynamic shared memory once
       if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -258,9 +266,9 @@ struct OpsImpl {
   static constexpr Ops table{S::Q,      S::D,  &pull,         &aa,           &init,      &get_pop,
                              &set_pop, &macro, &test_collide, &check_finite, &get_cells, &diagnostics,
                              &attributes,
-                             (TbTile<S, real>::TX > 0) ? &pull2 : nullptr,
-                             TbTile<S, real>::TX,
-                             TbTile<S, real>::TY,
+                             (TbTile<S, real, SPACE>::TX > 0) ? &pull2 : nullptr,
+                             TbTile<S, real, SPACE>::TX,
+                             TbTile<S, real, SPACE>::TY,
                              S::D == 2 ? &resident : nullptr};
 };
 

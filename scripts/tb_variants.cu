@@ -19,11 +19,11 @@ using namespace lbm;
     }                                                                                           \
   } while (0)
 
-template <class S, int SP, int REG, int TX, int TY, class real = double>
+template <class S, int SP, int REG, int TX, int TY, class real = double, int MINB = 1, bool PF = false>
 float time_tb(const GridParams &g, real *a, real *b, const Rates<real> &r, const Force<real> &fr) {
   using T = Tile2<TX, TY>;
   const size_t smem = (size_t)3 * S::Q * T::HW * sizeof(real);
-  auto kern = k_pull2<S, SP, REG, real, RS_GENERAL, TX, TY>;
+  auto kern = k_pull2<S, SP, REG, real, RS_GENERAL, TX, TY, MINB, PF>;
   if (smem > 232448) return -1.f;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid(g.nx / TX, g.ny / TY, 1);
@@ -47,8 +47,8 @@ float time_tb(const GridParams &g, real *a, real *b, const Rates<real> &r, const
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T::THREADS, smem);
   cudaFuncAttributes at{};
   cudaFuncGetAttributes(&at, kern);
-  printf("  TB %2dx%-2d threads %4d smem %6zu B  blocks/SM %d regs %3d  -> %7.3f ms per 2 steps\n", TX, TY,
-         T::THREADS, smem, nb, at.numRegs, ms / reps);
+  printf("  TB %2dx%-2d minB %d pf %d threads %4d smem %6zu B  blocks/SM %d regs %3d local %3zu -> %7.3f ms per 2 steps\n",
+         TX, TY, MINB, (int)PF, T::THREADS, smem, nb, at.numRegs, at.localSizeBytes, ms / reps);
   return ms / reps;
 }
 
@@ -98,15 +98,21 @@ int main() {
     CK(cudaMemset(b, 0, elems * 8));
     printf("D3Q27 cumulant zc+eq fp64\n");
     time_single<D3Q27, SPACE_CUMULANT, REG_ZC_ABS>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 32, 8>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 16, 16>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 16, 8>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 32, 4>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 8, 8>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 16, 8, double, 1, true>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 8, 8, double, 3, true>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 8, 8, double, 2, true>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 16, 4, double, 2, true>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 32, 4, double, 1, true>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 16, 16, double, 1, true>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 24, 8, double, 1, true>(g, a, b, r, fr);
+    printf("D3Q27 central zc+eq fp64\n");
+    time_single<D3Q27, SPACE_CENTRAL, REG_ZC_ABS>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CENTRAL, REG_ZC_ABS, 16, 8, double, 1, true>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CENTRAL, REG_ZC_ABS, 8, 8, double, 3, true>(g, a, b, r, fr);
     printf("D3Q27 raw zc+delta fp64\n");
     time_single<D3Q27, SPACE_RAW, REG_DELTA>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_RAW, REG_DELTA, 32, 8>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_RAW, REG_DELTA, 16, 8>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_RAW, REG_DELTA, 16, 8, double, 1, true>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_RAW, REG_DELTA, 8, 8, double, 3, true>(g, a, b, r, fr);
     cudaFree(a);
     cudaFree(b);
   }
@@ -120,22 +126,23 @@ int main() {
     CK(cudaMemset(b, 0, elems * 8));
     printf("D3Q19 raw zc+delta fp64\n");
     time_single<D3Q19, SPACE_RAW, REG_DELTA>(g, a, b, r, fr);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 32, 8>(g, a, b, r, fr);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 8>(g, a, b, r, fr);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 32, 4>(g, a, b, r, fr);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 8, 8>(g, a, b, r, fr);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 4>(g, a, b, r, fr);
+    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 8, double, 2, true>(g, a, b, r, fr);
+    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 8, 8, double, 3, true>(g, a, b, r, fr);
+    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 16, double, 1, true>(g, a, b, r, fr);
+    printf("D3Q19 cumulant zc+eq fp64\n");
+    time_single<D3Q19, SPACE_CUMULANT, REG_ZC_ABS>(g, a, b, r, fr);
+    time_tb<D3Q19, SPACE_CUMULANT, REG_ZC_ABS, 16, 8>(g, a, b, r, fr);
+    time_tb<D3Q19, SPACE_CUMULANT, REG_ZC_ABS, 16, 8, double, 2, true>(g, a, b, r, fr);
     float *af = reinterpret_cast<float *>(a), *bf = reinterpret_cast<float *>(b);
     Rates<float> rf;
     for (int i = 0; i < 27; ++i) rf.w[i] = 1.0f + 0.02f * i;
     Force<float> ff{};
     printf("D3Q19 raw zc+delta fp32\n");
     time_single<D3Q19, SPACE_RAW, REG_DELTA, float>(g, af, bf, rf, ff);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 32, 8, float>(g, af, bf, rf, ff);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 8, float>(g, af, bf, rf, ff);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 16, float>(g, af, bf, rf, ff);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 32, 16, float>(g, af, bf, rf, ff);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 8, 8, float>(g, af, bf, rf, ff);
+    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 8, float, 3, true>(g, af, bf, rf, ff);
+    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 8, float, 4, true>(g, af, bf, rf, ff);
+    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 8, 8, float, 5, true>(g, af, bf, rf, ff);
+    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 4, float, 5, true>(g, af, bf, rf, ff);
     cudaFree(a);
     cudaFree(b);
   }
