@@ -99,10 +99,10 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(config_name, kernel_key, cells):
+def ncu_traffic(config_name, kernel_key, cells, steps_per_launch=1):
     """Per-launch DRAM bytes (read + write) of the timed kernel from the committed
     ncu --set full capture (profiles/ncu_summary.json: bytes per cell of the same
-    kernel) times this launch's cells, or None."""
+    kernel, single-step or two fused steps) times this launch's cells, or None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
@@ -110,7 +110,7 @@ def ncu_traffic(config_name, kernel_key, cells):
         with open(p) as fh:
             d = json.load(fh)
         e = d.get(config_name)
-        if e and e.get("kernel_key") == kernel_key:
+        if e and e.get("kernel_key") == kernel_key and int(e.get("time_steps_per_launch", 1)) == steps_per_launch:
             return round(float(e["dram_bytes_per_cell"]) * cells)
     except Exception:
         return None
@@ -423,7 +423,7 @@ def main():
     kernel_ms = ms_step * tb  # one launch covers tb steps on this stream
     achieved = bpc * cells_local / (kernel_ms * 1e-3) / 1e9
     kkey = f"{args.config}:{dtype_name(cfg)}"
-    traffic = ncu_traffic(args.config, kkey, cells_local)
+    traffic = None if resident else ncu_traffic(args.config, kkey, cells_local, tb)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "algorithmic_bytes_per_cell": bpc, "cells_per_launch": cells_local,
