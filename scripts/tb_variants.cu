@@ -99,50 +99,20 @@ int main() {
     printf("D3Q27 cumulant zc+eq fp64\n");
     time_single<D3Q27, SPACE_CUMULANT, REG_ZC_ABS>(g, a, b, r, fr);
     time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 16, 8, double, 1, true>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 8, 8, double, 3, true>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 16, 6, double, 2, true>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 12, 8, double, 2, true>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 16, 6, double, 2, false>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 32, 2, double, 2, true>(g, a, b, r, fr);
     time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 8, 8, double, 2, true>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 16, 4, double, 2, true>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 32, 4, double, 1, true>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 16, 16, double, 1, true>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_CUMULANT, REG_ZC_ABS, 24, 8, double, 1, true>(g, a, b, r, fr);
     printf("D3Q27 central zc+eq fp64\n");
     time_single<D3Q27, SPACE_CENTRAL, REG_ZC_ABS>(g, a, b, r, fr);
     time_tb<D3Q27, SPACE_CENTRAL, REG_ZC_ABS, 16, 8, double, 1, true>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_CENTRAL, REG_ZC_ABS, 8, 8, double, 3, true>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CENTRAL, REG_ZC_ABS, 16, 6, double, 2, true>(g, a, b, r, fr);
+    time_tb<D3Q27, SPACE_CENTRAL, REG_ZC_ABS, 12, 8, double, 2, true>(g, a, b, r, fr);
     printf("D3Q27 raw zc+delta fp64\n");
     time_single<D3Q27, SPACE_RAW, REG_DELTA>(g, a, b, r, fr);
     time_tb<D3Q27, SPACE_RAW, REG_DELTA, 16, 8, double, 1, true>(g, a, b, r, fr);
-    time_tb<D3Q27, SPACE_RAW, REG_DELTA, 8, 8, double, 3, true>(g, a, b, r, fr);
-    cudaFree(a);
-    cudaFree(b);
-  }
-  {
-    g.plane = 19LL * g.pop;
-    size_t elems = (size_t)(nz + 2) * g.plane;
-    double *a, *b;
-    CK(cudaMalloc(&a, elems * 8));
-    CK(cudaMalloc(&b, elems * 8));
-    CK(cudaMemset(a, 0, elems * 8));
-    CK(cudaMemset(b, 0, elems * 8));
-    printf("D3Q19 raw zc+delta fp64\n");
-    time_single<D3Q19, SPACE_RAW, REG_DELTA>(g, a, b, r, fr);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 8, double, 2, true>(g, a, b, r, fr);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 8, 8, double, 3, true>(g, a, b, r, fr);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 16, double, 1, true>(g, a, b, r, fr);
-    printf("D3Q19 cumulant zc+eq fp64\n");
-    time_single<D3Q19, SPACE_CUMULANT, REG_ZC_ABS>(g, a, b, r, fr);
-    time_tb<D3Q19, SPACE_CUMULANT, REG_ZC_ABS, 16, 8>(g, a, b, r, fr);
-    time_tb<D3Q19, SPACE_CUMULANT, REG_ZC_ABS, 16, 8, double, 2, true>(g, a, b, r, fr);
-    float *af = reinterpret_cast<float *>(a), *bf = reinterpret_cast<float *>(b);
-    Rates<float> rf;
-    for (int i = 0; i < 27; ++i) rf.w[i] = 1.0f + 0.02f * i;
-    Force<float> ff{};
-    printf("D3Q19 raw zc+delta fp32\n");
-    time_single<D3Q19, SPACE_RAW, REG_DELTA, float>(g, af, bf, rf, ff);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 8, float, 3, true>(g, af, bf, rf, ff);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 8, float, 4, true>(g, af, bf, rf, ff);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 8, 8, float, 5, true>(g, af, bf, rf, ff);
-    time_tb<D3Q19, SPACE_RAW, REG_DELTA, 16, 4, float, 5, true>(g, af, bf, rf, ff);
+    time_tb<D3Q27, SPACE_RAW, REG_DELTA, 16, 6, double, 2, true>(g, a, b, r, fr);
     cudaFree(a);
     cudaFree(b);
   }
