@@ -358,7 +358,7 @@ def main():
                         if cfg["streaming"] == L.LBM_PULL else
                         "peer: AA odd-step boundary kernels access the neighbours' planes over NVLink peer "
                         "memory (CUDA IPC), device flags")
-            except L.LbmError as ex:
+            except (L.LbmError, D.PeerUnavailable) as ex:
                 if args.halo == "peer":
                     raise
                 print(f"warning: fused halo push unavailable ({ex}); using the NCCL exchange", file=sys.stderr)

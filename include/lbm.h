@@ -231,7 +231,8 @@ typedef struct {
 lbm_status lbm_peer_export(lbm_ctx *ctx, lbm_peer_info *out);
 /* Maps the neighbours' grids and flags; LBM_EINVAL if their lattice, stencil, precision or
    ranks do not match this context's ring; LBM_EUNSUPPORTED for Esoteric Pull / Twist or one rank
-   (at export); LBM_ECUDA if the memory cannot be mapped (no peer access). Resets the flags. */
+   (at export); LBM_ECUDA if the memory cannot be mapped (no peer access; nothing stays mapped).
+   Resets the flags.  lower = upper = NULL disconnects (unmaps the neighbours; synchronises). */
 lbm_status lbm_peer_connect(lbm_ctx *ctx, const lbm_peer_info *lower, const lbm_peer_info *upper);
 /* PULL: pushes the current grid's boundary planes into the neighbours' ghost planes; AA:
    only the handshake (orders the neighbours' initialisation before the first step). */

@@ -949,9 +949,24 @@ lbm_status lbm_peer_export(lbm_ctx *c, lbm_peer_info *out) {
   return LBM_OK;
 }
 
+lbm_status peer_connect_impl(lbm_ctx *c, const lbm_peer_info *lo, const lbm_peer_info *hi);
+
 lbm_status lbm_peer_connect(lbm_ctx *c, const lbm_peer_info *lo, const lbm_peer_info *hi) {
   NvtxRange nvtx_("lbm_peer_connect");
-  if (!c || !lo || !hi) return LBM_EINVAL;
+  if (!c || (!lo) != (!hi)) return LBM_EINVAL;
+  if (!lo) {  // disconnect: unmap the neighbours (back to lbm_step_region + an external exchange)
+    LBM_CUDA(c, cudaSetDevice(c->device));
+    LBM_CUDA(c, cudaDeviceSynchronize());
+    peer_release(c);
+    drop_graphs(c);
+    return LBM_OK;
+  }
+  const lbm_status s = peer_connect_impl(c, lo, hi);
+  if (s != LBM_OK) peer_release(c);  // no half-mapped ring stays behind
+  return s;
+}
+
+lbm_status peer_connect_impl(lbm_ctx *c, const lbm_peer_info *lo, const lbm_peer_info *hi) {
   if (!c->peer_flags) return fail(c, LBM_EINVAL, "lbm_peer_export first");
   const lbm_peer_info *nb[2] = {lo, hi};
   const int want[2] = {(c->rank + c->nranks - 1) % c->nranks, (c->rank + 1) % c->nranks};

@@ -227,6 +227,10 @@ def step_peer_local(lats, n: int):
         assert not l.peer_timed_out(), "a neighbour wait timed out"
 
 
+class PeerUnavailable(RuntimeError):
+    """Raised on EVERY rank when any rank cannot set up the fused halo push."""
+
+
 class PeerRunner:
     """Multi-process time stepping with the fused halo push: the boundary-plane kernel
     stores the slab-crossing populations straight into the neighbours' ghost planes
@@ -238,12 +242,33 @@ class PeerRunner:
         import torch.distributed as dist
 
         self.lat, self.rank, self.nranks, self.group = lat, rank, nranks, group
-        mine = lat.peer_export()
+        # collective setup: every rank takes part in every gather even when its own export or
+        # connect fails, and either all ranks run the fused push or none does (a rank that
+        # mapped its neighbours unmaps them again), so a fallback cannot deadlock the group
+        err = None
+        try:
+            mine = lat.peer_export()
+        except Exception as ex:  # noqa: BLE001 — reported collectively below
+            mine, err = None, ex
         infos = [None] * nranks
         dist.all_gather_object(infos, mine, group=group)
         lo, hi = neighbours(rank, nranks)
-        lat.peer_connect(infos[lo], infos[hi])
-        lat.sync()
+        connected = False
+        if err is None and infos[lo] is not None and infos[hi] is not None:
+            try:
+                lat.peer_connect(infos[lo], infos[hi])
+                lat.sync()
+                connected = True
+            except Exception as ex:  # noqa: BLE001
+                err = ex
+        oks = [None] * nranks
+        dist.all_gather_object(oks, connected, group=group)
+        if not all(oks):
+            if connected:
+                lat.peer_disconnect()
+            bad = [r for r, o in enumerate(oks) if not o]
+            raise PeerUnavailable(f"rank {rank}: fused halo push unavailable on ranks {bad}"
+                                  + (f" ({err})" if err else ""))
         dist.barrier(group=group)
 
     def prime(self):

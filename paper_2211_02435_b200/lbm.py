@@ -279,6 +279,9 @@ class Lattice:
         hi = lbm_peer_info.from_buffer_copy(upper)
         _check(lib().lbm_peer_connect(self._ctx, ctypes.byref(lo), ctypes.byref(hi)), self._ctx)
 
+    def peer_disconnect(self):
+        _check(lib().lbm_peer_connect(self._ctx, None, None), self._ctx)
+
     def peer_prime(self):
         _check(lib().lbm_peer_prime(self._ctx), self._ctx)
 

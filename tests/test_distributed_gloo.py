@@ -192,3 +192,52 @@ def test_peer_runner_host_protocol(world):
         calls = out[r]
         lo, hi = (r - 1) % world, (r + 1) % world
         assert calls == ["export", ("connect", lo, hi), "sync", "sync", "prime", ("step", 7)], calls
+
+
+class _FailingPeerLattice(_FakePeerLattice):
+    """Rank `bad` cannot map its neighbours (as without NVLink peer access)."""
+
+    bad = 1
+
+    def peer_connect(self, lower, upper):
+        if self.rank == self.bad:
+            self.calls.append("connect-failed")
+            raise L.LbmError(L.LBM_ECUDA, "cudaIpcOpenMemHandle: peer access unsupported")
+        super().peer_connect(lower, upper)
+
+    def peer_disconnect(self):
+        self.calls.append("disconnect")
+
+
+def _peer_fail_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lat = _FailingPeerLattice(rank, world)
+        try:
+            D.PeerRunner(lat, rank, world)
+            out[rank] = ("no error", lat.calls)
+        except D.PeerUnavailable as ex:
+            out[rank] = (str(ex), lat.calls)
+        dist.barrier()  # the group is still usable: the fallback's collectives line up
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_runner_fails_collectively(world):
+    """One rank's failed peer mapping makes EVERY rank raise PeerUnavailable (no deadlock, no
+    rank left on the fused path); ranks that had connected unmap their neighbours again, so
+    bench.py's fallback to the NCCL exchange is taken by the whole group."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_peer_fail_worker, args=(world, free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        msg, calls = out[r]
+        assert "unavailable on ranks [1]" in msg, msg
+        if r == _FailingPeerLattice.bad:
+            assert calls == ["export", "connect-failed"], calls
+        else:
+            assert calls[-1] == "disconnect" and calls[0] == "export", calls
