@@ -316,3 +316,43 @@ def test_peer_aa_graph_replay_and_macroscopic():
     np.testing.assert_array_equal(f, f1)
     np.testing.assert_array_equal(rho, rho1)
     np.testing.assert_array_equal(u, u1)
+
+
+@pytest.mark.parametrize("streaming,space,eq,model", [
+    (L.LBM_PULL, W.CENTRAL, W.EQ_DELTA, L.LBM_FORCE_HE),
+    (L.LBM_PULL, W.CUMULANT, W.EQ_ABSOLUTE, L.LBM_FORCE_GUO),
+    (L.LBM_AA, W.RAW, W.EQ_ABSOLUTE, L.LBM_FORCE_GUO),
+])
+def test_peer_forced_then_disconnect_equals_single_rank(streaming, space, eq, model):
+    """Body forces (He, cumulant first-order source) through the fused peer path, then
+    lbm_peer_connect(NULL, NULL) on every rank and more steps through the exchange path
+    (lbm_step_region + LocalTransport): the whole run equals the single-rank one bitwise."""
+    st, zc, nranks = W.D3Q27, 1, 3
+    shape = (20, 10, 12)
+    rates = W.rate_set_p(st)
+    F = np.array([2e-4, -1e-4, 3e-4])
+    f0 = initial_state(st, space, eq, zc, shape)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, streaming=streaming) as lat:
+        lat.set_populations(f0)
+        lat.set_force(F, model=model)
+        lat.step(9 + 6)
+        single = lat.get_populations()
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, rank=r, nranks=nranks, streaming=streaming)
+            for r in range(nranks)]
+    for lat in lats:
+        lat.set_populations(np.ascontiguousarray(f0[:, lat.offset:lat.offset + lat.extent]))
+        lat.set_force(F, model=model)
+    D.connect_local(lats)
+    D.step_peer_local(lats, 9)
+    mid = np.concatenate([lat.get_populations() for lat in lats], axis=1)
+    for lat in lats:
+        lat.sync()
+        lat.peer_disconnect()
+    for lat in lats:  # reload the canonical state and continue on the exchange path
+        lat.set_populations(np.ascontiguousarray(mid[:, lat.offset:lat.offset + lat.extent]))
+    D.prime_local(lats)
+    D.step_local(lats, 6)
+    multi = np.concatenate([lat.get_populations() for lat in lats], axis=1)
+    for lat in lats:
+        lat.close()
+    np.testing.assert_array_equal(multi, single)
