@@ -195,11 +195,9 @@ struct OpsImpl {
       const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
       const size_t smem = (size_t)3 * S::Q * T::HW * sizeof(real);
       auto kern = k_pull2<S, SPACE, REG, real, RS, TX, TY, TT::MINB, true>;
-      static bool configured = false;  // opt in to > 48 KB of dynamic shared memory once
-      if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-      }
+      // opt in to > 48 KB of dynamic shared memory (per device: set on every launch, ~1 us
+      // against a multi-ms sweep; a process-wide "done once" flag would miss a second GPU)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       kern<<<dim3((unsigned)(g.nx / TX), (unsigned)(g.ny / TY), (unsigned)zchunks), T::THREADS, smem, s>>>(
           static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
     } else if constexpr (S::D == 2) {
@@ -210,11 +208,7 @@ struct OpsImpl {
       // next row's loads prefetched; SRT (light collision): 3 CTAs/SM without the prefetch
       constexpr bool srt = SPACE == SPACE_POPULATION;
       auto kern = k_pull2_2d<S, SPACE, REG, real, RS, TX, srt ? 3 : 2, !srt>;
-      static bool configured = false;
-      if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-      }
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       kern<<<dim3((unsigned)(g.nx / TX), (unsigned)zchunks, 1), T::THREADS, smem, s>>>(
           static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
     }
