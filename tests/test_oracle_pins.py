@@ -502,6 +502,26 @@ def test_tgv_energy_decay(space, eq, zc, nu):
     assert abs(ratio / ref - 1) < 1e-2, (ratio, ref)
 
 
+@pytest.mark.parametrize("space,eq,zc", [
+    (W.POPULATION, W.EQ_DELTA, 1), (W.RAW, W.EQ_DELTA, 1), (W.CENTRAL, W.EQ_ABSOLUTE, 1),
+    (W.CUMULANT, W.EQ_ABSOLUTE, 1),
+])
+def test_tgv_second_order_convergence(space, eq, zc):
+    """The deviation of E/E0 from exp(-4 nu kappa^2 t) (eq:TGA_kin_energy) converges at second
+    order under diffusive scaling (L = 16, 32, 64; u0 = 0.05 * 32 / L; t to E/E0 ~ 1/2): the
+    error ratio between successive lattices is 4 (LBM is second-order accurate in space; the
+    Mach-number error u0^2 shrinks at the same rate)."""
+    nu = 0.05
+    errs = []
+    for L in (16, 32, 64):
+        k = 2 * math.pi / L
+        steps = int(round(math.log(2) / (4 * nu * k * k)))
+        ratio = run_tgv(W.D2Q9, space, eq, zc, nu, 0.05 * 32 / L, L, steps, prec=oracle.DOUBLE)
+        errs.append(abs(ratio / W.tgv_energy_ratio(nu, L, steps) - 1))
+    for a, b in zip(errs, errs[1:]):
+        assert 3.6 < a / b < 4.4, errs
+
+
 FORCE = np.array([2e-4, -1e-4, 3e-4])
 
 
