@@ -72,3 +72,34 @@ def test_fp32_in_place_patterns_equal_pull(st):
             outs.append(lat.get_populations())
     for other in outs[1:]:
         np.testing.assert_array_equal(outs[0], other)
+
+
+@pytest.mark.parametrize("st,space,eq,streaming", [
+    (W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, L.LBM_PULL),
+    (W.D3Q27, W.CENTRAL, W.EQ_ABSOLUTE, L.LBM_AA),
+    (W.D3Q19, W.RAW, W.EQ_DELTA, L.LBM_PULL),
+])
+def test_gpu_tgv_second_order_convergence(st, space, eq, streaming):
+    """Physics of the GPU path beyond the sizes the oracle reaches: the Taylor-Green decay
+    E/E0 = exp(-4 nu kappa^2 t) (eq:TGA_kin_energy) at L = 32, 64, 128 (extruded along z,
+    4 planes) converges at second order under diffusive scaling (error ratio ~4)."""
+    nu = 0.05
+    om = W.omega_from_nu(nu)
+    rates = W.regularized_rates(st, om)
+    errs = []
+    for Ln in (32, 64, 128):
+        shape = (Ln, Ln, 4)
+        k = 2 * np.pi / Ln
+        steps = int(round(np.log(2) / (4 * nu * k * k)))
+        rho, u = W.tgv_fields(Ln, Ln, 4, 0.05 * 64 / Ln)
+        with L.Lattice(st, space, eq, rates, shape, zero_centered=True, streaming=streaming) as lat:
+            lat.init_macroscopic(rho, u)
+            r0, u0 = lat.get_macroscopic()
+            e0 = 0.5 * (r0 * (u0 ** 2).sum(0)).sum()
+            lat.step(steps)
+            r1, u1 = lat.get_macroscopic()
+            e1 = 0.5 * (r1 * (u1 ** 2).sum(0)).sum()
+        errs.append(abs(e1 / e0 / W.tgv_energy_ratio(nu, Ln, steps) - 1))
+    assert errs[-1] < 5e-3, errs
+    for a, b in zip(errs, errs[1:]):
+        assert 3.5 < a / b < 4.5, errs
