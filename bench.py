@@ -231,9 +231,11 @@ def reference_arm(args, cfg, name):
     q = W.Q_OF[st]
     rates = rates_of(cfg)
     g = W.swe_lattice_parameters()[0] if cfg["eq"] == W.EQ_SWE else 0.0
-    # a bounded sample per step, sized by a probe so the run ends in a few minutes
+    # a bounded sample per step, sized by a probe so the whole --steps K --warmup W run ends in
+    # a few minutes: <= 4 s per step and <= ~150 s for the K + W steps
     mlups0, cores, _ = oracle_mlups(cfg, target_seconds=2.0)
-    per_step_cells = int(min(4e6, max(4096, mlups0 * 1e6 * 4.0)))  # ~4 s per step
+    per_step_s = min(4.0, max(0.05, 150.0 / max(1, args.steps + args.warmup)))
+    per_step_cells = int(min(4e6, max(4096, mlups0 * 1e6 * per_step_s)))
     if W.DIM_OF[st] == 2:
         ny = max(64, (per_step_cells // 1024) // 8 * 8)
         shape = (1024, ny, 1)
