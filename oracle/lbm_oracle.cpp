@@ -25,7 +25,8 @@
  *       absolute storage           eq:MrtUpdateGeneral
  *       zero-centered + delta eq   eq:MrtUpdateGeneralDeviationOnly
  *       zero-centered + abs eq     eq:MrtUpdateAbsoluteFromZeroCentered
- *   * equilibria: continuous Maxwellian (eq:ContMaxwellian)
+ *   * equilibria: the discrete second-order polynomial f_eq (q_eq = T(f_eq), PAPER.md:485-487;
+ *     DESIGN.md reading R29) or the continuous Maxwellian (eq:ContMaxwellian)
  *     represented in the method's own collision space and truncated at second
  *     order in u (reading R4); background
  *     f0 = M^{-1} m0; the shallow-water discrete
@@ -59,7 +60,7 @@ namespace {
 
 enum { ST_D2Q9 = 0, ST_D3Q19 = 1, ST_D3Q27 = 2 };
 enum { SP_POPULATION = 0, SP_RAW = 1, SP_CENTRAL = 2, SP_CUMULANT = 3 };
-enum { EQ_ABSOLUTE = 0, EQ_DELTA = 1, EQ_SWE = 2 };
+enum { EQ_ABSOLUTE = 0, EQ_DELTA = 1, EQ_SWE = 2, EQ_DISCRETE = 3, EQ_DISCRETE_DELTA = 4 };
 enum { BC_PERIODIC = 0, BC_NOSLIP = 1 };
 
 struct Term {
@@ -473,6 +474,18 @@ template <class R> static bool he_force(const Method<R> &m, R rho, const R u[3],
   return true;
 }
 
+/* Discrete second-order hydrodynamic equilibrium (reading R29): the equilibrium "specified as a */
+/* discrete distribution f_eq", represented in collision space as q_eq = T(f_eq)              */
+/* (the algebraic form "discrete or continuous"):             */
+/*   f_eq_i = w_i rho [1 + 3 xi.u + 9/2 (xi.u)^2 - 3/2 u.u]   (c_s^2 = 1/3).                 */
+template <class R> static void discrete_equilibrium(const Method<R> &m, R rho, const R u[3], R *feq) {
+  const R uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+  for (int i = 0; i < m.q; ++i) {
+    const R cu = R(m.xi[i][0]) * u[0] + R(m.xi[i][1]) * u[1] + R(m.xi[i][2]) * u[2];
+    feq[i] = m.w[i] * rho * (R(1) + R(3) * cu + R(9) * cu * cu / R(2) - R(3) * uu / R(2));
+  }
+}
+
 /* K(u)[p][i] = p(xi_i - u) */
 template <class R> static void central_matrix(const Method<R> &m, const R u[3], R *K) {
   int q = m.q;
@@ -573,7 +586,9 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
   macroscopic(m, fin, rho, u);
   R fabs_[27], q0[27], qeq[27], qs[27], K[27 * 27];
 
-  const bool delta = (m.eq == EQ_DELTA);  // deviation-only (eq:MrtUpdateGeneralDeviationOnly)
+  // deviation-only (eq:MrtUpdateGeneralDeviationOnly)
+  const bool delta = (m.eq == EQ_DELTA || m.eq == EQ_DISCRETE_DELTA);
+  const bool discrete = (m.eq == EQ_DISCRETE || m.eq == EQ_DISCRETE_DELTA);
   const R u0[3] = {0, 0, 0};                // background state rho0 = 1, u = 0
   // absolute populations for the absolute-equilibrium regimes
   for (int i = 0; i < q; ++i) fabs_[i] = (m.zc && !delta) ? fin[i] + m.w[i] : fin[i];
@@ -591,14 +606,24 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
     }
   }
 
+  // discrete equilibrium (reading R29) in the form of the regime: f_eq, or f_eq - f0 (delta)
+  R fd[27];
+  if (discrete) {
+    discrete_equilibrium(m, rho, u, fd);
+    if (delta)
+      for (int i = 0; i < q; ++i) fd[i] -= m.w[i];
+  }
+
   if (m.space == SP_POPULATION) {
-    // T = identity; f_eq = M^{-1} m_eq (reading R4)
+    // T = identity; f_eq = M^{-1} m_eq (reading R4), or the discrete f_eq (R29)
     R meq[27], feq[27];
     for (int p = 0; p < q; ++p) {
       meq[p] = raw_eq_poly(m, p, rho, u);
       if (delta) meq[p] -= raw_eq_poly(m, p, R(1), u0);
     }
     matvec(q, m.Minv.data(), meq, feq);
+    if (discrete)
+      for (int i = 0; i < q; ++i) feq[i] = fd[i];
     for (int i = 0; i < q; ++i)
       qs[i] = fabs_[i] + m.omega[0] * (feq[i] - fabs_[i]) + (R(1) - m.omega[0] / R(2)) * FG[i];
     for (int i = 0; i < q; ++i) fout[i] = (m.zc && !delta) ? qs[i] - m.w[i] : qs[i];
@@ -612,6 +637,7 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
       qeq[p] = raw_eq_poly(m, p, rho, u);
       if (delta) qeq[p] -= raw_eq_poly(m, p, R(1), u0);  // dq_eq = q_eq - q0
     }
+    if (discrete) matvec(q, m.M.data(), fd, qeq);  // q_eq = M f_eq
     for (int p = 0; p < q; ++p)
       qs[p] = q0[p] + m.omega[p] * (qeq[p] - q0[p]) + (R(1) - m.omega[p] / R(2)) * qF[p];
     matvec(q, m.Minv.data(), qs, fout);
@@ -628,6 +654,8 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
       R feq[27];
       swe_equilibrium(m, rho, u, feq);
       matvec(q, K, feq, qeq);  // q_eq = T(f_eq)
+    } else if (discrete) {
+      matvec(q, K, fd, qeq);  // kappa_eq = K(u) f_eq (or K(u)(f_eq - f0))
     } else {
       for (int p = 0; p < q; ++p) qeq[p] = central_eq_poly(m, p, rho);
       if (delta) {  // dq_eq = q_eq - T(f0) with T = K(u)
@@ -658,6 +686,13 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
   // all other cumulants of order >= 2 vanish.  Shallow water (Venturi):
   // the same Maxwellian with cs2 = g h / 2, h = the local water height.
   const R cs2 = (m.eq == EQ_SWE) ? m.g * rho / R(2) : R(CS2);
+  // discrete equilibrium (R29): its own cumulants, C_eq = T(f_eq)
+  Series<R> Cd;
+  if (discrete) {
+    R kd[27];
+    central_monomials27(m, fd, u, kd);
+    Cd = cumulants_from_central(kd, rho);
+  }
   for (int p = 0; p < q; ++p) {
     int ord = order_of(m.basis[p]);
     if (ord < 2) {
@@ -666,6 +701,10 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
     }
     R ceq = 0;
     for (auto &t : m.basis[p]) {
+      if (discrete) {
+        ceq += R(t.c) * Cd.c[sidx(t.e)];
+        continue;
+      }
       bool diag2 = (t.e[0] + t.e[1] + t.e[2] == 2) && (t.e[0] == 2 || t.e[1] == 2 || t.e[2] == 2);
       if (diag2) ceq += R(t.c) * rho * cs2;
     }
@@ -707,6 +746,12 @@ template <class R> static bool equilibrium_cell(const Method<R> &m, R rho, const
   if (m.eq == EQ_SWE && m.space != SP_CUMULANT) {
     swe_equilibrium(m, rho, u, f);
     if (m.zc) return false;
+    return true;
+  }
+  if (m.eq == EQ_DISCRETE || m.eq == EQ_DISCRETE_DELTA) {  // reading R29
+    discrete_equilibrium(m, rho, u, f);
+    if (m.zc)
+      for (int i = 0; i < q; ++i) f[i] -= m.w[i];
     return true;
   }
   if (m.space == SP_POPULATION || m.space == SP_RAW) {

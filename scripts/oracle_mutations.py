@@ -61,6 +61,10 @@ MUTANTS = [
      "cF += (R(m.xi[i][a]) + u[a]) * m.F[a];"),
     ("He force: equilibrium without the background for zero-centered storage (R27)",
      "R fa = m.zc ? feq[i] + m.w[i] : feq[i];", "R fa = feq[i];"),
+    ("discrete f_eq: 9/2 -> 3 on (xi.u)^2 (R29)", "R(3) * cu + R(9) * cu * cu / R(2) - R(3) * uu / R(2)",
+     "R(3) * cu + R(3) * cu * cu - R(3) * uu / R(2)"),
+    ("discrete f_eq: cumulant method falls back to the continuous C_eq (R29)",
+     "ceq += R(t.c) * Cd.c[sidx(t.e)];\n        continue;", "(void)Cd;"),
     ("stencil order: swap (1,1) and (-1,-1) in-plane", "{1, 1}, {-1, -1}, {1, -1}, {-1, 1}};",
      "{-1, -1}, {1, 1}, {1, -1}, {-1, 1}};"),
 ]

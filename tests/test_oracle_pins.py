@@ -788,3 +788,102 @@ def test_paper_values():
     v, tol = vals["tgv_rho_origin_u0_0.25"]
     rho, u = W.tgv_fields(8, 8, 1, 0.25)
     assert abs(rho[0, 0, 0] - v) < tol
+
+
+# ----------------------------------------------------------- discrete equilibrium (reading R29)
+DISC_REGIMES = [(W.EQ_DISCRETE, 0), (W.EQ_DISCRETE_DELTA, 1), (W.EQ_DISCRETE, 1)]
+
+
+def _abs(f, w, eq, zc):
+    return f + w if zc else f
+
+
+@pytest.mark.parametrize("st", [W.D2Q9, W.D3Q27])
+@pytest.mark.parametrize("space", [W.POPULATION, W.RAW])
+def test_discrete_equals_continuous_for_full_stencils(st, space):
+    """On D2Q9 and D3Q27 the truncated continuous Maxwellian's raw moments ARE those of the
+    textbook discrete f_eq (reading R4), so the two equilibrium forms give the same SRT and
+    raw-moment collision in every regime (q_eq = T(f_eq))."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    fa = random_cells(st, 10)
+    rates = rates_for(st, space)
+    for (deq, zc), (ceq, _) in zip(DISC_REGIMES, ALL_REGIMES):
+        fin = fa - w if zc else fa
+        d = oracle.collide(st, space, deq, zc, rates, fin)
+        c = oracle.collide(st, space, ceq, zc, rates, fin)
+        np.testing.assert_allclose(d, c, atol=2e-17)
+
+
+def test_discrete_d3q19_differs_and_is_bgk():
+    """D3Q19: the discrete f_eq differs from M^-1 m_eq of the truncated Maxwellian (by the
+    -rho u_z^2/6 terms of reading R4), and SRT with it is BGK with the textbook polynomial."""
+    st = W.D3Q19
+    xi, opp, w, M, Minv = oracle.tables(st)
+    fa = random_cells(st, 10)
+    rho = fa.sum(1)
+    u = (fa @ xi) / rho[:, None]
+    om = 1.3
+    d = oracle.collide(st, W.POPULATION, W.EQ_DISCRETE, 0, [om], fa)
+    c = oracle.collide(st, W.POPULATION, W.EQ_ABSOLUTE, 0, [om], fa)
+    np.testing.assert_allclose(d, fa + om * (textbook_feq(st, rho, u) - fa), atol=1e-16)
+    assert np.abs(d - c).max() > 1e-7
+    rates = rates_for(st, W.RAW)
+    assert np.abs(oracle.collide(st, W.RAW, W.EQ_DISCRETE, 0, rates, fa)
+                  - oracle.collide(st, W.RAW, W.EQ_ABSOLUTE, 0, rates, fa)).max() > 1e-7
+
+
+@pytest.mark.parametrize("st", STENCILS)
+def test_discrete_central_moments_at_equal_rates_is_bgk(st):
+    """T = K(u) is linear: relaxing every central moment at the same rate towards K(u) f_eq is
+    f* = f + omega (f_eq - f) with the textbook discrete f_eq, in every regime."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    fa = random_cells(st, 10)
+    rho = fa.sum(1)
+    u = (fa @ xi) / rho[:, None]
+    om = 1.37
+    ref = fa + om * (textbook_feq(st, rho, u) - fa)
+    for eq, zc in DISC_REGIMES:
+        fin = fa - w if zc else fa
+        out = oracle.collide(st, W.CENTRAL, eq, zc, np.full(len(w), om), fin)
+        np.testing.assert_allclose(_abs(out, w, eq, zc), ref, atol=2e-16)
+
+
+@pytest.mark.parametrize("st", [W.D2Q9, W.D3Q27])
+def test_discrete_cumulant_unit_rates_give_feq(st):
+    """With every rate one the cumulant collision returns the distribution whose cumulants are
+    those of f_eq: on the full stencils that is the textbook f_eq itself."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    fa = random_cells(st, 10)
+    rho = fa.sum(1)
+    u = (fa @ xi) / rho[:, None]
+    for zc in (0, 1):
+        fin = fa - w if zc else fa
+        out = oracle.collide(st, W.CUMULANT, W.EQ_DISCRETE, zc, np.ones(len(w)), fin)
+        np.testing.assert_allclose(_abs(out, w, W.EQ_DISCRETE, zc), textbook_feq(st, rho, u), atol=2e-16)
+
+
+@pytest.mark.parametrize("st", STENCILS)
+@pytest.mark.parametrize("space", [W.POPULATION, W.RAW, W.CENTRAL, W.CUMULANT])
+def test_discrete_equilibrium_fixed_point_and_conservation(st, space):
+    """f_eq is a fixed point of the collision with the discrete equilibrium (any rates), and
+    every collision conserves mass and momentum."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    rng = np.random.default_rng(4)
+    n = 8
+    rho = 1 + rng.uniform(-0.05, 0.05, n)
+    u = rng.uniform(-0.08, 0.08, (n, 3))
+    if W.DIM_OF[st] == 2:
+        u[:, 2] = 0
+    feq = textbook_feq(st, rho, u)
+    fa = random_cells(st, n)
+    regimes = [(W.EQ_DISCRETE, 0), (W.EQ_DISCRETE, 1)] + ([] if space == W.CUMULANT else
+                                                           [(W.EQ_DISCRETE_DELTA, 1)])
+    for eq, zc in regimes:
+        rates = rates_for(st, space)
+        out = oracle.collide(st, space, eq, zc, rates, feq - w if zc else feq)
+        np.testing.assert_allclose(_abs(out, w, eq, zc), feq, atol=3e-16)
+        got = oracle.equilibrium(st, space, eq, zc, rho, u)
+        np.testing.assert_allclose(_abs(got, w, eq, zc), feq, atol=3e-16)
+        out = _abs(oracle.collide(st, space, eq, zc, rates, fa - w if zc else fa), w, eq, zc)
+        np.testing.assert_allclose(out.sum(1), fa.sum(1), atol=2e-15)
+        np.testing.assert_allclose(out @ xi, fa @ xi, atol=2e-16)

@@ -28,7 +28,7 @@ DIM_OF = {D2Q9: 2, D3Q19: 3, D3Q27: 3}
 
 POPULATION, RAW, CENTRAL, CUMULANT = 0, 1, 2, 3
 SPACES = {"POPULATION": POPULATION, "RAW": RAW, "CENTRAL": CENTRAL, "CUMULANT": CUMULANT}
-EQ_ABSOLUTE, EQ_DELTA, EQ_SWE = 0, 1, 2
+EQ_ABSOLUTE, EQ_DELTA, EQ_SWE, EQ_DISCRETE, EQ_DISCRETE_DELTA = 0, 1, 2, 3, 4
 PERIODIC, NOSLIP = 0, 1
 
 SEED = 221102435
