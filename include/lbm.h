@@ -80,10 +80,16 @@ typedef enum {
   LBM_EQ_ABSOLUTE = 0, /* continuous Maxwellian, absolute form                    */
   LBM_EQ_DELTA = 1,    /* deviation-only delta equilibrium: zero-centered only,
                           not with cumulants                                       */
-  LBM_EQ_SWE = 2       /* shallow water, D2Q9 + absolute storage only; the density slot is the height h:
+  LBM_EQ_SWE = 2,      /* shallow water, D2Q9 + absolute storage only; the density slot is the height h:
                           with CENTRAL: Zhou's discrete equilibrium (de Rosis; PAPER.md:998-1021,
                           reading R5); with CUMULANT: the Maxwellian with cs2 = g h / 2 (Venturi;
                           PAPER.md:1023-1026)                                                          */
+  LBM_EQ_DISCRETE = 3, /* the equilibrium given as a discrete distribution (
+                          reading R29): f_eq_i = w_i rho [1 + 3 xi.u + 9/2 (xi.u)^2 - 3/2 u.u], used
+                          in collision space as q_eq = T(f_eq); absolute form.  Equals LBM_EQ_ABSOLUTE
+                          for population / raw moments on D2Q9 and D3Q27 (reading R4).  General rates
+                          only (no rate specialisation), no body force.                              */
+  LBM_EQ_DISCRETE_DELTA = 4 /* its deviation f_eq - f0: zero-centered only, not with cumulants       */
 } lbm_equilibrium;
 typedef enum { LBM_FP64 = 0, LBM_FP32 = 1 } lbm_precision;
 /* Streaming patterns: two-grid pull; in place: AA (Bailey 2009; several

@@ -684,6 +684,7 @@ __device__ __forceinline__ void add_background(real (&c)[NC], real sgn) {
 // gains exactly F (kappa_100: -F/2 before, +F/2 after).
 // --------------------------------------------------------------------------
 enum { RS_FORCE = 4, RS_FORCE_HE = 8 };  // flag bits of the RS template parameter (Guo / He)
+enum { RS_DISCRETE = 16 };               // equilibrium given as a discrete f_eq (reading R29)
 
 template <class real>
 struct Force {
@@ -707,6 +708,24 @@ __device__ __forceinline__ real signed_add(real acc, real a) {
   else if constexpr (v < 0) return acc - a;
   else return acc;
 }
+
+// Discrete second-order equilibrium f_eq_i = w_i rho [1 + X_i], X_i = 3 xi.u + 9/2 (xi.u)^2 -
+// 3/2 u.u (reading R29) in the cube layout, in absolute form or as the
+// deviation f_eq - w = w (drho + rho X) written without the cancellation.
+template <class S, class real, int NC>
+__device__ __forceinline__ void discrete_feq_cube(real (&fe)[NC], real rho, real ux, real uy, real uz,
+                                                  bool deviation) {
+  const real uu = fma(uz, uz, fma(uy, uy, ux * ux));
+  const real drho = rho - real(1);
+  sfor<NC>([&](auto k) { fe[k] = real(0); });
+  sfor<S::Q>([&](auto i) {
+    constexpr int vx = S::vx(i), vy = S::vy(i), vz = S::vz(i);
+    const real cu = signed_add<vz>(signed_add<vy>(signed_add<vx>(real(0), ux), uy), uz);
+    const real X = fma(real(4.5) * cu, cu, fma(real(3), cu, real(-1.5) * uu));
+    const real wi = real(weight<S>(i));
+    fe[S::pos(i)] = deviation ? wi * fma(rho, X, drho) : wi * fma(rho, X, rho);
+  });
+}
 template <class S, class real, int NC>
 __device__ __forceinline__ void guo_cube(real (&s)[NC], const Force<real> &fr, real ux, real uy, real uz) {
   const real uF = fma(uz, fr.F[2], fma(uy, fr.F[1], ux * fr.F[0]));
@@ -719,7 +738,7 @@ __device__ __forceinline__ void guo_cube(real (&s)[NC], const Force<real> &fr, r
   });
 }
 
-template <class S, int SPACE, int REG, class real>
+template <class S, int SPACE, int REG, class real, bool DISC = false>
 __device__ __forceinline__ void equilibrium(real (&f)[S::Q], real rho, real ux, real uy, real uz, real swe_g);
 
 // He's force term F^He_i = f_eq_i(rho, u) (xi_i - u).F / (rho c_s^2) (He, Shan, Doolen 1998,
@@ -754,6 +773,14 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
   constexpr bool zc = (REG != REG_ABS);
   constexpr int NC = S::NC;
   constexpr bool FORCED = (RS & (RS_FORCE | RS_FORCE_HE)) != 0;
+  constexpr bool DISC = (RS & RS_DISCRETE) != 0;  // q_eq = T(f_eq) of the discrete f_eq (R29)
+  static_assert(!DISC || (SPACE != SPACE_SWE && SPACE != SPACE_SWE_K && !FORCED),
+                "discrete hydrodynamic equilibrium: unforced, not for shallow water");
+  // the discrete f_eq in the regime's form: deviation for zc + delta, absolute otherwise
+  // (moment-space kernels add the background to q for zc + absolute equilibrium)
+  auto disc_cube = [&](real(&fe)[NC], real rho_, real ux_, real uy_, real uz_) {
+    discrete_feq_cube<S>(fe, rho_, ux_, uy_, uz_, REG == REG_DELTA);
+  };
   static_assert(!(RS & RS_FORCE_HE) || SPACE == SPACE_POPULATION || SPACE == SPACE_RAW || SPACE == SPACE_CENTRAL,
                 "He forcing: population, raw- and central-moment collisions (cumulants: R26 = Guo)");
   static_assert(!FORCED || SPACE == SPACE_POPULATION || SPACE == SPACE_RAW || SPACE == SPACE_CENTRAL ||
@@ -786,25 +813,29 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
     }
     RawU<real> U{ux, uy, uz, ux * ux, uy * uy, uz * uz};
     real g[NC];
-    if constexpr (REG == REG_DELTA) {
-      EqRawDelta<real> eq{m000, rho, U};
-      sfor<NC>([&](auto e) {
-        if constexpr (EqRawDelta<real>::template zero<e>()) g[e] = real(0);
-        else g[e] = eq.template get<e>();
-      });
-      g[0] = m000;
+    if constexpr (DISC) {  // the discrete f_eq directly, stored form (f_eq - f0 when zero-centered)
+      discrete_feq_cube<S>(g, rho, ux, uy, uz, zc);
     } else {
-      EqRawAbs<real> eq{rho, U};
-      sfor<NC>([&](auto e) {
-        if constexpr (EqRawAbs<real>::template zero<e>()) g[e] = real(0);
-        else g[e] = eq.template get<e>();
-      });
-      g[0] = rho;
-      if constexpr (REG == REG_ZC_ABS) add_background<NC>(g, real(-1)), g[0] = m000;  // f_eq - f0
+      if constexpr (REG == REG_DELTA) {
+        EqRawDelta<real> eq{m000, rho, U};
+        sfor<NC>([&](auto e) {
+          if constexpr (EqRawDelta<real>::template zero<e>()) g[e] = real(0);
+          else g[e] = eq.template get<e>();
+        });
+        g[0] = m000;
+      } else {
+        EqRawAbs<real> eq{rho, U};
+        sfor<NC>([&](auto e) {
+          if constexpr (EqRawAbs<real>::template zero<e>()) g[e] = real(0);
+          else g[e] = eq.template get<e>();
+        });
+        g[0] = rho;
+        if constexpr (REG == REG_ZC_ABS) add_background<NC>(g, real(-1)), g[0] = m000;  // f_eq - f0
+      }
+      if constexpr (S::Q == 27) bwd_raw3_full(g);
+      else if constexpr (S::Q == 19) bwd_raw3_d3q19(g);
+      else bwd_raw2(g);
     }
-    if constexpr (S::Q == 27) bwd_raw3_full(g);
-    else if constexpr (S::Q == 19) bwd_raw3_d3q19(g);
-    else bwd_raw2(g);
     const real w = r.w[0];
     if constexpr (REG == REG_ZC_ABS) {
       // absolute populations f = df + f0 relaxed against the absolute f_eq
@@ -857,7 +888,12 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
       sfor<NC>([&](auto e) { c[e] += s[e]; });
     };
 
-    if constexpr (SPACE == SPACE_RAW) {
+    if constexpr (SPACE == SPACE_RAW && DISC) {
+      EqTable<real, NC> eq;  // m_eq = M f_eq
+      disc_cube(eq.v, rho, ux, uy, uz);
+      if constexpr (S::D == 3) fwd_raw3<S>(eq.v); else fwd_raw2(eq.v);
+      if constexpr (S::D == 3) relax_basis3<S, RSR>(c, eq, r); else relax_basis2<RSR>(c, eq, r);
+    } else if constexpr (SPACE == SPACE_RAW) {
       RawU<real> U{ux, uy, uz, ux * ux, uy * uy, uz * uz};
       if constexpr (REG == REG_DELTA) {
         EqRawDelta<real> eq{m000, rho, U};
@@ -878,7 +914,13 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
         c[E(0, 1, 0)] = SHIFT_U ? real(-0.5) * fr.F[1] : real(0);
         if constexpr (S::D == 3) c[E(0, 0, 1)] = SHIFT_U ? real(-0.5) * fr.F[2] : real(0);
       }
-      if constexpr (SPACE == SPACE_CENTRAL) {
+      if constexpr (SPACE == SPACE_CENTRAL && DISC) {
+        EqTable<real, NC> eq;  // kappa_eq = K(u) f_eq
+        disc_cube(eq.v, rho, ux, uy, uz);
+        if constexpr (S::D == 3) fwd_raw3<S>(eq.v); else fwd_raw2(eq.v);
+        if constexpr (S::D == 3) bin_fwd3(eq.v, ux, uy, uz); else bin_fwd2(eq.v, ux, uy);
+        if constexpr (S::D == 3) relax_basis3<S, RSR>(c, eq, r); else relax_basis2<RSR>(c, eq, r);
+      } else if constexpr (SPACE == SPACE_CENTRAL) {
         if constexpr (REG == REG_DELTA) {
           EqCentralDelta<real> eq{m000, CentralV<real>{ux, uy, uz, ux * ux, uy * uy, uz * uz}};
           if constexpr (S::D == 3) relax_basis3<S, RSR>(c, eq, r); else relax_basis2<RSR>(c, eq, r);
@@ -912,10 +954,23 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
       } else {  // SPACE_CUMULANT
         if constexpr (S::D == 3) central_to_cumulant3<S>(c, inv); else central_to_cumulant2(c, inv);
         // C_eq = rho cs2 on the diagonal: cs2 = 1/3, or g h / 2 for shallow water (h = rho)
-        real cs2 = real(1.0 / 3.0);
-        if constexpr (SPACE == SPACE_SWE_K) cs2 = real(0.5) * swe_g * rho;
-        EqCumulant<real> eq{rho * cs2};
-        if constexpr (S::D == 3) relax_basis3<S, RSR>(c, eq, r); else relax_basis2<RSR>(c, eq, r);
+        if constexpr (DISC) {  // C_eq: the cumulants of the discrete f_eq
+          EqTable<real, NC> eq;
+          disc_cube(eq.v, rho, ux, uy, uz);
+          if constexpr (S::D == 3) fwd_raw3<S>(eq.v); else fwd_raw2(eq.v);
+          if constexpr (S::D == 3) bin_fwd3(eq.v, ux, uy, uz); else bin_fwd2(eq.v, ux, uy);
+          eq.v[0] = rho;  // sum f_eq = rho, first-order central moments vanish
+          eq.v[E(1, 0, 0)] = real(0);
+          eq.v[E(0, 1, 0)] = real(0);
+          if constexpr (S::D == 3) eq.v[E(0, 0, 1)] = real(0);
+          if constexpr (S::D == 3) central_to_cumulant3<S>(eq.v, inv); else central_to_cumulant2(eq.v, inv);
+          if constexpr (S::D == 3) relax_basis3<S, RSR>(c, eq, r); else relax_basis2<RSR>(c, eq, r);
+        } else {
+          real cs2 = real(1.0 / 3.0);
+          if constexpr (SPACE == SPACE_SWE_K) cs2 = real(0.5) * swe_g * rho;
+          EqCumulant<real> eq{rho * cs2};
+          if constexpr (S::D == 3) relax_basis3<S, RSR>(c, eq, r); else relax_basis2<RSR>(c, eq, r);
+        }
         if constexpr (S::D == 3) cumulant_to_central3<S>(c, inv); else cumulant_to_central2(c, inv);
         if constexpr (FORCED) {  // C*_100 = C_100 + F_x: the post-collision mean is (j + F)/rho
           ux = fma(fr.F[0], inv, ux);
@@ -944,10 +999,16 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
 // Equilibrium populations of the method at (rho, u) in stored form: f_eq = T^{-1}(q_eq).
 // RAW / POPULATION: M^{-1} m_eq (truncated Maxwellian); CENTRAL / CUMULANT: the Gaussian
 // central moments, i.e. raw moments rho prod_a (1, u_a, cs2 + u_a^2); SWE: Zhou f_eq.
-template <class S, int SPACE, int REG, class real>
+template <class S, int SPACE, int REG, class real, bool DISC>
 __device__ __forceinline__ void equilibrium(real (&f)[S::Q], real rho, real ux, real uy, real uz, real swe_g) {
   constexpr int NC = S::NC;
   constexpr bool zc = (REG != REG_ABS);
+  if constexpr (DISC && SPACE != SPACE_SWE && SPACE != SPACE_SWE_K) {  // reading R29
+    real fe[NC];
+    discrete_feq_cube<S>(fe, rho, ux, uy, uz, zc);
+    sfor<S::Q>([&](auto i) { f[i] = fe[S::pos(i)]; });
+    return;
+  }
   if constexpr (SPACE == SPACE_SWE) {
     const real uu = ux * ux + uy * uy, gh = swe_g * rho;
     sfor<9>([&](auto i) {

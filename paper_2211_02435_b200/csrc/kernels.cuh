@@ -362,7 +362,7 @@ struct Canon {
 };
 
 // host staging layouts: f[i][z][y][x] (fp64), rho[z][y][x], u[d][z][y][x]
-template <class S, int SPACE, int REG, class real>
+template <class S, int SPACE, int REG, class real, bool DISC = false>
 __global__ void k_init(real *mem, const GridParams g, int aa, const double *__restrict__ rho,
                        const double *__restrict__ u, real swe_g) {
   const int x = blockIdx.x * BLOCK_X + threadIdx.x;
@@ -381,7 +381,7 @@ __global__ void k_init(real *mem, const GridParams g, int aa, const double *__re
     uz = real(0);
   }
   real f[S::Q];
-  equilibrium<S, SPACE, REG, real>(f, r, ux, uy, uz, swe_g);
+  equilibrium<S, SPACE, REG, real, DISC>(f, r, ux, uy, uz, swe_g);
   // post-collision state at t = 0 written in state A (AA) or the current grid (pull)
   sfor<S::Q>([&](auto i) { mem[Canon<S>::template at<i>(g, x, y, zl, aa, 0)] = f[i]; });
 }

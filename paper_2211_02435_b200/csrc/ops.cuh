@@ -148,7 +148,7 @@ struct OpsImpl {
   }
   static void init(void *mem, const GridParams &g, int aa, const double *rho, const double *u, double swe_g,
                    cudaStream_t s) {
-    k_init<S, SPACE, REG, real><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<real *>(mem), g, aa, rho, u,
+    k_init<S, SPACE, REG, real, (RS & RS_DISCRETE) != 0><<<cell_grid(g, g.nzl), BLOCK_X, 0, s>>>(static_cast<real *>(mem), g, aa, rho, u,
                                                                         (real)swe_g);
   }
   static void get_pop(const void *mem, const GridParams &g, int aa, int state, double *out, cudaStream_t s) {

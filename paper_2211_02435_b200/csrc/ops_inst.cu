@@ -33,7 +33,11 @@ const Ops *with_rs(int rs) {
   if constexpr (SP_ == SPACE_POPULATION || SP_ == SPACE_RAW || SP_ == SPACE_CENTRAL) {
     if (rs == (RS_GENERAL | RS_FORCE_HE)) return &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL | RS_FORCE_HE>::table;
   }
-  if (rs & (RS_FORCE | RS_FORCE_HE)) return nullptr;
+  // discrete equilibrium q_eq = T(f_eq) (reading R29): general rates, unforced
+  if constexpr (SP_ == SPACE_POPULATION || SP_ == SPACE_RAW || SP_ == SPACE_CENTRAL || SP_ == SPACE_CUMULANT) {
+    if (rs == (RS_GENERAL | RS_DISCRETE)) return &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL | RS_DISCRETE>::table;
+  }
+  if (rs & (RS_FORCE | RS_FORCE_HE | RS_DISCRETE)) return nullptr;
   if constexpr (SP_ == SPACE_POPULATION) {
     return rs == RS_GENERAL ? &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL>::table : nullptr;
   } else {

@@ -569,13 +569,15 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   if (stencil < LBM_D2Q9 || stencil > LBM_D3Q27) return fail(nullptr, LBM_EINVAL, "unknown stencil");
   if (collision_space < LBM_SPACE_POPULATION || collision_space > LBM_SPACE_CUMULANT)
     return fail(nullptr, LBM_EINVAL, "unknown collision space");
-  if (equilibrium < LBM_EQ_ABSOLUTE || equilibrium > LBM_EQ_SWE)
+  if (equilibrium < LBM_EQ_ABSOLUTE || equilibrium > LBM_EQ_DISCRETE_DELTA)
     return fail(nullptr, LBM_EINVAL, "unknown equilibrium");
   const int zc = zero_centered ? 1 : 0;
+  const bool delta_eq = equilibrium == LBM_EQ_DELTA || equilibrium == LBM_EQ_DISCRETE_DELTA;
+  const bool discrete_eq = equilibrium == LBM_EQ_DISCRETE || equilibrium == LBM_EQ_DISCRETE_DELTA;
   // admissibility
-  if (equilibrium == LBM_EQ_DELTA && !zc)
+  if (delta_eq && !zc)
     return fail(nullptr, LBM_EUNSUPPORTED, "delta equilibrium requires zero-centered storage (PAPER.md:546)");
-  if (equilibrium == LBM_EQ_DELTA && collision_space == LBM_SPACE_CUMULANT)
+  if (delta_eq && collision_space == LBM_SPACE_CUMULANT)
     return fail(nullptr, LBM_EUNSUPPORTED,
                 "cumulant space is incompatible with the delta equilibrium (PAPER.md:430-431, 547)");
   if (equilibrium == LBM_EQ_SWE &&
@@ -620,7 +622,7 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
                 "Esoteric Pull / Twist are provided for a single rank with periodic faces");
 
   int regime = lbm::REG_ABS;
-  if (zc) regime = (equilibrium == LBM_EQ_DELTA) ? lbm::REG_DELTA : lbm::REG_ZC_ABS;
+  if (zc) regime = delta_eq ? lbm::REG_DELTA : lbm::REG_ZC_ABS;
   int kspace = (int)collision_space;
   if (equilibrium == LBM_EQ_SWE)
     kspace = (collision_space == LBM_SPACE_CUMULANT) ? (int)lbm::SPACE_SWE_K : (int)lbm::SPACE_SWE;
@@ -636,6 +638,7 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
       for (int i = 23; i < 27; ++i) high &= (relaxation_rates[i] == 1.0);
     if (allow) rs = reg ? lbm::RS_REG : (high ? lbm::RS_HIGH : lbm::RS_GENERAL);
   }
+  if (discrete_eq) rs = lbm::RS_GENERAL | lbm::RS_DISCRETE;  // q_eq = T(f_eq), general rates
   const Ops *ops = find_ops(stencil, D.precision, kspace, regime, rs);
   if (!ops) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
 
@@ -763,7 +766,7 @@ lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
   info->bytes_per_element = c->esize;
   info->device_bytes = c->grid_elems * c->esize * (c->streaming == LBM_PULL ? 2 : 1);
   info->steps_done = c->steps;
-  info->rate_specialization = c->rs;
+  info->rate_specialization = c->rs & 3;
   info->temporal_blocking = use_temporal_blocking(c) ? 2 : 1;
   info->resident_cluster = resident_cluster(c);
   info->cuda_graph_steps = (c->nranks == 1 && !info->resident_cluster && use_graphs(c)) ? kGraphSteps : 0;
@@ -1166,6 +1169,8 @@ lbm_status lbm_set_force(lbm_ctx *c, const double *force) {
   if (c->d == 2 && force[2] != 0.0) return fail(c, LBM_EINVAL, "a D2Q9 force has no z component");
   const bool any = force[0] != 0.0 || force[1] != 0.0 || force[2] != 0.0;
   if (any) {
+    if (c->rs & lbm::RS_DISCRETE)
+      return fail(c, LBM_EUNSUPPORTED, "no body force with the discrete equilibrium (reading R29)");
     if (!(c->kspace == LBM_SPACE_POPULATION || c->kspace == LBM_SPACE_RAW || c->kspace == LBM_SPACE_CENTRAL ||
           c->kspace == LBM_SPACE_CUMULANT))
       return fail(c, LBM_EUNSUPPORTED,

@@ -48,8 +48,8 @@ MUTANTS = [
     ("bounce-back: same slot instead of the opposite", "f[i] = src[(long long)s.m.opp[i] * N + c];",
      "f[i] = src[(long long)i * N + c];"),
     ("SWE: printed -u.u/3 (the garble of Eq. 5.3)", "+ xu * xu / R(2) - uu / R(6));", "+ xu * xu / R(2) - uu / R(3));"),
-    ("SWE cumulant: cs2 = g h", "const R cs2 = (m.eq == EQ_SWE) ? m.g * rho / R(2) : R(CS2);\n  for",
-     "const R cs2 = (m.eq == EQ_SWE) ? m.g * rho : R(CS2);\n  for"),
+    ("SWE cumulant: cs2 = g h", "const R cs2 = (m.eq == EQ_SWE) ? m.g * rho / R(2) : R(CS2);\n  // discrete",
+     "const R cs2 = (m.eq == EQ_SWE) ? m.g * rho : R(CS2);\n  // discrete"),
     ("velocity: u = j (no division by rho)", "u[a] = (j[a] + R(half) * m.F[a] / R(2)) / rho;",
      "u[a] = (j[a] + R(half) * m.F[a] / R(2));"),
     ("cumulant force: F/2 instead of F on the first-order cumulants (R26)",

@@ -106,6 +106,14 @@ def test_admissibility_errors():
     assert st == L.LBM_EUNSUPPORTED
     st, _ = create_status(streaming=4)
     assert st == L.LBM_EINVAL
+    # discrete equilibrium (reading R29): its delta form needs zero-centered storage and is
+    # incompatible with cumulants, like the continuous one
+    st, _ = create_status(eq=L.LBM_EQ_DISCRETE_DELTA, zc=0, space=L.LBM_SPACE_RAW)
+    assert st == L.LBM_EUNSUPPORTED
+    st, _ = create_status(eq=L.LBM_EQ_DISCRETE_DELTA, zc=1, space=L.LBM_SPACE_CUMULANT)
+    assert st == L.LBM_EUNSUPPORTED
+    st, _ = create_status(eq=5)
+    assert st == L.LBM_EINVAL
     st, _ = create_status(streaming=L.LBM_AA, bc=[[1, 1], [0, 0], [0, 0]], nranks=2, rank=0)
     assert st == L.LBM_EUNSUPPORTED
     st, _ = create_status(streaming=L.LBM_AA, bc=[[1, 1], [0, 0], [0, 0]])
