@@ -57,6 +57,12 @@ CONFIGS = {
     "c3twist": dict(stencil=W.D3Q27, space=W.CENTRAL, eq=W.EQ_ABSOLUTE, zc=1, prec=0, streaming=3,
                     shape=lambda n: (384, 384, 384), slab=2, scaling="strong",
                     desc="D3Q27 central-moment MRT TGV 384^3, fp64, zero-centered + absolute eq, Esoteric Twist"),
+    "c4disc": dict(stencil=W.D3Q27, space=W.CUMULANT, eq=W.EQ_DISCRETE, zc=1, prec=0, streaming=0,
+                   shape=lambda n: (1024, 1024, 128 * n), slab=2, scaling="weak",
+                   desc="D3Q27 cumulant TGV 1024x1024x(128*N), fp64, zero-centered, DISCRETE f_eq (R29), pull"),
+    "c3disc": dict(stencil=W.D3Q27, space=W.CENTRAL, eq=W.EQ_DISCRETE, zc=1, prec=0, streaming=1,
+                   shape=lambda n: (384, 384, 384), slab=2, scaling="strong",
+                   desc="D3Q27 central-moment MRT TGV 384^3, fp64, zero-centered, DISCRETE f_eq (R29), AA"),
     "c2_f64": dict(stencil=W.D3Q19, space=W.RAW, eq=W.EQ_DELTA, zc=1, prec=0, streaming=0,
                    shape=lambda n: (256, 256, 256), slab=2, scaling="strong",
                    desc="D3Q19 raw-moment MRT TGV 256^3, fp64, zero-centered + delta eq, pull"),
