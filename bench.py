@@ -422,10 +422,16 @@ def main():
     # per TWO steps when the library fuses pairs of steps: temporal blocking, D3Q19)
     peak, peak_src = measured_peaks()
     bpc = bytes_per_cell(cfg)  # every population read once and written once per launch
-    tb = lat.info().temporal_blocking if n == 1 else 1
+    tb = lat.info().temporal_blocking if (n == 1 or isinstance(runner, D.PeerRunner)) else 1
     resident = lat.info().resident_cluster if n == 1 else 0
-    # N > 1: interior + 2 boundary launches (+ wait and signal kernels of the fused push)
-    launches_per_step = (1.0 / tb) if n == 1 else (5 if isinstance(runner, D.PeerRunner) else 3)
+    # N > 1: interior + 2 boundary launches (+ wait and signal kernels of the fused push); with
+    # two-step sweeps across ranks per PAIR: interior sweep + 2 waits + 4 boundary + 2 signals
+    if n == 1:
+        launches_per_step = 1.0 / tb
+    elif isinstance(runner, D.PeerRunner):
+        launches_per_step = 4.5 if tb == 2 else 5
+    else:
+        launches_per_step = 3
     if resident:  # one cluster launch runs all K steps of lbm_step(K)
         launches_per_step = 1.0 / args.steps
     kernel_ms = ms_step * tb  # one launch covers tb steps on this stream

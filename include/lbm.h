@@ -245,7 +245,12 @@ lbm_status lbm_peer_connect(lbm_ctx *ctx, const lbm_peer_info *lower, const lbm_
 lbm_status lbm_peer_prime(lbm_ctx *ctx);
 /* n time steps with the fused halo push (asynchronous on the context stream).  The phase
    counters live on the device, so the loop is a fixed launch sequence: n >= 32 replays
-   captured 32-step CUDA graphs (one per grid parity; LBM_CUDA_GRAPHS=0 disables).  Several
+   captured 32-step CUDA graphs (one per grid parity; LBM_CUDA_GRAPHS=0 disables).  PULL
+   methods with two-step sweeps (lbm_info.temporal_blocking == 2 on a connected context: >= 6
+   planes per slab, no walls) advance pairs of steps: interior planes by the fused sweep, the
+   boundary regions by two single steps through 8 scratch planes behind grid 0 with pushes into
+   the neighbours' scratch and ghost planes; every rank must call with the same n.
+   LBM_PEER_TB=0 (read at create) keeps single steps.  Several
    contexts driven from ONE host thread must be stepped in small interleaved chunks: a
    context's stream waits on the GPU for its neighbours, and enqueuing many of its steps
    first can fill the launch queue before the neighbours' work is enqueued (one process per

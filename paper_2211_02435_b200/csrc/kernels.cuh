@@ -30,6 +30,7 @@ struct GridParams {
   int pitch;
   int nx, ny, nzl, nzg, z0;  // local view: x, y, slab axis (nzl local planes from global z0)
   int zbegin;                // first local plane of this launch
+  int zcount = 0;            // two-step sweeps: output planes [zbegin, zbegin + zcount) (0: all)
   int wrapz;                 // single rank: periodic wrap along the slab axis by index
   int bcmask;                // bit (2 * axis + side): no-slip face (axis 0 x, 1 y, 2 slab)
   // fused halo push (lbm_step_peer): ghost plane of the lower / upper neighbour's next grid
@@ -545,13 +546,18 @@ __global__ void __launch_bounds__(Tile2<TX, TY>::THREADS, MINB)
   const int n = g.nzl;
   // blockIdx.z: chunk [p0, p1) of the output planes (more CTAs for short slabs); each chunk
   // recomputes the two step-(t+1) planes at its ends
-  const int p0 = (int)((long long)n * blockIdx.z / gridDim.z), p1 = (int)((long long)n * (blockIdx.z + 1) / gridDim.z);
+  // output planes [zb, zb + zn): the whole slab (single rank, periodic wrap) or, across ranks,
+  // the planes whose two-step dependence stays inside the slab (no wrap: ghost planes are real)
+  const int zb = g.zcount ? g.zbegin : 0, zn = g.zcount ? g.zcount : n;
+  const int p0 = zb + (int)((long long)zn * blockIdx.z / gridDim.z);
+  const int p1 = zb + (int)((long long)zn * (blockIdx.z + 1) / gridDim.z);
+  auto zw = [&](int k) { return g.wrapz ? wrapi(k, n) : k; };
   // step-t populations of the halo-extended tile at plane k (pull: plane k - xi_z)
   auto load = [&](int k, real (&f)[S::Q]) {
-    const int zc = wrapi(k, n);
+    const int zc = zw(k);
     long long zo[3];
 #pragma unroll
-    for (int s = -1; s <= 1; ++s) zo[s + 1] = (long long)(wrapi(zc + s, n) + 1) * g.plane;
+    for (int s = -1; s <= 1; ++s) zo[s + 1] = (long long)(zw(zc + s) + 1) * g.plane;
     sfor<S::Q>([&](auto i) {
       constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
       f[i] = ld_nc(src + zo[1 - cz] + (long long)i * g.pop + ys[1 - cy] + xs[1 - cx]);
@@ -699,13 +705,15 @@ __global__ void __launch_bounds__(Tile1<TX>::THREADS, MINB)
   const int gx = wrapi(x0 - 1 + t, g.nx);
   const int xs[3] = {wrapi(gx - 1, g.nx), gx, wrapi(gx + 1, g.nx)};
   const int n = g.nzl;
-  const int p0 = (int)((long long)n * blockIdx.y / gridDim.y);
-  const int p1 = (int)((long long)n * (blockIdx.y + 1) / gridDim.y);
+  const int zb = g.zcount ? g.zbegin : 0, zn = g.zcount ? g.zcount : n;  // as in k_pull2
+  const int p0 = zb + (int)((long long)zn * blockIdx.y / gridDim.y);
+  const int p1 = zb + (int)((long long)zn * (blockIdx.y + 1) / gridDim.y);
+  auto zw = [&](int k) { return g.wrapz ? wrapi(k, n) : k; };
   // step-t populations of the halo-extended strip at row k (pull: row k - xi_y)
   auto load = [&](int k, real (&f)[S::Q]) {
-    const int zc = wrapi(k, n);
-    const long long zo[3] = {(long long)(wrapi(zc - 1, n) + 1) * g.plane, (long long)(zc + 1) * g.plane,
-                             (long long)(wrapi(zc + 1, n) + 1) * g.plane};
+    const int zc = zw(k);
+    const long long zo[3] = {(long long)(zw(zc - 1) + 1) * g.plane, (long long)(zc + 1) * g.plane,
+                             (long long)(zw(zc + 1) + 1) * g.plane};
     sfor<S::Q>([&](auto i) {
       constexpr int cx = S::mx(i), cz = S::mz(i);
       f[i] = ld_nc(src + zo[1 - cz] + (long long)i * g.pop + xs[1 - cx]);

@@ -113,6 +113,11 @@ struct lbm_ctx {
   bool forced = false;
   int force_model = LBM_FORCE_GUO;
   bool resident_failed = false;  // the cluster-resident launch was refused once: do not retry
+  // two-step sweeps across ranks (peer path): 8 scratch planes behind the planes of each grid
+  // (grid 0's are used: the neighbours map grid 0 anyway), element offset scratch_off
+  bool peer_tb_cap = false;
+  size_t scratch_off = 0;
+  void *peer_scr[2] = {};  // the lower / upper neighbour's scratch (plane 0)
   int last_cluster = 0;
   const Ops *ops_plain = nullptr;  // the unforced kernels chosen at create
   bool tb_allowed = false;         // temporal blocking (two fused steps) eligible
@@ -243,6 +248,16 @@ int tb_zchunks(const lbm_ctx *c) {
   const long long tiles = tb_tiles(c);
   const long long need = (kTbMinCtas + tiles - 1) / tiles;
   const int maxch = n / kTbMinChunkPlanes > 1 ? n / kTbMinChunkPlanes : 1;
+  return (int)(need < maxch ? need : maxch);
+}
+
+// two fused steps per call pair on the peer path (multi-rank): interior planes [2, nzl - 2)
+// by the two-step sweep, the two boundary regions by two single steps through the scratch
+bool use_peer_tb(const lbm_ctx *c) { return c->peer_tb_cap && c->peer_on && c->streaming == LBM_PULL; }
+int peer_tb_chunks(const lbm_ctx *c) {
+  const long long tiles = tb_tiles(c);
+  const long long need = (kTbMinCtas + tiles - 1) / tiles;
+  const int maxch = (c->g.nzl - 4) / kTbMinChunkPlanes > 1 ? (c->g.nzl - 4) / kTbMinChunkPlanes : 1;
   return (int)(need < maxch ? need : maxch);
 }
 
@@ -411,13 +426,62 @@ void peer_release(lbm_ctx *c) {
 // (k_pull<PEER>: local stores + halo stores into the neighbours' next grid), signal.
 int pull_parity(const lbm_ctx *c) { return c->streaming == LBM_PULL ? c->cur : c->aa_state; }
 
-void enqueue_peer_steps(lbm_ctx *c, int n, int cur) {
+int enqueue_peer_steps(lbm_ctx *c, int n, int cur) {
   const unsigned long long tmo = peer_timeout_ns();
   const int nzl = c->g.nzl;
   const bool pull = c->streaming == LBM_PULL;
   cudaEventRecord(c->ev_b, c->stream);
   cudaEventRecord(c->ev_i, c->stream);
-  for (int t = 0; t < n; ++t) {
+  int t = 0;
+  if (use_peer_tb(c)) {
+    // Pairs of steps t -> t+2 (A = current grid, B = next): on s_int the two-step sweep of
+    // the interior planes [2, nzl - 2) (its step-(t+1) halo planes 1 and nzl - 2 are recomputed
+    // from A's own planes: no ghost data, no neighbour dependence); on the context stream:
+    // wait, step t+1 of the boundary regions {0,1,2} and {nzl-3,..,nzl-1} from A into the
+    // scratch (planes -1..2 and nzl-3..nzl of scratch planes 0..3 / 4..7; planes 0 and nzl-1
+    // push their slab-crossing populations into the neighbours' scratch ghost planes), signal,
+    // wait, step t+2 of planes {0,1} and {nzl-2,nzl-1} from the scratch into B (pushing into
+    // the neighbours' ghost planes of B), signal.  Two phases per pair, as two single steps.
+    const size_t PB = (size_t)c->g.plane * c->esize;
+    char *scr = static_cast<char *>(c->buf[0]) + c->scratch_off * c->esize;
+    void *s_lo = scr;                                          // plane z at scr + (z + 1) P
+    void *s_hi = scr - (long long)(nzl - 6) * (long long)PB;   // plane nzl-3 at scratch plane 4
+    void *nb_lo7 = static_cast<char *>(c->peer_scr[0]) + 7 * PB;  // lower's scratch plane 7
+    void *nb_hi0 = c->peer_scr[1];                                // upper's scratch plane 0
+    for (; t + 2 <= n; t += 2) {
+      void *A = c->buf[cur], *B = c->buf[1 - cur];
+      cudaStreamWaitEvent(c->stream, c->ev_i, 0);
+      cudaStreamWaitEvent(c->s_int, c->ev_b, 0);
+      GridParams gi = c->g;
+      gi.zbegin = 2;
+      gi.zcount = nzl - 4;
+      c->ops->pull2(A, B, gi, c->params, c->swe_g, peer_tb_chunks(c), c->s_int);
+      cudaEventRecord(c->ev_i, c->s_int);
+      k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, tmo);
+      GridParams g1 = c->g;
+      g1.peer_lo = nb_lo7;
+      g1.peer_hi = nb_hi0;
+      g1.peer_fence = peer_fence();
+      g1.zbegin = 0;
+      c->ops->pull(A, s_lo, g1, c->params, c->swe_g, c->bb, 3, c->stream);
+      g1.zbegin = nzl - 3;
+      c->ops->pull(A, s_hi, g1, c->params, c->swe_g, c->bb, 3, c->stream);
+      k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_remote[0], c->peer_remote[1]);
+      k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, tmo);
+      GridParams g2 = c->g;
+      g2.peer_lo = c->peer_ghost[1 - cur][0];
+      g2.peer_hi = c->peer_ghost[1 - cur][1];
+      g2.peer_fence = peer_fence();
+      g2.zbegin = 0;
+      c->ops->pull(s_lo, B, g2, c->params, c->swe_g, c->bb, 2, c->stream);
+      g2.zbegin = nzl - 2;
+      c->ops->pull(s_hi, B, g2, c->params, c->swe_g, c->bb, 2, c->stream);
+      k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_remote[0], c->peer_remote[1]);
+      cudaEventRecord(c->ev_b, c->stream);
+      cur ^= 1;
+    }
+  }
+  for (; t < n; ++t) {
     // pull: cur = current grid; in place (AA): cur = state (0: the odd kernel runs)
     const int pat = pull ? 0 : inplace_pattern(c, cur);
     auto launch = [&](GridParams g, int z0, int np, cudaStream_t s) {
@@ -446,6 +510,7 @@ void enqueue_peer_steps(lbm_ctx *c, int n, int cur) {
     cur ^= 1;
   }
   cudaStreamWaitEvent(c->stream, c->ev_i, 0);
+  return cur;  // the grid (pull) / state (in place) the steps end on
 }
 
 // In-place (AA) peer mode after an odd step (state B): the canonical post-collision values of
@@ -718,11 +783,19 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
     c->own_stream = true;
   }
   c->grid_elems = (size_t)(g.nzl + 2) * (size_t)g.plane;
+  {  // two-step sweeps across ranks need 8 scratch planes (LBM_PEER_TB=0 disables, at create)
+    const char *env = getenv("LBM_PEER_TB");
+    c->peer_tb_cap = !(env && env[0] == '0') && D.nranks > 1 && D.streaming == LBM_PULL && !c->bb &&
+                     ops->pull2 && ops->tile_x > 0 && g.nx % ops->tile_x == 0 && g.ny % ops->tile_y == 0 &&
+                     g.nzl >= 6;
+    c->scratch_off = c->grid_elems;
+  }
+  const size_t alloc_elems = c->grid_elems + (c->peer_tb_cap ? (size_t)8 * g.plane : 0);
   const int ngrids = (D.streaming == LBM_PULL) ? 2 : 1;
   for (int k = 0; k < ngrids; ++k) {
-    e = cudaMalloc(&c->buf[k], c->grid_elems * c->esize);
+    e = cudaMalloc(&c->buf[k], alloc_elems * c->esize);
     if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaMalloc(populations)"));
-    e = cudaMemsetAsync(c->buf[k], 0, c->grid_elems * c->esize, c->stream);
+    e = cudaMemsetAsync(c->buf[k], 0, alloc_elems * c->esize, c->stream);
     if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaMemset"));
   }
   e = cudaMalloc(&c->flag, sizeof(int));
@@ -767,7 +840,7 @@ lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
   info->device_bytes = c->grid_elems * c->esize * (c->streaming == LBM_PULL ? 2 : 1);
   info->steps_done = c->steps;
   info->rate_specialization = c->rs & 3;
-  info->temporal_blocking = use_temporal_blocking(c) ? 2 : 1;
+  info->temporal_blocking = (use_temporal_blocking(c) || use_peer_tb(c)) ? 2 : 1;
   info->resident_cluster = resident_cluster(c);
   info->cuda_graph_steps = (c->nranks == 1 && !info->resident_cluster && use_graphs(c)) ? kGraphSteps : 0;
   return LBM_OK;
@@ -1030,6 +1103,8 @@ lbm_status peer_connect_impl(lbm_ctx *c, const lbm_peer_info *lo, const lbm_peer
       c->peer_ghost[0][1] = static_cast<char *>(g[0][1]) + P;        // AA: upper's first plane
     }
   }
+  for (int k = 0; k < 2; ++k)  // the neighbours' scratch planes (two-step sweeps across ranks)
+    c->peer_scr[k] = c->peer_tb_cap ? static_cast<char *>(g[0][k]) + c->scratch_off * c->esize : nullptr;
   c->peer_remote[0] = static_cast<long long *>(f[0]) + 1;  // I am the lower's upper neighbour
   c->peer_remote[1] = static_cast<long long *>(f[1]) + 0;
   LBM_CUDA(c, cudaMemset(c->peer_flags, 0, 4 * sizeof(long long)));
@@ -1100,11 +1175,9 @@ lbm_status lbm_step_peer(lbm_ctx *c, int n) {
     }
   }
   if (t < n) {
-    enqueue_peer_steps(c, n - t, pull_parity(c));
-    if ((n - t) & 1) {
-      if (c->streaming == LBM_PULL) c->cur ^= 1;
-      else c->aa_state ^= 1;
-    }
+    const int end = enqueue_peer_steps(c, n - t, pull_parity(c));
+    if (c->streaming == LBM_PULL) c->cur = end;
+    else c->aa_state = end;
     c->steps += n - t;
   }
   return check_launch(c, "lbm_step_peer");

@@ -216,12 +216,16 @@ def connect_local(lats):
         l.peer_prime()
 
 
-def step_peer_local(lats, n: int):
+def step_peer_local(lats, n: int, chunk: int = 1):
     """n steps of every context of one process with the fused halo push.  The ranks'
-    launches are interleaved step by step (a context waits on the GPU for its neighbours)."""
-    for _ in range(n):
+    launches are interleaved in chunks of `chunk` steps (a context waits on the GPU for its
+    neighbours; chunk = 2 lets the two-step sweeps run across ranks)."""
+    done = 0
+    while done < n:
+        k = min(chunk, n - done)
         for l in lats:
-            l.step_peer(1)
+            l.step_peer(k)
+        done += k
     for l in lats:
         l.sync()
         assert not l.peer_timed_out(), "a neighbour wait timed out"

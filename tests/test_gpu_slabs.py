@@ -356,3 +356,49 @@ def test_peer_forced_then_disconnect_equals_single_rank(streaming, space, eq, mo
     for lat in lats:
         lat.close()
     np.testing.assert_array_equal(multi, single)
+
+
+@pytest.mark.parametrize("st,space,eq,zc,prec,shape,nranks", [
+    (W.D3Q19, W.RAW, W.EQ_DELTA, 1, L.LBM_FP64, (32, 16, 24), 2),
+    (W.D3Q19, W.CENTRAL, W.EQ_ABSOLUTE, 1, L.LBM_FP64, (32, 16, 24), 3),
+    (W.D3Q19, W.RAW, W.EQ_DELTA, 1, L.LBM_FP32, (32, 16, 24), 4),
+    (W.D3Q27, W.RAW, W.EQ_DELTA, 1, L.LBM_FP64, (32, 16, 18), 3),
+    (W.D2Q9, W.CENTRAL, W.EQ_SWE, 0, L.LBM_FP64, (256, 36, 1), 3),
+    (W.D2Q9, W.POPULATION, W.EQ_DELTA, 1, L.LBM_FP64, (256, 24, 1), 4),
+])
+def test_peer_two_step_sweeps_match_single_rank(st, space, eq, zc, prec, shape, nranks):
+    """Temporal blocking across ranks on the peer path: interior planes by the two-step sweep,
+    the boundary regions by two single steps through the scratch planes with pushes into the
+    neighbours' scratch and ghost planes; pairs plus a trailing single step match the
+    single-rank run to rounding and the oracle at full parity."""
+    from gpu_helpers import round_to
+    g = W.swe_lattice_parameters()[0] if eq == W.EQ_SWE else 0.0
+    rates = W.rate_set_p(st) if space != W.POPULATION else [1.3]
+    if eq == W.EQ_SWE:
+        f0 = initial_state(st, space, eq, zc, shape, g=g, noise=0.0, dam=(8.0, 6.25, 1.25))
+    else:
+        f0 = round_to(initial_state(st, space, eq, zc, shape), prec)
+    steps = 9
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, precision=prec, swe_g=g) as lat:
+        lat.set_populations(f0)
+        lat.step(steps)
+        single = lat.get_populations()
+    slab_axis = 2 if W.DIM_OF[st] == 2 else 1
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, precision=prec, swe_g=g, rank=r,
+                      nranks=nranks) for r in range(nranks)]
+    for lat in lats:
+        sl = [slice(None)] * 4
+        sl[slab_axis] = slice(lat.offset, lat.offset + lat.extent)
+        lat.set_populations(np.ascontiguousarray(f0[tuple(sl)]))
+    D.connect_local(lats)
+    assert all(lat.info().temporal_blocking == 2 for lat in lats)
+    D.step_peer_local(lats, steps, chunk=2)
+    multi = np.concatenate([lat.get_populations() for lat in lats], axis=slab_axis)
+    for lat in lats:
+        lat.close()
+    norm = "cell" if eq == W.EQ_SWE else "population"
+    tol = 1e-13 if prec == L.LBM_FP64 else 2e-6
+    assert gate_error(st, multi, single, zc, norm=norm) < tol
+    if prec == L.LBM_FP64:
+        ref = oracle_run(st, space, eq, zc, rates, shape, f0, steps, g=g)
+        assert gate_error(st, multi, ref, zc, norm=norm) < F64_TOL
