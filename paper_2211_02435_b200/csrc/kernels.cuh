@@ -521,7 +521,8 @@ struct Tile2 {
   static constexpr int THREADS = (HW + 31) / 32 * 32;
 };
 
-template <class S, int SPACE, int REG, class real, int RS, int TX, int TY, int MINB = 1, bool PF = false>
+template <class S, int SPACE, int REG, class real, int RS, int TX, int TY, int MINB = 1, bool PF = false,
+          bool RANGE = false>
 __global__ void __launch_bounds__(Tile2<TX, TY>::THREADS, MINB)
     k_pull2(const real *__restrict__ src, real *__restrict__ dst, const GridParams g, const Rates<real> r,
             const real swe_g, const Force<real> fr) {
@@ -546,12 +547,16 @@ __global__ void __launch_bounds__(Tile2<TX, TY>::THREADS, MINB)
   const int n = g.nzl;
   // blockIdx.z: chunk [p0, p1) of the output planes (more CTAs for short slabs); each chunk
   // recomputes the two step-(t+1) planes at its ends
-  // output planes [zb, zb + zn): the whole slab (single rank, periodic wrap) or, across ranks,
-  // the planes whose two-step dependence stays inside the slab (no wrap: ghost planes are real)
-  const int zb = g.zcount ? g.zbegin : 0, zn = g.zcount ? g.zcount : n;
+  // output planes [zb, zb + zn): the whole slab (single rank, periodic wrap) or, with RANGE
+  // (across ranks), [zbegin, zbegin + zcount) whose two-step dependence stays inside the slab
+  // (no wrap).  A template switch: a runtime wrap test in the loads cost the sweep 8-16 %.
+  const int zb = RANGE ? g.zbegin : 0, zn = RANGE ? g.zcount : n;
   const int p0 = zb + (int)((long long)zn * blockIdx.z / gridDim.z);
   const int p1 = zb + (int)((long long)zn * (blockIdx.z + 1) / gridDim.z);
-  auto zw = [&](int k) { return g.wrapz ? wrapi(k, n) : k; };
+  auto zw = [&](int k) {
+    if constexpr (RANGE) return k;
+    else return wrapi(k, n);
+  };
   // step-t populations of the halo-extended tile at plane k (pull: plane k - xi_z)
   auto load = [&](int k, real (&f)[S::Q]) {
     const int zc = zw(k);
@@ -691,7 +696,7 @@ struct Tile1 {
   static constexpr int THREADS = (HW + 31) / 32 * 32;
 };
 
-template <class S, int SPACE, int REG, class real, int RS, int TX, int MINB = 1, bool PF = true>
+template <class S, int SPACE, int REG, class real, int RS, int TX, int MINB = 1, bool PF = true, bool RANGE = false>
 __global__ void __launch_bounds__(Tile1<TX>::THREADS, MINB)
     k_pull2_2d(const real *__restrict__ src, real *__restrict__ dst, const GridParams g, const Rates<real> r,
                const real swe_g, const Force<real> fr) {
@@ -705,10 +710,13 @@ __global__ void __launch_bounds__(Tile1<TX>::THREADS, MINB)
   const int gx = wrapi(x0 - 1 + t, g.nx);
   const int xs[3] = {wrapi(gx - 1, g.nx), gx, wrapi(gx + 1, g.nx)};
   const int n = g.nzl;
-  const int zb = g.zcount ? g.zbegin : 0, zn = g.zcount ? g.zcount : n;  // as in k_pull2
+  const int zb = RANGE ? g.zbegin : 0, zn = RANGE ? g.zcount : n;  // as in k_pull2
   const int p0 = zb + (int)((long long)zn * blockIdx.y / gridDim.y);
   const int p1 = zb + (int)((long long)zn * (blockIdx.y + 1) / gridDim.y);
-  auto zw = [&](int k) { return g.wrapz ? wrapi(k, n) : k; };
+  auto zw = [&](int k) {
+    if constexpr (RANGE) return k;
+    else return wrapi(k, n);
+  };
   // step-t populations of the halo-extended strip at row k (pull: row k - xi_y)
   auto load = [&](int k, real (&f)[S::Q]) {
     const int zc = zw(k);

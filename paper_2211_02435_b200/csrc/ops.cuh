@@ -84,6 +84,19 @@ struct TbTile {
   static constexpr int MINB = S::Q == 27 ? 1 : (f64 ? 2 : 3);  // 3D: CTAs per SM
 };
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel instantiation, device):
+// `configured` is a static of the calling launcher (one per instantiation), bit d = device d
+// (benign race: setting the attribute twice is harmless)
+template <class K>
+inline void opt_in_smem_once(K kern, size_t smem, unsigned &configured) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned bit = dev < 32 ? (1u << dev) : 0u;
+  if (bit && (configured & bit)) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  configured |= bit;
+}
+
 inline dim3 cell_grid(const GridParams &g, int nplanes) {
   return dim3((unsigned)((g.nx + BLOCK_X - 1) / BLOCK_X), (unsigned)g.ny, (unsigned)nplanes);
 }
@@ -194,12 +207,15 @@ struct OpsImpl {
       using T = Tile2<TX, TY>;
       const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
       const size_t smem = (size_t)3 * S::Q * T::HW * sizeof(real);
-      auto kern = k_pull2<S, SPACE, REG, real, RS, TX, TY, TT::MINB, true>;
-      // opt in to > 48 KB of dynamic shared memory (per device: set on every launch, ~1 us
-      // against a multi-ms sweep; a process-wide "done once" flag would miss a second GPU)
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kern<<<dim3((unsigned)(g.nx / TX), (unsigned)(g.ny / TY), (unsigned)zchunks), T::THREADS, smem, s>>>(
-          static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
+      // whole slab with periodic wrap (single rank) or a plane range without wrap (across ranks)
+      auto go = [&](auto kern, unsigned &configured) {
+        opt_in_smem_once(kern, smem, configured);  // > 48 KB of shared memory, once per device
+        kern<<<dim3((unsigned)(g.nx / TX), (unsigned)(g.ny / TY), (unsigned)zchunks), T::THREADS, smem, s>>>(
+            static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
+      };
+      static unsigned conf_slab = 0, conf_range = 0;
+      if (g.zcount) go(k_pull2<S, SPACE, REG, real, RS, TX, TY, TT::MINB, true, true>, conf_range);
+      else go(k_pull2<S, SPACE, REG, real, RS, TX, TY, TT::MINB, true, false>, conf_slab);
     } else if constexpr (S::D == 2) {
       using T = Tile1<TX>;
       const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
@@ -207,10 +223,14 @@ struct OpsImpl {
       // scripts/tb2d_variants.cu on B200 (profiles/r1/tb2d_variants.txt): >= 2 CTAs/SM with the
       // next row's loads prefetched; SRT (light collision): 3 CTAs/SM without the prefetch
       constexpr bool srt = SPACE == SPACE_POPULATION;
-      auto kern = k_pull2_2d<S, SPACE, REG, real, RS, TX, srt ? 3 : 2, !srt>;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kern<<<dim3((unsigned)(g.nx / TX), (unsigned)zchunks, 1), T::THREADS, smem, s>>>(
-          static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
+      auto go = [&](auto kern, unsigned &configured) {
+        opt_in_smem_once(kern, smem, configured);
+        kern<<<dim3((unsigned)(g.nx / TX), (unsigned)zchunks, 1), T::THREADS, smem, s>>>(
+            static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
+      };
+      static unsigned conf_slab = 0, conf_range = 0;
+      if (g.zcount) go(k_pull2_2d<S, SPACE, REG, real, RS, TX, srt ? 3 : 2, !srt, true>, conf_range);
+      else go(k_pull2_2d<S, SPACE, REG, real, RS, TX, srt ? 3 : 2, !srt, false>, conf_slab);
     }
   }
   template <bool BB>
