@@ -1,0 +1,3 @@
+# final: full GPU suite + smoke with the final build
+timeout 2000 python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1

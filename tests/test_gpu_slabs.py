@@ -402,3 +402,30 @@ def test_peer_two_step_sweeps_match_single_rank(st, space, eq, zc, prec, shape, 
     if prec == L.LBM_FP64:
         ref = oracle_run(st, space, eq, zc, rates, shape, f0, steps, g=g)
         assert gate_error(st, multi, ref, zc, norm=norm) < F64_TOL
+
+
+def test_peer_two_step_sweeps_graph_replay():
+    """Two-step sweeps across ranks inside the captured 32-step graphs (16 pairs per graph)
+    plus a remainder of pairs and a single step: equal to the single-rank run to rounding."""
+    st, space, eq, zc = W.D3Q19, W.RAW, W.EQ_DELTA, 1
+    shape, nranks, steps = (32, 16, 24), 2, 71
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc) as lat:
+        lat.set_populations(f0)
+        lat.step(steps)
+        single = lat.get_populations()
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, rank=r, nranks=nranks) for r in range(nranks)]
+    for lat in lats:
+        lat.set_populations(np.ascontiguousarray(f0[:, lat.offset:lat.offset + lat.extent]))
+    D.connect_local(lats)
+    for chunk in (64, 7):  # two graph replays per context, then 3 pairs + 1 single step
+        for lat in lats:
+            lat.step_peer(chunk)
+    for lat in lats:
+        lat.sync()
+        assert not lat.peer_timed_out()
+    multi = np.concatenate([lat.get_populations() for lat in lats], axis=1)
+    for lat in lats:
+        lat.close()
+    assert gate_error(st, multi, single, zc) < 1e-13
