@@ -492,6 +492,9 @@ def run_tgv(st, space, eq, zc, nu, u0, L, steps, prec=oracle.LONG_DOUBLE):
     (W.RAW, W.EQ_DELTA, 1, 0.05),
     (W.CENTRAL, W.EQ_ABSOLUTE, 1, 0.05),
     (W.CUMULANT, W.EQ_ABSOLUTE, 1, 0.05),
+    (W.CENTRAL, W.EQ_DISCRETE, 1, 0.05),
+    (W.CUMULANT, W.EQ_DISCRETE, 1, 0.05),
+    (W.RAW, W.EQ_DISCRETE_DELTA, 1, 0.05),
 ])
 def test_tgv_energy_decay(space, eq, zc, nu):
     """E/E0 = exp(-4 nu kappa^2 t) (eq:TGA_kin_energy) within 1 %
