@@ -78,6 +78,7 @@ def test_fp32_in_place_patterns_equal_pull(st):
     (W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, L.LBM_PULL),
     (W.D3Q27, W.CENTRAL, W.EQ_ABSOLUTE, L.LBM_AA),
     (W.D3Q19, W.RAW, W.EQ_DELTA, L.LBM_PULL),
+    (W.D3Q27, W.CENTRAL, W.EQ_DISCRETE, L.LBM_ESOTERIC_TWIST),
 ])
 def test_gpu_tgv_second_order_convergence(st, space, eq, streaming):
     """Physics of the GPU path beyond the sizes the oracle reaches: the Taylor-Green decay
