@@ -98,7 +98,21 @@ typedef enum { LBM_FP64 = 0, LBM_FP32 = 1 } lbm_precision;
    x + {0,1}^d; single rank, periodic).  All three in-place patterns move the same bytes. */
 typedef enum { LBM_PULL = 0, LBM_AA = 1, LBM_ESOTERIC_PULL = 2, LBM_ESOTERIC_TWIST = 3 } lbm_streaming;
 typedef enum { LBM_BC_PERIODIC = 0, LBM_BC_NOSLIP = 1 } lbm_bc;
-typedef enum { LBM_REGION_ALL = 0, LBM_REGION_BOUNDARY = 1, LBM_REGION_INTERIOR = 2 } lbm_region;
+typedef enum {
+  LBM_REGION_ALL = 0,
+  LBM_REGION_BOUNDARY = 1,
+  LBM_REGION_INTERIOR = 2,
+  /* two fused steps across ranks with an external exchange (multi-rank pull contexts whose
+     kernels run two-step sweeps, >= 6 planes per slab, no walls; else LBM_EUNSUPPORTED):
+     PAIR_INTERIOR: steps t+1 and t+2 of planes [2, nzl - 2) from the current grid into the
+     next (no neighbour data); PAIR_BOUNDARY1: step t+1 of planes {0,1,2} and {nzl-3..nzl-1}
+     into 8 scratch planes, then exchange lbm_get_halo(2); PAIR_BOUNDARY2: step t+2 of planes
+     {0,1} and {nzl-2,nzl-1} from the scratch into the next grid, then exchange
+     lbm_get_halo(1) and lbm_swap once (PAIR_BOUNDARY2 counts the pair's first step). */
+  LBM_REGION_PAIR_INTERIOR = 3,
+  LBM_REGION_PAIR_BOUNDARY1 = 4,
+  LBM_REGION_PAIR_BOUNDARY2 = 5
+} lbm_region;
 
 typedef struct {
   int nx, ny, nz;  /* GLOBAL lattice extents; D2Q9: nz = 1 (the slab axis is then y)        */
@@ -203,7 +217,8 @@ lbm_status lbm_step(lbm_ctx *ctx, int n);
    the neighbours); even steps touch only their own cells and need no exchange. */
 lbm_status lbm_step_region(lbm_ctx *ctx, lbm_region region, void *stream);
 lbm_status lbm_swap(lbm_ctx *ctx);
-/* PULL: which = 0 the current grid, 1 the next grid.  AA: which = 0 pre-odd, 1 post-odd. */
+/* PULL: which = 0 the current grid, 1 the next grid, 2 the scratch of the two-step regions
+   (LBM_REGION_PAIR_*).  AA: which = 0 pre-odd, 1 post-odd. */
 lbm_status lbm_get_halo(lbm_ctx *ctx, int which, lbm_halo *out);
 
 lbm_status lbm_sync(lbm_ctx *ctx);

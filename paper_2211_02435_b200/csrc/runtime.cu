@@ -947,6 +947,36 @@ lbm_status lbm_step_region(lbm_ctx *c, lbm_region region, void *stream) {
       run(n - 1, 1);
       break;
     case LBM_REGION_INTERIOR: run(1, n - 2); break;
+    case LBM_REGION_PAIR_INTERIOR:
+    case LBM_REGION_PAIR_BOUNDARY1:
+    case LBM_REGION_PAIR_BOUNDARY2: {
+      // two-step sweeps across ranks with an external exchange (the lbm_step_peer pair
+      // sequence of DESIGN.md section 8, without the peer pushes)
+      if (!c->peer_tb_cap)
+        return fail(c, LBM_EUNSUPPORTED, "two-step regions need a multi-rank pull context with two-step sweeps");
+      void *A = c->buf[c->cur], *B = c->buf[1 - c->cur];
+      const size_t PB = (size_t)g.plane * c->esize;
+      char *scr = static_cast<char *>(c->buf[0]) + c->scratch_off * c->esize;
+      void *s_lo = scr, *s_hi = scr - (long long)(n - 6) * (long long)PB;
+      GridParams gb = c->g;
+      if (region == LBM_REGION_PAIR_INTERIOR) {
+        gb.zbegin = 2;
+        gb.zcount = n - 4;
+        c->ops->pull2(A, B, gb, c->params, c->swe_g, peer_tb_chunks(c), s);
+      } else if (region == LBM_REGION_PAIR_BOUNDARY1) {
+        gb.zbegin = 0;
+        c->ops->pull(A, s_lo, gb, c->params, c->swe_g, c->bb, 3, s);
+        gb.zbegin = n - 3;
+        c->ops->pull(A, s_hi, gb, c->params, c->swe_g, c->bb, 3, s);
+      } else {
+        gb.zbegin = 0;
+        c->ops->pull(s_lo, B, gb, c->params, c->swe_g, c->bb, 2, s);
+        gb.zbegin = n - 2;
+        c->ops->pull(s_hi, B, gb, c->params, c->swe_g, c->bb, 2, s);
+        c->steps++;  // the pair's first step (lbm_swap counts the second)
+      }
+      break;
+    }
     default: return fail(c, LBM_EINVAL, "unknown region");
   }
   return check_launch(c, "stream_collide(region)");
@@ -964,13 +994,27 @@ lbm_status lbm_get_halo(lbm_ctx *c, int which, lbm_halo *out) {
   if (!c || !out) return LBM_EINVAL;
   if (c->streaming == LBM_ESOTERIC_PULL || c->streaming == LBM_ESOTERIC_TWIST)
     return fail(c, LBM_EUNSUPPORTED, "Esoteric Pull / Twist are single-rank");
-  char *base = static_cast<char *>(grid_ptr(c, which));
+  if (which == 2 && !c->peer_tb_cap)
+    return fail(c, LBM_EUNSUPPORTED, "no scratch halo: the context does not run two-step sweeps across ranks");
+  if (which < 0 || which > 2) return fail(c, LBM_EINVAL, "which must be 0, 1 or 2");
   lbm_layout lay;
   lbm_status s = lbm_grid_layout((lbm_stencil)c->stencil, (lbm_precision)c->prec, c->gnx, c->gny, c->gnz,
                                  c->nranks, &lay);
   if (s != LBM_OK) return fail(c, s, "layout");
   const size_t E = c->esize;
   size_t o[4] = {lay.send_lo, lay.send_hi, lay.recv_lo, lay.recv_hi};
+  if (which == 2) {  // the scratch of the two-step regions: planes -1, 0 at scratch planes 0, 1
+    // (the grid's offsets), planes nzl - 1, nzl at scratch planes 6, 7
+    char *scr = static_cast<char *>(c->buf[0]) + c->scratch_off * E;
+    const size_t shift = (size_t)(c->g.nzl - 6) * (size_t)c->g.plane;
+    out->send_lo = scr + o[0] * E;
+    out->send_hi = scr + (o[1] - shift) * E;
+    out->recv_lo = scr + o[2] * E;
+    out->recv_hi = scr + (o[3] - shift) * E;
+    out->bytes = lay.halo_elems * E;
+    return LBM_OK;
+  }
+  char *base = static_cast<char *>(grid_ptr(c, which));
   if (c->streaming == LBM_AA) {
     const size_t pre[4] = {lay.aa_pre_send_lo, lay.aa_pre_send_hi, lay.aa_pre_recv_lo, lay.aa_pre_recv_hi};
     const size_t post[4] = {lay.aa_post_send_lo, lay.aa_post_send_hi, lay.aa_post_recv_lo, lay.aa_post_recv_hi};

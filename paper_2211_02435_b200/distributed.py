@@ -145,10 +145,35 @@ def exchange_after_boundary(lat: "L.Lattice") -> int:
     return 1 if odd else 0
 
 
-def step_local(lats, n: int):
+def supports_pairs(lat: "L.Lattice") -> bool:
+    """The context runs two-step sweeps across ranks (LBM_REGION_PAIR_*, lbm_get_halo(2))."""
+    try:
+        lat.get_halo(2)
+        return True
+    except L.LbmError:
+        return False
+
+
+def step_local(lats, n: int, pairs: bool = False):
     """n time steps of all slab contexts of one process (LocalTransport), with the
-    same boundary/interior split as the multi-process driver."""
+    same boundary/interior split as the multi-process driver (pairs: the two-step regions)."""
     tr = LocalTransport(lats)
+    if pairs and all(supports_pairs(l) for l in lats):
+        while n >= 2:
+            for l in lats:
+                l.step_region(L.LBM_REGION_PAIR_INTERIOR)
+                l.step_region(L.LBM_REGION_PAIR_BOUNDARY1)
+            for l in lats:
+                l.sync()
+            tr.exchange_all(2)
+            for l in lats:
+                l.step_region(L.LBM_REGION_PAIR_BOUNDARY2)
+            for l in lats:
+                l.sync()
+            tr.exchange_all(1)
+            for l in lats:
+                l.swap()
+            n -= 2
     for _ in range(n):
         which = exchange_after_boundary(lats[0])
         for l in lats:
@@ -179,6 +204,7 @@ class SlabRunner:
         self.tr = TorchTransport(lat, rank, nranks, group)
         self.s_int = torch.cuda.Stream()
         self.s_main = torch.cuda.current_stream()
+        self.pairs = lat.streaming == L.LBM_PULL and supports_pairs(lat)  # same on every rank
 
     def prime(self):
         self.lat.sync()
@@ -188,6 +214,22 @@ class SlabRunner:
         import torch
 
         main = self.s_main
+        # two fused steps per pair: the interior sweep on s_int overlaps both boundary steps and
+        # both exchanges (scratch halo after the first, next-grid halo after the second)
+        while self.pairs and n >= 2:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            self.s_int.wait_event(ev)
+            self.lat.step_region(L.LBM_REGION_PAIR_INTERIOR, self.s_int.cuda_stream)
+            self.lat.step_region(L.LBM_REGION_PAIR_BOUNDARY1, main.cuda_stream)
+            with torch.cuda.stream(main):
+                self.tr.exchange(2)
+            self.lat.step_region(L.LBM_REGION_PAIR_BOUNDARY2, main.cuda_stream)
+            with torch.cuda.stream(main):
+                self.tr.exchange(1)
+            main.wait_stream(self.s_int)
+            self.lat.swap()
+            n -= 2
         for _ in range(n):
             which = exchange_after_boundary(self.lat)
             # boundary planes on the main stream, then the exchange (NCCL waits on main)

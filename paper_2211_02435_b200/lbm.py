@@ -24,6 +24,7 @@ LBM_PULL, LBM_AA, LBM_ESOTERIC_PULL, LBM_ESOTERIC_TWIST = 0, 1, 2, 3
 LBM_BC_PERIODIC, LBM_BC_NOSLIP = 0, 1
 LBM_FORCE_GUO, LBM_FORCE_HE = 0, 1
 LBM_REGION_ALL, LBM_REGION_BOUNDARY, LBM_REGION_INTERIOR = 0, 1, 2
+LBM_REGION_PAIR_INTERIOR, LBM_REGION_PAIR_BOUNDARY1, LBM_REGION_PAIR_BOUNDARY2 = 3, 4, 5
 
 Q_OF = {LBM_D2Q9: 9, LBM_D3Q19: 19, LBM_D3Q27: 27}
 

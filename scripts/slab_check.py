@@ -107,7 +107,7 @@ def main():
                 one.init_macroscopic(np.ascontiguousarray(r), np.ascontiguousarray(u[:one.d]))
                 one.step(args.steps)
                 single = one.get_populations()
-            if name.endswith("TB") and args.halo == "peer":
+            if name.endswith("TB"):  # two-step sweeps across ranks (both transports): to rounding
                 w = lattice_weights(st) if zc else 0.0
                 same = bool(np.max(np.abs(multi - single) / np.abs(single + w)) < 1e-13)
             else:

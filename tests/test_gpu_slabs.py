@@ -429,3 +429,36 @@ def test_peer_two_step_sweeps_graph_replay():
     for lat in lats:
         lat.close()
     assert gate_error(st, multi, single, zc) < 1e-13
+
+
+@pytest.mark.parametrize("st,space,eq,zc,shape,nranks", [
+    (W.D3Q19, W.RAW, W.EQ_DELTA, 1, (32, 16, 24), 2),
+    (W.D3Q19, W.CUMULANT, W.EQ_ABSOLUTE, 1, (32, 16, 24), 4),
+    (W.D2Q9, W.CENTRAL, W.EQ_ABSOLUTE, 1, (256, 36, 1), 3),
+])
+def test_exchange_path_two_step_regions(st, space, eq, zc, shape, nranks):
+    """Two-step sweeps across ranks with an external exchange (LBM_REGION_PAIR_* +
+    lbm_get_halo(2), the SlabRunner sequence with LocalTransport): pairs plus a single step
+    equal the single-rank run to rounding and the oracle at the gate."""
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape)
+    steps = 9
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc) as lat:
+        lat.set_populations(f0)
+        lat.step(steps)
+        single = lat.get_populations()
+    slab_axis = 2 if W.DIM_OF[st] == 2 else 1
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, rank=r, nranks=nranks) for r in range(nranks)]
+    for lat in lats:
+        sl = [slice(None)] * 4
+        sl[slab_axis] = slice(lat.offset, lat.offset + lat.extent)
+        lat.set_populations(np.ascontiguousarray(f0[tuple(sl)]))
+    assert all(D.supports_pairs(lat) for lat in lats)
+    D.prime_local(lats)
+    D.step_local(lats, steps, pairs=True)
+    assert lats[0].info().steps_done == steps
+    multi = np.concatenate([lat.get_populations() for lat in lats], axis=slab_axis)
+    for lat in lats:
+        lat.close()
+    assert gate_error(st, multi, single, zc) < 1e-13
+    assert gate_error(st, multi, oracle_run(st, space, eq, zc, rates, shape, f0, steps), zc) < F64_TOL
