@@ -123,6 +123,75 @@ def ncu_traffic(config_name, kernel_key, cells, steps_per_launch=1):
     return None
 
 
+def global_sums(lat, n, dist):
+    """mass and momentum of the whole lattice (lbm_get_diagnostics of every rank's slab,
+    all-reduced in fp64)."""
+    d = lat.get_diagnostics()
+    v = np.array([d["mass"], *d["momentum"]], dtype=np.float64)
+    if n > 1:
+        import torch
+
+        t = torch.from_numpy(v).to("cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t)
+        v = t.cpu().numpy()
+    return v
+
+
+def multi_rank_probe(cfg, n, rank, dev, dist, L, D, use_nccl, want_peer):
+    """N ranks vs rank 0 alone on a small lattice of the same method and halo path: every rank
+    runs its slab of (64, 64, 8 N) (2D: (256, 16 N)) for 6 steps; rank 0 also runs the whole
+    lattice as one rank and compares the gathered populations.  Returns (bitwise, max |diff|)
+    on rank 0 (None elsewhere).  The first multi-GPU run proves its own halos."""
+    st = cfg["stencil"]
+    two_d = W.DIM_OF[st] == 2
+    shape = (256, 16 * n, 1) if two_d else (64, 64, 8 * n)
+    rates = rates_of(cfg)
+    g = W.swe_lattice_parameters()[0] if cfg["eq"] == W.EQ_SWE else 0.0
+    kw = dict(zero_centered=cfg["zc"], precision=cfg["prec"], streaming=cfg["streaming"], swe_g=g, device=dev)
+    nid = None
+    if use_nccl:
+        box = [L.nccl_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        nid = box[0]
+    lat = L.Lattice(st, cfg["space"], cfg["eq"], rates, shape, rank=rank, nranks=n, nccl_id=nid, **kw)
+    nx, ny, nz = shape
+    if cfg["eq"] == W.EQ_SWE:
+        rho, u = W.dam_break_fields(nx, ny, nx * 2.5 / 40, 6.25, 1.25, y0=lat.offset, ny_local=lat.extent)
+    elif two_d:
+        rho_g, u_g = W.tgv_fields(nx, ny, 1, 0.05)
+        rho, u = rho_g[:, lat.offset:lat.offset + lat.extent], u_g[:, :, lat.offset:lat.offset + lat.extent]
+    else:
+        rho, u = W.tgv_fields(nx, ny, lat.extent, 0.05, z0=lat.offset, nz_global=nz, plane="xz")
+    lat.init_macroscopic(np.ascontiguousarray(rho), np.ascontiguousarray(u[:lat.d]))
+    runner = None
+    if want_peer:
+        try:
+            runner = D.PeerRunner(lat, rank, n)
+        except (L.LbmError, D.PeerUnavailable):
+            runner = None
+    if runner is None and not use_nccl:
+        runner = D.SlabRunner(lat, rank, n)
+        runner.prime()
+    steps = 6
+    (runner.step if runner is not None else lat.step)(steps)
+    lat.sync()
+    mine = lat.get_populations()
+    parts = [None] * n
+    dist.all_gather_object(parts, mine)
+    dist.barrier()
+    lat.close()
+    if rank != 0:
+        return None, None
+    got = np.concatenate(parts, axis=2 if two_d else 1)
+    with L.Lattice(st, cfg["space"], cfg["eq"], rates, shape, **kw) as one:
+        rho, u = (W.dam_break_fields(nx, ny, nx * 2.5 / 40, 6.25, 1.25) if cfg["eq"] == W.EQ_SWE else
+                  (W.tgv_fields(nx, ny, 1, 0.05) if two_d else W.tgv_fields(nx, ny, nz, 0.05, plane="xz")))
+        one.init_macroscopic(np.ascontiguousarray(rho), np.ascontiguousarray(u[:one.d]))
+        one.step(steps)
+        ref = one.get_populations()
+    return bool(np.array_equal(got, ref)), float(np.max(np.abs(got - ref)))
+
+
 # ---------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons sampled during the timed region."""
@@ -290,10 +359,12 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--backend", default=None, choices=["nccl", "gloo"],
                     help="torch.distributed backend for N > 1 (default: nccl with one GPU per rank)")
-    ap.add_argument("--halo", default="auto", choices=["auto", "peer", "exchange"],
+    ap.add_argument("--halo", default="auto", choices=["auto", "peer", "nccl", "exchange"],
                     help="N > 1 halo path: peer = boundary kernels store into (pull) or access (AA) "
-                         "the neighbours' planes over NVLink peer memory; exchange = torch.distributed "
-                         "P2P (NCCL); auto = peer")
+                         "the neighbours' planes over NVLink peer memory; nccl = the library's own "
+                         "NCCL send/recv in lbm_step; exchange = torch.distributed P2P driven from "
+                         "Python; auto = peer, else nccl")
+    ap.add_argument("--no-probe", action="store_true", help="skip the N-rank vs 1-rank bitwise probe")
     ap.add_argument("--shape", type=int, nargs=3, default=None,
                     help="override the global lattice shape (profiling runs only)")
     args = ap.parse_args()
@@ -339,9 +410,21 @@ def main():
     # events of the timed region are recorded on the same stream
     main_stream = torch.cuda.Stream()
     torch.cuda.set_stream(main_stream)
+    use_nccl = n > 1 and dist.get_backend() == "nccl" and args.halo in ("auto", "nccl", "peer")
+    want_peer = n > 1 and (args.halo == "peer" or (args.halo == "auto" and cfg["streaming"] in (L.LBM_PULL, L.LBM_AA)))
+    probe = None
+    if n > 1 and not args.no_probe:  # N ranks vs one rank, bitwise, before anything is timed
+        bitwise, maxdiff = multi_rank_probe(cfg, n, rank, dev, dist, L, D, use_nccl, want_peer)
+        probe = {"multi_rank_bitwise": bitwise, "multi_rank_max_abs_diff": maxdiff,
+                 "probe": "6 steps of a (64, 64, 8 N) lattice (2D: 256 x 16 N), N ranks vs rank 0 alone"}
+    nccl_id = None
+    if use_nccl:  # in-library NCCL communicator (lbm_domain.nccl_id): the transport when no peer push
+        box = [L.nccl_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        nccl_id = box[0]
     lat = L.Lattice(st, cfg["space"], cfg["eq"], rates, shape, zero_centered=cfg["zc"], precision=cfg["prec"],
                     streaming=cfg["streaming"], swe_g=g, device=local_rank, stream=main_stream.cuda_stream,
-                    rank=rank, nranks=n)
+                    rank=rank, nranks=n, nccl_id=nccl_id)
     d = lat.d
     # synthetic initial state of this rank's slab
     if cfg["eq"] == W.EQ_SWE:
@@ -357,25 +440,30 @@ def main():
     lat.init_macroscopic(rho, u)
     runner = None
     halo = None
+    path = "single"
     if n > 1:
-        want_peer = args.halo == "peer" or (args.halo == "auto" and cfg["streaming"] in (L.LBM_PULL, L.LBM_AA))
         if want_peer:
             try:
-                runner = D.PeerRunner(lat, rank, n)
-                halo = ("peer: fused boundary-plane push over NVLink peer memory (CUDA IPC), device flags"
-                        if cfg["streaming"] == L.LBM_PULL else
+                D.PeerRunner(lat, rank, n)  # connects the ring; lbm_step then runs the fused push
+                path = "peer"
+                halo = ("peer: fused boundary-plane push over NVLink peer memory (CUDA IPC), device flags, "
+                        "lbm_step" if cfg["streaming"] == L.LBM_PULL else
                         "peer: AA odd-step boundary kernels access the neighbours' planes over NVLink peer "
-                        "memory (CUDA IPC), device flags")
+                        "memory (CUDA IPC), device flags, lbm_step")
             except (L.LbmError, D.PeerUnavailable) as ex:
                 if args.halo == "peer":
                     raise
                 print(f"warning: fused halo push unavailable ({ex}); using the NCCL exchange", file=sys.stderr)
-        if runner is None:
+        if path == "single" and nccl_id is not None:
+            path = "nccl"
+            halo = "nccl: in-library ncclSend/ncclRecv group per step (lbm_step), overlapped with the interior"
+        elif path == "single":
+            path = "exchange"
             runner = D.SlabRunner(lat, rank, n)
+            runner.prime()
             halo = f"exchange: torch.distributed P2P ({dist.get_backend()}) overlapped with the interior"
-        runner.prime()
 
-    def do_steps(k):
+    def do_steps(k):  # the library's own collective lbm_step on every path but the external one
         if runner is None:
             lat.step(k)
         else:
@@ -385,21 +473,27 @@ def main():
     # warm-up
     do_steps(args.warmup)
     torch.cuda.synchronize()
+    sums0 = global_sums(lat, n, dist)
     if n > 1:
         dist.barrier()
     sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.3)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # the K timed steps in (up to) 5 windows of consecutive steps, CUDA events between them
+    nwin = max(1, min(5, args.steps))
+    bounds = [round(k * args.steps / nwin) for k in range(nwin + 1)]
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(nwin + 1)]
     torch.cuda.synchronize()
     if n > 1:
         dist.barrier()
-    ev0.record(main_stream)
-    do_steps(args.steps)
-    ev1.record(main_stream)
+    evs[0].record(main_stream)
+    for k in range(nwin):
+        do_steps(bounds[k + 1] - bounds[k])
+        evs[k + 1].record(main_stream)
     torch.cuda.synchronize()
     clocks = sampler.stop()
-    ms = ev0.elapsed_time(ev1)
+    ms = evs[0].elapsed_time(evs[-1])
+    win_ms = [evs[k].elapsed_time(evs[k + 1]) / (bounds[k + 1] - bounds[k]) for k in range(nwin)]
     def max_over_ranks(v):
         if n == 1:
             return v
@@ -409,11 +503,20 @@ def main():
         return float(t.item())
 
     ms = max_over_ranks(ms)
+    win_ms = [max_over_ranks(w) for w in win_ms]
     if n > 1:
-        if isinstance(runner, D.PeerRunner):
-            runner.check()
+        if path == "peer" and lat.peer_timed_out():
+            raise RuntimeError(f"rank {rank}: a wait for a neighbour's halo timed out")
         dist.barrier()
     lat.check_finite()
+    # conservation over the timed steps (periodic box: mass and momentum are invariants)
+    sums1 = global_sums(lat, n, dist)
+    mass_drift = float(abs(sums1[0] - sums0[0]) / sums0[0])
+    momentum_drift = float(np.max(np.abs(sums1[1:] - sums0[1:])) / sums0[0])
+    drift_tol = 1e-12 if cfg["prec"] == 0 else 1e-9
+    if not (mass_drift <= drift_tol and momentum_drift <= drift_tol):
+        raise RuntimeError(f"conservation violated over the timed steps: mass {mass_drift:.3e}, "
+                           f"momentum {momentum_drift:.3e} (tolerance {drift_tol:g})")
     total_cells = nx * ny * nz
     value = total_cells * args.steps / (ms * 1e-3) / 1e6
     ms_step = ms / args.steps
@@ -422,16 +525,20 @@ def main():
     # per TWO steps when the library fuses pairs of steps: temporal blocking, D3Q19)
     peak, peak_src = measured_peaks()
     bpc = bytes_per_cell(cfg)  # every population read once and written once per launch
-    tb = lat.info().temporal_blocking if (n == 1 or isinstance(runner, D.PeerRunner)) else 1
-    resident = lat.info().resident_cluster if n == 1 else 0
-    # N > 1: interior + 2 boundary launches (+ wait and signal kernels of the fused push); with
-    # two-step sweeps across ranks per PAIR: interior sweep + 2 waits + 4 boundary + 2 signals
+    info = lat.info()
+    tb = info.temporal_blocking
+    if path == "exchange" and not runner.pairs:
+        tb = 1
+    resident = info.resident_cluster if n == 1 else 0
+    # our kernels per step.  N > 1: interior + 2 boundary launches (+ wait and signal kernels of
+    # the fused push; NCCL's own kernels are not counted); per PAIR of steps with two-step sweeps
+    # across ranks: interior sweep + 4 boundary (+ 2 waits + 2 signals on the peer path)
     if n == 1:
         launches_per_step = 1.0 / tb
-    elif isinstance(runner, D.PeerRunner):
+    elif path == "peer":
         launches_per_step = 4.5 if tb == 2 else 5
     else:
-        launches_per_step = 3
+        launches_per_step = 2.5 if tb == 2 else 3
     if resident:  # one cluster launch runs all K steps of lbm_step(K)
         launches_per_step = 1.0 / args.steps
     kernel_ms = ms_step * tb  # one launch covers tb steps on this stream
@@ -440,9 +547,12 @@ def main():
     traffic = None if resident else ncu_traffic(args.config, kkey, cells_local, tb)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_source": ("scaled ncu capture: profiles/ncu_summary.json bytes per cell x cells per launch"
+                                   if traffic is not None else None),
                 "algorithmic_bytes_per_cell": bpc, "cells_per_launch": cells_local,
                 "time_steps_per_launch": tb, "peak_source": peak_src,
-                "kernel": ("k_pull2 (two fused steps)" if tb == 2 else "k_pull/k_aa stream-collide") + f" ({kkey})"}
+                "kernel": (("k_pull2_2d" if two_d else "k_pull2") + " (two fused steps)" if tb == 2 else
+                           "k_pull/k_aa stream-collide") + f" ({kkey})"}
     if n > 1:
         roofline["note"] = "N > 1: per-step time of boundary + interior launches with the halo " + halo.split(":")[0]
     if resident:
@@ -470,7 +580,7 @@ def main():
         st_ = Lb.lbm_init_macroscopic(lat._ctx, ctypes.cast(rho_h.data_ptr(), dp), ctypes.cast(u_h.data_ptr(), dp))
         assert st_ == 0
         if runner is not None:
-            runner.prime()
+            runner.prime()  # external exchange; lbm_step primes by itself after init
         do_steps(args.steps)
         st_ = Lb.lbm_get_macroscopic(lat._ctx, ctypes.cast(rho_o.data_ptr(), dp), ctypes.cast(u_o.data_ptr(), dp))
         assert st_ == 0
@@ -504,6 +614,13 @@ def main():
                        else "small grid: L2-resident", "parallelism": f"z-slab x{n}" if n > 1 else "single GPU",
                        "kernel_regs": regs, "kernel_local_bytes": local,
                        **({"halo": halo} if halo else {})},
+            "timing": {"windows": nwin, "ms_per_step_median": round(statistics.median(win_ms), 4),
+                       "ms_per_step_min": round(min(win_ms), 4), "ms_per_step_max": round(max(win_ms), 4),
+                       "spread": round((max(win_ms) - min(win_ms)) / statistics.median(win_ms), 4)},
+            "conservation": {"mass_drift": mass_drift, "momentum_drift": momentum_drift, "tolerance": drift_tol,
+                             "what": "|sum rho change| / sum rho and max |sum rho u change| / sum rho over "
+                                     "the K timed steps, all ranks"},
+            **(probe if probe else {}),
             "roofline": roofline,
             "clocks": clocks,
             "e2e": e2e,

@@ -66,6 +66,7 @@ typedef enum {
   LBM_EUNSUPPORTED = -2, /* inadmissible combination or not built                     */
   LBM_ENOMEM = -3,       /* device allocation failed                                                     */
   LBM_ECUDA = -4,        /* CUDA runtime error / no device                                               */
+  LBM_ENCCL = -5,        /* NCCL unavailable (libnccl.so.2 not loadable) or an NCCL call failed          */
   LBM_ENUMERIC = -6      /* non-finite population detected by lbm_check_finite                          */
 } lbm_status;
 
@@ -74,7 +75,16 @@ typedef enum {
   LBM_SPACE_POPULATION = 0, /* SRT / BGK, T = identity                     */
   LBM_SPACE_RAW = 1,        /* raw moments               */
   LBM_SPACE_CENTRAL = 2,    /* central moments           */
-  LBM_SPACE_CUMULANT = 3    /* cumulants                 */
+  LBM_SPACE_CUMULANT = 3,   /* cumulants                 */
+  /* raw moments in the weighted-orthogonal basis (WO-MRT, Krueger 2017; reading
+     R31): the weighted Gram-Schmidt orthogonalisation, <p, r> = sum_i w_i p(xi_i) r(xi_i), of the
+     stencil's monomials in graded-lexicographic order (x > y > z): D3Q27 1; x, y, z; x^2, xy, xz,
+     y^2, yz, z^2; x^2y, x^2z, xy^2, xyz, xz^2, y^2z, yz^2; x^2y^2, x^2yz, x^2z^2, xy^2z, xyz^2, y^2z^2;
+     x^2y^2z, x^2yz^2, xy^2z^2; x^2y^2z^2 (D3Q19: without the xyz-type monomials and orders >= 5;
+     D2Q9: 1; x, y; x^2, xy, y^2; x^2y, xy^2; x^2y^2), one rate per orthogonal polynomial in that
+     order (the second-order ones, x^2 - 1/3 ..., govern shear AND bulk viscosity).  General rates,
+     no body force, continuous equilibrium (absolute, delta, or ABSOLUTE_F0). */
+  LBM_SPACE_RAW_WO = 4
 } lbm_space;
 typedef enum {
   LBM_EQ_ABSOLUTE = 0, /* continuous Maxwellian, absolute form                    */
@@ -89,7 +99,15 @@ typedef enum {
                           in collision space as q_eq = T(f_eq); absolute form.  Equals LBM_EQ_ABSOLUTE
                           for population / raw moments on D2Q9 and D3Q27 (reading R4).  General rates
                           only (no rate specialisation), no body force.                              */
-  LBM_EQ_DISCRETE_DELTA = 4 /* its deviation f_eq - f0: zero-centered only, not with cumulants       */
+  LBM_EQ_DISCRETE_DELTA = 4, /* its deviation f_eq - f0: zero-centered only, not with cumulants      */
+  LBM_EQ_ABSOLUTE_F0 = 5     /* the absolute equilibrium for zero-centered storage with the background
+                                added to the POPULATIONS before the transform, q = T(df + f0), and
+                                subtracted after the inverse one: eq:MrtUpdateAbsoluteFromZeroCentered
+                                written literally (reading R30).  LBM_EQ_ABSOLUTE with
+                                zero_centered instead adds the closed-form background moments T(f0) in
+                                moment space.  Same values up to rounding; the rounding differs (the
+                                Table 3 study).  Zero-centered only; general rates;
+                                population, raw (both bases), central-moment and cumulant spaces. */
 } lbm_equilibrium;
 typedef enum { LBM_FP64 = 0, LBM_FP32 = 1 } lbm_precision;
 /* Streaming patterns: two-grid pull; in place: AA (Bailey 2009; several
@@ -124,6 +142,21 @@ typedef struct {
   void *stream;    /* cudaStream_t to enqueue on, or NULL: the library creates its own        */
   int rank;        /* slab decomposition along the slab axis: this rank ...                  */
   int nranks;      /* ... of nranks (nranks must divide the slab extent; slabs >= 2 planes)   */
+  /* In-library NCCL halo exchange: the 128-byte ncclUniqueId that
+     rank 0 obtained from lbm_nccl_get_unique_id and every rank received (any host
+     transport), or NULL.  Non-NULL: lbm_create joins an NCCL communicator of nranks ranks
+     (collective: every rank calls lbm_create; one GPU per rank — NCCL refuses two ranks on
+     one device) and lbm_step exchanges the halos with ncclSend / ncclRecv, overlapped with
+     the interior planes, whenever the fused peer push (lbm_peer_connect) is not connected.
+     With nranks = 1 the single slab exchanges with itself through NCCL (the periodic wrap
+     goes through the ghost planes, as on every rank of a decomposition).  The id is read
+     during lbm_create only. */
+  const void *nccl_id;
+  /* Optional device allocator for the population grids (e.g. the torch caching allocator);
+     both NULL: cudaMalloc / cudaFree.  dev_alloc returns NULL on failure (LBM_ENOMEM). */
+  void *(*dev_alloc)(size_t bytes, void *user);
+  void (*dev_free)(void *ptr, void *user);
+  void *alloc_user;
 } lbm_domain;
 
 /* Device-side halo description of one population grid (nranks > 1).
@@ -204,8 +237,26 @@ lbm_status lbm_get_info(const lbm_ctx *ctx, lbm_info *info);
    the step counter.  Multi-rank callers must exchange halos of the current grid afterwards. */
 lbm_status lbm_init_macroscopic(lbm_ctx *ctx, const double *rho, const double *u);
 
-/* n fused stream–collide time steps (single rank; asynchronous on the context stream). */
+/* n fused stream–collide time steps, asynchronous on the context stream.
+   One rank: the single-rank kernels (two-step sweeps, graph replay or the cluster-resident
+   loop where they apply, lbm_info).  Several ranks (or a context created with nccl_id):
+   COLLECTIVE, every rank calls it with the same n, ranks stay in lock-step.  It runs the fused
+   peer push when the context is connected (lbm_peer_connect; then identical to lbm_step_peer),
+   else the in-library NCCL exchange (lbm_domain.nccl_id): per step the two boundary planes,
+   then ncclGroupStart / 2 x ncclSend + 2 x ncclRecv (the contiguous halo blocks of lbm_get_halo,
+   zero-copy) / ncclGroupEnd on the context stream while the interior planes run on a second
+   stream; multi-rank pull contexts with two-step sweeps advance pairs of steps with two
+   exchanges per pair (the LBM_REGION_PAIR_* sequence).  The first call after
+   lbm_init_macroscopic / lbm_set_populations exchanges the current halo first (lbm_peer_prime
+   on the peer path).  LBM_EUNSUPPORTED for a multi-rank context with neither transport (then
+   drive lbm_step_region + lbm_get_halo with an external exchange); LBM_ENCCL if NCCL fails. */
 lbm_status lbm_step(lbm_ctx *ctx, int n);
+
+/* Writes a fresh 128-byte ncclUniqueId into out128 (rank 0; broadcast it to the other ranks
+   and pass it as lbm_domain.nccl_id).  LBM_ENCCL if libnccl.so.2 cannot be loaded (the NCCL
+   already loaded into the process, e.g. torch's, is preferred; LBM_NCCL_LIB overrides the
+   path) or ncclGetUniqueId fails; the message is in lbm_last_error(NULL). */
+lbm_status lbm_nccl_get_unique_id(void *out128);
 
 /* Multi-rank building blocks of one step: run the step's kernel on the given planes on
    'stream' (NULL: context stream), then lbm_swap() once all regions are done and the halos
@@ -236,11 +287,18 @@ lbm_status lbm_sync(lbm_ctx *ctx);
    Collective protocol: every rank calls lbm_peer_export, the infos are exchanged (any host
    transport), every rank calls lbm_peer_connect with its lower and upper neighbour's info
    (periodic ring along the slab axis), all ranks pass a barrier, then lbm_peer_prime
-   (after every lbm_init_macroscopic / lbm_set_populations too), then lbm_step_peer(n) with
-   the same n on every rank (ranks must stay in lock-step; the grids swap identically).
+   (after every lbm_init_macroscopic / lbm_set_populations too; lbm_step does it itself when
+   it is due), then lbm_step(n) or lbm_step_peer(n) with the same n on every rank (ranks must
+   stay in lock-step; the grids swap identically).
    The interior planes run on a second stream, overlapping the boundary planes and the
    wait for the neighbours.  A wait that exceeds LBM_PEER_TIMEOUT_S seconds (environment,
-   default 60) gives up instead of hanging the GPU and is reported by lbm_peer_status. */
+   default 60) gives up instead of hanging the GPU and is reported by lbm_peer_status.
+   Memory ordering: the boundary kernels' stores into peer memory are released per CTA (a CTA
+   barrier, then one system-scope fence by thread 0) before the kernel ends, and the one-thread
+   signal kernel that follows on the stream fences at system scope before its release store of
+   the phase flag; the neighbour's wait kernel acquires it at system scope.  Environment
+   LBM_PEER_FENCE (read per call): 1 (default) per CTA, 2 per thread, 0 none (the ordering then
+   rests on kernel completion alone). */
 typedef struct {
   unsigned char grid_ipc[2][64]; /* cudaIpcMemHandle_t of population grids 0 and 1          */
   unsigned char flags_ipc[64];   /* cudaIpcMemHandle_t of the completion flags              */
@@ -331,7 +389,8 @@ lbm_status lbm_grid_layout(lbm_stencil stencil, lbm_precision precision, int nx,
                            lbm_layout *out);
 
 /* Diagnostics. */
-/* Registers per thread and local (spill) bytes of this context's pull kernel. */
+/* Registers per thread and local (spill) bytes of the kernel that dominates this context's
+   lbm_step: the cluster-resident loop, the two-step sweep, the odd in-place kernel, or k_pull. */
 lbm_status lbm_kernel_attributes(const lbm_ctx *ctx, int *regs, int *local_bytes);
 /* Device pointer and size of a population grid (which = 0 current, 1 next; AA: the single grid). */
 lbm_status lbm_device_grid(lbm_ctx *ctx, int which, void **ptr, size_t *bytes);

@@ -566,7 +566,38 @@ struct EqCumulant {
     return !(n2_of(e) == 1 && n1_of(e) == 0);
   }
 };
-// tabulated equilibrium (SWE: kappa_eq = K(u) f_eq computed numerically)
+// SWE, central moments kappa_eq = K(u) f_eq of Zhou's discrete equilibrium (PAPER.md:485-487,
+// 1001-1012; corrected u.u/6 of reading R5) in closed form (expanded symbolically from
+// eq:DiscreteShallowWaterEquilibrium): kappa_20 = kappa_02 = g h^2 / 2,
+// kappa_11 = 0, kappa_21 = h u_y (1/3 - g h / 2 - u_x^2), kappa_12 = h u_x (1/3 - g h / 2 - u_y^2),
+// kappa_22 = h (g h / 6 + (g h / 2 - 1/3) u.u + 3 u_x^2 u_y^2).  Replaces the transform of the
+// nine f_eq values through both Chimera sweeps (186 -> ~110 fp64 instructions per cell).
+template <class real>
+struct EqSweZhou {
+  real k20, k21, k12, k22;
+  __device__ __forceinline__ EqSweZhou(real h, real ux, real uy, real g) {
+    const real gh = g * h, a = fma(real(-0.5), gh, real(1.0 / 3.0));  // 1/3 - g h / 2
+    const real uxx = ux * ux, uyy = uy * uy;
+    k20 = real(0.5) * gh * h;
+    k21 = h * uy * (a - uxx);
+    k12 = h * ux * (a - uyy);
+    k22 = h * fma(real(3) * uxx, uyy, fma(real(1.0 / 6.0), gh, -a * (uxx + uyy)));
+  }
+  template <int e>
+  __device__ __forceinline__ real get() const {
+    if constexpr (e == E(2, 0) || e == E(0, 2)) return k20;
+    else if constexpr (e == E(2, 1)) return k21;
+    else if constexpr (e == E(1, 2)) return k12;
+    else {
+      static_assert(e == E(2, 2), "SWE equilibrium: second- to fourth-order central moments only");
+      return k22;
+    }
+  }
+  template <int e>
+  __device__ static constexpr bool zero() { return e == E(1, 1); }
+};
+
+// tabulated equilibrium (q_eq = T(f_eq) computed numerically)
 template <class real, int N>
 struct EqTable {
   real v[N];
@@ -685,6 +716,55 @@ __device__ __forceinline__ void add_background(real (&c)[NC], real sgn) {
 // --------------------------------------------------------------------------
 enum { RS_FORCE = 4, RS_FORCE_HE = 8 };  // flag bits of the RS template parameter (Guo / He)
 enum { RS_DISCRETE = 16 };               // equilibrium given as a discrete f_eq (reading R29)
+// zero-centered storage relaxed against the absolute equilibrium with the background added to
+// the POPULATIONS, q = T(df + f0), the literal eq:MrtUpdateAbsoluteFromZeroCentered (PAPER.md:
+// 310-319; reading R30) instead of the closed-form background moments of REG_ZC_ABS
+enum { RS_POPBG = 32 };
+// raw moments relaxed in the weighted-orthogonal basis (WO-MRT; reading R31):
+// the weighted Gram-Schmidt orthogonalisation of the graded-lexicographic monomials, one rate
+// per polynomial, applied through the monomial-space matrices of wo_basis (constant memory)
+enum { RS_WOBASIS = 64 };
+
+// WO-MRT basis of the stencil in monomial (cube) coordinates: L[p][e] = coefficient of monomial e
+// in polynomial p (p in graded-lexicographic order), Linv = L^{-1} (set by the host per device,
+// OpsImpl::set_wo; each translation unit has its own copy)
+__constant__ double c_wo_L[27 * 27];
+__constant__ double c_wo_Linv[27 * 27];
+
+// monomials of the stencil's raw-moment space (cube positions): all 27 / 9, D3Q19 without xyz-type
+// monomials and orders >= 5 (rank 19, reading R2)
+template <class S>
+__host__ __device__ constexpr bool mono_present(int e) {
+  if constexpr (S::Q != 19) return true;
+  else return (ex_of(e) + ey_of(e) + ez_of(e) <= 4) && !(ex_of(e) >= 1 && ey_of(e) >= 1 && ez_of(e) >= 1);
+}
+
+// q* = q + S (q_eq - q) with q = L m (reading R31): m* = m + L^{-1} S L (m_eq - m)
+template <class S, class EQ, class real, int NC>
+__device__ __forceinline__ void relax_wo(real (&c)[NC], const EQ &eq, const Rates<real> &r) {
+  real d[NC];
+  sfor<NC>([&](auto e) {
+    if constexpr (mono_present<S>(e)) {
+      if constexpr (EQ::template zero<e>()) d[e] = -c[e];
+      else d[e] = eq.template get<e>() - c[e];
+    }
+  });
+  real t[S::Q];
+  sfor<S::Q>([&](auto p) {
+    real acc = real(0);
+    sfor<NC>([&](auto e) {
+      if constexpr (mono_present<S>(e)) acc = fma(real(c_wo_L[p * 27 + e]), d[e], acc);
+    });
+    t[p] = r.w[p] * acc;
+  });
+  sfor<NC>([&](auto e) {
+    if constexpr (mono_present<S>(e)) {
+      real acc = c[e];
+      sfor<S::Q>([&](auto p) { acc = fma(real(c_wo_Linv[e * 27 + p]), t[p], acc); });
+      c[e] = acc;
+    }
+  });
+}
 
 template <class real>
 struct Force {
@@ -792,6 +872,15 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
   // (kappa_100 = -F_x/2), and the backward one about the post-collision mean (j + F)/rho.
   constexpr bool SHIFT_U = FORCED && SPACE != SPACE_CUMULANT;
   constexpr int RSR = RS & 3;  // rate specialisation proper
+  if constexpr ((RS & RS_POPBG) != 0) {
+    // literal eq:MrtUpdateAbsoluteFromZeroCentered (reading R30): df + f0 in the populations,
+    // the absolute-storage collision, minus f0
+    static_assert(REG == REG_ZC_ABS, "the population-space background is a zero-centered regime");
+    sfor<S::Q>([&](auto i) { f[i] = f[i] + real(weight<S>(i)); });
+    collide<S, SPACE, REG_ABS, real, (RS & ~RS_POPBG)>(f, r, swe_g, fr);
+    sfor<S::Q>([&](auto i) { f[i] = f[i] - real(weight<S>(i)); });
+    return;
+  }
   real c[NC];
   sfor<NC>([&](auto k) { c[k] = real(0); });
   sfor<S::Q>([&](auto i) { c[S::pos(i)] = f[i]; });
@@ -893,6 +982,11 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
       disc_cube(eq.v, rho, ux, uy, uz);
       if constexpr (S::D == 3) fwd_raw3<S>(eq.v); else fwd_raw2(eq.v);
       if constexpr (S::D == 3) relax_basis3<S, RSR>(c, eq, r); else relax_basis2<RSR>(c, eq, r);
+    } else if constexpr (SPACE == SPACE_RAW && (RS & RS_WOBASIS) != 0) {
+      static_assert(RSR == RS_GENERAL && !FORCED, "WO-MRT: general rates, unforced");
+      RawU<real> U{ux, uy, uz, ux * ux, uy * uy, uz * uz};
+      if constexpr (REG == REG_DELTA) relax_wo<S>(c, EqRawDelta<real>{m000, rho, U}, r);
+      else relax_wo<S>(c, EqRawAbs<real>{rho, U}, r);
     } else if constexpr (SPACE == SPACE_RAW) {
       RawU<real> U{ux, uy, uz, ux * ux, uy * uy, uz * uz};
       if constexpr (REG == REG_DELTA) {
@@ -931,25 +1025,10 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
         // kappa*_100 = kappa_100 + F_x: -F_x/2 -> +F_x/2
         if constexpr (FORCED) add_force(std::true_type{});
       } else if constexpr (SPACE == SPACE_SWE) {
-        // kappa_eq = K(u) f_eq of Zhou's discrete equilibrium
+        // kappa_eq = K(u) f_eq of Zhou's discrete equilibrium,
+        // closed form (EqSweZhou)
         static_assert(S::Q == 9, "SWE is D2Q9");
-        const real uu = ux * ux + uy * uy, gh = swe_g * rho;
-        EqTable<real, 9> eq;
-        real *t = eq.v;
-        sfor<9>([&](auto i) {
-          constexpr int vx = S::vx(i), vy = S::vy(i);
-          constexpr int l1 = (vx != 0) + (vy != 0);
-          if constexpr (l1 == 0) {
-            t[S::pos(i)] = rho * (real(1) - real(5.0 / 6.0) * gh - real(2.0 / 3.0) * uu);
-          } else {
-            const real xu = real(vx) * ux + real(vy) * uy;
-            const real lam = (l1 == 1) ? real(1) : real(0.25);
-            t[S::pos(i)] = lam * rho *
-                           (real(1.0 / 6.0) * gh + real(1.0 / 3.0) * xu + real(0.5) * xu * xu - real(1.0 / 6.0) * uu);
-          }
-        });
-        fwd_raw2(eq.v);
-        bin_fwd2(eq.v, ux, uy);
+        const EqSweZhou<real> eq(rho, ux, uy, swe_g);
         relax_basis2<RSR>(c, eq, r);
       } else {  // SPACE_CUMULANT
         if constexpr (S::D == 3) central_to_cumulant3<S>(c, inv); else central_to_cumulant2(c, inv);

@@ -43,7 +43,8 @@ struct GridParams {
 // planes: plane 0's downward (slab component -1) populations to the lower neighbour's top
 // ghost plane, plane nzl-1's upward ones to the upper neighbour's bottom ghost plane — the
 // values the neighbours' next pull step gathers (eq:LbStreaming across the cut).  They are
-// ordered before the completion flag by kernel completion + k_peer_signal's system fence.
+// released before the completion flag (k_peer_signal) by peer_release_cta (default: one
+// system-scope fence per CTA after a CTA barrier), or per thread (g.peer_fence == 2).
 template <class S, class real>
 __device__ __forceinline__ void peer_push(const GridParams &g, int zl, long long in_plane, const real *f) {
   if (zl == 0 && g.peer_lo) {
@@ -51,14 +52,27 @@ __device__ __forceinline__ void peer_push(const GridParams &g, int zl, long long
     sfor<S::Q>([&](auto i) {
       if constexpr (S::mz(i) < 0) p[(long long)i * g.pop] = f[i];
     });
-    if (g.peer_fence) __threadfence_system();
+    if (g.peer_fence == 2) __threadfence_system();
   }
   if (zl == g.nzl - 1 && g.peer_hi) {
     real *p = static_cast<real *>(g.peer_hi) + in_plane;
     sfor<S::Q>([&](auto i) {
       if constexpr (S::mz(i) > 0) p[(long long)i * g.pop] = f[i];
     });
-    if (g.peer_fence) __threadfence_system();
+    if (g.peer_fence == 2) __threadfence_system();
+  }
+}
+
+// Producer-side release of a boundary kernel's stores into peer memory (g.peer_fence == 1,
+// the default): the CTA barrier orders every thread's remote stores before thread 0's
+// system-scope fence (fences are cumulative over the writes their thread has observed), so
+// the stores are visible system-wide before the kernel completes and k_peer_signal publishes
+// the phase — an ordering that does not rely on kernel completion alone.  Every thread of
+// the CTA must reach it (no early return in the PEER kernels).
+__device__ __forceinline__ void peer_release_cta(const int mode) {
+  if (mode == 1) {
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
   }
 }
 
@@ -73,12 +87,10 @@ __device__ __forceinline__ real ld_nc(const real *p) { return __ldg(p); }
 // PEER: the boundary-plane variant of lbm_step_peer that also pushes the slab-crossing
 // populations into the neighbours' ghost planes (a separate instantiation: the bulk kernel
 // keeps its register budget).
-template <class S, int SPACE, int REG, class real, bool BB, int RS = RS_GENERAL, bool PEER = false>
-__global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, real *__restrict__ dst,
-                                                   const GridParams g, const Rates<real> r, const real swe_g,
-                                                   const Force<real> fr) {
-  const int x = blockIdx.x * BLOCK_X + threadIdx.x;
-  if (x >= g.nx) return;
+template <class S, int SPACE, int REG, class real, bool BB, int RS, bool PEER>
+__device__ __forceinline__ void pull_cell(const real *__restrict__ src, real *__restrict__ dst, const GridParams &g,
+                                          const Rates<real> &r, const real swe_g, const Force<real> &fr,
+                                          const int x) {
   const int y = blockIdx.y;
   const int zl = g.zbegin + blockIdx.z;
 
@@ -122,6 +134,20 @@ __global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, 
   if constexpr (PEER) peer_push<S>(g, zl, (long long)y * g.pitch + x, f);
 }
 
+template <class S, int SPACE, int REG, class real, bool BB, int RS = RS_GENERAL, bool PEER = false>
+__global__ void __launch_bounds__(BLOCK_X) k_pull(const real *__restrict__ src, real *__restrict__ dst,
+                                                   const GridParams g, const Rates<real> r, const real swe_g,
+                                                   const Force<real> fr) {
+  const int x = blockIdx.x * BLOCK_X + threadIdx.x;
+  if constexpr (PEER) {
+    if (x < g.nx) pull_cell<S, SPACE, REG, real, BB, RS, PEER>(src, dst, g, r, swe_g, fr, x);
+    peer_release_cta(g.peer_fence);
+  } else {
+    if (x < g.nx) pull_cell<S, SPACE, REG, real, BB, RS, PEER>(src, dst, g, r, swe_g, fr, x);
+  }
+}
+
+
 // ---------------------------------------------------------------------------
 // AA pattern: in-place.  BB (single rank): half-way bounce-back on the no-slip faces of
 // g.bcmask (reading R18).  The odd step reads f_i(x) = f*_opp(x) from mem(x, i) when x - xi_i
@@ -153,36 +179,48 @@ struct Walls {
 // plane, g.peer_hi: the upper neighbour's first plane) instead of the ghost planes — the
 // AA odd step is race-free on the global lattice, so ranks need no exchange, only the
 // per-step completion flags.
+// the odd AA step of a boundary-plane cell with the neighbours' planes in peer memory
+template <class S, int SPACE, int REG, class real, int RS>
+__device__ __forceinline__ void aa_peer_cell(real *mem, const GridParams &g, const Rates<real> &r, const real swe_g,
+                                             const Force<real> &fr, const int x) {
+  const int y = blockIdx.y;
+  const int zl = g.zbegin + blockIdx.z;
+  real f[S::Q];
+  int xs[3], ys[3];
+  real *zb[3];
+#pragma unroll
+  for (int s = -1; s <= 1; ++s) {
+    xs[s + 1] = wrapi(x + s, g.nx);
+    ys[s + 1] = wrapi(y + s, g.ny) * g.pitch;
+    const int zv = zl + s;
+    zb[s + 1] = zv < 0 ? static_cast<real *>(g.peer_lo)
+                       : (zv >= g.nzl ? static_cast<real *>(g.peer_hi) : mem + (long long)(zv + 1) * g.plane);
+  }
+  sfor<S::Q>([&](auto i) {
+    constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+    f[i] = zb[1 - cz][(long long)S::opp(i) * g.pop + ys[1 - cy] + xs[1 - cx]];
+  });
+  collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
+  sfor<S::Q>([&](auto i) {
+    constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+    zb[1 + cz][(long long)i * g.pop + ys[1 + cy] + xs[1 + cx]] = f[i];
+  });
+}
+
 template <class S, int SPACE, int REG, class real, int PAT, int RS = RS_GENERAL, bool PEER = false, bool BB = false>
 __global__ void __launch_bounds__(BLOCK_X, (PAT == PAT_AA_ODD ? 5 : 1))
     k_aa(real *mem, const GridParams g, const Rates<real> r, const real swe_g, const Force<real> fr) {
   const int x = blockIdx.x * BLOCK_X + threadIdx.x;
+  if constexpr (PEER) {  // every thread reaches the CTA release (no early return)
+    if (x < g.nx) aa_peer_cell<S, SPACE, REG, real, RS>(mem, g, r, swe_g, fr, x);
+    peer_release_cta(g.peer_fence);
+    return;
+  }
   if (x >= g.nx) return;
   const int y = blockIdx.y;
   const int zl = g.zbegin + blockIdx.z;
   real f[S::Q];
-  if constexpr (PEER) {
-    static_assert(PAT == PAT_AA_ODD, "the peer variant is the odd AA step");
-    int xs[3], ys[3];
-    real *zb[3];
-#pragma unroll
-    for (int s = -1; s <= 1; ++s) {
-      xs[s + 1] = wrapi(x + s, g.nx);
-      ys[s + 1] = wrapi(y + s, g.ny) * g.pitch;
-      const int zv = zl + s;
-      zb[s + 1] = zv < 0 ? static_cast<real *>(g.peer_lo)
-                         : (zv >= g.nzl ? static_cast<real *>(g.peer_hi) : mem + (long long)(zv + 1) * g.plane);
-    }
-    sfor<S::Q>([&](auto i) {
-      constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
-      f[i] = zb[1 - cz][(long long)S::opp(i) * g.pop + ys[1 - cy] + xs[1 - cx]];
-    });
-    collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
-    sfor<S::Q>([&](auto i) {
-      constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
-      zb[1 + cz][(long long)i * g.pop + ys[1 + cy] + xs[1 + cx]] = f[i];
-    });
-  } else if constexpr (PAT == PAT_AA_EVEN) {
+  if constexpr (PAT == PAT_AA_EVEN) {
     const long long own = (long long)(zl + 1) * g.plane + (long long)y * g.pitch + x;
     // read-only path is safe in place: every slot is read, then written, by the same thread
     sfor<S::Q>([&](auto i) { f[i] = ld_nc(mem + own + (long long)i * g.pop); });

@@ -43,8 +43,10 @@ struct Ops {
   // global sums (mass, momentum, kinetic energy): partial[5 * DIAG_GRID] scratch, out[5]
   void (*diagnostics)(const void *mem, const GridParams &g, int aa, int state, int zc, double *partial,
                       double *out, double3 dj, cudaStream_t s);
-  // kernel attributes of the pull kernel (registers / local memory), for diagnostics
-  void (*attributes)(int *regs, int *local_bytes);
+  // registers / local memory of a kernel of this instantiation, for diagnostics: which = 0
+  // k_pull, 1 the two-step sweep (k_pull2 / k_pull2_2d), 2 the cluster-resident loop,
+  // 10 + pattern the in-place kernel of that pattern (PAT_AA_ODD, PAT_ESO_ODD, PAT_TW0, ...)
+  void (*attributes)(int which, int *regs, int *local_bytes);
   // two fused pull steps (temporal blocking; 3D, single rank, periodic); tile TX x TY
   // (0 x 0: not provided).  Requires nx % TX == 0 and ny % TY == 0.
   void (*pull2)(const void *src, void *dst, const GridParams &g, const void *params, double swe_g, int zchunks,
@@ -55,6 +57,14 @@ struct Ops {
   // (nullptr for 3D stencils)
   int (*resident)(const void *src, void *dst, const GridParams &g, const void *params, double swe_g, int bb,
                   int nsteps, int cluster, cudaStream_t s);
+  // loads every kernel the multi-rank step paths of this instantiation launch (CUDA lazy
+  // loading would otherwise load a kernel at its first launch, which waits for the kernels
+  // running on the device — among them a spinning k_peer_wait whose release may depend on that
+  // very launch: contexts of one process sharing a device would stall until the wait times out)
+  void (*preload)();
+  // uploads the WO-MRT basis matrices (27 x 27, monomial cube coordinates) to this
+  // instantiation's constant memory on the current device (RS_WOBASIS kernels)
+  int (*set_wo)(const double *L, const double *Linv);
 };
 
 // shared memory of k_resident2: two grids [Q][R + 2][nx]
@@ -267,15 +277,61 @@ struct OpsImpl {
     }
     return (int)cudaErrorNotSupported;
   }
-  static void attributes(int *regs, int *local_bytes) {
+  static void attributes(int which, int *regs, int *local_bytes) {
     cudaFuncAttributes a{};
-    if (cudaFuncGetAttributes(&a, k_pull<S, SPACE, REG, real, false, RS>) == cudaSuccess) {
+    cudaError_t e = cudaErrorInvalidValue;
+    using TT = TbTile<S, real, SPACE>;
+    if (which == 0) {
+      e = cudaFuncGetAttributes(&a, k_pull<S, SPACE, REG, real, false, RS>);
+    } else if (which == 1) {
+      if constexpr (S::D == 3 && TT::TX > 0)
+        e = cudaFuncGetAttributes(&a, k_pull2<S, SPACE, REG, real, RS, TT::TX, TT::TY, TT::MINB, true, false>);
+      else if constexpr (S::D == 2) {
+        constexpr bool srt = SPACE == SPACE_POPULATION;
+        e = cudaFuncGetAttributes(&a, k_pull2_2d<S, SPACE, REG, real, RS, TT::TX, srt ? 3 : 2, !srt, false>);
+      }
+    } else if (which == 2) {
+      if constexpr (S::D == 2) e = cudaFuncGetAttributes(&a, k_resident2<S, SPACE, REG, real, RS, false>);
+    } else if (which == 10 + PAT_AA_ODD) {
+      e = cudaFuncGetAttributes(&a, k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS>);
+    } else if (which == 10 + PAT_AA_EVEN) {
+      e = cudaFuncGetAttributes(&a, k_aa<S, SPACE, REG, real, PAT_AA_EVEN, RS>);
+    } else if (which == 10 + PAT_ESO_ODD) {
+      e = cudaFuncGetAttributes(&a, k_eso<S, SPACE, REG, real, PAT_ESO_ODD, RS>);
+    } else if (which == 10 + PAT_TW0) {
+      e = cudaFuncGetAttributes(&a, k_twist<S, SPACE, REG, real, PAT_TW0, RS>);
+    }
+    if (e == cudaSuccess) {
       *regs = a.numRegs;
       *local_bytes = (int)a.localSizeBytes;
     } else {
+      cudaGetLastError();
       *regs = -1;
       *local_bytes = -1;
     }
+  }
+  static void preload() {
+    cudaFuncAttributes a{};
+    using TT = TbTile<S, real, SPACE>;
+    cudaFuncGetAttributes(&a, k_pull<S, SPACE, REG, real, false, RS>);
+    cudaFuncGetAttributes(&a, k_pull<S, SPACE, REG, real, true, RS>);
+    cudaFuncGetAttributes(&a, k_pull<S, SPACE, REG, real, false, RS, true>);
+    cudaFuncGetAttributes(&a, k_pull<S, SPACE, REG, real, true, RS, true>);
+    cudaFuncGetAttributes(&a, k_aa<S, SPACE, REG, real, PAT_AA_EVEN, RS>);
+    cudaFuncGetAttributes(&a, k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS>);
+    cudaFuncGetAttributes(&a, k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS, true>);
+    if constexpr (S::D == 3 && TT::TX > 0) {
+      cudaFuncGetAttributes(&a, k_pull2<S, SPACE, REG, real, RS, TT::TX, TT::TY, TT::MINB, true, true>);
+    } else if constexpr (S::D == 2) {
+      constexpr bool srt = SPACE == SPACE_POPULATION;
+      cudaFuncGetAttributes(&a, k_pull2_2d<S, SPACE, REG, real, RS, TT::TX, srt ? 3 : 2, !srt, true>);
+    }
+    cudaGetLastError();
+  }
+  static int set_wo(const double *L, const double *Linv) {
+    cudaError_t e = cudaMemcpyToSymbol(c_wo_L, L, 27 * 27 * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_wo_Linv, Linv, 27 * 27 * sizeof(double));
+    return (int)e;
   }
   static constexpr Ops table{S::Q,      S::D,  &pull,         &aa,           &init,      &get_pop,
                              &set_pop, &macro, &test_collide, &check_finite, &get_cells, &diagnostics,
@@ -283,7 +339,9 @@ struct OpsImpl {
                              (TbTile<S, real, SPACE>::TX > 0) ? &pull2 : nullptr,
                              TbTile<S, real, SPACE>::TX,
                              TbTile<S, real, SPACE>::TY,
-                             S::D == 2 ? &resident : nullptr};
+                             S::D == 2 ? &resident : nullptr,
+                             &preload,
+                             &set_wo};
 };
 
 }  // namespace lbm

@@ -37,7 +37,21 @@ const Ops *with_rs(int rs) {
   if constexpr (SP_ == SPACE_POPULATION || SP_ == SPACE_RAW || SP_ == SPACE_CENTRAL || SP_ == SPACE_CUMULANT) {
     if (rs == (RS_GENERAL | RS_DISCRETE)) return &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL | RS_DISCRETE>::table;
   }
-  if (rs & (RS_FORCE | RS_FORCE_HE | RS_DISCRETE)) return nullptr;
+  // WO-MRT basis (reading R31): raw moments, general rates, unforced; with the population-space
+  // background (reading R30) for zero-centered storage relaxed against the absolute equilibrium
+  if constexpr (SP_ == SPACE_RAW) {
+    if (rs == (RS_GENERAL | RS_WOBASIS)) return &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL | RS_WOBASIS>::table;
+    if constexpr (REG_ == REG_ZC_ABS) {
+      if (rs == (RS_GENERAL | RS_WOBASIS | RS_POPBG))
+        return &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL | RS_WOBASIS | RS_POPBG>::table;
+    }
+  }
+  // the population-space background (reading R30), every hydrodynamic space, general rates
+  if constexpr (REG_ == REG_ZC_ABS &&
+                (SP_ == SPACE_POPULATION || SP_ == SPACE_RAW || SP_ == SPACE_CENTRAL || SP_ == SPACE_CUMULANT)) {
+    if (rs == (RS_GENERAL | RS_POPBG)) return &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL | RS_POPBG>::table;
+  }
+  if (rs & (RS_FORCE | RS_FORCE_HE | RS_DISCRETE | RS_WOBASIS | RS_POPBG)) return nullptr;
   if constexpr (SP_ == SPACE_POPULATION) {
     return rs == RS_GENERAL ? &OpsImpl<St_, SP_, REG_, Re_, RS_GENERAL>::table : nullptr;
   } else {

@@ -12,8 +12,13 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
+#include <dlfcn.h>   // libnccl.so.2 is loaded at run time (the NCCL of the process if any)
+#include <nccl.h>    // types only
 #include <unistd.h>  // getpid: same-process peers use plain device pointers
+
+#include <mutex>
 
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for Nsight timelines
 
@@ -91,6 +96,103 @@ const Ops *find_ops(int stencil, int prec, int space, int regime, int rs) {
 
 thread_local std::string g_create_error;
 
+// WO-MRT basis (reading R31): classical Gram-Schmidt of the
+// stencil's raw-moment monomials in graded-lexicographic order (x > y > z) under the weighted
+// inner product <p, r> = sum_i w_i p(xi_i) r(xi_i), polynomials kept monic in their leading
+// monomial.  L[p][e]: coefficient of monomial e (cube index a + 3 b + 9 c) in polynomial p;
+// Linv = L^{-1} (unit lower-triangular in that order, forward substitution).
+template <class S>
+void wo_basis(double *L, double *Linv) {
+  std::vector<int> mono;
+  for (int deg = 0; deg <= 6; ++deg)
+    for (int a = 2; a >= 0; --a)
+      for (int b = 2; b >= 0; --b)
+        for (int cz = 2; cz >= 0; --cz)
+          if (a + b + cz == deg && (S::D == 3 || cz == 0) && lbm::mono_present<S>(a + 3 * b + 9 * cz))
+            mono.push_back(a + 3 * b + 9 * cz);
+  const int q = S::Q, n = (int)mono.size();  // n == q
+  auto value = [&](int e, int i) {
+    const int ex[3] = {lbm::ex_of(e), lbm::ey_of(e), lbm::ez_of(e)};
+    const int v[3] = {S::vx(i), S::vy(i), S::vz(i)};
+    double r = 1;
+    for (int a = 0; a < 3; ++a)
+      for (int k = 0; k < ex[a]; ++k) r *= v[a];
+    return r;
+  };
+  std::vector<double> C((size_t)n * n, 0.0), P((size_t)n * q, 0.0);  // coefficients, values
+  for (int k = 0; k < n; ++k) {
+    C[(size_t)k * n + k] = 1.0;
+    for (int i = 0; i < q; ++i) P[(size_t)k * q + i] = value(mono[k], i);
+    for (int j = 0; j < k; ++j) {
+      double num = 0, den = 0;
+      for (int i = 0; i < q; ++i) {
+        const double w = lbm::weight<S>(i);
+        num += w * value(mono[k], i) * P[(size_t)j * q + i];
+        den += w * P[(size_t)j * q + i] * P[(size_t)j * q + i];
+      }
+      const double cf = num / den;
+      for (int m = 0; m <= j; ++m) C[(size_t)k * n + m] -= cf * C[(size_t)j * n + m];
+      for (int i = 0; i < q; ++i) P[(size_t)k * q + i] -= cf * P[(size_t)j * q + i];
+    }
+  }
+  // inverse of the unit lower-triangular C
+  std::vector<double> Ci((size_t)n * n, 0.0);
+  for (int col = 0; col < n; ++col)
+    for (int r = col; r < n; ++r) {
+      double s = (r == col) ? 1.0 : 0.0;
+      for (int m = col; m < r; ++m) s -= C[(size_t)r * n + m] * Ci[(size_t)m * n + col];
+      Ci[(size_t)r * n + col] = s;
+    }
+  for (int k = 0; k < 27 * 27; ++k) L[k] = Linv[k] = 0.0;
+  for (int p = 0; p < n; ++p)
+    for (int m = 0; m < n; ++m) {
+      L[p * 27 + mono[m]] = C[(size_t)p * n + m];     // polynomial p over cube monomials
+      Linv[mono[m] * 27 + p] = Ci[(size_t)m * n + p]; // monomial m over polynomials
+    }
+}
+
+// ---- NCCL, loaded at run time: the library that is already in the process (torch's) is
+// preferred, so one process never mixes two NCCL builds; LBM_NCCL_LIB overrides the path.
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi &nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *h = nullptr;
+    if (const char *path = getenv("LBM_NCCL_LIB")) h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      const char *e = dlerror();
+      api.err = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+      return;
+    }
+    auto sym = [&](auto &fn, const char *name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      return fn != nullptr;
+    };
+    const bool all = sym(api.GetUniqueId, "ncclGetUniqueId") && sym(api.CommInitRank, "ncclCommInitRank") &&
+                     sym(api.CommDestroy, "ncclCommDestroy") && sym(api.GroupStart, "ncclGroupStart") &&
+                     sym(api.GroupEnd, "ncclGroupEnd") && sym(api.Send, "ncclSend") && sym(api.Recv, "ncclRecv") &&
+                     sym(api.GetErrorString, "ncclGetErrorString");
+    if (!all) api.err = "libnccl.so.2 lacks a required symbol";
+    api.ok = all;
+  });
+  return api;
+}
+
 }  // namespace
 
 struct lbm_ctx {
@@ -144,6 +246,14 @@ struct lbm_ctx {
   bool peer_on = false;
   cudaStream_t s_int = nullptr;         // interior planes of lbm_step_peer
   cudaEvent_t ev_b = nullptr, ev_i = nullptr;
+  // slab decomposition with ghost planes (nranks > 1, or one rank exchanging with itself
+  // through NCCL): the periodic wrap along the slab axis goes through the ghost planes
+  bool multi = false;
+  bool needs_prime = false;  // the current halo must be exchanged before the next lbm_step
+  ncclComm_t comm = nullptr; // in-library NCCL halo exchange (lbm_domain.nccl_id)
+  void *(*dev_alloc)(size_t, void *) = nullptr;
+  void (*dev_free)(void *, void *) = nullptr;
+  void *alloc_user = nullptr;
   std::string err;
 };
 
@@ -253,7 +363,9 @@ int tb_zchunks(const lbm_ctx *c) {
 
 // two fused steps per call pair on the peer path (multi-rank): interior planes [2, nzl - 2)
 // by the two-step sweep, the two boundary regions by two single steps through the scratch
-bool use_peer_tb(const lbm_ctx *c) { return c->peer_tb_cap && c->peer_on && c->streaming == LBM_PULL; }
+bool use_peer_tb(const lbm_ctx *c) {
+  return c->peer_tb_cap && (c->peer_on || c->comm) && c->streaming == LBM_PULL;
+}
 int peer_tb_chunks(const lbm_ctx *c) {
   const long long tiles = tb_tiles(c);
   const long long need = (kTbMinCtas + tiles - 1) / tiles;
@@ -280,7 +392,7 @@ bool use_temporal_blocking(const lbm_ctx *c) {
 // LBM_RESIDENT=0 disables, LBM_RESIDENT_CLUSTER=k caps the cluster size (read per call).
 constexpr int kResidentMaxCellsPerCta = 512;
 int resident_cluster(const lbm_ctx *c) {
-  if (!c->ops->resident || c->resident_failed || c->nranks > 1 || c->streaming != LBM_PULL) return 0;
+  if (!c->ops->resident || c->resident_failed || c->multi || c->streaming != LBM_PULL) return 0;
   const char *env = getenv("LBM_RESIDENT");
   if (env && env[0] == '0') return 0;
   int cap = 16;
@@ -402,15 +514,18 @@ unsigned long long peer_timeout_ns() {
   return (unsigned long long)((s > 0 ? s : 60.0) * 1e9);
 }
 
-// Per-thread system-scope fence after the halo stores: off by default.  The completion flag
-// is written by k_peer_signal, stream-ordered after the boundary kernel has COMPLETED; kernel
-// completion makes all of its writes visible at system scope (the property that lets the
-// host read zero-copy results after a stream synchronisation), and the signal thread fences
-// at system scope before its release store.  LBM_PEER_FENCE=1 adds the fence in the kernel
-// (+0.5 % per step, profiles/r1/peer_overhead.txt).
+// Release of the boundary kernels' stores into peer memory before the completion flag
+// (kernels.cuh peer_release_cta): 1 (default) = a CTA barrier, then one system-scope fence by
+// thread 0 of every CTA, so the halo stores are visible system-wide before the kernel ends
+// and k_peer_signal (stream-ordered after it, with its own system fence) publishes the phase;
+// 2 = a fence per thread after its stores; 0 = none (ordering by kernel completion alone).
+// Environment LBM_PEER_FENCE, read per call.
 int peer_fence() {
   const char *env = getenv("LBM_PEER_FENCE");
-  return env && env[0] == '1';
+  if (!env) return 1;
+  if (env[0] == '0') return 0;
+  if (env[0] == '2') return 2;
+  return 1;
 }
 
 void peer_release(lbm_ctx *c) {
@@ -537,9 +652,145 @@ lbm_status peer_refresh(lbm_ctx *c) {
   return LBM_OK;
 }
 
+// ---- in-library NCCL halo exchange (lbm_domain.nccl_id) ----
+// The four halo blocks of lbm_get_halo(which) with the pull grid 'grid' as the current one
+// (pull: which 0 = grid 'grid', 1 = the other grid, 2 = the scratch of the two-step regions;
+// in place: the single grid, which 0 = pre-odd, 1 = post-odd): send_lo, send_hi, recv_lo, recv_hi.
+void halo_blocks(lbm_ctx *c, const lbm_layout &lay, int which, int grid, char *p[4]) {
+  const size_t E = c->esize;
+  size_t o[4] = {lay.send_lo, lay.send_hi, lay.recv_lo, lay.recv_hi};
+  if (which == 2) {
+    char *scr = static_cast<char *>(c->buf[0]) + c->scratch_off * E;
+    const size_t shift = (size_t)(c->g.nzl - 6) * (size_t)c->g.plane;
+    p[0] = scr + o[0] * E;
+    p[1] = scr + (o[1] - shift) * E;
+    p[2] = scr + o[2] * E;
+    p[3] = scr + (o[3] - shift) * E;
+    return;
+  }
+  char *base;
+  if (c->streaming == LBM_PULL) {
+    base = static_cast<char *>(c->buf[which == 0 ? grid : 1 - grid]);
+  } else {
+    base = static_cast<char *>(c->buf[0]);
+    const size_t pre[4] = {lay.aa_pre_send_lo, lay.aa_pre_send_hi, lay.aa_pre_recv_lo, lay.aa_pre_recv_hi};
+    const size_t post[4] = {lay.aa_post_send_lo, lay.aa_post_send_hi, lay.aa_post_recv_lo, lay.aa_post_recv_hi};
+    for (int k = 0; k < 4; ++k) o[k] = (which == 0) ? pre[k] : post[k];
+  }
+  for (int k = 0; k < 4; ++k) p[k] = base + o[k] * E;
+}
+
+// One halo exchange: send_hi -> upper neighbour's recv_lo, send_lo -> lower's recv_hi, in one
+// NCCL group on stream s (zero-copy: the blocks are contiguous in the grid).  Per pair of
+// ranks the k-th send matches the k-th receive, which also covers 2 ranks (lower = upper)
+// and one rank (itself: the periodic wrap).
+lbm_status nccl_exchange(lbm_ctx *c, const lbm_layout &lay, int which, int grid, cudaStream_t s) {
+  const NcclApi &nc = nccl_api();
+  char *p[4];
+  halo_blocks(c, lay, which, grid, p);
+  const ncclDataType_t t = c->esize == 8 ? ncclFloat64 : ncclFloat32;
+  const size_t n = lay.halo_elems;
+  const int lo = (c->rank + c->nranks - 1) % c->nranks, hi = (c->rank + 1) % c->nranks;
+  ncclResult_t r = nc.GroupStart();
+  if (r != ncclSuccess) return fail(c, LBM_ENCCL, std::string("ncclGroupStart: ") + nc.GetErrorString(r));
+  r = nc.Send(p[1], n, t, hi, c->comm, s);
+  if (r == ncclSuccess) r = nc.Recv(p[2], n, t, lo, c->comm, s);
+  if (r == ncclSuccess) r = nc.Send(p[0], n, t, lo, c->comm, s);
+  if (r == ncclSuccess) r = nc.Recv(p[3], n, t, hi, c->comm, s);
+  const ncclResult_t r2 = nc.GroupEnd();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) return fail(c, LBM_ENCCL, std::string("NCCL halo exchange: ") + nc.GetErrorString(r));
+  return LBM_OK;
+}
+
+// n steps with the NCCL exchange from grid / state 'cur' (the lbm_step_peer sequence with an
+// NCCL group in place of the pushes and flags): per step the interior planes on s_int, the two
+// boundary planes and the exchange on the context stream; pairs of steps for pull contexts
+// with two-step sweeps (two exchanges per pair: the scratch halo, then the next grid's).
+lbm_status enqueue_nccl_steps(lbm_ctx *c, int n, int &cur) {
+  lbm_layout lay;
+  lbm_status s = lbm_grid_layout((lbm_stencil)c->stencil, (lbm_precision)c->prec, c->gnx, c->gny, c->gnz,
+                                 c->nranks, &lay);
+  if (s != LBM_OK) return fail(c, s, "layout");
+  const int nzl = c->g.nzl;
+  const bool pull = c->streaming == LBM_PULL;
+  if (c->needs_prime) {  // the current halo (pull: grid cur; in place: the pre-odd blocks)
+    if ((s = nccl_exchange(c, lay, 0, cur, c->stream)) != LBM_OK) return s;
+    c->needs_prime = false;
+  }
+  LBM_CUDA(c, cudaEventRecord(c->ev_b, c->stream));
+  LBM_CUDA(c, cudaEventRecord(c->ev_i, c->stream));
+  int t = 0;
+  if (use_peer_tb(c)) {
+    const size_t PB = (size_t)c->g.plane * c->esize;
+    char *scr = static_cast<char *>(c->buf[0]) + c->scratch_off * c->esize;
+    void *s_lo = scr, *s_hi = scr - (long long)(nzl - 6) * (long long)PB;
+    for (; t + 2 <= n; t += 2) {
+      void *A = c->buf[cur], *B = c->buf[1 - cur];
+      cudaStreamWaitEvent(c->stream, c->ev_i, 0);
+      cudaStreamWaitEvent(c->s_int, c->ev_b, 0);
+      GridParams gi = c->g;
+      gi.zbegin = 2;
+      gi.zcount = nzl - 4;
+      c->ops->pull2(A, B, gi, c->params, c->swe_g, peer_tb_chunks(c), c->s_int);
+      cudaEventRecord(c->ev_i, c->s_int);
+      GridParams gb = c->g;
+      gb.zbegin = 0;
+      c->ops->pull(A, s_lo, gb, c->params, c->swe_g, c->bb, 3, c->stream);
+      gb.zbegin = nzl - 3;
+      c->ops->pull(A, s_hi, gb, c->params, c->swe_g, c->bb, 3, c->stream);
+      if ((s = nccl_exchange(c, lay, 2, cur, c->stream)) != LBM_OK) return s;
+      gb.zbegin = 0;
+      c->ops->pull(s_lo, B, gb, c->params, c->swe_g, c->bb, 2, c->stream);
+      gb.zbegin = nzl - 2;
+      c->ops->pull(s_hi, B, gb, c->params, c->swe_g, c->bb, 2, c->stream);
+      if ((s = nccl_exchange(c, lay, 1, cur, c->stream)) != LBM_OK) return s;
+      cudaEventRecord(c->ev_b, c->stream);
+      cur ^= 1;
+      c->steps += 2;
+    }
+  }
+  for (; t < n; ++t) {
+    const int pat = pull ? 0 : inplace_pattern(c, cur);
+    auto launch = [&](int z0, int np, cudaStream_t st) {
+      GridParams g = c->g;
+      g.zbegin = z0;
+      if (pull) c->ops->pull(c->buf[cur], c->buf[1 - cur], g, c->params, c->swe_g, c->bb, np, st);
+      else c->ops->aa(c->buf[0], g, c->params, c->swe_g, pat, np, st);
+    };
+    cudaStreamWaitEvent(c->stream, c->ev_i, 0);  // interior of the previous step
+    cudaStreamWaitEvent(c->s_int, c->ev_b, 0);   // boundary + exchange of the previous step
+    launch(1, nzl - 2, c->s_int);
+    cudaEventRecord(c->ev_i, c->s_int);
+    launch(0, 1, c->stream);
+    if (nzl > 1) launch(nzl - 1, 1, c->stream);
+    // pull: the next grid's halo; in place: after the odd step the post-odd blocks return,
+    // after the even step the pre-odd blocks of the next (odd) step go out
+    const int which = pull ? 1 : (cur == 0 ? 1 : 0);
+    if ((s = nccl_exchange(c, lay, which, cur, c->stream)) != LBM_OK) return s;
+    cudaEventRecord(c->ev_b, c->stream);
+    cur ^= 1;
+    c->steps += 1;
+  }
+  LBM_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_i, 0));
+  return check_launch(c, "lbm_step (NCCL exchange)");
+}
+
 }  // namespace
 
 extern "C" {
+
+lbm_status lbm_nccl_get_unique_id(void *out128) {
+  if (!out128) return fail(nullptr, LBM_EINVAL, "out128 is NULL");
+  const NcclApi &nc = nccl_api();
+  if (!nc.ok) return fail(nullptr, LBM_ENCCL, nc.err);
+  ncclUniqueId id;
+  const ncclResult_t r = nc.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, LBM_ENCCL, std::string("ncclGetUniqueId: ") + nc.GetErrorString(r));
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(out128, &id, sizeof(id));
+  return LBM_OK;
+}
 
 const char *lbm_version(void) { return "lbm-b200 0.1 (sm_100a; arXiv 2211.02435 hot path)"; }
 
@@ -632,13 +883,20 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   if (!domain) return fail(nullptr, LBM_EINVAL, "domain is NULL");
   if (!relaxation_rates) return fail(nullptr, LBM_EINVAL, "relaxation_rates is NULL");
   if (stencil < LBM_D2Q9 || stencil > LBM_D3Q27) return fail(nullptr, LBM_EINVAL, "unknown stencil");
-  if (collision_space < LBM_SPACE_POPULATION || collision_space > LBM_SPACE_CUMULANT)
+  if (collision_space < LBM_SPACE_POPULATION || collision_space > LBM_SPACE_RAW_WO)
     return fail(nullptr, LBM_EINVAL, "unknown collision space");
-  if (equilibrium < LBM_EQ_ABSOLUTE || equilibrium > LBM_EQ_DISCRETE_DELTA)
+  if (equilibrium < LBM_EQ_ABSOLUTE || equilibrium > LBM_EQ_ABSOLUTE_F0)
     return fail(nullptr, LBM_EINVAL, "unknown equilibrium");
   const int zc = zero_centered ? 1 : 0;
   const bool delta_eq = equilibrium == LBM_EQ_DELTA || equilibrium == LBM_EQ_DISCRETE_DELTA;
   const bool discrete_eq = equilibrium == LBM_EQ_DISCRETE || equilibrium == LBM_EQ_DISCRETE_DELTA;
+  const bool popbg = equilibrium == LBM_EQ_ABSOLUTE_F0;        // reading R30
+  const bool wo = collision_space == LBM_SPACE_RAW_WO;          // reading R31
+  if (popbg && !zc)
+    return fail(nullptr, LBM_EUNSUPPORTED,
+                "LBM_EQ_ABSOLUTE_F0 adds the background f0 to zero-centered populations: zero_centered = 1");
+  if (wo && (discrete_eq || equilibrium == LBM_EQ_SWE))
+    return fail(nullptr, LBM_EUNSUPPORTED, "the WO-MRT basis is provided with the continuous equilibrium");
   // admissibility
   if (delta_eq && !zc)
     return fail(nullptr, LBM_EUNSUPPORTED, "delta equilibrium requires zero-centered storage (PAPER.md:546)");
@@ -680,15 +938,19 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   if (slab_extent / D.nranks < 2) return fail(nullptr, LBM_EINVAL, "slabs need at least 2 planes");
   bool any_wall = false;
   for (int a = 0; a < 3; ++a) any_wall |= (D.bc[a][0] == LBM_BC_NOSLIP);
-  if (D.streaming == LBM_AA && any_wall && D.nranks > 1)
+  // ghost planes along the slab axis: several ranks, or one rank exchanging with itself
+  const bool multi = D.nranks > 1 || D.nccl_id != nullptr;
+  if (D.streaming == LBM_AA && any_wall && multi)
     return fail(nullptr, LBM_EUNSUPPORTED, "AA streaming with no-slip faces is provided for a single rank");
-  if ((D.streaming == LBM_ESOTERIC_PULL || D.streaming == LBM_ESOTERIC_TWIST) && (any_wall || D.nranks > 1))
+  if ((D.streaming == LBM_ESOTERIC_PULL || D.streaming == LBM_ESOTERIC_TWIST) && (any_wall || multi))
     return fail(nullptr, LBM_EUNSUPPORTED,
                 "Esoteric Pull / Twist are provided for a single rank with periodic faces");
+  if ((D.dev_alloc == nullptr) != (D.dev_free == nullptr))
+    return fail(nullptr, LBM_EINVAL, "dev_alloc and dev_free must be given together");
 
   int regime = lbm::REG_ABS;
-  if (zc) regime = delta_eq ? lbm::REG_DELTA : lbm::REG_ZC_ABS;
-  int kspace = (int)collision_space;
+  if (zc) regime = delta_eq ? lbm::REG_DELTA : lbm::REG_ZC_ABS;  // ABSOLUTE_F0: REG_ZC_ABS + RS_POPBG
+  int kspace = wo ? (int)LBM_SPACE_RAW : (int)collision_space;
   if (equilibrium == LBM_EQ_SWE)
     kspace = (collision_space == LBM_SPACE_CUMULANT) ? (int)lbm::SPACE_SWE_K : (int)lbm::SPACE_SWE;
   // rate specialisation: rates equal to one become compile-time constants
@@ -704,6 +966,8 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
     if (allow) rs = reg ? lbm::RS_REG : (high ? lbm::RS_HIGH : lbm::RS_GENERAL);
   }
   if (discrete_eq) rs = lbm::RS_GENERAL | lbm::RS_DISCRETE;  // q_eq = T(f_eq), general rates
+  if (wo || popbg)  // general rates (no rate specialisation) with the basis / background flags
+    rs = lbm::RS_GENERAL | (wo ? lbm::RS_WOBASIS : 0) | (popbg ? lbm::RS_POPBG : 0);
   const Ops *ops = find_ops(stencil, D.precision, kspace, regime, rs);
   if (!ops) return fail(nullptr, LBM_EUNSUPPORTED, "no kernel instantiated for this combination");
 
@@ -727,6 +991,10 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   c->nranks = D.nranks;
   c->swe_g = D.swe_g;
   c->device = D.device;
+  c->multi = multi;
+  c->dev_alloc = D.dev_alloc;
+  c->dev_free = D.dev_free;
+  c->alloc_user = D.alloc_user;
   c->esize = (D.precision == LBM_FP64) ? 8 : 4;
   lbm_slab_extent(slab_extent, D.rank, D.nranks, &c->offset, &c->extent);
 
@@ -738,7 +1006,7 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   g.nzg = slab_extent;
   g.z0 = c->offset;
   g.zbegin = 0;
-  g.wrapz = (D.nranks == 1) ? 1 : 0;
+  g.wrapz = multi ? 0 : 1;
   const size_t align = 128 / c->esize;  // 128-byte aligned rows
   g.pitch = (int)(((size_t)D.nx + align - 1) / align * align);
   g.pop = (long long)g.ny * g.pitch;
@@ -765,7 +1033,7 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   fill_params(c);
   {  // temporal blocking: single rank, pull, periodic (LBM_TEMPORAL_BLOCKING=0 disables)
     const char *env = getenv("LBM_TEMPORAL_BLOCKING");
-    c->tb_allowed = !(env && env[0] == '0') && D.streaming == LBM_PULL && D.nranks == 1 && !c->bb;
+    c->tb_allowed = !(env && env[0] == '0') && D.streaming == LBM_PULL && !multi && !c->bb;
   }
 
   auto bail = [&](lbm_status s) {
@@ -775,6 +1043,14 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   };
   cudaError_t e = cudaSetDevice(D.device);
   if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaSetDevice"));
+  if (wo) {  // the WO-MRT basis matrices into the kernels' constant memory (reading R31)
+    double L[27 * 27], Linv[27 * 27];
+    if (stencil == LBM_D2Q9) wo_basis<lbm::D2Q9>(L, Linv);
+    else if (stencil == LBM_D3Q19) wo_basis<lbm::D3Q19>(L, Linv);
+    else wo_basis<lbm::D3Q27>(L, Linv);
+    e = (cudaError_t)ops->set_wo(L, Linv);
+    if (e != cudaSuccess) return bail(cuda_fail(c, e, "WO-MRT basis upload"));
+  }
   if (D.stream) {
     c->stream = (cudaStream_t)D.stream;
   } else {
@@ -785,16 +1061,24 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   c->grid_elems = (size_t)(g.nzl + 2) * (size_t)g.plane;
   {  // two-step sweeps across ranks need 8 scratch planes (LBM_PEER_TB=0 disables, at create)
     const char *env = getenv("LBM_PEER_TB");
-    c->peer_tb_cap = !(env && env[0] == '0') && D.nranks > 1 && D.streaming == LBM_PULL && !c->bb &&
-                     ops->pull2 && ops->tile_x > 0 && g.nx % ops->tile_x == 0 && g.ny % ops->tile_y == 0 &&
-                     g.nzl >= 6;
+    c->peer_tb_cap = !(env && env[0] == '0') && multi && D.streaming == LBM_PULL && !c->bb && ops->pull2 &&
+                     ops->tile_x > 0 && g.nx % ops->tile_x == 0 && g.ny % ops->tile_y == 0 && g.nzl >= 6;
+    // enough CTAs for the interior sweep of one rank: >= 2 waves (the single-rank rule is 4;
+    // a slab of a decomposition keeps its pairs down to 2, e.g. 8192^2 SWE on 8 ranks)
+    if (c->peer_tb_cap && !(env && env[0] == '1') && tb_tiles(c) * peer_tb_chunks(c) < kTbMinCtas / 2)
+      c->peer_tb_cap = false;
     c->scratch_off = c->grid_elems;
   }
   const size_t alloc_elems = c->grid_elems + (c->peer_tb_cap ? (size_t)8 * g.plane : 0);
   const int ngrids = (D.streaming == LBM_PULL) ? 2 : 1;
   for (int k = 0; k < ngrids; ++k) {
-    e = cudaMalloc(&c->buf[k], alloc_elems * c->esize);
-    if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaMalloc(populations)"));
+    if (c->dev_alloc) {
+      c->buf[k] = c->dev_alloc(alloc_elems * c->esize, c->alloc_user);
+      if (!c->buf[k]) return bail(fail(c, LBM_ENOMEM, "dev_alloc(populations) returned NULL"));
+    } else {
+      e = cudaMalloc(&c->buf[k], alloc_elems * c->esize);
+      if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaMalloc(populations)"));
+    }
     e = cudaMemsetAsync(c->buf[k], 0, alloc_elems * c->esize, c->stream);
     if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaMemset"));
   }
@@ -802,6 +1086,21 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaMalloc(flag)"));
   e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return bail(cuda_fail(c, e, "cudaStreamSynchronize"));
+  if (D.nccl_id) {  // in-library NCCL communicator (collective over the nranks ranks)
+    const NcclApi &nc = nccl_api();
+    if (!nc.ok) return bail(fail(c, LBM_ENCCL, nc.err));
+    ncclUniqueId id;
+    memcpy(&id, D.nccl_id, sizeof(id));
+    const ncclResult_t r = nc.CommInitRank(&c->comm, D.nranks, id, D.rank);
+    if (r != ncclSuccess) {
+      c->comm = nullptr;
+      return bail(fail(c, LBM_ENCCL, std::string("ncclCommInitRank: ") + nc.GetErrorString(r)));
+    }
+    e = cudaStreamCreateWithFlags(&c->s_int, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_i, cudaEventDisableTiming);
+    if (e != cudaSuccess) return bail(cuda_fail(c, e, "NCCL exchange streams"));
+  }
   *out = c;
   return LBM_OK;
 }
@@ -817,8 +1116,12 @@ lbm_status lbm_destroy(lbm_ctx *c) {
   if (c->ev_i) cudaEventDestroy(c->ev_i);
   if (c->s_int) cudaStreamDestroy(c->s_int);
   if (c->peer_flags) cudaFree(c->peer_flags);
+  if (c->comm) nccl_api().CommDestroy(c->comm);
   for (int k = 0; k < 2; ++k)
-    if (c->buf[k]) cudaFree(c->buf[k]);
+    if (c->buf[k]) {
+      if (c->dev_free) c->dev_free(c->buf[k], c->alloc_user);
+      else cudaFree(c->buf[k]);
+    }
   if (c->staging) cudaFree(c->staging);
   if (c->flag) cudaFree(c->flag);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -840,7 +1143,9 @@ lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
   info->device_bytes = c->grid_elems * c->esize * (c->streaming == LBM_PULL ? 2 : 1);
   info->steps_done = c->steps;
   info->rate_specialization = c->rs & 3;
-  info->temporal_blocking = (use_temporal_blocking(c) || use_peer_tb(c)) ? 2 : 1;
+  // multi-rank pull contexts with the pair sequence (peer path, in-library NCCL, or the
+  // LBM_REGION_PAIR_* regions of an external exchange) run two steps per interior sweep
+  info->temporal_blocking = (use_temporal_blocking(c) || (c->multi && c->peer_tb_cap)) ? 2 : 1;
   info->resident_cluster = resident_cluster(c);
   info->cuda_graph_steps = (c->nranks == 1 && !info->resident_cluster && use_graphs(c)) ? kGraphSteps : 0;
   return LBM_OK;
@@ -866,6 +1171,7 @@ lbm_status lbm_init_macroscopic(lbm_ctx *c, const double *rho, const double *u) 
   s = check_launch(c, "k_init");
   if (s != LBM_OK) return s;
   c->steps = 0;
+  c->needs_prime = c->multi;
   LBM_CUDA(c, cudaStreamSynchronize(c->stream));
   return LBM_OK;
 }
@@ -874,8 +1180,19 @@ lbm_status lbm_step(lbm_ctx *c, int n) {
   NvtxRange nvtx_("lbm_step");
   if (!c) return LBM_EINVAL;
   if (n < 0) return fail(c, LBM_EINVAL, "negative step count");
-  if (c->nranks > 1)
-    return fail(c, LBM_EUNSUPPORTED, "multi-rank contexts step through lbm_step_region + halo exchange");
+  if (c->multi) {  // collective: fused peer push, else the in-library NCCL exchange
+    if (c->peer_on) return lbm_step_peer(c, n);
+    if (!c->comm)
+      return fail(c, LBM_EUNSUPPORTED,
+                  "multi-rank context without a transport: lbm_peer_connect, create with nccl_id, or drive "
+                  "lbm_step_region + lbm_get_halo with an external exchange");
+    LBM_CUDA(c, cudaSetDevice(c->device));
+    int cur = pull_parity(c);
+    const lbm_status s = enqueue_nccl_steps(c, n, cur);
+    if (c->streaming == LBM_PULL) c->cur = cur;
+    else c->aa_state = cur;
+    return s;
+  }
   LBM_CUDA(c, cudaSetDevice(c->device));
   GridParams g = c->g;
   int t = 0;
@@ -1152,6 +1469,15 @@ lbm_status peer_connect_impl(lbm_ctx *c, const lbm_peer_info *lo, const lbm_peer
   c->peer_remote[0] = static_cast<long long *>(f[0]) + 1;  // I am the lower's upper neighbour
   c->peer_remote[1] = static_cast<long long *>(f[1]) + 0;
   LBM_CUDA(c, cudaMemset(c->peer_flags, 0, 4 * sizeof(long long)));
+  // load the wait / signal kernels and every step kernel now, before any wait can spin
+  // (lazy module loading at a first launch waits for the running kernels: Ops::preload)
+  {
+    cudaFuncAttributes a{};
+    LBM_CUDA(c, cudaFuncGetAttributes(&a, k_peer_wait));
+    LBM_CUDA(c, cudaFuncGetAttributes(&a, k_peer_signal));
+    c->ops->preload();
+    if (c->ops_plain != c->ops) c->ops_plain->preload();
+  }
   if (!c->s_int) {
     LBM_CUDA(c, cudaStreamCreateWithFlags(&c->s_int, cudaStreamNonBlocking));
     LBM_CUDA(c, cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming));
@@ -1167,6 +1493,7 @@ lbm_status lbm_peer_prime(lbm_ctx *c) {
   if (!c) return LBM_EINVAL;
   if (!c->peer_on) return fail(c, LBM_EINVAL, "lbm_peer_connect first");
   LBM_CUDA(c, cudaSetDevice(c->device));
+  c->needs_prime = false;
   lbm_layout lay;
   lbm_status s = lbm_grid_layout((lbm_stencil)c->stencil, (lbm_precision)c->prec, c->gnx, c->gny, c->gnz,
                                  c->nranks, &lay);
@@ -1196,6 +1523,10 @@ lbm_status lbm_step_peer(lbm_ctx *c, int n) {
   if (n < 0) return fail(c, LBM_EINVAL, "negative step count");
   if (!c->peer_on) return fail(c, LBM_EINVAL, "lbm_peer_connect first");
   LBM_CUDA(c, cudaSetDevice(c->device));
+  if (c->needs_prime) {  // after init / set: push the current boundary planes first
+    const lbm_status ps = lbm_peer_prime(c);
+    if (ps != LBM_OK) return ps;
+  }
   int t = 0;
   if (n >= kGraphSteps && graphs_enabled()) {  // replay captured 32-step loops (same launches)
     for (int par = 0; par < 2; ++par) {
@@ -1288,6 +1619,8 @@ lbm_status lbm_set_force(lbm_ctx *c, const double *force) {
   if (any) {
     if (c->rs & lbm::RS_DISCRETE)
       return fail(c, LBM_EUNSUPPORTED, "no body force with the discrete equilibrium (reading R29)");
+    if (c->rs & (lbm::RS_WOBASIS | lbm::RS_POPBG))
+      return fail(c, LBM_EUNSUPPORTED, "no body force with the WO-MRT basis or LBM_EQ_ABSOLUTE_F0");
     if (!(c->kspace == LBM_SPACE_POPULATION || c->kspace == LBM_SPACE_RAW || c->kspace == LBM_SPACE_CENTRAL ||
           c->kspace == LBM_SPACE_CUMULANT))
       return fail(c, LBM_EUNSUPPORTED,
@@ -1299,6 +1632,7 @@ lbm_status lbm_set_force(lbm_ctx *c, const double *force) {
                             lbm::RS_GENERAL | (he ? lbm::RS_FORCE_HE : lbm::RS_FORCE));
     if (!f) return fail(c, LBM_EUNSUPPORTED, "no forced kernel instantiated for this combination");
     c->ops = f;
+    if (c->peer_on) f->preload();  // before any neighbour wait can spin (Ops::preload)
   } else {
     c->ops = c->ops_plain;
   }
@@ -1383,6 +1717,7 @@ lbm_status lbm_set_populations(lbm_ctx *c, const double *f) {
   s = check_launch(c, "k_set_populations");
   if (s != LBM_OK) return s;
   c->steps = 0;
+  c->needs_prime = c->multi;
   LBM_CUDA(c, cudaStreamSynchronize(c->stream));
   return LBM_OK;
 }
@@ -1419,10 +1754,14 @@ lbm_status lbm_test_collide(lbm_ctx *c, const double *f_in, double *f_out, long 
   return LBM_OK;
 }
 
-/* diagnostics: registers / local memory of this context's pull kernel */
+/* diagnostics: registers / local memory of the kernel that dominates this context's lbm_step */
 lbm_status lbm_kernel_attributes(const lbm_ctx *c, int *regs, int *local_bytes) {
   if (!c || !regs || !local_bytes) return LBM_EINVAL;
-  c->ops->attributes(regs, local_bytes);
+  int which = 0;
+  if (resident_cluster(c)) which = 2;
+  else if (use_temporal_blocking(c) || (c->multi && c->peer_tb_cap)) which = 1;
+  else if (c->streaming != LBM_PULL) which = 10 + inplace_pattern(c, 0);
+  c->ops->attributes(which, regs, local_bytes);
   return LBM_OK;
 }
 

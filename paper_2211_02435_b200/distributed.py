@@ -197,14 +197,20 @@ class SlabRunner:
     """Multi-process time stepping of one rank's slab: boundary planes, then the
     halo exchange (NCCL P2P on its own stream) overlapped with the interior planes."""
 
-    def __init__(self, lat: "L.Lattice", rank: int, nranks: int, group=None):
+    def __init__(self, lat: "L.Lattice", rank: int, nranks: int, group=None, pairs=None):
+        """pairs: None = two-step sweeps across ranks where the context supports them (equal to
+        the single-rank run to rounding), False = single steps (bitwise equal to it), True =
+        require them (ValueError if unsupported).  The choice must be the same on every rank."""
         import torch
 
         self.lat, self.rank, self.nranks = lat, rank, nranks
         self.tr = TorchTransport(lat, rank, nranks, group)
         self.s_int = torch.cuda.Stream()
         self.s_main = torch.cuda.current_stream()
-        self.pairs = lat.streaming == L.LBM_PULL and supports_pairs(lat)  # same on every rank
+        can = lat.streaming == L.LBM_PULL and supports_pairs(lat)
+        if pairs and not can:
+            raise ValueError("this context has no two-step regions (LBM_REGION_PAIR_*)")
+        self.pairs = can if pairs is None else bool(pairs)
 
     def prime(self):
         self.lat.sync()
@@ -259,14 +265,15 @@ def connect_local(lats):
 
 
 def step_peer_local(lats, n: int, chunk: int = 1):
-    """n steps of every context of one process with the fused halo push.  The ranks'
-    launches are interleaved in chunks of `chunk` steps (a context waits on the GPU for its
-    neighbours; chunk = 2 lets the two-step sweeps run across ranks)."""
+    """n steps of every context of one process with the fused halo push (lbm_step on the
+    connected contexts).  The ranks' launches are interleaved in chunks of `chunk` steps (a
+    context waits on the GPU for its neighbours; chunk = 2 lets the two-step sweeps run across
+    ranks)."""
     done = 0
     while done < n:
         k = min(chunk, n - done)
         for l in lats:
-            l.step_peer(k)
+            l.step(k)
         done += k
     for l in lats:
         l.sync()
@@ -325,7 +332,7 @@ class PeerRunner:
         self.lat.peer_prime()
 
     def step(self, n: int = 1):
-        self.lat.step_peer(n)
+        self.lat.step(n)  # lbm_step runs the fused push on a connected context (collective)
 
     def check(self):
         if self.lat.peer_timed_out():

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblbm.so")
 
 # enums of include/lbm.h
-LBM_OK, LBM_EINVAL, LBM_EUNSUPPORTED, LBM_ENOMEM, LBM_ECUDA, LBM_ENUMERIC = 0, -1, -2, -3, -4, -6
+LBM_OK, LBM_EINVAL, LBM_EUNSUPPORTED, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_ENUMERIC = 0, -1, -2, -3, -4, -5, -6
 LBM_D2Q9, LBM_D3Q19, LBM_D3Q27 = 0, 1, 2
 LBM_SPACE_POPULATION, LBM_SPACE_RAW, LBM_SPACE_CENTRAL, LBM_SPACE_CUMULANT = 0, 1, 2, 3
 LBM_EQ_ABSOLUTE, LBM_EQ_DELTA, LBM_EQ_SWE, LBM_EQ_DISCRETE, LBM_EQ_DISCRETE_DELTA = 0, 1, 2, 3, 4
@@ -29,7 +29,7 @@ LBM_REGION_PAIR_INTERIOR, LBM_REGION_PAIR_BOUNDARY1, LBM_REGION_PAIR_BOUNDARY2 =
 Q_OF = {LBM_D2Q9: 9, LBM_D3Q19: 19, LBM_D3Q27: 27}
 
 STATUS_NAMES = {0: "LBM_OK", -1: "LBM_EINVAL", -2: "LBM_EUNSUPPORTED", -3: "LBM_ENOMEM", -4: "LBM_ECUDA",
-                -6: "LBM_ENUMERIC"}
+                -5: "LBM_ENCCL", -6: "LBM_ENUMERIC"}
 
 
 class LbmError(RuntimeError):
@@ -38,11 +38,16 @@ class LbmError(RuntimeError):
         self.status = status
 
 
+DEV_ALLOC = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+DEV_FREE = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+
+
 class lbm_domain(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int),
                 ("bc", (ctypes.c_int * 2) * 3), ("precision", ctypes.c_int), ("streaming", ctypes.c_int),
                 ("swe_g", ctypes.c_double), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
-                ("rank", ctypes.c_int), ("nranks", ctypes.c_int)]
+                ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
+                ("dev_alloc", DEV_ALLOC), ("dev_free", DEV_FREE), ("alloc_user", ctypes.c_void_p)]
 
 
 class lbm_halo(ctypes.Structure):
@@ -91,6 +96,7 @@ SIGNATURES = [
     ("lbm_get_info", ctypes.c_int, [_vp, ctypes.POINTER(lbm_info)]),
     ("lbm_init_macroscopic", ctypes.c_int, [_vp, _dp, _dp]),
     ("lbm_step", ctypes.c_int, [_vp, ctypes.c_int]),
+    ("lbm_nccl_get_unique_id", ctypes.c_int, [_vp]),
     ("lbm_step_region", ctypes.c_int, [_vp, ctypes.c_int, _vp]),
     ("lbm_swap", ctypes.c_int, [_vp]),
     ("lbm_get_halo", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(lbm_halo)]),
@@ -177,6 +183,13 @@ def version() -> str:
     return lib().lbm_version().decode()
 
 
+def nccl_get_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (rank 0; pass it to every rank's Lattice(nccl_id=...))."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().lbm_nccl_get_unique_id(buf))
+    return buf.raw
+
+
 class Lattice:
     """One lbm_ctx: a rank's slab of an MRT LBM simulation on a CUDA device.
 
@@ -185,7 +198,11 @@ class Lattice:
     """
 
     def __init__(self, stencil, space, equilibrium, rates, shape, zero_centered=True, precision=LBM_FP64,
-                 streaming=LBM_PULL, bc=None, swe_g=0.0, device=0, stream=None, rank=0, nranks=1):
+                 streaming=LBM_PULL, bc=None, swe_g=0.0, device=0, stream=None, rank=0, nranks=1, nccl_id=None,
+                 allocator=None):
+        """nccl_id: 128 bytes from nccl_get_unique_id() (same on every rank): in-library NCCL halo
+        exchange in lbm_step (collective create).  allocator: optional (alloc(nbytes) -> int device
+        pointer, free(ptr)) pair used for the population grids (lbm_domain.dev_alloc/dev_free)."""
         L = lib()
         dom = lbm_domain()
         dom.nx, dom.ny, dom.nz = (int(v) for v in shape)
@@ -200,6 +217,17 @@ class Lattice:
         dom.stream = stream
         dom.rank = int(rank)
         dom.nranks = int(nranks)
+        self._nccl_id = None
+        if nccl_id is not None:
+            assert len(nccl_id) == 128, "an ncclUniqueId is 128 bytes"
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            dom.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
+        self._alloc_cbs = None
+        if allocator is not None:
+            alloc_fn, free_fn = allocator
+            self._alloc_cbs = (DEV_ALLOC(lambda n, _u: int(alloc_fn(int(n))) or None),
+                               DEV_FREE(lambda p, _u: free_fn(int(p))))
+            dom.dev_alloc, dom.dev_free = self._alloc_cbs
         r = np.ascontiguousarray(np.asarray(rates, dtype=np.float64).reshape(-1))
         h = _vp()
         self._ctx = None
@@ -339,36 +367,48 @@ class Lattice:
 
     def run(self, n, check_every=0, callback=None, every=0):
         """n steps; optionally lbm_check_finite every `check_every` steps (raises LbmError
-        LBM_ENUMERIC with the step index) and callback(self, steps_done) every `every` steps."""
+        LBM_ENUMERIC with the step index) and callback(self, steps_done) every `every` steps.
+        Intervals count from the start of this call; chunks end on every multiple of either."""
         done = 0
-        chunk = min(x for x in (check_every, every, n) if x > 0) if n > 0 else 0
         while done < n:
-            k = min(chunk, n - done)
+            k = n - done
+            if check_every > 0:
+                k = min(k, check_every - done % check_every)
+            if every > 0:
+                k = min(k, every - done % every)
             self.step(k)
             done += k
-            steps = self.info().steps_done
-            if check_every and steps % check_every == 0:
+            if check_every > 0 and done % check_every == 0:
                 self.check_finite()
-            if callback is not None and every and steps % every == 0:
-                callback(self, steps)
+            if callback is not None and every > 0 and done % every == 0:
+                callback(self, self.info().steps_done)
 
     # -- checkpoint / restart: the canonical state (independent of the streaming pattern)
-    def save(self, path):
+    def save(self, path, rates=None):
         """Checkpoint of this rank's slab: canonical populations + method metadata (npz)."""
         info = self.info()
         np.savez(path, f=self.get_populations(), steps=info.steps_done, stencil=self.stencil, space=self.space,
                  equilibrium=self.equilibrium, zero_centered=self.zero_centered, shape=np.array(self.global_shape),
-                 offset=self.offset, extent=self.extent)
+                 offset=self.offset, extent=self.extent, precision=self.precision, streaming=self.streaming,
+                 rates=np.asarray(rates if rates is not None else [], dtype=np.float64))
 
-    def load(self, path):
-        """Restore a checkpoint written by save() for the same method and slab."""
+    def load(self, path, rates=None):
+        """Restore a checkpoint written by save() for the same method, precision and slab.
+        Returns the saved step count; the context's own counter (lbm_info.steps_done) restarts at
+        zero like after any lbm_set_populations, the canonical state is independent of it.  On
+        several ranks the next lbm_step exchanges the halo first (an external-exchange driver,
+        SlabRunner, must call prime())."""
         d = np.load(path)
         for k, v in (("stencil", self.stencil), ("space", self.space), ("equilibrium", self.equilibrium),
-                     ("zero_centered", self.zero_centered), ("offset", self.offset), ("extent", self.extent)):
-            if int(d[k]) != int(v):
+                     ("zero_centered", self.zero_centered), ("offset", self.offset), ("extent", self.extent),
+                     ("precision", self.precision)):
+            if k in d and int(d[k]) != int(v):
                 raise ValueError(f"checkpoint {k} = {d[k]} does not match this lattice ({v})")
         if tuple(d["shape"]) != tuple(self.global_shape):
             raise ValueError("checkpoint lattice shape differs")
+        if rates is not None and "rates" in d and d["rates"].size and not np.array_equal(
+                d["rates"], np.asarray(rates, dtype=np.float64).reshape(-1)):
+            raise ValueError("checkpoint relaxation rates differ")
         self.set_populations(d["f"])
         return int(d["steps"])
 

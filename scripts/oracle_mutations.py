@@ -67,6 +67,20 @@ MUTANTS = [
      "ceq += R(t.c) * Cd.c[sidx(t.e)];\n        continue;", "(void)Cd;"),
     ("stencil order: swap (1,1) and (-1,-1) in-plane", "{1, 1}, {-1, -1}, {1, -1}, {-1, 1}};",
      "{-1, -1}, {1, 1}, {1, -1}, {-1, 1}};"),
+    # the bulk rate (reading R3) acting on a wrong polynomial: pinned by the acoustic attenuation
+    ("D2Q9: bulk rate on x^2 - y^2, shear rate on x^2 + y^2 (rows swapped)",
+     "    B.push_back(P({T(1, 2, 0, 0), T(-1, 0, 2, 0)}));\n    B.push_back(P({T(1, 2, 0, 0), T(1, 0, 2, 0)}));",
+     "    B.push_back(P({T(1, 2, 0, 0), T(1, 0, 2, 0)}));\n    B.push_back(P({T(1, 2, 0, 0), T(-1, 0, 2, 0)}));"),
+    ("3D: bulk rate on x^2 - z^2, shear rate on x^2 + y^2 + z^2 (rows swapped)",
+     "B.push_back(P({T(1, 2, 0, 0), T(-1, 0, 0, 2)}));                   // 8  x^2 - z^2\n"
+     "  B.push_back(P({T(1, 2, 0, 0), T(1, 0, 2, 0), T(1, 0, 0, 2)}));     // 9  x^2 + y^2 + z^2",
+     "B.push_back(P({T(1, 2, 0, 0), T(1, 0, 2, 0), T(1, 0, 0, 2)}));     // 8\n"
+     "  B.push_back(P({T(1, 2, 0, 0), T(-1, 0, 0, 2)}));                   // 9"),
+    # invisible to isotropy and to the incompressible TGV / shear-wave / Poiseuille pins
+    ("bulk polynomial relaxed with the shear rate (omega_b ignored)",
+     "    for (int i = 0; i < q; ++i) m.omega[i] = R(rates[i]);",
+     "    for (int i = 0; i < q; ++i) m.omega[i] = R(rates[i]);\n"
+     "    m.omega[stencil == ST_D2Q9 ? 5 : 9] = m.omega[stencil == ST_D2Q9 ? 4 : 7];"),
 ]
 
 
@@ -75,7 +89,10 @@ def main():
     tmp = tempfile.mkdtemp(prefix="oracle_mut_")
     gomp = subprocess.run(["g++", "-print-file-name=libgomp.so"], capture_output=True, text=True).stdout.strip()
     survived = []
+    only = sys.argv[1:]  # optional substrings: run the matching mutants only
     for desc, old, new in MUTANTS:
+        if only and not any(o in desc for o in only):
+            continue
         if src.count(old) < 1:
             print(f"!! snippet not found: {desc}")
             survived.append(desc)
@@ -101,8 +118,9 @@ def main():
         if not killed and "[equivalent]" not in desc:
             survived.append(desc)
     shutil.rmtree(tmp, ignore_errors=True)
-    n_eq = sum("[equivalent]" in m[0] for m in MUTANTS)
-    print(f"{len(MUTANTS) - n_eq - len(survived)}/{len(MUTANTS) - n_eq} non-equivalent mutants killed "
+    run = [m for m in MUTANTS if not only or any(o in m[0] for o in only)]
+    n_eq = sum("[equivalent]" in m[0] for m in run)
+    print(f"{len(run) - n_eq - len(survived)}/{len(run) - n_eq} non-equivalent mutants killed "
           f"({n_eq} equivalent mutant(s) listed for the record)")
     return 1 if survived else 0
 

@@ -65,6 +65,8 @@ def main():
     ap.add_argument("--halo", choices=["exchange", "peer"], default="exchange",
                     help="exchange: SlabRunner (NCCL/gloo P2P); peer: PeerRunner (fused push over CUDA IPC)")
     args = ap.parse_args()
+    # the TB case's small slabs keep their two-step sweeps (below the 2-wave rule of lbm_create)
+    os.environ.setdefault("LBM_PEER_TB", "1")
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
     ngpu = torch.cuda.device_count()

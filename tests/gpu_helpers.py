@@ -81,3 +81,19 @@ def oracle_run(st, space, eq, zc, rates, shape, f0, steps, bc=None, g=0.0):
     sim.set(f0)
     sim.step(steps)
     return sim.get()
+
+
+def oracle_fp64_discrepancy(st, space, eq, zc, rates, shape, f0, steps, ref, bc=None, g=0.0):
+    """The oracle's own fp64 instantiation against its long-double reference `ref`, on the
+    per-population gate metric: the error any correct fp64 implementation of the same run
+    incurs (reading R25)."""
+    sim = oracle.Sim(st, space, eq, zc, rates, shape, bc=bc, g=g, prec=oracle.DOUBLE)
+    sim.set(f0)
+    sim.step(steps)
+    return gate_error(st, sim.get(), ref, zc)
+
+
+def population_bound(disc):
+    """Gate on the per-population metric where the parameters amplify round-off: the larger
+    of the fp64 tolerance and 10x the oracle's own fp64-vs-long-double discrepancy."""
+    return max(F64_TOL, 10.0 * disc)

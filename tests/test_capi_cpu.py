@@ -174,3 +174,18 @@ def test_binding_structs_match_the_header(tmp_path):
         assert int(got[name]) == ctypes.sizeof(cls), name
         for field in cls._fields_:
             assert int(got[f"{name}.{field[0]}"]) == getattr(cls, field[0]).offset, (name, field[0])
+
+
+def test_nccl_unique_id_without_gpu():
+    """lbm_nccl_get_unique_id needs no GPU: it returns a 128-byte id, or LBM_ENCCL with a
+    message when no libnccl.so.2 can be loaded (never a crash)."""
+    import ctypes as C
+
+    buf = C.create_string_buffer(128)
+    st = L.lib().lbm_nccl_get_unique_id(buf)
+    assert st in (L.LBM_OK, L.LBM_ENCCL)
+    if st == L.LBM_OK:
+        assert any(buf.raw)
+    else:
+        assert L.lib().lbm_last_error(None)
+    assert L.lib().lbm_nccl_get_unique_id(None) == L.LBM_EINVAL

@@ -158,7 +158,7 @@ class _FakePeerLattice:
     def peer_prime(self):
         self.calls.append("prime")
 
-    def step_peer(self, n):
+    def step(self, n):  # lbm_step on the connected context (the fused push)
         self.calls.append(("step", n))
 
     def peer_timed_out(self):

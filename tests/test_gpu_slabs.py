@@ -136,7 +136,7 @@ def test_peer_push_equals_single_rank_bitwise(st, space, eq, zc, nranks, nz):
     np.testing.assert_array_equal(multi, single)
 
 
-@pytest.mark.parametrize("fence", ["0", "1"])
+@pytest.mark.parametrize("fence", ["0", "1", "2"])
 def test_peer_push_with_walls_matches_oracle(fence, monkeypatch):
     monkeypatch.setenv("LBM_PEER_FENCE", fence)  # per-thread system fence after the pushes
     st, space, eq, zc = W.D3Q27, W.RAW, W.EQ_DELTA, 1
@@ -366,12 +366,13 @@ def test_peer_forced_then_disconnect_equals_single_rank(streaming, space, eq, mo
     (W.D2Q9, W.CENTRAL, W.EQ_SWE, 0, L.LBM_FP64, (256, 36, 1), 3),
     (W.D2Q9, W.POPULATION, W.EQ_DELTA, 1, L.LBM_FP64, (256, 24, 1), 4),
 ])
-def test_peer_two_step_sweeps_match_single_rank(st, space, eq, zc, prec, shape, nranks):
+def test_peer_two_step_sweeps_match_single_rank(st, space, eq, zc, prec, shape, nranks, monkeypatch):
     """Temporal blocking across ranks on the peer path: interior planes by the two-step sweep,
     the boundary regions by two single steps through the scratch planes with pushes into the
     neighbours' scratch and ghost planes; pairs plus a trailing single step match the
     single-rank run to rounding and the oracle at full parity."""
     from gpu_helpers import round_to
+    monkeypatch.setenv("LBM_PEER_TB", "1")  # small lattices: pairs despite < 2 waves of CTAs
     g = W.swe_lattice_parameters()[0] if eq == W.EQ_SWE else 0.0
     rates = W.rate_set_p(st) if space != W.POPULATION else [1.3]
     if eq == W.EQ_SWE:
@@ -404,9 +405,10 @@ def test_peer_two_step_sweeps_match_single_rank(st, space, eq, zc, prec, shape, 
         assert gate_error(st, multi, ref, zc, norm=norm) < F64_TOL
 
 
-def test_peer_two_step_sweeps_graph_replay():
+def test_peer_two_step_sweeps_graph_replay(monkeypatch):
     """Two-step sweeps across ranks inside the captured 32-step graphs (16 pairs per graph)
     plus a remainder of pairs and a single step: equal to the single-rank run to rounding."""
+    monkeypatch.setenv("LBM_PEER_TB", "1")
     st, space, eq, zc = W.D3Q19, W.RAW, W.EQ_DELTA, 1
     shape, nranks, steps = (32, 16, 24), 2, 71
     rates = W.rate_set_p(st)
@@ -436,10 +438,11 @@ def test_peer_two_step_sweeps_graph_replay():
     (W.D3Q19, W.CUMULANT, W.EQ_ABSOLUTE, 1, (32, 16, 24), 4),
     (W.D2Q9, W.CENTRAL, W.EQ_ABSOLUTE, 1, (256, 36, 1), 3),
 ])
-def test_exchange_path_two_step_regions(st, space, eq, zc, shape, nranks):
+def test_exchange_path_two_step_regions(st, space, eq, zc, shape, nranks, monkeypatch):
     """Two-step sweeps across ranks with an external exchange (LBM_REGION_PAIR_* +
     lbm_get_halo(2), the SlabRunner sequence with LocalTransport): pairs plus a single step
     equal the single-rank run to rounding and the oracle at the gate."""
+    monkeypatch.setenv("LBM_PEER_TB", "1")
     rates = W.rate_set_p(st)
     f0 = initial_state(st, space, eq, zc, shape)
     steps = 9

@@ -890,3 +890,57 @@ def test_discrete_equilibrium_fixed_point_and_conservation(st, space):
         out = _abs(oracle.collide(st, space, eq, zc, rates, fa - w if zc else fa), w, eq, zc)
         np.testing.assert_allclose(out.sum(1), fa.sum(1), atol=2e-15)
         np.testing.assert_allclose(out @ xi, fa @ xi, atol=2e-16)
+
+
+def _acoustic_decay(st, space, eq, zc, om_s, om_b, L=64, steps=700, A=1e-4):
+    """Standing longitudinal wave rho = 1 + A cos(k x), u = 0 on an L-periodic box (2D: L x 4,
+    3D: L x 2 x 2); returns the amplitude series a(t) / A of the cos(k x) mode of rho."""
+    d = W.DIM_OF[st]
+    shape = (L, 4, 1) if d == 2 else (L, 2, 2)
+    nx, ny, nz = shape
+    zz = nz if d == 3 else 1
+    x = np.arange(nx)
+    k = 2 * math.pi / L
+    rho = np.broadcast_to(1 + A * np.cos(k * x), (zz, ny, nx))
+    u = np.zeros((rho.size, 3))
+    q = W.Q_OF[st]
+    feq = oracle.equilibrium(st, space, eq, zc, np.ascontiguousarray(rho).reshape(-1), u)
+    sim = oracle.Sim(st, space, eq, zc, W.rates_from_groups(st, {"s": om_s, "b": om_b}), shape, prec=oracle.DOUBLE)
+    sim.set(np.ascontiguousarray(feq.T.reshape(q, zz, ny, nx)))
+    c = np.cos(k * x)
+    amps = np.empty(steps)
+    for t in range(steps):
+        r, _ = sim.macroscopic()
+        amps[t] = ((r.reshape(-1, nx).mean(0) - 1) * c).sum() / (c * c).sum()
+        sim.step(1)
+    return amps / A
+
+
+@pytest.mark.parametrize("st,space,eq,zc", [
+    (W.D2Q9, W.RAW, W.EQ_DELTA, 1), (W.D2Q9, W.CENTRAL, W.EQ_ABSOLUTE, 1), (W.D2Q9, W.CUMULANT, W.EQ_ABSOLUTE, 1),
+    (W.D3Q19, W.RAW, W.EQ_DELTA, 1), (W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1),
+])
+@pytest.mark.parametrize("om_b", [0.8, 1.6])
+def test_acoustic_attenuation_pins_bulk_rate(st, space, eq, zc, om_b):
+    """The bulk rate (reading R3: omega_b on x^2 + y^2 (+ z^2)) fixes the attenuation of sound.
+    Linearised isothermal Navier-Stokes with the viscous stress of the relaxed second moments,
+    sigma = rho cs2 [tau_s (S - (2/D) div(u) I) + tau_b (2/D) div(u) I], tau = 1/omega - 1/2,
+    gives for a standing wave rho' ~ exp(-Gamma t) (cos(w t) + Gamma / w sin(w t)) with
+    Gamma = nu_L k^2 / 2, w^2 = cs2 k^2 - Gamma^2 and the longitudinal viscosity
+    nu_L = 2 (D - 1) / D nu + (2 / D) cs2 tau_b (nu = cs2 tau_s).  The fitted Gamma matches
+    within 1 % (observed <= 0.05 % at L = 64) for two bulk rates with the shear rate fixed: a
+    bulk rate acting on the wrong polynomial group, or not at all, moves Gamma by 3.5x."""
+    from scipy.optimize import curve_fit
+
+    cs2, om_s, L, steps = 1 / 3, 1.6, 64, 700
+    D = W.DIM_OF[st]
+    k = 2 * math.pi / L
+    tau_s, tau_b = 1 / om_s - 0.5, 1 / om_b - 0.5
+    nu_L = 2 * (D - 1) / D * cs2 * tau_s + 2 / D * cs2 * tau_b
+    G0 = nu_L * k * k / 2
+    w0 = math.sqrt(cs2 * k * k - G0 * G0)
+    a = _acoustic_decay(st, space, eq, zc, om_s, om_b, L, steps)
+    model = lambda t, G, w: np.exp(-G * t) * (np.cos(w * t) + G / w * np.sin(w * t))  # noqa: E731
+    (G, w), _ = curve_fit(model, np.arange(steps, dtype=np.float64), a, p0=(G0, w0))
+    assert abs(G / G0 - 1) < 1e-2, (G, G0)
+    assert abs(w / w0 - 1) < 1e-2, (w, w0)
