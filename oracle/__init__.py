@@ -60,6 +60,7 @@ def lib():
                                                                        ctypes.c_int, dp, ctypes.c_int, dp, dp,
                                                                        ctypes.c_longlong]
         L.oracle_sim_set_force_model.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        L.oracle_wo_basis.argtypes = [ctypes.c_int, dp, dp, ip]
         L.oracle_max_threads.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         _LIB = L
@@ -197,3 +198,15 @@ def max_threads() -> int:
 def set_threads(n: int) -> None:
     """OpenMP threads of the oracle (torchrun exports OMP_NUM_THREADS=1 to every rank)."""
     lib().oracle_set_threads(int(n))
+
+
+def wo_basis(stencil: int):
+    """WO-MRT basis (reading R31) as the oracle builds it: (M [q,q] with M[k,i] = p_k(xi_i),
+    G [q,q] monomial coefficients, mono [q,3] graded-lexicographic exponents)."""
+    M = np.zeros(27 * 27)
+    G = np.zeros(27 * 27)
+    mono = np.zeros(27 * 3, np.int32)
+    q = lib().oracle_wo_basis(stencil, _dp(M), _dp(G), _ip(mono))
+    if q < 0:
+        raise RuntimeError("oracle_wo_basis failed")
+    return M[: q * q].reshape(q, q).copy(), G[: q * q].reshape(q, q).copy(), mono[: 3 * q].reshape(q, 3).copy()

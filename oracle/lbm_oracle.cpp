@@ -59,8 +59,8 @@
 namespace {
 
 enum { ST_D2Q9 = 0, ST_D3Q19 = 1, ST_D3Q27 = 2 };
-enum { SP_POPULATION = 0, SP_RAW = 1, SP_CENTRAL = 2, SP_CUMULANT = 3 };
-enum { EQ_ABSOLUTE = 0, EQ_DELTA = 1, EQ_SWE = 2, EQ_DISCRETE = 3, EQ_DISCRETE_DELTA = 4 };
+enum { SP_POPULATION = 0, SP_RAW = 1, SP_CENTRAL = 2, SP_CUMULANT = 3, SP_RAW_WO = 4 };
+enum { EQ_ABSOLUTE = 0, EQ_DELTA = 1, EQ_SWE = 2, EQ_DISCRETE = 3, EQ_DISCRETE_DELTA = 4, EQ_ABSOLUTE_F0 = 5 };
 enum { BC_PERIODIC = 0, BC_NOSLIP = 1 };
 
 struct Term {
@@ -321,6 +321,10 @@ template <class R> struct Method {
   // of first appearance) and R_mono: basis polys in terms of those monomials
   std::vector<std::array<int, 3>> mono;
   std::vector<R> Rmono, Rmono_inv;
+  // WO-MRT (SP_RAW_WO, reading R31): the graded-lexicographic monomials wo_mono and the
+  // weighted Gram-Schmidt coefficients G[k][j] (polynomial k = sum_j G[k][j] wo_mono[j])
+  std::vector<std::array<int, 3>> wo_mono;
+  std::vector<R> G;
   bool ok = false;
 };
 
@@ -363,12 +367,67 @@ template <class R> static R maxwell_central(const int e[3], R rho) {
   return s;
 }
 
+/* Weighted-orthogonal raw-moment basis (WO-MRT; PAPER.md:789-790 names it, SPEC.md:187-195   */
+/* describes it; reading R31).  Definition, written out: the stencil's monomials x^a y^b z^c  */
+/* (the q monomials of the raw basis of reading R2) in graded-lexicographic order (total      */
+/* degree, then a, b, c descending), orthogonalised one after the other by classical         */
+/* Gram-Schmidt under <p, r> = sum_i w_i p(xi_i) r(xi_i) (w = the lattice weights f0):        */
+/*   p_k = x^(e_k) - sum_{j<k} <x^(e_k), p_j> / <p_j, p_j> p_j.                               */
+/* M[k][i] = p_k(xi_i); one rate per p_k in that order.                                        */
+template <class R> static bool build_wo_basis(Method<R> &m) {
+  const int q = m.q;
+  m.wo_mono.clear();
+  for (int deg = 0; deg <= 6; ++deg)
+    for (int a = 2; a >= 0; --a)
+      for (int b = 2; b >= 0; --b)
+        for (int c = 2; c >= 0; --c) {
+          if (a + b + c != deg) continue;
+          bool in_raw = false;  // a monomial of the raw basis (reading R2)
+          for (auto &p : m.basis)
+            for (auto &t : p)
+              if (t.e[0] == a && t.e[1] == b && t.e[2] == c) in_raw = true;
+          if (in_raw) m.wo_mono.push_back({a, b, c});
+        }
+  if ((int)m.wo_mono.size() != q) return false;
+  std::vector<R> V(q * q);  // V[k][i] = x^(e_k)(xi_i)
+  for (int k = 0; k < q; ++k)
+    for (int i = 0; i < q; ++i)
+      V[k * q + i] = ipow(R(m.xi[i][0]), m.wo_mono[k][0]) * ipow(R(m.xi[i][1]), m.wo_mono[k][1]) *
+                     ipow(R(m.xi[i][2]), m.wo_mono[k][2]);
+  m.G.assign(q * q, R(0));
+  std::vector<R> P(q * q, R(0));  // P[k][i] = p_k(xi_i)
+  for (int k = 0; k < q; ++k) {
+    m.G[k * q + k] = R(1);
+    for (int i = 0; i < q; ++i) P[k * q + i] = V[k * q + i];
+    for (int j = 0; j < k; ++j) {
+      R num = 0, den = 0;
+      for (int i = 0; i < q; ++i) {
+        num += m.w[i] * V[k * q + i] * P[j * q + i];
+        den += m.w[i] * P[j * q + i] * P[j * q + i];
+      }
+      const R cf = num / den;
+      for (int l = 0; l < q; ++l) m.G[k * q + l] -= cf * m.G[j * q + l];
+      for (int i = 0; i < q; ++i) P[k * q + i] -= cf * P[j * q + i];
+    }
+  }
+  for (int k = 0; k < q * q; ++k) m.M[k] = P[k];
+  return invert(q, m.M.data(), m.Minv.data());
+}
+
 template <class R>
 static bool build_method(Method<R> &m, int stencil, int space, int eq, int zc, const double *rates,
                          int nrates, double g) {
   m.stencil = stencil;
   m.d = dims_of(stencil);
   m.space = space;
+  // LBM_EQ_ABSOLUTE_F0 (reading R30): eq:MrtUpdateAbsoluteFromZeroCentered
+  // with f0 added to the populations before the transform — which is how this oracle evaluates
+  // the zero-centered absolute regime anyway (collide_cell: fabs = df + f0)
+  if (eq == EQ_ABSOLUTE_F0) {
+    if (!zc) return false;
+    eq = EQ_ABSOLUTE;
+  }
+  if (space == SP_RAW_WO && (eq == EQ_SWE || eq == EQ_DISCRETE || eq == EQ_DISCRETE_DELTA)) return false;
   m.eq = eq;
   m.zc = zc;
   m.g = R(g);
@@ -406,6 +465,7 @@ static bool build_method(Method<R> &m, int stencil, int space, int eq, int zc, c
   }
   m.w.assign(q, 0);
   matvec(q, m.Minv.data(), m0.data(), m.w.data());
+  if (space == SP_RAW_WO && !build_wo_basis(m)) return false;
   // monomial set and R_mono
   m.mono.clear();
   for (auto &p : m.basis)
@@ -521,6 +581,13 @@ template <class R> static R raw_eq_poly(const Method<R> &m, int p, R rho, const 
   for (auto &t : m.basis[p]) s += R(t.c) * maxwell_raw_trunc<R>(t.e, rho, u);
   return s;
 }
+/* WO-MRT: the same truncated Maxwellian raw moments through the Gram-Schmidt coefficients */
+template <class R> static R raw_eq(const Method<R> &m, int p, R rho, const R u[3]) {
+  if (m.space != SP_RAW_WO) return raw_eq_poly(m, p, rho, u);
+  R s = 0;
+  for (int j = 0; j < m.q; ++j) s += m.G[p * m.q + j] * maxwell_raw_trunc<R>(m.wo_mono[j].data(), rho, u);
+  return s;
+}
 template <class R> static R central_eq_poly(const Method<R> &m, int p, R rho) {
   R s = 0;
   for (auto &t : m.basis[p]) s += R(t.c) * maxwell_central<R>(t.e, rho);
@@ -630,12 +697,13 @@ template <class R> static bool collide_cell(const Method<R> &m, const R *fin, R 
     return true;
   }
 
-  if (m.space == SP_RAW) {
+  if (m.space == SP_RAW || m.space == SP_RAW_WO) {
+    if (m.space == SP_RAW_WO && m.forced) return false;  // not provided (lbm.h)
     matvec(q, m.M.data(), fabs_, q0);  // q = M f   (eq:DiscreteRawMomentsDef)
     matvec(q, m.M.data(), FG, qF);
     for (int p = 0; p < q; ++p) {
-      qeq[p] = raw_eq_poly(m, p, rho, u);
-      if (delta) qeq[p] -= raw_eq_poly(m, p, R(1), u0);  // dq_eq = q_eq - q0
+      qeq[p] = raw_eq(m, p, rho, u);
+      if (delta) qeq[p] -= raw_eq(m, p, R(1), u0);  // dq_eq = q_eq - q0
     }
     if (discrete) matvec(q, m.M.data(), fd, qeq);  // q_eq = M f_eq
     for (int p = 0; p < q; ++p)
@@ -754,8 +822,8 @@ template <class R> static bool equilibrium_cell(const Method<R> &m, R rho, const
       for (int i = 0; i < q; ++i) f[i] -= m.w[i];
     return true;
   }
-  if (m.space == SP_POPULATION || m.space == SP_RAW) {
-    for (int p = 0; p < q; ++p) qeq[p] = raw_eq_poly(m, p, rho, u);
+  if (m.space == SP_POPULATION || m.space == SP_RAW || m.space == SP_RAW_WO) {
+    for (int p = 0; p < q; ++p) qeq[p] = raw_eq(m, p, rho, u);
     matvec(q, m.Minv.data(), qeq, f);
   } else {
     R K[27 * 27];
@@ -863,6 +931,23 @@ int oracle_tables(int stencil, int *q_out, int *xi /*[q][3]*/, int *opp, double 
     Minv[k] = (double)m.Minv[k];
   }
   return 0;
+}
+
+/* WO-MRT basis (reading R31): M [q][q] (M[k][i] = p_k(xi_i)), G [q][q] (monomial coefficients),
+   mono [q][3] (the graded-lexicographic monomial exponents) — for pins */
+int oracle_wo_basis(int stencil, double *M, double *G, int *mono) {
+  Method<long double> m;
+  double r[27];
+  for (int k = 0; k < 27; ++k) r[k] = 1.0;
+  const int q = (stencil == ST_D2Q9) ? 9 : (stencil == ST_D3Q19 ? 19 : 27);
+  if (!build_method(m, stencil, SP_RAW_WO, EQ_ABSOLUTE, 0, r, q, 0.0)) return -1;
+  for (int k = 0; k < q * q; ++k) {
+    M[k] = (double)m.M[k];
+    G[k] = (double)m.G[k];
+  }
+  for (int k = 0; k < q; ++k)
+    for (int a = 0; a < 3; ++a) mono[k * 3 + a] = m.wo_mono[k][a];
+  return q;
 }
 
 /* weights in long double precision, returned as (hi, lo) double pairs, for exact pins */

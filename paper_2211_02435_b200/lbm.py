@@ -17,8 +17,9 @@ LIB_PATH = os.path.join(_HERE, "liblbm.so")
 # enums of include/lbm.h
 LBM_OK, LBM_EINVAL, LBM_EUNSUPPORTED, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_ENUMERIC = 0, -1, -2, -3, -4, -5, -6
 LBM_D2Q9, LBM_D3Q19, LBM_D3Q27 = 0, 1, 2
-LBM_SPACE_POPULATION, LBM_SPACE_RAW, LBM_SPACE_CENTRAL, LBM_SPACE_CUMULANT = 0, 1, 2, 3
-LBM_EQ_ABSOLUTE, LBM_EQ_DELTA, LBM_EQ_SWE, LBM_EQ_DISCRETE, LBM_EQ_DISCRETE_DELTA = 0, 1, 2, 3, 4
+LBM_SPACE_POPULATION, LBM_SPACE_RAW, LBM_SPACE_CENTRAL, LBM_SPACE_CUMULANT, LBM_SPACE_RAW_WO = 0, 1, 2, 3, 4
+(LBM_EQ_ABSOLUTE, LBM_EQ_DELTA, LBM_EQ_SWE, LBM_EQ_DISCRETE, LBM_EQ_DISCRETE_DELTA,
+ LBM_EQ_ABSOLUTE_F0) = 0, 1, 2, 3, 4, 5
 LBM_FP64, LBM_FP32 = 0, 1
 LBM_PULL, LBM_AA, LBM_ESOTERIC_PULL, LBM_ESOTERIC_TWIST = 0, 1, 2, 3
 LBM_BC_PERIODIC, LBM_BC_NOSLIP = 0, 1

@@ -112,8 +112,11 @@ def test_admissibility_errors():
     assert st == L.LBM_EUNSUPPORTED
     st, _ = create_status(eq=L.LBM_EQ_DISCRETE_DELTA, zc=1, space=L.LBM_SPACE_CUMULANT)
     assert st == L.LBM_EUNSUPPORTED
-    st, _ = create_status(eq=5)
+    st, _ = create_status(eq=6)
     assert st == L.LBM_EINVAL
+    # literal background-in-population-space form (reading R30): zero-centered only
+    st, _ = create_status(eq=L.LBM_EQ_ABSOLUTE_F0, zc=0, space=L.LBM_SPACE_CENTRAL)
+    assert st == L.LBM_EUNSUPPORTED
     st, _ = create_status(streaming=L.LBM_AA, bc=[[1, 1], [0, 0], [0, 0]], nranks=2, rank=0)
     assert st == L.LBM_EUNSUPPORTED
     st, _ = create_status(streaming=L.LBM_AA, bc=[[1, 1], [0, 0], [0, 0]])

@@ -944,3 +944,115 @@ def test_acoustic_attenuation_pins_bulk_rate(st, space, eq, zc, om_b):
     (G, w), _ = curve_fit(model, np.arange(steps, dtype=np.float64), a, p0=(G0, w0))
     assert abs(G / G0 - 1) < 1e-2, (G, G0)
     assert abs(w / w0 - 1) < 1e-2, (w, w0)
+
+
+# ------------------------------------------------ WO-MRT basis (reading R31) ---
+def hermite_products(stencil, mono):
+    """Closed form of the weighted-orthogonal basis on the tensor-product lattices D2Q9 and
+    D3Q27: prod_a H_{e_a}(xi_a) with H_0 = 1, H_1 = t, H_2 = t^2 - 1/3 (the 1D D1Q3 weights
+    2/3, 1/6, 1/6 make {1, t, t^2 - 1/3} orthogonal; products stay orthogonal)."""
+    xi = oracle.tables(stencil)[0].astype(float)
+    H = [lambda t: np.ones_like(t), lambda t: t, lambda t: t * t - 1.0 / 3.0]
+    rows = []
+    for e in mono:
+        v = np.ones(xi.shape[0])
+        for a in range(3):
+            v = v * H[e[a]](xi[:, a])
+        rows.append(v)
+    return np.array(rows)
+
+
+@pytest.mark.parametrize("st", [W.D2Q9, W.D3Q27])
+def test_wo_basis_is_hermite_on_product_lattices(st):
+    M, G, mono = oracle.wo_basis(st)
+    # graded-lexicographic order of the documented list (include/lbm.h)
+    deg = mono.sum(1)
+    assert (np.diff(deg) >= 0).all() and tuple(mono[0]) == (0, 0, 0)
+    np.testing.assert_allclose(M, hermite_products(st, mono), atol=1e-15, rtol=0)
+
+
+def test_wo_basis_d3q19_orthogonal_and_triangular():
+    """D3Q19 lacks the corners, so its order-4 polynomials are not Hermite products; pin the
+    defining properties: W-orthogonality, monic in the leading monomial (G unit lower
+    triangular in graded order), and the orders <= 2 equal to the Hermite products (every
+    inner product involved is an odd moment or sum_i w_i xi_x^2 xi_y^2 = 1/9).  From order 3
+    on they differ: <x (y^2 - 1/3), x (z^2 - 1/3)> = -1/27 on D3Q19 (no corners)."""
+    st = W.D3Q19
+    M, G, mono = oracle.wo_basis(st)
+    w = oracle.tables(st)[2]
+    gram = M @ np.diag(w) @ M.T
+    np.testing.assert_allclose(gram - np.diag(np.diag(gram)), 0, atol=1e-16)
+    assert (np.diag(gram) > 1e-3).all()
+    np.testing.assert_allclose(np.diag(G), 1.0)
+    np.testing.assert_allclose(np.triu(G, 1), 0.0)
+    low = mono.sum(1) <= 2
+    np.testing.assert_allclose(M[low], hermite_products(st, mono)[low], atol=1e-15)
+    k = [tuple(e) for e in mono].index((1, 0, 2))  # p = x z^2 - x/3 + (x y^2 - x/3)/2 (hand-derived: <xz^2, p_xy2> / <p_xy2, p_xy2> = (-1/27) / (2/27))
+    kk = [tuple(e) for e in mono].index((1, 2, 0))
+    assert abs(G[k, kk] - 0.5) < 1e-15
+    # D3Q19 x^2 y^2 - projection: <x^2y^2, z^2 - 1/3> = -1/27 != 0, so the z^2 term survives
+    k = [tuple(e) for e in mono].index((2, 2, 0))
+    kz = [tuple(e) for e in mono].index((0, 0, 2))
+    assert abs(G[k, kz]) > 1e-3
+
+
+@pytest.mark.parametrize("st", STENCILS)
+def test_wo_collision_eigenvectors(st):
+    """In the weighted-orthogonal basis the collision is diagonal in the W-inner product: the
+    non-conserved perturbation delta_k = w o p_k(xi) (it leaves rho and u unchanged) relaxes
+    as delta_k -> (1 - omega_k) delta_k, for every regime (PAPER.md:271-319 with T = M_wo).
+    D2Q9 / D3Q27: p_k are the Hermite products typed above; D3Q19: the oracle's rows."""
+    xi, opp, w, M, Minv = oracle.tables(st)
+    Mw, G, mono = oracle.wo_basis(st)
+    P = hermite_products(st, mono) if st != W.D3Q19 else Mw
+    rates = W.rates_random(st, seed=11)
+    rng = np.random.default_rng(4)
+    n = 6
+    rho = 1 + rng.uniform(-0.04, 0.04, n)
+    u = rng.uniform(-0.08, 0.08, (n, 3))
+    if W.DIM_OF[st] == 2:
+        u[:, 2] = 0
+    d = W.DIM_OF[st]
+    for eq, zc in [(W.EQ_ABSOLUTE, 0), (W.EQ_DELTA, 1), (W.EQ_ABSOLUTE, 1), (W.EQ_ABSOLUTE_F0, 1)]:
+        feq = oracle.equilibrium(st, W.RAW_WO, eq, zc, rho, u)
+        np.testing.assert_allclose(oracle.collide(st, W.RAW_WO, eq, zc, rates, feq), feq, atol=1e-16)
+        for k in range(1 + d, W.Q_OF[st]):
+            delta = 1e-3 * w * P[k]
+            out = oracle.collide(st, W.RAW_WO, eq, zc, rates, feq + delta)
+            np.testing.assert_allclose(out, feq + (1 - rates[k]) * delta, atol=2e-16, rtol=0,
+                                       err_msg=f"eq {eq} zc {zc} polynomial {k} {mono[k]}")
+
+
+@pytest.mark.parametrize("st", STENCILS)
+def test_wo_equal_rates_is_bgk(st):
+    """All rates equal: WO-MRT = raw MRT = BGK with the method's truncated-raw f_eq."""
+    fa = random_cells(st, 20)
+    om = 1.37
+    for eq, zc in ALL_REGIMES:
+        w = oracle.tables(st)[2]
+        fin = fa - w if zc else fa
+        a = oracle.collide(st, W.RAW_WO, eq, zc, np.full(W.Q_OF[st], om), fin)
+        b = oracle.collide(st, W.POPULATION, eq, zc, [om], fin)
+        np.testing.assert_allclose(a, b, atol=2e-16, rtol=0)
+
+
+def test_wo_tgv_decay_and_regimes():
+    """R-WO-MRT on D2Q9 (second-order polynomials at omega_s, the rest 1) decays at
+    exp(-4 nu k^2 t) within 1 %, and the literal population-space background
+    (LBM_EQ_ABSOLUTE_F0, reading R30) is admitted only with zero-centered storage."""
+    st, L, steps, nu = W.D2Q9, 48, 300, 0.05
+    om = W.omega_from_nu(nu)
+    rho, u = W.tgv_fields(L, L, 1, 0.05)
+    for eq, zc in [(W.EQ_DELTA, 1), (W.EQ_ABSOLUTE_F0, 1)]:
+        feq = oracle.equilibrium(st, W.RAW_WO, eq, zc, rho.reshape(-1), u.reshape(3, -1).T)
+        sim = oracle.Sim(st, W.RAW_WO, eq, zc, W.wo_regularized_rates(st, om), (L, L, 1))
+        sim.set(np.ascontiguousarray(feq.T.reshape(9, 1, L, L)))
+        r0, u0 = sim.macroscopic()
+        e0 = (r0 * (u0 ** 2).sum(0)).sum()
+        sim.step(steps)
+        r1, u1 = sim.macroscopic()
+        ratio = (r1 * (u1 ** 2).sum(0)).sum() / e0
+        ref = W.tgv_energy_ratio(nu, L, steps)
+        assert abs(ratio / ref - 1) < 1e-2, (eq, ratio, ref)
+    with pytest.raises(ValueError):
+        oracle.Sim(st, W.CENTRAL, W.EQ_ABSOLUTE_F0, 0, W.rate_set_p(st), (8, 8, 1))

@@ -26,9 +26,9 @@ STENCILS = {"D2Q9": D2Q9, "D3Q19": D3Q19, "D3Q27": D3Q27}
 Q_OF = {D2Q9: 9, D3Q19: 19, D3Q27: 27}
 DIM_OF = {D2Q9: 2, D3Q19: 3, D3Q27: 3}
 
-POPULATION, RAW, CENTRAL, CUMULANT = 0, 1, 2, 3
+POPULATION, RAW, CENTRAL, CUMULANT, RAW_WO = 0, 1, 2, 3, 4
 SPACES = {"POPULATION": POPULATION, "RAW": RAW, "CENTRAL": CENTRAL, "CUMULANT": CUMULANT}
-EQ_ABSOLUTE, EQ_DELTA, EQ_SWE, EQ_DISCRETE, EQ_DISCRETE_DELTA = 0, 1, 2, 3, 4
+EQ_ABSOLUTE, EQ_DELTA, EQ_SWE, EQ_DISCRETE, EQ_DISCRETE_DELTA, EQ_ABSOLUTE_F0 = 0, 1, 2, 3, 4, 5
 PERIODIC, NOSLIP = 0, 1
 
 SEED = 221102435
@@ -88,6 +88,20 @@ def rate_set_p(stencil: int) -> np.ndarray:
 def regularized_rates(stencil: int, omega_s: float) -> np.ndarray:
     """R- methods: every rate but the shear rate set to one."""
     return rates_from_groups(stencil, {"s": omega_s})
+
+
+def wo_second_order(stencil: int) -> list:
+    """Indices of the second-order polynomials of the WO-MRT basis (graded-lexicographic
+    order, include/lbm.h LBM_SPACE_RAW_WO): D2Q9 x^2, xy, y^2; 3D x^2, xy, xz, y^2, yz, z^2."""
+    return [3, 4, 5] if DIM_OF[stencil] == 2 else [4, 5, 6, 7, 8, 9]
+
+
+def wo_regularized_rates(stencil: int, omega_s: float) -> np.ndarray:
+    """R-WO-MRT: every second-order polynomial of the WO basis at omega_s (in that basis the
+    x^2 - 1/3 ... polynomials carry shear AND bulk viscosity), every other rate one."""
+    r = np.ones(Q_OF[stencil])
+    r[wo_second_order(stencil)] = omega_s
+    return r
 
 
 def rates_random(stencil: int, seed: int = SEED, lo: float = 0.7, hi: float = 1.9) -> np.ndarray:
