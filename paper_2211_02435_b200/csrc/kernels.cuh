@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 
 #include "collide.cuh"
+#include "tma.cuh"
 
 namespace lbm {
 
@@ -637,6 +638,149 @@ __global__ void __launch_bounds__(Tile2<TX, TY>::THREADS, MINB)
       sfor<S::Q>([&](auto i) { dst[own + (long long)i * g.pop] = f[i]; });
     }
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Temporal blocking with TMA staging (sm_100a): the same two-step sweep as k_pull2, but the
+// step-t populations of the next plane are not prefetched into registers by every thread.
+// One thread issues, per plane and population i, a cp.async.bulk.tensor box load of the
+// halo-extended tile shifted by -xi_i in y from plane k - xi_z,i into a shared-memory stage
+// (the pull gather done by the TMA unit; the box start along x must be 16-byte aligned, so the
+// x shift is applied when the box is read); an mbarrier counts the bytes.  The per-thread
+// prefetch registers and the per-population address arithmetic of k_pull2 disappear, and the
+// loads of plane k + STAGES are in flight during the collisions of plane k.
+// The step-(t+1) ring is trimmed to what the step-(t+2) pull still reads: the populations
+// with xi_z = +1 are read one plane later (3 planes live), xi_z = 0 in the same plane (2),
+// xi_z = -1 one plane earlier (1) — 3 n+ + 2 n0 + n- slots instead of 3 Q.
+// The TMA does not wrap: at the periodic x / y faces the box elements that fall outside the
+// lattice arrive zero-filled and the (CTA-uniform) edge tiles reload them from the wrapped
+// address.  Same collide() as k_pull / k_pull2.
+// ---------------------------------------------------------------------------
+template <class S, class real, int TX, int TY, int STAGES>
+struct TmaTile {
+  static constexpr int HX = TX + 2, HY = TY + 2, HW = HX * HY;
+  static constexpr int THREADS = (HW + 31) / 32 * 32;
+  // the box starts at x0 - A (16-byte aligned: the TMA faults on an unaligned inner start) and
+  // covers the pull sources x0 - 2 .. x0 + TX + 1 of the halo cells, in 16-byte multiples
+  static constexpr int A = (int)(16 / sizeof(real));
+  static constexpr int BX = (TX + A + 2 + A - 1) / A * A;
+  static constexpr int BOX = BX * HY;  // elements of one population box
+  // box stride in shared memory, 128-byte aligned destinations
+  static constexpr int BOXP = (int)(((BOX * sizeof(real) + 127) / 128 * 128) / sizeof(real));
+  static constexpr int STAGE = S::Q * BOXP;  // elements of one staged plane
+  static constexpr unsigned STAGE_TX = (unsigned)(S::Q * BOX * sizeof(real));  // bytes the TMA writes
+  static constexpr int slots(int i) { return S::mz(i) > 0 ? 3 : (S::mz(i) == 0 ? 2 : 1); }
+  static constexpr int ring_off(int i) {
+    int o = 0;
+    for (int j = 0; j < i; ++j) o += slots(j) * HW;
+    return o;
+  }
+  static constexpr int RING = ring_off(S::Q);  // elements of the trimmed ring
+  static constexpr size_t SMEM = (size_t)(STAGES * STAGE + RING) * sizeof(real) + 16 * STAGES;
+};
+
+template <class S, int SPACE, int REG, class real, int RS, int TX, int TY, int MINB = 1, bool RANGE = false,
+          int STAGES = 1>
+__global__ void __launch_bounds__(TmaTile<S, real, TX, TY, STAGES>::THREADS, MINB)
+    k_pull2_tma(const real *__restrict__ src, real *__restrict__ dst, const GridParams g, const Rates<real> r,
+                const real swe_g, const Force<real> fr, const __grid_constant__ CUtensorMap tmap) {
+  using T = TmaTile<S, real, TX, TY, STAGES>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  real *stage = reinterpret_cast<real *>(smem_raw);  // [STAGES][Q][BOXP]
+  real *ring = stage + STAGES * T::STAGE;            // trimmed ring
+  uint64_t *bar = reinterpret_cast<uint64_t *>(ring + T::RING);
+  const int t = threadIdx.x;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const bool act1 = t < T::HW;
+  const int hx = t % T::HX, hy = t / T::HX;
+  const bool act2 = t < TX * TY;
+  const int ix = t % TX, iy = t / TX;
+  const int n = g.nzl;
+  const int zb = RANGE ? g.zbegin : 0, zn = RANGE ? g.zcount : n;
+  const int p0 = zb + (int)((long long)zn * blockIdx.z / gridDim.z);
+  const int p1 = zb + (int)((long long)zn * (blockIdx.z + 1) / gridDim.z);
+  auto zw = [&](int k) {
+    if constexpr (RANGE) return k;
+    else return wrapi(k, n);
+  };
+  // generic address of the __grid_constant__ parameter itself (a copy would live in local memory,
+  // which the TMA cannot read)
+  const CUtensorMap *map = &tmap;
+  // periodic wrap at the x / y faces: only tiles touching a face see out-of-range box elements
+  const bool edge = x0 == 0 || x0 + TX >= g.nx || y0 == 0 || y0 + TY >= g.ny;
+  if (t == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(bar + s, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  // plane k of step t into stage slot b: box of population i from plane k - xi_z at -xi_i
+  auto issue = [&](int k, int b) {
+    const int zc = zw(k);
+    int zz[3];
+#pragma unroll
+    for (int s = -1; s <= 1; ++s) zz[s + 1] = zw(zc + s) + 1;
+    real *st = stage + b * T::STAGE;
+    mbar_arrive_expect_tx(bar + b, T::STAGE_TX);
+    sfor<S::Q>([&](auto i) {
+      constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+      (void)cx;
+      tma_load_4d(st + i * T::BOXP, map, x0 - T::A, y0 - 1 - cy, (int)i, zz[1 - cz], bar + b);
+    });
+  };
+  if (t == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s)
+      if (p0 - 1 + s <= p1) issue(p0 - 1 + s, s);
+  }
+  for (int k = p0 - 1; k <= p1; ++k) {
+    const int it = k - (p0 - 1);
+    const int b = it % STAGES;
+    real f[S::Q];
+    if (act1) {
+      mbar_wait(bar + b, (uint32_t)((it / STAGES) & 1));
+      const real *st = stage + b * T::STAGE + hy * T::BX + hx + T::A - 1;
+      sfor<S::Q>([&](auto i) { f[i] = st[i * T::BOXP - S::mx(i)]; });
+      if (edge) {  // out-of-range sources: reload from the wrapped address
+        const int gx = x0 - 1 + hx, gy = y0 - 1 + hy;
+        const int zc = zw(k);
+        sfor<S::Q>([&](auto i) {
+          constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+          const int sx = gx - cx, sy = gy - cy;
+          if (sx < 0 || sx >= g.nx || sy < 0 || sy >= g.ny) {
+            const long long a = (long long)(zw(zc - cz) + 1) * g.plane + (long long)i * g.pop +
+                                (long long)wrapi(sy, g.ny) * g.pitch + wrapi(sx, g.nx);
+            f[i] = ld_nc(src + a);
+          }
+        });
+      }
+    }
+    __syncthreads();  // stage b consumed by every thread; ring slots of plane k free
+    if (t == 0 && k + STAGES <= p1) {
+      fence_proxy_async_smem();
+      issue(k + STAGES, b);
+    }
+    if (act1) {
+      collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
+      sfor<S::Q>([&](auto i) {
+        constexpr int ns = T::slots(i);
+        ring[T::ring_off(i) + ((k + 3) % ns) * T::HW + t] = f[i];  // k >= -1
+      });
+    }
+    __syncthreads();
+    if (k >= p0 + 1 && act2) {
+      const int p = k - 1;  // plane of step t+2
+      real h[S::Q];
+      sfor<S::Q>([&](auto i) {
+        constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
+        constexpr int ns = T::slots(i);
+        h[i] = ring[T::ring_off(i) + ((p - cz + 3) % ns) * T::HW + (iy + 1 - cy) * T::HX + (ix + 1 - cx)];
+      });
+      collide<S, SPACE, REG, real, RS>(h, r, swe_g, fr);
+      const long long own = (long long)(p + 1) * g.plane + (long long)(y0 + iy) * g.pitch + (x0 + ix);
+      sfor<S::Q>([&](auto i) { dst[own + (long long)i * g.pop] = h[i]; });
+    }
   }
 }
 
