@@ -57,6 +57,9 @@ CONFIGS = {
     "c3twist": dict(stencil=W.D3Q27, space=W.CENTRAL, eq=W.EQ_ABSOLUTE, zc=1, prec=0, streaming=3,
                     shape=lambda n: (384, 384, 384), slab=2, scaling="strong",
                     desc="D3Q27 central-moment MRT TGV 384^3, fp64, zero-centered + absolute eq, Esoteric Twist"),
+    "c3push": dict(stencil=W.D3Q27, space=W.CENTRAL, eq=W.EQ_ABSOLUTE, zc=1, prec=0, streaming=4,
+                   shape=lambda n: (384, 384, 384), slab=2, scaling="strong",
+                   desc="D3Q27 central-moment MRT TGV 384^3, fp64, zero-centered + absolute eq, Esoteric Push"),
     "c4disc": dict(stencil=W.D3Q27, space=W.CUMULANT, eq=W.EQ_DISCRETE, zc=1, prec=0, streaming=0,
                    shape=lambda n: (1024, 1024, 128 * n), slab=2, scaling="weak",
                    desc="D3Q27 cumulant TGV 1024x1024x(128*N), fp64, zero-centered, DISCRETE f_eq (R29), pull"),

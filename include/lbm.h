@@ -113,8 +113,17 @@ typedef enum { LBM_FP64 = 0, LBM_FP32 = 1 } lbm_precision;
 /* Streaming patterns: two-grid pull; in place: AA (Bailey 2009; several
    ranks with periodic faces, or one rank with periodic and/or no-slip faces), Esoteric Pull (Lehmann 2022; single rank, periodic) and Esoteric
    Twist (Geier & Schoenherr 2017, reading R28: every cell touches only its positive octant
-   x + {0,1}^d; single rank, periodic).  All three in-place patterns move the same bytes. */
-typedef enum { LBM_PULL = 0, LBM_AA = 1, LBM_ESOTERIC_PULL = 2, LBM_ESOTERIC_TWIST = 3 } lbm_streaming;
+   x + {0,1}^d; single rank, periodic) and Esoteric Push (Lehmann 2022, reading R32: the mirror
+   of Esoteric Pull — in each opposite pair the member stored at its streaming destination is
+   the second one, opp i > i, so a cell touches its negative half-neighbourhood; single rank,
+   periodic).  All four in-place patterns move the same bytes (PAPER.md:861-862 lists them). */
+typedef enum {
+  LBM_PULL = 0,
+  LBM_AA = 1,
+  LBM_ESOTERIC_PULL = 2,
+  LBM_ESOTERIC_TWIST = 3,
+  LBM_ESOTERIC_PUSH = 4
+} lbm_streaming;
 typedef enum { LBM_BC_PERIODIC = 0, LBM_BC_NOSLIP = 1 } lbm_bc;
 typedef enum {
   LBM_REGION_ALL = 0,

@@ -280,13 +280,23 @@ __global__ void __launch_bounds__(BLOCK_X, (PAT == PAT_AA_ODD ? 5 : 1))
 //                        mem(x + xi_i, i) = f*_i,   mem(x, opp) = f*_opp
 // (state E: mem(x + xi_i, i) = f*_i(x), mem(x, opp) = f*_opp(x); state O swaps the slots;
 // every slot is read and written by one cell only: race-free in place.)
+// Esoteric Push (same source; reading R32): the mirror image — the LEAD member of each pair,
+// the one stored at its streaming destination x + xi (pushed by the write) while the other is
+// pulled by the read, is the second member opp i (i > opp i) instead of the first, so a cell
+// touches its negative half-neighbourhood x - xi_i.  Same kernel with `lead` mirrored.
 // ---------------------------------------------------------------------------
 template <class S>
 __host__ __device__ constexpr bool first_of_pair(int i) {
   return i != 0 && i < S::opp(i);
 }
+// the lead member of a pair: Esoteric Pull the first, Esoteric Push (MIRROR) the second
+template <class S, bool MIRROR>
+__host__ __device__ constexpr bool eso_lead(int i) {
+  return MIRROR ? (i != 0 && i > S::opp(i)) : first_of_pair<S>(i);
+}
 
 enum { PAT_ESO_EVEN = 3, PAT_ESO_ODD = 4 };
+enum { PAT_ESOP_EVEN = 7, PAT_ESOP_ODD = 8 };  // Esoteric Push
 
 template <class S, int SPACE, int REG, class real, int PAT, int RS = RS_GENERAL>
 __global__ void __launch_bounds__(BLOCK_X)
@@ -295,7 +305,8 @@ __global__ void __launch_bounds__(BLOCK_X)
   if (x >= g.nx) return;
   const int y = blockIdx.y;
   const int zl = g.zbegin + blockIdx.z;
-  constexpr bool odd = (PAT == PAT_ESO_ODD);
+  constexpr bool odd = (PAT == PAT_ESO_ODD || PAT == PAT_ESOP_ODD);
+  constexpr bool mirror = (PAT == PAT_ESOP_ODD || PAT == PAT_ESOP_EVEN);
   const long long own = (long long)(zl + 1) * g.plane + (long long)y * g.pitch + x;
   int xs[3], ys[3];
   long long zo[3];
@@ -308,7 +319,7 @@ __global__ void __launch_bounds__(BLOCK_X)
   real f[S::Q];
   f[0] = ld_nc(mem + own);
   sfor<S::Q>([&](auto i) {
-    if constexpr (first_of_pair<S>(i)) {
+    if constexpr (eso_lead<S, mirror>(i)) {
       constexpr int o = S::opp(i), cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
       const long long nb = zo[1 + cz] + ys[1 + cy] + xs[1 + cx];  // cell x + xi_i
       f[i] = ld_nc(mem + own + (long long)(odd ? i : o) * g.pop);
@@ -318,7 +329,7 @@ __global__ void __launch_bounds__(BLOCK_X)
   collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
   mem[own] = f[0];
   sfor<S::Q>([&](auto i) {
-    if constexpr (first_of_pair<S>(i)) {
+    if constexpr (eso_lead<S, mirror>(i)) {
       constexpr int o = S::opp(i), cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
       const long long nb = zo[1 + cz] + ys[1 + cy] + xs[1 + cx];
       mem[nb + (long long)(odd ? o : i) * g.pop] = f[i];
@@ -368,8 +379,8 @@ __global__ void __launch_bounds__(BLOCK_X)
 // ---------------------------------------------------------------------------
 // helpers: init from macroscopic fields, canonical get/set, macroscopic moments,
 // collision-only test kernel, finiteness probe.  'pat' = lbm_streaming (0 pull, 1 AA,
-// 2 Esoteric Pull, 3 Esoteric Twist); 'state' for AA: 0 = A, 1 = B; for Esoteric Pull:
-// 0 = E, 1 = O; for Esoteric Twist: 0 = T0, 1 = T1.
+// 2 Esoteric Pull, 3 Esoteric Twist, 4 Esoteric Push); 'state' for AA: 0 = A, 1 = B; for
+// Esoteric Pull / Push: 0 = E, 1 = O; for Esoteric Twist: 0 = T0, 1 = T1.
 // ---------------------------------------------------------------------------
 template <class S>
 struct Canon {
@@ -397,7 +408,8 @@ struct Canon {
     }
     if constexpr (i == 0) return own;
     const int slot = state == 0 ? i : S::opp(i);
-    return (first_of_pair<S>(i) ? nb : own) + (long long)slot * g.pop;
+    const bool lead = pat == 4 ? eso_lead<S, true>(i) : first_of_pair<S>(i);  // Esoteric Push / Pull
+    return (lead ? nb : own) + (long long)slot * g.pop;
   }
 };
 

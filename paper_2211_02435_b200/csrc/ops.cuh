@@ -24,7 +24,8 @@ struct Ops {
   // pull stream–collide of planes [zbegin, zbegin + nplanes) from src into dst
   void (*pull)(const void *src, void *dst, const GridParams &g, const void *params, double swe_g, int bb,
                int nplanes, cudaStream_t s);
-  // in-place step (PAT_AA_EVEN / PAT_AA_ODD / PAT_ESO_EVEN / PAT_ESO_ODD / PAT_TW0 / PAT_TW1),
+  // in-place step (PAT_AA_EVEN / PAT_AA_ODD / PAT_ESO_EVEN / PAT_ESO_ODD / PAT_ESOP_EVEN /
+  // PAT_ESOP_ODD / PAT_TW0 / PAT_TW1),
   // planes [zbegin, zbegin + nplanes)
   void (*aa)(void *mem, const GridParams &g, const void *params, double swe_g, int pattern, int nplanes,
              cudaStream_t s);
@@ -153,6 +154,14 @@ struct OpsImpl {
         break;
       case PAT_ESO_EVEN:
         k_eso<S, SPACE, REG, real, PAT_ESO_EVEN, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,
+                                                                                            (real)swe_g, p.force);
+        break;
+      case PAT_ESOP_EVEN:
+        k_eso<S, SPACE, REG, real, PAT_ESOP_EVEN, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,
+                                                                                             (real)swe_g, p.force);
+        break;
+      case PAT_ESOP_ODD:
+        k_eso<S, SPACE, REG, real, PAT_ESOP_ODD, RS><<<cell_grid(g, nplanes), BLOCK_X, 0, s>>>(m, g, p.rates,
                                                                                             (real)swe_g, p.force);
         break;
       case PAT_TW0:
@@ -298,6 +307,8 @@ struct OpsImpl {
       e = cudaFuncGetAttributes(&a, k_aa<S, SPACE, REG, real, PAT_AA_EVEN, RS>);
     } else if (which == 10 + PAT_ESO_ODD) {
       e = cudaFuncGetAttributes(&a, k_eso<S, SPACE, REG, real, PAT_ESO_ODD, RS>);
+    } else if (which == 10 + PAT_ESOP_ODD) {
+      e = cudaFuncGetAttributes(&a, k_eso<S, SPACE, REG, real, PAT_ESOP_ODD, RS>);
     } else if (which == 10 + PAT_TW0) {
       e = cudaFuncGetAttributes(&a, k_twist<S, SPACE, REG, real, PAT_TW0, RS>);
     }

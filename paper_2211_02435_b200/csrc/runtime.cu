@@ -423,6 +423,7 @@ bool use_graphs(const lbm_ctx *c) {
 int inplace_pattern(const lbm_ctx *c, int state) {
   if (c->streaming == LBM_AA) return state == 0 ? lbm::PAT_AA_ODD : lbm::PAT_AA_EVEN;
   if (c->streaming == LBM_ESOTERIC_TWIST) return state == 0 ? lbm::PAT_TW0 : lbm::PAT_TW1;
+  if (c->streaming == LBM_ESOTERIC_PUSH) return state == 0 ? lbm::PAT_ESOP_ODD : lbm::PAT_ESOP_EVEN;
   return state == 0 ? lbm::PAT_ESO_ODD : lbm::PAT_ESO_EVEN;
 }
 int inplace_pattern(const lbm_ctx *c) { return inplace_pattern(c, c->aa_state); }
@@ -929,7 +930,7 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   }
   if (D.precision != LBM_FP64 && D.precision != LBM_FP32) return fail(nullptr, LBM_EINVAL, "unknown precision");
   if (D.streaming != LBM_PULL && D.streaming != LBM_AA && D.streaming != LBM_ESOTERIC_PULL &&
-      D.streaming != LBM_ESOTERIC_TWIST)
+      D.streaming != LBM_ESOTERIC_TWIST && D.streaming != LBM_ESOTERIC_PUSH)
     return fail(nullptr, LBM_EINVAL, "unknown streaming");
   if (D.nranks < 1 || D.rank < 0 || D.rank >= D.nranks) return fail(nullptr, LBM_EINVAL, "bad rank/nranks");
   const int slab_extent = two_d ? D.ny : D.nz;
@@ -942,9 +943,10 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
   const bool multi = D.nranks > 1 || D.nccl_id != nullptr;
   if (D.streaming == LBM_AA && any_wall && multi)
     return fail(nullptr, LBM_EUNSUPPORTED, "AA streaming with no-slip faces is provided for a single rank");
-  if ((D.streaming == LBM_ESOTERIC_PULL || D.streaming == LBM_ESOTERIC_TWIST) && (any_wall || multi))
+  if ((D.streaming == LBM_ESOTERIC_PULL || D.streaming == LBM_ESOTERIC_TWIST || D.streaming == LBM_ESOTERIC_PUSH) &&
+      (any_wall || multi))
     return fail(nullptr, LBM_EUNSUPPORTED,
-                "Esoteric Pull / Twist are provided for a single rank with periodic faces");
+                "Esoteric Pull / Push / Twist are provided for a single rank with periodic faces");
   if ((D.dev_alloc == nullptr) != (D.dev_free == nullptr))
     return fail(nullptr, LBM_EINVAL, "dev_alloc and dev_free must be given together");
 
@@ -1309,8 +1311,8 @@ lbm_status lbm_swap(lbm_ctx *c) {
 
 lbm_status lbm_get_halo(lbm_ctx *c, int which, lbm_halo *out) {
   if (!c || !out) return LBM_EINVAL;
-  if (c->streaming == LBM_ESOTERIC_PULL || c->streaming == LBM_ESOTERIC_TWIST)
-    return fail(c, LBM_EUNSUPPORTED, "Esoteric Pull / Twist are single-rank");
+  if (c->streaming == LBM_ESOTERIC_PULL || c->streaming == LBM_ESOTERIC_TWIST || c->streaming == LBM_ESOTERIC_PUSH)
+    return fail(c, LBM_EUNSUPPORTED, "Esoteric Pull / Push / Twist are single-rank");
   if (which == 2 && !c->peer_tb_cap)
     return fail(c, LBM_EUNSUPPORTED, "no scratch halo: the context does not run two-step sweeps across ranks");
   if (which < 0 || which > 2) return fail(c, LBM_EINVAL, "which must be 0, 1 or 2");
@@ -1354,8 +1356,8 @@ lbm_status lbm_sync(lbm_ctx *c) {
 
 lbm_status lbm_peer_export(lbm_ctx *c, lbm_peer_info *out) {
   if (!c || !out) return LBM_EINVAL;
-  if (c->streaming == LBM_ESOTERIC_PULL || c->streaming == LBM_ESOTERIC_TWIST)
-    return fail(c, LBM_EUNSUPPORTED, "Esoteric Pull / Twist are single-rank");
+  if (c->streaming == LBM_ESOTERIC_PULL || c->streaming == LBM_ESOTERIC_TWIST || c->streaming == LBM_ESOTERIC_PUSH)
+    return fail(c, LBM_EUNSUPPORTED, "Esoteric Pull / Push / Twist are single-rank");
   if (c->nranks < 2) return fail(c, LBM_EUNSUPPORTED, "the fused halo push needs nranks > 1");
   LBM_CUDA(c, cudaSetDevice(c->device));
   if (!c->peer_flags) {

@@ -21,7 +21,7 @@ LBM_SPACE_POPULATION, LBM_SPACE_RAW, LBM_SPACE_CENTRAL, LBM_SPACE_CUMULANT, LBM_
 (LBM_EQ_ABSOLUTE, LBM_EQ_DELTA, LBM_EQ_SWE, LBM_EQ_DISCRETE, LBM_EQ_DISCRETE_DELTA,
  LBM_EQ_ABSOLUTE_F0) = 0, 1, 2, 3, 4, 5
 LBM_FP64, LBM_FP32 = 0, 1
-LBM_PULL, LBM_AA, LBM_ESOTERIC_PULL, LBM_ESOTERIC_TWIST = 0, 1, 2, 3
+LBM_PULL, LBM_AA, LBM_ESOTERIC_PULL, LBM_ESOTERIC_TWIST, LBM_ESOTERIC_PUSH = 0, 1, 2, 3, 4
 LBM_BC_PERIODIC, LBM_BC_NOSLIP = 0, 1
 LBM_FORCE_GUO, LBM_FORCE_HE = 0, 1
 LBM_REGION_ALL, LBM_REGION_BOUNDARY, LBM_REGION_INTERIOR = 0, 1, 2

@@ -104,7 +104,11 @@ def test_admissibility_errors():
     assert st == L.LBM_EUNSUPPORTED
     st, _ = create_status(streaming=L.LBM_ESOTERIC_TWIST, bc=[[1, 1], [0, 0], [0, 0]])
     assert st == L.LBM_EUNSUPPORTED
-    st, _ = create_status(streaming=4)
+    st, _ = create_status(streaming=L.LBM_ESOTERIC_PUSH, nranks=2, rank=0)
+    assert st == L.LBM_EUNSUPPORTED
+    st, _ = create_status(streaming=L.LBM_ESOTERIC_PUSH, bc=[[0, 0], [1, 1], [0, 0]])
+    assert st == L.LBM_EUNSUPPORTED
+    st, _ = create_status(streaming=5)
     assert st == L.LBM_EINVAL
     # discrete equilibrium (reading R29): its delta form needs zero-centered storage and is
     # incompatible with cumulants, like the continuous one
