@@ -78,6 +78,10 @@ CONFIGS = {
     "c5": dict(stencil=W.D2Q9, space=W.CENTRAL, eq=W.EQ_SWE, zc=0, prec=0, streaming=0,
                shape=lambda n: (8192, 8192, 1), slab=1, scaling="strong",
                desc="D2Q9 shallow-water CM LBM (Zhou eq.) dam break 8192^2, fp64, absolute, pull"),
+    "c5zc": dict(stencil=W.D2Q9, space=W.CENTRAL, eq=W.EQ_SWE, zc=1, prec=0, streaming=0,
+                 shape=lambda n: (8192, 8192, 1), slab=1, scaling="strong",
+                 desc="D2Q9 shallow-water CM LBM (Zhou eq.) dam break 8192^2, fp64, zero-centered about the "
+                      "rest state (R33), pull"),
 }
 
 

@@ -367,6 +367,8 @@ template <class R> static R maxwell_central(const int e[3], R rho) {
   return s;
 }
 
+template <class R> static bool equilibrium_cell(const Method<R> &m, R rho, const R u[3], R *f);
+
 /* Weighted-orthogonal raw-moment basis (WO-MRT; PAPER.md:789-790 names it, SPEC.md:187-195   */
 /* describes it; reading R31).  Definition, written out: the stencil's monomials x^a y^b z^c  */
 /* (the q monomials of the raw basis of reading R2) in graded-lexicographic order (total      */
@@ -483,6 +485,17 @@ static bool build_method(Method<R> &m, int stencil, int space, int eq, int zc, c
       m.Rmono[p * q + k] += R(t.c);
     }
   if (!invert(q, m.Rmono.data(), m.Rmono_inv.data())) return false;
+  // zero-centered shallow water (reading R33): the
+  // background is the method's own rest state f0 = f_eq(h0 = 1, u = 0), h = h0 + sum df:
+  // Zhou's discrete equilibrium (eq:DiscreteShallowWaterEquilibrium) for
+  // central moments, the Maxwellian at c_s^2 = g h0 / 2 for cumulants
+  if (eq == EQ_SWE && zc) {
+    const R u0[3] = {0, 0, 0};
+    m.zc = 0;
+    const bool ok = equilibrium_cell(m, R(1), u0, m.w.data());
+    m.zc = zc;
+    if (!ok) return false;
+  }
   m.ok = true;
   return true;
 }
@@ -813,7 +826,8 @@ template <class R> static bool equilibrium_cell(const Method<R> &m, R rho, const
   R qeq[27];
   if (m.eq == EQ_SWE && m.space != SP_CUMULANT) {
     swe_equilibrium(m, rho, u, f);
-    if (m.zc) return false;
+    if (m.zc)
+      for (int i = 0; i < q; ++i) f[i] -= m.w[i];
     return true;
   }
   if (m.eq == EQ_DISCRETE || m.eq == EQ_DISCRETE_DELTA) {  // reading R29

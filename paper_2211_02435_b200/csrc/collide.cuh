@@ -704,6 +704,23 @@ __device__ __forceinline__ void add_background(real (&c)[NC], real sgn) {
   });
 }
 
+// Zero-centered shallow water (reading R33): the background is the method's
+// own rest state f0 = f_eq(h0 = 1, u = 0) — Zhou's discrete equilibrium (SPACE_SWE,
+// PAPER.md:1001-1012) or the Maxwellian at cs2 = g h0 / 2 (SPACE_SWE_K).
+// Its non-zero raw moments besides m_00 = 1: m_20 = m_02 = g/2; m_22 = g/6 (Zhou) or
+// (g/2)^2 (Maxwellian).
+template <int SPACE, class real>
+__device__ __forceinline__ real swe_bg_m22(real g) {
+  if constexpr (SPACE == SPACE_SWE_K) return real(0.25) * g * g;
+  else return g * real(1.0 / 6.0);
+}
+template <int SPACE, int NC, class real>
+__device__ __forceinline__ void add_background_swe(real (&c)[NC], real sgn, real g) {
+  c[E(2, 0, 0)] = fma(sgn, real(0.5) * g, c[E(2, 0, 0)]);
+  c[E(0, 2, 0)] = fma(sgn, real(0.5) * g, c[E(0, 2, 0)]);
+  c[E(2, 2, 0)] = fma(sgn, swe_bg_m22<SPACE>(g), c[E(2, 2, 0)]);
+}
+
 // --------------------------------------------------------------------------
 // the collision of one cell: f in/out in the documented population order,
 // STORED form (delta f for REG_DELTA / REG_ZC_ABS).
@@ -960,8 +977,10 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
       uy = fma(real(0.5) * fr.F[1], inv, uy);
       uz = fma(real(0.5) * fr.F[2], inv, uz);
     }
+    constexpr bool SWEZ = (SPACE == SPACE_SWE || SPACE == SPACE_SWE_K);
     if constexpr (REG == REG_ZC_ABS) {  // q = T(df + f0): add m0 = M f0
-      add_background<NC>(c, real(1));
+      if constexpr (SWEZ) add_background_swe<SPACE>(c, real(1), swe_g);
+      else add_background<NC>(c, real(1));
       c[0] = rho;
     }
     // source term q^F = (I - S/2) T(F^G) added after relaxation (FORCED only)
@@ -1060,7 +1079,10 @@ __device__ __forceinline__ void collide(real (&f)[S::Q], const Rates<real> &r, r
       // ---- central -> raw
       if constexpr (S::D == 3) bin_bwd3(c, ux, uy, uz); else bin_bwd2(c, ux, uy);
     }
-    if constexpr (REG == REG_ZC_ABS) add_background<NC>(c, real(-1));
+    if constexpr (REG == REG_ZC_ABS) {
+      if constexpr (SWEZ) add_background_swe<SPACE>(c, real(-1), swe_g);
+      else add_background<NC>(c, real(-1));
+    }
     // conserved raw moments pass through unchanged, the momentum gains the
     // force: m*_100 = rho u_x + F_x/2 = j_x + F_x
     c[0] = m000;
@@ -1100,6 +1122,10 @@ __device__ __forceinline__ void equilibrium(real (&f)[S::Q], real rho, real ux, 
         const real lam = (l1 == 1) ? real(1) : real(0.25);
         f[i] = lam * rho * (real(1.0 / 6.0) * gh + real(1.0 / 3.0) * xu + real(0.5) * xu * xu - real(1.0 / 6.0) * uu);
       }
+      if constexpr (zc) {  // minus the rest state f_eq(1, 0) (reading R33)
+        if constexpr (l1 == 0) f[i] -= real(1) - real(5.0 / 6.0) * swe_g;
+        else f[i] -= ((l1 == 1) ? real(1) : real(0.25)) * real(1.0 / 6.0) * swe_g;
+      }
     });
     return;
   } else {
@@ -1131,7 +1157,11 @@ __device__ __forceinline__ void equilibrium(real (&f)[S::Q], real rho, real ux, 
                        g(std::integral_constant<int, az>{}, uz);
         constexpr double h = hprod(e);
         if constexpr (e == 0) c[e] = zc ? drho : rho;
-        else if constexpr (h != 0.0) c[e] = zc ? fma(rho, p, real(-h)) : rho * p;
+        else if constexpr (SPACE == SPACE_SWE_K && zc) {  // minus the rest state's moments (R33)
+          if constexpr (e == E(2, 0, 0) || e == E(0, 2, 0)) c[e] = fma(rho, p, real(-0.5) * swe_g);
+          else if constexpr (e == E(2, 2, 0)) c[e] = fma(rho, p, -swe_bg_m22<SPACE_SWE_K>(swe_g));
+          else c[e] = rho * p;
+        } else if constexpr (h != 0.0) c[e] = zc ? fma(rho, p, real(-h)) : rho * p;
         else c[e] = rho * p;
       });
     }

@@ -572,14 +572,29 @@ struct Tile2 {
   static constexpr int THREADS = (HW + 31) / 32 * 32;
 };
 
+// TRIM: the step-(t+1) ring keeps only what the step-(t+2) pull still reads (3 planes of the
+// xi_z = +1 populations, 2 of xi_z = 0, 1 of xi_z = -1; Tile2::trim_*): 2/3 of the shared memory
+template <int TX, int TY, class S>
+struct Tile2Trim {
+  static constexpr int HW = (TX + 2) * (TY + 2);
+  static constexpr int slots(int i) { return S::mz(i) > 0 ? 3 : (S::mz(i) == 0 ? 2 : 1); }
+  static constexpr int off(int i) {
+    int o = 0;
+    for (int j = 0; j < i; ++j) o += slots(j) * HW;
+    return o;
+  }
+  static constexpr int RING = off(S::Q);
+};
+
 template <class S, int SPACE, int REG, class real, int RS, int TX, int TY, int MINB = 1, bool PF = false,
-          bool RANGE = false>
+          bool RANGE = false, bool TRIM = false>
 __global__ void __launch_bounds__(Tile2<TX, TY>::THREADS, MINB)
     k_pull2(const real *__restrict__ src, real *__restrict__ dst, const GridParams g, const Rates<real> r,
             const real swe_g, const Force<real> fr) {
   using T = Tile2<TX, TY>;
+  using TR = Tile2Trim<TX, TY, S>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  real *ring = reinterpret_cast<real *>(smem_raw);  // [3][Q][HW]
+  real *ring = reinterpret_cast<real *>(smem_raw);  // [3][Q][HW], or the trimmed ring
   const int t = threadIdx.x;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   // step t+1 cell of this thread on the halo-extended tile
@@ -633,8 +648,12 @@ __global__ void __launch_bounds__(Tile2<TX, TY>::THREADS, MINB)
         load(k, f);
       }
       collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
-      real *slot = ring + (size_t)((k + 3) % 3) * S::Q * T::HW;  // k >= -1
-      sfor<S::Q>([&](auto i) { slot[i * T::HW + t] = f[i]; });
+      if constexpr (TRIM) {
+        sfor<S::Q>([&](auto i) { ring[TR::off(i) + ((k + 3) % TR::slots(i)) * T::HW + t] = f[i]; });
+      } else {
+        real *slot = ring + (size_t)((k + 3) % 3) * S::Q * T::HW;  // k >= -1
+        sfor<S::Q>([&](auto i) { slot[i * T::HW + t] = f[i]; });
+      }
     }
     __syncthreads();
     if (k >= p0 + 1 && act2) {
@@ -642,8 +661,13 @@ __global__ void __launch_bounds__(Tile2<TX, TY>::THREADS, MINB)
       real f[S::Q];
       sfor<S::Q>([&](auto i) {
         constexpr int cx = S::mx(i), cy = S::my(i), cz = S::mz(i);
-        const real *slot = ring + (size_t)((p - cz + 3) % 3) * S::Q * T::HW;
-        f[i] = slot[i * T::HW + (iy + 1 - cy) * T::HX + (ix + 1 - cx)];
+        const int at = (iy + 1 - cy) * T::HX + (ix + 1 - cx);
+        if constexpr (TRIM) {
+          f[i] = ring[TR::off(i) + ((p - cz + 3) % TR::slots(i)) * T::HW + at];
+        } else {
+          const real *slot = ring + (size_t)((p - cz + 3) % 3) * S::Q * T::HW;
+          f[i] = slot[i * T::HW + at];
+        }
       });
       collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
       const long long own = (long long)(p + 1) * g.plane + (long long)(y0 + iy) * g.pitch + (x0 + ix);
@@ -698,8 +722,8 @@ __global__ void __launch_bounds__(TmaTile<S, real, TX, TY, STAGES>::THREADS, MIN
     k_pull2_tma(const real *__restrict__ src, real *__restrict__ dst, const GridParams g, const Rates<real> r,
                 const real swe_g, const Force<real> fr, const __grid_constant__ CUtensorMap tmap) {
   using T = TmaTile<S, real, TX, TY, STAGES>;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  real *stage = reinterpret_cast<real *>(smem_raw);  // [STAGES][Q][BOXP]
+  extern __shared__ __align__(128) unsigned char smem_tma[];
+  real *stage = reinterpret_cast<real *>(smem_tma);  // [STAGES][Q][BOXP]
   real *ring = stage + STAGES * T::STAGE;            // trimmed ring
   uint64_t *bar = reinterpret_cast<uint64_t *>(ring + T::RING);
   const int t = threadIdx.x;

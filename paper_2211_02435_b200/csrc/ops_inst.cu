@@ -69,7 +69,8 @@ const Ops *with_rs(int rs) {
 template <class St_, class Re_, int SP_, int REG_>
 const Ops *select_ops(int rs) {
   if constexpr (SP_ == SPACE_SWE || SP_ == SPACE_SWE_K) {
-    if constexpr (St_::Q == 9 && REG_ == REG_ABS) return with_rs<St_, SP_, REG_, Re_>(rs);
+    // absolute storage, or zero-centered about the method's rest state (reading R33)
+    if constexpr (St_::Q == 9 && (REG_ == REG_ABS || REG_ == REG_ZC_ABS)) return with_rs<St_, SP_, REG_, Re_>(rs);
     return nullptr;
   } else if constexpr (SP_ == SPACE_CUMULANT && REG_ == REG_DELTA) {
     return nullptr;  // cumulants admit no delta equilibrium

@@ -905,11 +905,10 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
     return fail(nullptr, LBM_EUNSUPPORTED,
                 "cumulant space is incompatible with the delta equilibrium (PAPER.md:430-431, 547)");
   if (equilibrium == LBM_EQ_SWE &&
-      !(stencil == LBM_D2Q9 &&
-        (collision_space == LBM_SPACE_CENTRAL || collision_space == LBM_SPACE_CUMULANT) && !zc))
+      !(stencil == LBM_D2Q9 && (collision_space == LBM_SPACE_CENTRAL || collision_space == LBM_SPACE_CUMULANT)))
     return fail(nullptr, LBM_EUNSUPPORTED,
                 "the shallow-water methods are provided for D2Q9, central moments (Zhou equilibrium) or "
-                "cumulants (Maxwellian with cs2 = g h / 2), absolute storage");
+                "cumulants (Maxwellian with cs2 = g h / 2)");
   const int q = q_of(stencil);
   const int need = (collision_space == LBM_SPACE_POPULATION) ? 1 : q;
   if (n_rates != need)

@@ -5,11 +5,13 @@ Taylor-Green vortex energy for D3Q27 methods and storage/equilibrium formats.
 Setup: TGV eq:TGA_init with u0 = 0.25, nu = 1/6 (omega = 1),
 kappa = 2 pi / L, L = 256, periodic L^3 box (the 2D field extruded along z,
 reading R9); 200 000 time steps; E(t)/E0 with E = sum rho |u|^2 / 2 over the
-lattice nodes (eq:TGA_kin_energy).  Methods: SRT, R-RAW (standing in for R-WO-MRT:
-with every rate equal to one the raw-moment collision is basis-independent,
-f* = M^{-1} m_eq for any basis of the same monomial span), R-CM, R-K; formats:
-absolute storage, zero-centered + absolute equilibrium, zero-centered + delta
-equilibrium (admissible ones only).
+lattice nodes (eq:TGA_kin_energy).  Methods: SRT, R-WO-MRT (the weighted-orthogonal raw
+basis, LBM_SPACE_RAW_WO, reading R31), R-RAW (the raw basis of reading R2), R-CM, R-K;
+formats: absolute storage; zero-centered + absolute equilibrium written literally, f0 added
+to the populations before the transform (LBM_EQ_ABSOLUTE_F0, reading R30: the paper's
+"zc + f^eq"); zero-centered + absolute equilibrium with the background added in moment space
+(LBM_EQ_ABSOLUTE, our default); zero-centered + delta equilibrium (admissible ones only,
+PAPER.md:545-547).
 
   python scripts/table3_roundoff.py [--L 256] [--steps 200000] [--every 2000] [--out FILE]
 """
@@ -38,14 +40,22 @@ PAPER = {
     ("R-K", "abs"): 9.1e-27, ("R-K", "zc+eq"): 1.1e-32,
 }
 
-METHODS = [("SRT", W.POPULATION), ("R-WO-MRT", W.RAW), ("R-CM", W.CENTRAL), ("R-K", W.CUMULANT)]
-FORMATS = {"abs": (W.EQ_ABSOLUTE, 0), "zc+eq": (W.EQ_ABSOLUTE, 1), "zc+delta": (W.EQ_DELTA, 1)}
+METHODS = [("SRT", W.POPULATION), ("R-WO-MRT", W.RAW_WO), ("R-RAW", W.RAW), ("R-CM", W.CENTRAL),
+           ("R-K", W.CUMULANT)]
+# "zc+eq" is the paper's zc + f^eq column: the literal form (f0 added to the populations)
+FORMATS = {"abs": (W.EQ_ABSOLUTE, 0), "zc+eq": (W.EQ_ABSOLUTE_F0, 1), "zc+eq(moments)": (W.EQ_ABSOLUTE, 1),
+           "zc+delta": (W.EQ_DELTA, 1)}
 
 
 def run_one(space, eq, zc, L_, steps, every, u0=0.25, nu=1.0 / 6.0):
     st = W.D3Q27
     om = W.omega_from_nu(nu)
-    rates = [om] if space == W.POPULATION else W.regularized_rates(st, om)
+    if space == W.POPULATION:
+        rates = [om]
+    elif space == W.RAW_WO:
+        rates = W.wo_regularized_rates(st, om)
+    else:
+        rates = W.regularized_rates(st, om)
     rho, u = W.tgv_fields(L_, L_, L_, u0)
     with L.Lattice(st, space, eq, rates, (L_, L_, L_), zero_centered=zc) as lat:
         lat.init_macroscopic(rho, u)
@@ -69,7 +79,7 @@ def main():
     ap.add_argument("--L", type=int, default=256)
     ap.add_argument("--steps", type=int, default=200000)
     ap.add_argument("--every", type=int, default=2000)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1", "table3_roundoff.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r2", "table3_roundoff.json"))
     ap.add_argument("--only", default=None, help="comma list of METHOD:FORMAT")
     args = ap.parse_args()
     nu = 1.0 / 6.0

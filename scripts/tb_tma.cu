@@ -136,6 +136,33 @@ void run_ref(const char *name, const Lat &L, real *a, real *b, real *ref, const 
          fa.numRegs, smem);
 }
 
+template <class S, int SPACE, int REG, class real, int TX, int TY, int MINB, bool PF>
+void run_trim(const char *name, const Lat &L, real *a, real *b, real *ref, const Rates<real> &r, int zch,
+              double cells) {
+  using T = Tile2<TX, TY>;
+  auto kern = k_pull2<S, SPACE, REG, real, RS_GENERAL, TX, TY, MINB, PF, false, true>;
+  const size_t smem = (size_t)Tile2Trim<TX, TY, S>::RING * sizeof(real);
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  Force<real> fr{};
+  dim3 grid((unsigned)(L.g.nx / TX), (unsigned)(L.g.ny / TY), (unsigned)zch);
+  kern<<<grid, T::THREADS, smem>>>(a, b, L.g, r, real(0), fr);
+  CK(cudaDeviceSynchronize());
+  double *dm;
+  CK(cudaMalloc(&dm, 8));
+  CK(cudaMemset(dm, 0, 8));
+  maxdiff<<<1184, 256>>>(b + L.g.plane, ref + L.g.plane, (size_t)L.g.nzl * L.g.plane, dm);
+  double md = 0;
+  CK(cudaMemcpy(&md, dm, 8, cudaMemcpyDeviceToHost));
+  cudaFree(dm);
+  int nb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T::THREADS, smem));
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  float ms = time_k([&](int p) { kern<<<grid, T::THREADS, smem>>>(p ? b : a, p ? a : b, L.g, r, real(0), fr); });
+  printf("%-44s %7.3f ms/2 steps %8.0f MLUPS  regs %3d  lmem %3zu  smem %6zu  %d CTA/SM  maxdiff %.3e\n", name, ms,
+         2.0 * cells / (ms * 1e-3) / 1e6, fa.numRegs, fa.localSizeBytes, smem, nb, md);
+}
+
 template <class S, int SPACE, int REG, class real>
 struct Bench {
   Lat L;
@@ -164,7 +191,7 @@ struct Bench {
 };
 
 template <class real, int MINB_REF>
-void c2(const char *tag) {
+void c2(const char *tag, bool tma) {
   using S = D3Q19;
   Bench<S, SPACE_RAW, REG_DELTA, real> B(256, 256, 256);
   char nm[128];
@@ -185,14 +212,38 @@ void c2(const char *tag) {
   }                                                                                                    \
   snprintf(nm, sizeof nm, "C2 %s tma %dx%d minb %d stages %d", tag, TX, TY, MINB, ST);                 \
   run_tma<S, SPACE_RAW, REG_DELTA, real, TX, TY, MINB, ST>(nm, B.L, B.a, B.b, B.ref, B.r, zch, B.cells);
-  TMA(16, 8, 2, 1)
-  TMA(16, 8, 2, 2)
-  TMA(16, 8, 3, 1)
-  TMA(32, 8, 1, 1)
-  TMA(32, 8, 1, 2)
-  TMA(16, 16, 1, 1)
-  TMA(32, 4, 2, 1)
+  if (tma) {
+    TMA(16, 8, 2, 1)
+    TMA(16, 8, 2, 2)
+    TMA(16, 8, 3, 1)
+    TMA(32, 8, 1, 1)
+    TMA(32, 8, 1, 2)
+    TMA(16, 16, 1, 1)
+    TMA(32, 4, 2, 1)
+  }
 #undef TMA
+#define TRIMV(TX, TY, MINB, PF)                                                                        \
+  B.reset();                                                                                           \
+  {                                                                                                    \
+    using T2 = Tile2<16, 8>;                                                                           \
+    auto kr = k_pull2<S, SPACE_RAW, REG_DELTA, real, RS_GENERAL, 16, 8, MINB_REF, true>;               \
+    Force<real> fr{};                                                                                  \
+    kr<<<dim3(256 / 16, 256 / 8, zch), T2::THREADS, (size_t)3 * S::Q * T2::HW * sizeof(real)>>>(      \
+        B.a, B.ref, B.L.g, B.r, real(0), fr);                                                          \
+    CK(cudaDeviceSynchronize());                                                                       \
+  }                                                                                                    \
+  snprintf(nm, sizeof nm, "C2 %s trim %dx%d minb %d pf %d", tag, TX, TY, MINB, (int)PF);              \
+  run_trim<S, SPACE_RAW, REG_DELTA, real, TX, TY, MINB, PF>(nm, B.L, B.a, B.b, B.ref, B.r, zch, B.cells);
+  TRIMV(16, 8, MINB_REF, true)
+  TRIMV(16, 8, MINB_REF + 1, true)
+  TRIMV(16, 8, MINB_REF + 1, false)
+  TRIMV(16, 12, MINB_REF, true)
+  TRIMV(16, 12, MINB_REF, false)
+  TRIMV(32, 8, 1, true)
+  TRIMV(32, 8, 2, false)
+  TRIMV(16, 16, 2, false)
+  TRIMV(16, 16, 1, true)
+#undef TRIMV
 }
 
 void c4() {
@@ -217,18 +268,42 @@ void c4() {
   B.reset();
   run_ref<S, SPACE_CUMULANT, REG_ZC_ABS, real, 16, 8, 1>("C4 cumulant k_pull2 16x8 PF", B.L, B.a, B.b, B.ref, B.r, zch,
                                                          B.cells);
-  TMA4(16, 8, 1, 1)
-  TMA4(16, 8, 1, 2)
-  TMA4(8, 8, 2, 1)
-  TMA4(16, 4, 2, 1)
-  TMA4(32, 8, 1, 1)
+  if (!getenv("TB_TRIM")) {
+    TMA4(16, 8, 1, 1)
+    TMA4(16, 8, 1, 2)
+    TMA4(8, 8, 2, 1)
+    TMA4(16, 4, 2, 1)
+    TMA4(32, 8, 1, 1)
+  }
 #undef TMA4
+#define TRIM4(TX, TY, MINB, PF)                                                                         \
+  B.reset();                                                                                            \
+  {                                                                                                     \
+    using T2 = Tile2<16, 8>;                                                                            \
+    auto kr = k_pull2<S, SPACE_CUMULANT, REG_ZC_ABS, real, RS_GENERAL, 16, 8, 1, true>;                 \
+    const size_t sm = (size_t)3 * S::Q * T2::HW * sizeof(real);                                         \
+    CK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));                 \
+    Force<real> fr{};                                                                                   \
+    kr<<<dim3(512 / 16, 512 / 8, zch), T2::THREADS, sm>>>(B.a, B.ref, B.L.g, B.r, real(0), fr);         \
+    CK(cudaDeviceSynchronize());                                                                        \
+  }                                                                                                     \
+  snprintf(nm, sizeof nm, "C4 cumulant trim %dx%d minb %d pf %d", TX, TY, MINB, (int)PF);              \
+  run_trim<S, SPACE_CUMULANT, REG_ZC_ABS, real, TX, TY, MINB, PF>(nm, B.L, B.a, B.b, B.ref, B.r, zch, B.cells);
+  if (getenv("TB_TRIM")) {
+    TRIM4(16, 8, 1, true)
+    TRIM4(16, 8, 1, false)
+    TRIM4(16, 8, 2, false)
+    TRIM4(32, 8, 1, false)
+    TRIM4(16, 16, 1, false)
+    TRIM4(32, 4, 1, false)
+  }
+#undef TRIM4
 }
 
 int main(int argc, char **argv) {
   const int which = argc > 1 ? atoi(argv[1]) : 7;
-  if (which & 1) c2<double, 2>("f64");
-  if (which & 2) c2<float, 3>("f32");
+  if (which & 1) c2<double, 2>("f64", which & 8);
+  if (which & 2) c2<float, 3>("f32", which & 8);
   if (which & 4) c4();
   return 0;
 }

@@ -94,7 +94,10 @@ def test_admissibility_errors():
     assert st == L.LBM_EUNSUPPORTED and "cumulant" in msg
     st, _ = create_status(eq=L.LBM_EQ_SWE, stencil=L.LBM_D3Q27, space=L.LBM_SPACE_CENTRAL, zc=0)
     assert st == L.LBM_EUNSUPPORTED
+    # zero-centered shallow water about the rest state (reading R33) passes validation
     st, _ = create_status(eq=L.LBM_EQ_SWE, stencil=L.LBM_D2Q9, space=L.LBM_SPACE_CENTRAL, zc=1, shape=(8, 8, 1))
+    assert st != L.LBM_EUNSUPPORTED
+    st, _ = create_status(eq=L.LBM_EQ_SWE, stencil=L.LBM_D2Q9, space=L.LBM_SPACE_RAW, zc=1, shape=(8, 8, 1))
     assert st == L.LBM_EUNSUPPORTED
     st, _ = create_status(streaming=L.LBM_ESOTERIC_PULL, nranks=2, rank=0)
     assert st == L.LBM_EUNSUPPORTED

@@ -57,6 +57,33 @@ def test_run_detects_non_finite_state():
     assert seen == [1]
 
 
+def test_run_intervals_count_from_the_call():
+    """run(n, check_every, every) with intervals that are not multiples of each other, on a
+    context that already advanced: the probe and the callback fire at every multiple of their
+    own interval counted from the start of the call."""
+    st = W.D2Q9
+    shape = (16, 12, 1)
+    f0 = initial_state(st, W.RAW, W.EQ_DELTA, 1, shape)
+    seen, probes = [], []
+    with L.Lattice(st, W.RAW, W.EQ_DELTA, W.rate_set_p(st), shape) as lat:
+        lat.set_populations(f0)
+        lat.step(1)
+        orig = lat.check_finite
+        lat.check_finite = lambda: (probes.append(lat.info().steps_done), orig())[1]
+        lat.run(12, check_every=2, callback=lambda l, s: seen.append(s), every=3)
+    assert probes == [3, 5, 7, 9, 11, 13]
+    assert seen == [4, 7, 10, 13]
+    # the same run in one go or in the run() chunks: identical state
+    with L.Lattice(st, W.RAW, W.EQ_DELTA, W.rate_set_p(st), shape) as a, \
+            L.Lattice(st, W.RAW, W.EQ_DELTA, W.rate_set_p(st), shape) as b:
+        a.set_populations(f0)
+        b.set_populations(f0)
+        a.step(13)
+        b.step(1)
+        b.run(12, check_every=5, every=7)
+        assert np.array_equal(a.get_populations(), b.get_populations())
+
+
 @pytest.mark.parametrize("st", [W.D2Q9, W.D3Q19, W.D3Q27])
 def test_fp32_in_place_patterns_equal_pull(st):
     shape = (20, 12, 1) if st == W.D2Q9 else (20, 10, 12)
@@ -64,7 +91,7 @@ def test_fp32_in_place_patterns_equal_pull(st):
     rates = W.rate_set_p(st)
     f0 = initial_state(st, space, eq, zc, shape).astype(np.float32).astype(np.float64)
     outs = []
-    for streaming in (L.LBM_PULL, L.LBM_AA, L.LBM_ESOTERIC_PULL, L.LBM_ESOTERIC_TWIST):
+    for streaming in (L.LBM_PULL, L.LBM_AA, L.LBM_ESOTERIC_PULL, L.LBM_ESOTERIC_TWIST, L.LBM_ESOTERIC_PUSH):
         with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, precision=L.LBM_FP32,
                        streaming=streaming) as lat:
             lat.set_populations(f0)

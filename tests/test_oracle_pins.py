@@ -771,6 +771,45 @@ def test_swe_collision_conserves(space):
                                oracle.equilibrium(st, space, W.EQ_SWE, 0, h2, u2, g=g), atol=1e-15)
 
 
+@pytest.mark.parametrize("space", [W.CENTRAL, W.CUMULANT])
+def test_swe_zero_centered_storage(space):
+    """Zero-centered shallow water (reading R33): the background is the
+    method's rest state f0 = f_eq(h0 = 1, u = 0), typed here from its definitions — Zhou's
+    f0 = (1 - 5g/6; g/6 on the axes; g/24 on the diagonals) and, for the cumulant method, the
+    product of the per-axis Gaussian moment conditions at cs2 = g/2 (phi(0) = 1 - cs2,
+    phi(+-1) = cs2 / 2); the rest state df = 0 is a fixed point; and the zero-centered update
+    equals the absolute one under df = f - f0 to one ulp."""
+    st = W.D2Q9
+    xi, *_ = oracle.tables(st)
+    g = 0.0613125
+    f0 = oracle.equilibrium(st, space, W.EQ_SWE, 0, np.ones(1), np.zeros((1, 3)), g=g)[0]
+    if space == W.CENTRAL:
+        l1 = np.abs(xi[:, :2]).sum(1)
+        typed = np.where(l1 == 0, 1 - 5 * g / 6, np.where(l1 == 1, g / 6, g / 24))
+    else:
+        cs2 = g / 2
+        phi = lambda x: np.where(x == 0, 1 - cs2, cs2 / 2)
+        typed = phi(xi[:, 0]) * phi(xi[:, 1])
+    np.testing.assert_allclose(f0, typed, rtol=2e-16, atol=1e-17)
+    # zero-centered rest state: equilibrium 0, collision fixed point
+    z = oracle.equilibrium(st, space, W.EQ_SWE, 1, np.ones(1), np.zeros((1, 3)), g=g)
+    assert np.abs(z).max() < 1e-17
+    rates = W.rates_random(st)
+    assert np.abs(oracle.collide(st, space, W.EQ_SWE, 1, rates, np.zeros((3, 9)), g=g)).max() < 1e-17
+    # regime equivalence on perturbed states
+    rng = np.random.default_rng(8)
+    n = 16
+    h = rng.uniform(1.0, 6.0, n)
+    u = np.zeros((n, 3))
+    u[:, :2] = rng.uniform(-0.05, 0.05, (n, 2))
+    fa = oracle.equilibrium(st, space, W.EQ_SWE, 0, h, u, g=g) * (1 + 0.02 * rng.uniform(-1, 1, (n, 9)))
+    oa = oracle.collide(st, space, W.EQ_SWE, 0, rates, fa, g=g)
+    oz = oracle.collide(st, space, W.EQ_SWE, 1, rates, fa - f0, g=g) + f0
+    np.testing.assert_allclose(oz, oa, rtol=0, atol=1e-15)
+    fz = oracle.equilibrium(st, space, W.EQ_SWE, 1, h, u, g=g)
+    np.testing.assert_allclose(fz + f0, oracle.equilibrium(st, space, W.EQ_SWE, 0, h, u, g=g), atol=1e-15)
+
+
 def paper_values():
     vals = {}
     for line in open(os.path.join(GOLDEN, "paper_values.txt")):
