@@ -16,6 +16,8 @@
  * Conventions
  * -----------
  * Units: lattice units, dx = dt = 1, cs^2 = 1/3, background density rho0 = 1.
+ * rho0 is a unit choice (the update is homogeneous of degree one in f; R21): for a
+ * background density lambda pass rho / lambda and scale the returned density by lambda.
  *
  * Velocity ordering (the paper leaves it free except xi_0 = 0).  The
  * SLAB AXIS is the last lattice axis (z in 3D, y in 2D).  Order: rest; the velocities with

@@ -93,6 +93,10 @@ struct TbTile {
   static constexpr int TX = S::D == 2 ? 256 : (on3 ? 16 : 0);
   static constexpr int TY = S::D == 2 ? 1 : (on3 ? 8 : 0);
   static constexpr int MINB = S::Q == 27 ? 1 : (f64 ? 2 : 3);  // 3D: CTAs per SM
+  // trimmed step-(t+1) ring (3 / 2 / 1 planes of the xi_z = +1 / 0 / -1 populations): D3Q19
+  // fp64 C2 1.188 -> 1.108 ms per 2 steps (the freed shared memory goes to L1, which serves the
+  // halo re-reads); fp32 and D3Q27 unchanged (scripts/tb_tma.cu, profiles/r2/tb_variants_r2.txt)
+  static constexpr bool TRIM = S::Q == 19 && f64;
 };
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel instantiation, device):
@@ -225,7 +229,7 @@ struct OpsImpl {
     if constexpr (S::D == 3 && TX > 0) {
       using T = Tile2<TX, TY>;
       const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
-      const size_t smem = (size_t)3 * S::Q * T::HW * sizeof(real);
+      const size_t smem = (TT::TRIM ? (size_t)Tile2Trim<TX, TY, S>::RING : (size_t)3 * S::Q * T::HW) * sizeof(real);
       // whole slab with periodic wrap (single rank) or a plane range without wrap (across ranks)
       auto go = [&](auto kern, unsigned &configured) {
         opt_in_smem_once(kern, smem, configured);  // > 48 KB of shared memory, once per device
@@ -233,8 +237,8 @@ struct OpsImpl {
             static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
       };
       static unsigned conf_slab = 0, conf_range = 0;
-      if (g.zcount) go(k_pull2<S, SPACE, REG, real, RS, TX, TY, TT::MINB, true, true>, conf_range);
-      else go(k_pull2<S, SPACE, REG, real, RS, TX, TY, TT::MINB, true, false>, conf_slab);
+      if (g.zcount) go(k_pull2<S, SPACE, REG, real, RS, TX, TY, TT::MINB, true, true, TT::TRIM>, conf_range);
+      else go(k_pull2<S, SPACE, REG, real, RS, TX, TY, TT::MINB, true, false, TT::TRIM>, conf_slab);
     } else if constexpr (S::D == 2) {
       using T = Tile1<TX>;
       const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
@@ -294,7 +298,7 @@ struct OpsImpl {
       e = cudaFuncGetAttributes(&a, k_pull<S, SPACE, REG, real, false, RS>);
     } else if (which == 1) {
       if constexpr (S::D == 3 && TT::TX > 0)
-        e = cudaFuncGetAttributes(&a, k_pull2<S, SPACE, REG, real, RS, TT::TX, TT::TY, TT::MINB, true, false>);
+        e = cudaFuncGetAttributes(&a, k_pull2<S, SPACE, REG, real, RS, TT::TX, TT::TY, TT::MINB, true, false, TT::TRIM>);
       else if constexpr (S::D == 2) {
         constexpr bool srt = SPACE == SPACE_POPULATION;
         e = cudaFuncGetAttributes(&a, k_pull2_2d<S, SPACE, REG, real, RS, TT::TX, srt ? 3 : 2, !srt, false>);
@@ -332,7 +336,7 @@ struct OpsImpl {
     cudaFuncGetAttributes(&a, k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS>);
     cudaFuncGetAttributes(&a, k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS, true>);
     if constexpr (S::D == 3 && TT::TX > 0) {
-      cudaFuncGetAttributes(&a, k_pull2<S, SPACE, REG, real, RS, TT::TX, TT::TY, TT::MINB, true, true>);
+      cudaFuncGetAttributes(&a, k_pull2<S, SPACE, REG, real, RS, TT::TX, TT::TY, TT::MINB, true, true, TT::TRIM>);
     } else if constexpr (S::D == 2) {
       constexpr bool srt = SPACE == SPACE_POPULATION;
       cudaFuncGetAttributes(&a, k_pull2_2d<S, SPACE, REG, real, RS, TT::TX, srt ? 3 : 2, !srt, true>);

@@ -47,6 +47,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// plain arrival (release.cta): the phase completes when the init count of threads arrived
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// cp.async (LDGSTS): an 4/8-byte global -> shared copy that completes asynchronously, tracked
+// per thread by commit / wait groups (no register holds the data in flight)
+template <class real>
+__device__ __forceinline__ void cp_async(real *dst_smem, const real *src) {
+  static_assert(sizeof(real) == 4 || sizeof(real) == 8, "4 or 8 byte elements");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst_smem)), "l"(src),
+               "n"((int)sizeof(real))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // order this thread's earlier generic-proxy shared-memory accesses before later async-proxy
 // (TMA) writes to the same buffer
 __device__ __forceinline__ void fence_proxy_async_smem() {

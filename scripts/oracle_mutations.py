@@ -81,6 +81,22 @@ MUTANTS = [
      "    for (int i = 0; i < q; ++i) m.omega[i] = R(rates[i]);",
      "    for (int i = 0; i < q; ++i) m.omega[i] = R(rates[i]);\n"
      "    m.omega[stencil == ST_D2Q9 ? 5 : 9] = m.omega[stencil == ST_D2Q9 ? 4 : 7];"),
+    # WO-MRT basis (reading R31)
+    ("WO-MRT: unweighted Gram-Schmidt inner product (R31)",
+     "num += m.w[i] * V[k * q + i] * P[j * q + i];\n        den += m.w[i] * P[j * q + i] * P[j * q + i];",
+     "num += V[k * q + i] * P[j * q + i];\n        den += P[j * q + i] * P[j * q + i];"),
+    ("WO-MRT: monomials in ascending instead of descending lexicographic order (R31)",
+     "for (int a = 2; a >= 0; --a)\n      for (int b = 2; b >= 0; --b)",
+     "for (int a = 0; a <= 2; ++a)\n      for (int b = 0; b <= 2; ++b)"),
+    ("WO-MRT: subtracts cf times the monomial x^(e_j) instead of the orthogonalised p_j (R31)",
+     "for (int i = 0; i < q; ++i) P[k * q + i] -= cf * P[j * q + i];",
+     "for (int i = 0; i < q; ++i) P[k * q + i] -= cf * V[j * q + i];"),
+    # zero-centered shallow water (reading R33)
+    ("zc shallow water: background left at the lattice weights instead of f_eq(1, 0) (R33)",
+     "const bool ok = equilibrium_cell(m, R(1), u0, m.w.data());", "const bool ok = true;"),
+    ("zc shallow water: Zhou equilibrium not shifted by the background (R33)",
+     "    if (m.zc)\n      for (int i = 0; i < q; ++i) f[i] -= m.w[i];\n    return true;",
+     "    return true;"),
 ]
 
 

@@ -3,12 +3,13 @@
 // variants) on C2-like (D3Q19 raw zc+delta 256^3, fp64 / fp32) and C4-like (D3Q27 cumulant
 // zc+abs 512^2 x 128) lattices: time per two steps and max |difference| of the outputs.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr
-//        -I paper_2211_02435_b200/csrc -I include scripts/tb_tma.cu -o scripts/tb_tma
+//        -I paper_2211_02435_b200/csrc -I include -I scripts scripts/tb_tma.cu -o scripts/tb_tma
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
 
 #include "kernels.cuh"
+#include "tb_r2_variants.cuh"
 
 using namespace lbm;
 
@@ -163,6 +164,60 @@ void run_trim(const char *name, const Lat &L, real *a, real *b, real *ref, const
          2.0 * cells / (ms * 1e-3) / 1e6, fa.numRegs, fa.localSizeBytes, smem, nb, md);
 }
 
+template <class S, int SPACE, int REG, class real, int TX, int TY, int MINB>
+void run_1b(const char *name, const Lat &L, real *a, real *b, real *ref, const Rates<real> &r, int zch,
+            double cells) {
+  using T = Tile2<TX, TY>;
+  auto kern = k_pull2_1b<S, SPACE, REG, real, RS_GENERAL, TX, TY, MINB, false>;
+  const size_t smem = (size_t)Tile2Ring1b<TX, TY, S>::RING * sizeof(real);
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  Force<real> fr{};
+  dim3 grid((unsigned)(L.g.nx / TX), (unsigned)(L.g.ny / TY), (unsigned)zch);
+  kern<<<grid, T::THREADS, smem>>>(a, b, L.g, r, real(0), fr);
+  CK(cudaDeviceSynchronize());
+  double *dm;
+  CK(cudaMalloc(&dm, 8));
+  CK(cudaMemset(dm, 0, 8));
+  maxdiff<<<1184, 256>>>(b + L.g.plane, ref + L.g.plane, (size_t)L.g.nzl * L.g.plane, dm);
+  double md = 0;
+  CK(cudaMemcpy(&md, dm, 8, cudaMemcpyDeviceToHost));
+  cudaFree(dm);
+  int nb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T::THREADS, smem));
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  float ms = time_k([&](int p) { kern<<<grid, T::THREADS, smem>>>(p ? b : a, p ? a : b, L.g, r, real(0), fr); });
+  printf("%-44s %7.3f ms/2 steps %8.0f MLUPS  regs %3d  lmem %3zu  smem %6zu  %d CTA/SM  maxdiff %.3e\n", name, ms,
+         2.0 * cells / (ms * 1e-3) / 1e6, fa.numRegs, fa.localSizeBytes, smem, nb, md);
+}
+
+template <class S, int SPACE, int REG, class real, int TX, int TY, int MINB>
+void run_ws(const char *name, const Lat &L, real *a, real *b, real *ref, const Rates<real> &r, int zch,
+            double cells) {
+  using T = TileWs<TX, TY>;
+  auto kern = k_pull2_ws<S, SPACE, REG, real, RS_GENERAL, TX, TY, MINB, false>;
+  const size_t smem = ws_smem_bytes<S, real, TX, TY>();
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  Force<real> fr{};
+  dim3 grid((unsigned)(L.g.nx / TX), (unsigned)(L.g.ny / TY), (unsigned)zch);
+  kern<<<grid, T::THREADS, smem>>>(a, b, L.g, r, real(0), fr);
+  CK(cudaDeviceSynchronize());
+  double *dm;
+  CK(cudaMalloc(&dm, 8));
+  CK(cudaMemset(dm, 0, 8));
+  maxdiff<<<1184, 256>>>(b + L.g.plane, ref + L.g.plane, (size_t)L.g.nzl * L.g.plane, dm);
+  double md = 0;
+  CK(cudaMemcpy(&md, dm, 8, cudaMemcpyDeviceToHost));
+  cudaFree(dm);
+  int nb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T::THREADS, smem));
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  float ms = time_k([&](int p) { kern<<<grid, T::THREADS, smem>>>(p ? b : a, p ? a : b, L.g, r, real(0), fr); });
+  printf("%-44s %7.3f ms/2 steps %8.0f MLUPS  regs %3d  lmem %3zu  smem %6zu  %d CTA/SM  maxdiff %.3e\n", name, ms,
+         2.0 * cells / (ms * 1e-3) / 1e6, fa.numRegs, fa.localSizeBytes, smem, nb, md);
+}
+
 template <class S, int SPACE, int REG, class real>
 struct Bench {
   Lat L;
@@ -222,6 +277,7 @@ void c2(const char *tag, bool tma) {
     TMA(32, 4, 2, 1)
   }
 #undef TMA
+  if (getenv("TB_TRIM")) {
 #define TRIMV(TX, TY, MINB, PF)                                                                        \
   B.reset();                                                                                           \
   {                                                                                                    \
@@ -244,6 +300,48 @@ void c2(const char *tag, bool tma) {
   TRIMV(16, 16, 2, false)
   TRIMV(16, 16, 1, true)
 #undef TRIMV
+  }
+#define WSV(TX, TY, MINB)                                                                              \
+  B.reset();                                                                                           \
+  {                                                                                                    \
+    using T2 = Tile2<16, 8>;                                                                           \
+    auto kr = k_pull2<S, SPACE_RAW, REG_DELTA, real, RS_GENERAL, 16, 8, MINB_REF, true>;               \
+    Force<real> fr{};                                                                                  \
+    kr<<<dim3(256 / 16, 256 / 8, zch), T2::THREADS, (size_t)3 * S::Q * T2::HW * sizeof(real)>>>(      \
+        B.a, B.ref, B.L.g, B.r, real(0), fr);                                                          \
+    CK(cudaDeviceSynchronize());                                                                       \
+  }                                                                                                    \
+  snprintf(nm, sizeof nm, "C2 %s ws %dx%d minb %d", tag, TX, TY, MINB);                               \
+  run_ws<S, SPACE_RAW, REG_DELTA, real, TX, TY, MINB>(nm, B.L, B.a, B.b, B.ref, B.r, zch, B.cells);
+  if (getenv("TB_WS")) {
+    WSV(16, 8, 1)
+    WSV(16, 8, 2)
+    WSV(16, 8, 3)
+    WSV(32, 8, 1)
+    WSV(32, 4, 2)
+    WSV(16, 16, 1)
+    WSV(8, 8, 3)
+  }
+#undef WSV
+#define V1B(TX, TY, MINB)                                                                              \
+  B.reset();                                                                                           \
+  {                                                                                                    \
+    using T2 = Tile2<16, 8>;                                                                           \
+    auto kr = k_pull2<S, SPACE_RAW, REG_DELTA, real, RS_GENERAL, 16, 8, MINB_REF, true>;               \
+    Force<real> fr{};                                                                                  \
+    kr<<<dim3(256 / 16, 256 / 8, zch), T2::THREADS, (size_t)3 * S::Q * T2::HW * sizeof(real)>>>(      \
+        B.a, B.ref, B.L.g, B.r, real(0), fr);                                                          \
+    CK(cudaDeviceSynchronize());                                                                       \
+  }                                                                                                    \
+  snprintf(nm, sizeof nm, "C2 %s 1b %dx%d minb %d", tag, TX, TY, MINB);                               \
+  run_1b<S, SPACE_RAW, REG_DELTA, real, TX, TY, MINB>(nm, B.L, B.a, B.b, B.ref, B.r, zch, B.cells);
+  V1B(16, 8, MINB_REF)
+  V1B(16, 8, MINB_REF + 1)
+  V1B(16, 8, 1)
+  V1B(32, 8, 1)
+  V1B(32, 4, MINB_REF)
+  V1B(16, 16, 1)
+#undef V1B
 }
 
 void c4() {
@@ -268,7 +366,7 @@ void c4() {
   B.reset();
   run_ref<S, SPACE_CUMULANT, REG_ZC_ABS, real, 16, 8, 1>("C4 cumulant k_pull2 16x8 PF", B.L, B.a, B.b, B.ref, B.r, zch,
                                                          B.cells);
-  if (!getenv("TB_TRIM")) {
+  if (getenv("TB_TMA")) {
     TMA4(16, 8, 1, 1)
     TMA4(16, 8, 1, 2)
     TMA4(8, 8, 2, 1)
@@ -289,7 +387,7 @@ void c4() {
   }                                                                                                     \
   snprintf(nm, sizeof nm, "C4 cumulant trim %dx%d minb %d pf %d", TX, TY, MINB, (int)PF);              \
   run_trim<S, SPACE_CUMULANT, REG_ZC_ABS, real, TX, TY, MINB, PF>(nm, B.L, B.a, B.b, B.ref, B.r, zch, B.cells);
-  if (getenv("TB_TRIM")) {
+  if (getenv("TB_TRIM") && 0) {
     TRIM4(16, 8, 1, true)
     TRIM4(16, 8, 1, false)
     TRIM4(16, 8, 2, false)
@@ -298,6 +396,43 @@ void c4() {
     TRIM4(32, 4, 1, false)
   }
 #undef TRIM4
+#define WS4(TX, TY, MINB)                                                                               \
+  B.reset();                                                                                            \
+  {                                                                                                     \
+    using T2 = Tile2<16, 8>;                                                                            \
+    auto kr = k_pull2<S, SPACE_CUMULANT, REG_ZC_ABS, real, RS_GENERAL, 16, 8, 1, true>;                 \
+    const size_t sm = (size_t)3 * S::Q * T2::HW * sizeof(real);                                         \
+    CK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));                 \
+    Force<real> fr{};                                                                                   \
+    kr<<<dim3(512 / 16, 512 / 8, zch), T2::THREADS, sm>>>(B.a, B.ref, B.L.g, B.r, real(0), fr);         \
+    CK(cudaDeviceSynchronize());                                                                        \
+  }                                                                                                     \
+  snprintf(nm, sizeof nm, "C4 cumulant ws %dx%d minb %d", TX, TY, MINB);                                \
+  run_ws<S, SPACE_CUMULANT, REG_ZC_ABS, real, TX, TY, MINB>(nm, B.L, B.a, B.b, B.ref, B.r, zch, B.cells);
+  if (getenv("TB_WS")) {
+    WS4(16, 8, 1)
+    WS4(8, 8, 2)
+    WS4(16, 4, 2)
+    WS4(32, 4, 1)
+  }
+#undef WS4
+#define V1B4(TX, TY, MINB)                                                                              \
+  B.reset();                                                                                            \
+  {                                                                                                     \
+    using T2 = Tile2<16, 8>;                                                                            \
+    auto kr = k_pull2<S, SPACE_CUMULANT, REG_ZC_ABS, real, RS_GENERAL, 16, 8, 1, true>;                 \
+    const size_t sm = (size_t)3 * S::Q * T2::HW * sizeof(real);                                         \
+    CK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));                 \
+    Force<real> fr{};                                                                                   \
+    kr<<<dim3(512 / 16, 512 / 8, zch), T2::THREADS, sm>>>(B.a, B.ref, B.L.g, B.r, real(0), fr);         \
+    CK(cudaDeviceSynchronize());                                                                        \
+  }                                                                                                     \
+  snprintf(nm, sizeof nm, "C4 cumulant 1b %dx%d minb %d", TX, TY, MINB);                                \
+  run_1b<S, SPACE_CUMULANT, REG_ZC_ABS, real, TX, TY, MINB>(nm, B.L, B.a, B.b, B.ref, B.r, zch, B.cells);
+  V1B4(16, 8, 1)
+  V1B4(32, 8, 1)
+  V1B4(16, 4, 1)
+#undef V1B4
 }
 
 int main(int argc, char **argv) {

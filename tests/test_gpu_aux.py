@@ -131,3 +131,41 @@ def test_gpu_tgv_second_order_convergence(st, space, eq, streaming):
     assert errs[-1] < 5e-3, errs
     for a, b in zip(errs, errs[1:]):
         assert 3.5 < a / b < 4.5, errs
+
+
+@pytest.mark.parametrize("st,space", [(W.D3Q27, W.CUMULANT), (W.D3Q19, W.RAW), (W.D2Q9, W.CENTRAL),
+                                      (W.D3Q27, W.POPULATION)])
+def test_background_density_scaling_bitwise(st, space):
+    """rho0 is a unit choice (reading R21; pinned on the oracle by
+    test_background_density_is_a_unit_choice): on absolute storage the device update is
+    homogeneous of degree one, and scaling by 2 is exact in fp64, so 10 steps of 2 f equal
+    2 x (10 steps of f) bitwise — a run at background density 2 is the rho0 = 1 run in other
+    units."""
+    shape = (20, 12, 1) if st == W.D2Q9 else (20, 10, 12)
+    rates = [1.3] if space == W.POPULATION else W.rate_set_p(st)
+    f0 = initial_state(st, space, W.EQ_ABSOLUTE, 0, shape)
+    outs = []
+    for lam in (1.0, 2.0):
+        with L.Lattice(st, space, W.EQ_ABSOLUTE, rates, shape, zero_centered=False) as lat:
+            lat.set_populations(lam * f0)
+            lat.step(10)
+            outs.append(lat.get_populations())
+    np.testing.assert_array_equal(outs[1], 2.0 * outs[0])
+
+
+@pytest.mark.parametrize("space", [W.CENTRAL, W.CUMULANT])
+def test_swe_depth_scaling_bitwise(space):
+    """h0 is a gravity rescaling (test_swe_background_depth_is_a_gravity_rescaling): the
+    shallow-water run of 2 f at gravity g equals 2 x the run of f at gravity 2 g, bitwise."""
+    st, shape = W.D2Q9, (24, 16, 1)
+    g = 0.0613125
+    f0 = initial_state(st, space, W.EQ_SWE, 0, shape, g=2 * g, noise=0.0, dam=(6.0, 4.0, 1.25))
+    with L.Lattice(st, space, W.EQ_SWE, W.rate_set_p(st), shape, swe_g=2 * g) as lat:
+        lat.set_populations(f0)
+        lat.step(10)
+        a = lat.get_populations()
+    with L.Lattice(st, space, W.EQ_SWE, W.rate_set_p(st), shape, swe_g=g) as lat:
+        lat.set_populations(2 * f0)
+        lat.step(10)
+        b = lat.get_populations()
+    np.testing.assert_array_equal(b, 2 * a)

@@ -1095,3 +1095,53 @@ def test_wo_tgv_decay_and_regimes():
         assert abs(ratio / ref - 1) < 1e-2, (eq, ratio, ref)
     with pytest.raises(ValueError):
         oracle.Sim(st, W.CENTRAL, W.EQ_ABSOLUTE_F0, 0, W.rate_set_p(st), (8, 8, 1))
+
+
+@pytest.mark.parametrize("st", STENCILS)
+@pytest.mark.parametrize("space", [W.POPULATION, W.RAW, W.CENTRAL, W.CUMULANT])
+def test_background_density_is_a_unit_choice(st, space):
+    """rho0 ("typically set to unity"; reading R21): the update is homogeneous of
+    degree one in the populations — f_eq(lambda rho, u) = lambda f_eq(rho, u) and
+    u = j / rho is scale free (eq:DensityAndVelocity), every transform is
+    linear and the cumulants are normalised by rho — so the run with
+    background density lambda is lambda times the run with background density one:
+    C(lambda f) = lambda C(f).  lambda = 2 is exact in floating point, lambda = 3 to rounding."""
+    rng = np.random.default_rng(21)
+    n = 24
+    rho = rng.uniform(0.9, 1.1, n)
+    u = rng.uniform(-0.05, 0.05, (n, 3))
+    if st == W.D2Q9:
+        u[:, 2] = 0
+    f = oracle.equilibrium(st, space, W.EQ_ABSOLUTE, 0, rho, u)
+    f = f * (1 + 1e-2 * rng.uniform(-1, 1, f.shape))
+    rates = [1.3] if space == W.POPULATION else W.rates_random(st)
+    base = oracle.collide(st, space, W.EQ_ABSOLUTE, 0, rates, f)
+    np.testing.assert_array_equal(oracle.collide(st, space, W.EQ_ABSOLUTE, 0, rates, 2 * f), 2 * base)
+    np.testing.assert_allclose(oracle.collide(st, space, W.EQ_ABSOLUTE, 0, rates, 3 * f), 3 * base,
+                               rtol=1e-14, atol=1e-17)
+    np.testing.assert_allclose(oracle.equilibrium(st, space, W.EQ_ABSOLUTE, 0, 3 * rho, u),
+                               3 * oracle.equilibrium(st, space, W.EQ_ABSOLUTE, 0, rho, u), rtol=1e-15)
+
+
+@pytest.mark.parametrize("space", [W.CENTRAL, W.CUMULANT])
+def test_swe_background_depth_is_a_gravity_rescaling(space):
+    """h0 (the shallow-water background depth, reading R33 fixes h0 = 1): Zhou's equilibrium
+    (eq:DiscreteShallowWaterEquilibrium) and the Maxwellian at
+    cs^2 = g h / 2 satisfy f_eq(lambda h, u; g) = lambda f_eq(h, u; lambda g)
+    (every g enters as g h^2 or g h cs-products), so a depth scale lambda is the h0 = 1 run with
+    gravity lambda g: C(lambda f; g) = lambda C(f; lambda g)."""
+    st, g = W.D2Q9, 0.0613125
+    rng = np.random.default_rng(22)
+    n = 16
+    h = rng.uniform(1.0, 3.0, n)
+    u = np.zeros((n, 3))
+    u[:, :2] = rng.uniform(-0.05, 0.05, (n, 2))
+    lam = 2.0
+    np.testing.assert_allclose(oracle.equilibrium(st, space, W.EQ_SWE, 0, lam * h, u, g=g),
+                               lam * oracle.equilibrium(st, space, W.EQ_SWE, 0, h, u, g=lam * g), rtol=1e-15,
+                               atol=1e-17)
+    f = oracle.equilibrium(st, space, W.EQ_SWE, 0, h, u, g=lam * g) * (1 + 1e-2 * rng.uniform(-1, 1, (n, 9)))
+    rates = W.rates_random(st)
+    np.testing.assert_allclose(oracle.collide(st, space, W.EQ_SWE, 0, rates, lam * f, g=g),
+                               lam * oracle.collide(st, space, W.EQ_SWE, 0, rates, f, g=lam * g), rtol=1e-14,
+                               atol=1e-16)
