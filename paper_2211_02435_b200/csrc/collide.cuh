@@ -756,6 +756,34 @@ __host__ __device__ constexpr bool mono_present(int e) {
   else return (ex_of(e) + ey_of(e) + ez_of(e) <= 4) && !(ex_of(e) >= 1 && ey_of(e) >= 1 && ez_of(e) >= 1);
 }
 
+// graded-lexicographic position of monomial e among the stencil's raw-moment monomials: the
+// index of the WO polynomial whose leading monomial is e (and of its rate; wo_basis order)
+template <class S>
+__host__ __device__ constexpr int wo_index(int e) {
+  int k = 0;
+  for (int deg = 0; deg <= 6; ++deg)
+    for (int a = 2; a >= 0; --a)
+      for (int b = 2; b >= 0; --b)
+        for (int z = 2; z >= 0; --z) {
+          if (a + b + z != deg || (S::D == 2 && z > 0) || !mono_present<S>(a + 3 * b + 9 * z)) continue;
+          if (a + 3 * b + 9 * z == e) return k;
+          ++k;
+        }
+  return -1;
+}
+
+// one axis of the Hermite factor {1, t, t^2 - 1/3}: L (sgn = -1) or L^{-1} (sgn = +1) along axis
+// `ax` of the moment cube: c[.. 2 ..] += sgn / 3 * c[.. 0 ..]
+template <int ax, int NC, class real>
+__device__ __forceinline__ void hermite_axis(real (&c)[NC], real sgn) {
+  constexpr int st = ax == 0 ? 1 : (ax == 1 ? 3 : 9);
+  sfor<NC>([&](auto e) {
+    constexpr int ie = e;
+    constexpr int digit = (ie / st) % 3;
+    if constexpr (digit == 2) c[e] = fma(sgn * real(1.0 / 3.0), c[ie - 2 * st], c[e]);
+  });
+}
+
 // q* = q + S (q_eq - q) with q = L m (reading R31): m* = m + L^{-1} S L (m_eq - m)
 template <class S, class EQ, class real, int NC>
 __device__ __forceinline__ void relax_wo(real (&c)[NC], const EQ &eq, const Rates<real> &r) {
@@ -766,6 +794,20 @@ __device__ __forceinline__ void relax_wo(real (&c)[NC], const EQ &eq, const Rate
       else d[e] = eq.template get<e>() - c[e];
     }
   });
+  if constexpr (S::Q == 27 || S::Q == 9) {
+    // product lattices: the WO basis is the tensor-product monic Hermite basis {1, t, t^2 - 1/3}
+    // per axis (pinned: test_wo_basis_is_hermite_on_product_lattices), so L = L1 (x) L1 (x) L1 is
+    // three axis sweeps, L^{-1} likewise — 2 x 9 d FMAs instead of the dense 2 q^2
+    hermite_axis<0>(d, real(-1));
+    hermite_axis<1>(d, real(-1));
+    if constexpr (S::D == 3) hermite_axis<2>(d, real(-1));
+    sfor<NC>([&](auto e) { d[e] = r.w[wo_index<S>(e)] * d[e]; });
+    hermite_axis<0>(d, real(1));
+    hermite_axis<1>(d, real(1));
+    if constexpr (S::D == 3) hermite_axis<2>(d, real(1));
+    sfor<NC>([&](auto e) { c[e] += d[e]; });
+    return;
+  }
   real t[S::Q];
   sfor<S::Q>([&](auto p) {
     real acc = real(0);

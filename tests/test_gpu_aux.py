@@ -160,11 +160,11 @@ def test_swe_depth_scaling_bitwise(space):
     st, shape = W.D2Q9, (24, 16, 1)
     g = 0.0613125
     f0 = initial_state(st, space, W.EQ_SWE, 0, shape, g=2 * g, noise=0.0, dam=(6.0, 4.0, 1.25))
-    with L.Lattice(st, space, W.EQ_SWE, W.rate_set_p(st), shape, swe_g=2 * g) as lat:
+    with L.Lattice(st, space, W.EQ_SWE, W.rate_set_p(st), shape, zero_centered=False, swe_g=2 * g) as lat:
         lat.set_populations(f0)
         lat.step(10)
         a = lat.get_populations()
-    with L.Lattice(st, space, W.EQ_SWE, W.rate_set_p(st), shape, swe_g=g) as lat:
+    with L.Lattice(st, space, W.EQ_SWE, W.rate_set_p(st), shape, zero_centered=False, swe_g=g) as lat:
         lat.set_populations(2 * f0)
         lat.step(10)
         b = lat.get_populations()
