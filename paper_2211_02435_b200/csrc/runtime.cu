@@ -1157,8 +1157,9 @@ lbm_status lbm_init_macroscopic(lbm_ctx *c, const double *rho, const double *u) 
   if (!c || !rho || !u) return fail(c, LBM_EINVAL, "null argument");
   LBM_CUDA(c, cudaSetDevice(c->device));
   const long long n = local_cells(c);
-  const size_t bytes = (size_t)n * (1 + c->d) * sizeof(double);
-  lbm_status s = ensure_staging(c, bytes);
+  // staging sized for lbm_get_macroscopic too (4 n doubles), so an init / get pair never frees and
+  // re-allocates it (a 2 GB cudaFree + cudaMalloc cost C5's end-to-end run ~0.5 s)
+  lbm_status s = ensure_staging(c, (size_t)n * 4 * sizeof(double));
   if (s != LBM_OK) return s;
   double *dr = static_cast<double *>(c->staging);
   double *du = dr + n;
