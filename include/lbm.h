@@ -317,6 +317,9 @@ typedef struct {
   void *flags;
   long long pid;                 /* exporting process id                                      */
   int device, rank, nranks, stencil, precision, nx, ny, nz;
+  long long grid_off[2];         /* byte offset of grid k inside the allocation its IPC handle
+                                    names (non-zero when lbm_domain.dev_alloc sub-allocates,
+                                    e.g. from a caching allocator; CUDA IPC maps whole blocks) */
 } lbm_peer_info;
 lbm_status lbm_peer_export(lbm_ctx *ctx, lbm_peer_info *out);
 /* Maps the neighbours' grids and flags; LBM_EINVAL if their lattice, stencil, precision or

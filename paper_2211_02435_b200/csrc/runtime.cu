@@ -1354,6 +1354,27 @@ lbm_status lbm_sync(lbm_ctx *c) {
   return LBM_OK;
 }
 
+// byte offset of p inside its allocation block (cuMemGetAddressRange, fetched through the runtime:
+// no -lcuda); the block is what a CUDA IPC handle of p names
+static lbm_status allocation_offset(lbm_ctx *c, void *p, long long *off) {
+  typedef CUresult (*RangeFn)(CUdeviceptr *, size_t *, CUdeviceptr);
+  static RangeFn range = nullptr;
+  if (!range) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    const cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !fn || q != cudaDriverEntryPointSuccess)
+      return fail(c, LBM_ECUDA, "cuMemGetAddressRange unavailable");
+    range = reinterpret_cast<RangeFn>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS)
+    return fail(c, LBM_ECUDA, "cuMemGetAddressRange failed");
+  *off = (long long)(reinterpret_cast<CUdeviceptr>(p) - base);
+  return LBM_OK;
+}
+
 lbm_status lbm_peer_export(lbm_ctx *c, lbm_peer_info *out) {
   if (!c || !out) return LBM_EINVAL;
   if (c->streaming == LBM_ESOTERIC_PULL || c->streaming == LBM_ESOTERIC_TWIST || c->streaming == LBM_ESOTERIC_PUSH)
@@ -1371,6 +1392,14 @@ lbm_status lbm_peer_export(lbm_ctx *c, lbm_peer_info *out) {
     LBM_CUDA(c, cudaIpcGetMemHandle(&h, c->buf[k]));
     memcpy(out->grid_ipc[k], &h, sizeof(h));
     out->grid[k] = c->buf[k];
+    // the handle names the whole allocation block: a grid sub-allocated through dev_alloc (a
+    // caching allocator) sits at an offset inside it, which the importer adds back
+    out->grid_off[k] = 0;
+    if (c->dev_alloc) {
+      long long off = 0;
+      if (lbm_status s = allocation_offset(c, c->buf[k], &off); s != LBM_OK) return s;
+      out->grid_off[k] = off;
+    }
   }
   cudaIpcMemHandle_t h;
   LBM_CUDA(c, cudaIpcGetMemHandle(&h, c->peer_flags));
@@ -1421,7 +1450,7 @@ lbm_status peer_connect_impl(lbm_ctx *c, const lbm_peer_info *lo, const lbm_peer
   drop_graphs(c);  // captured peer loops hold the old neighbour pointers
   const long long me = (long long)getpid();
   // maps a peer allocation: same process -> its pointer; else CUDA IPC (one mapping per handle)
-  auto map = [&](const lbm_peer_info *p, const unsigned char *ipc, void *raw, void **out) -> lbm_status {
+  auto map = [&](const lbm_peer_info *p, const unsigned char *ipc, void *raw, long long off, void **out) -> lbm_status {
     if (p->pid == me) {
       if (p->device != c->device) {
         cudaError_t e = cudaDeviceEnablePeerAccess(p->device, 0);
@@ -1433,7 +1462,7 @@ lbm_status peer_connect_impl(lbm_ctx *c, const lbm_peer_info *lo, const lbm_peer
     }
     for (int k = 0; k < c->n_mapped; ++k)  // the same neighbour on both sides (two ranks)
       if (c->peer_pid[k] == p->pid && c->peer_raw[k] == raw) {
-        *out = c->peer_mapped[k];
+        *out = static_cast<char *>(c->peer_mapped[k]) + off;
         return LBM_OK;
       }
     cudaIpcMemHandle_t h;
@@ -1442,18 +1471,18 @@ lbm_status peer_connect_impl(lbm_ctx *c, const lbm_peer_info *lo, const lbm_peer
     LBM_CUDA(c, cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
     c->peer_pid[c->n_mapped] = p->pid;
     c->peer_raw[c->n_mapped] = raw;
-    c->peer_mapped[c->n_mapped++] = ptr;
-    *out = ptr;
+    c->peer_mapped[c->n_mapped++] = ptr;  // the block base (what cudaIpcCloseMemHandle takes)
+    *out = static_cast<char *>(ptr) + off;
     return LBM_OK;
   };
   void *g[2][2], *f[2];
   for (int k = 0; k < 2; ++k) {
     const lbm_peer_info *p = nb[k];
     lbm_status s;
-    if ((s = map(p, p->grid_ipc[0], p->grid[0], &g[0][k])) != LBM_OK) return s;
+    if ((s = map(p, p->grid_ipc[0], p->grid[0], p->grid_off[0], &g[0][k])) != LBM_OK) return s;
     g[1][k] = nullptr;
-    if (p->grid[1] && (s = map(p, p->grid_ipc[1], p->grid[1], &g[1][k])) != LBM_OK) return s;
-    if ((s = map(p, p->flags_ipc, p->flags, &f[k])) != LBM_OK) return s;
+    if (p->grid[1] && (s = map(p, p->grid_ipc[1], p->grid[1], p->grid_off[1], &g[1][k])) != LBM_OK) return s;
+    if ((s = map(p, p->flags_ipc, p->flags, 0, &f[k])) != LBM_OK) return s;
   }
   const size_t P = c->g.plane * c->esize, nzl = (size_t)c->g.nzl;
   for (int b = 0; b < 2; ++b) {

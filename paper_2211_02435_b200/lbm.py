@@ -81,7 +81,7 @@ class lbm_peer_info(ctypes.Structure):
                 ("grid", ctypes.c_void_p * 2), ("flags", ctypes.c_void_p), ("pid", ctypes.c_longlong),
                 ("device", ctypes.c_int), ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
                 ("stencil", ctypes.c_int), ("precision", ctypes.c_int), ("nx", ctypes.c_int),
-                ("ny", ctypes.c_int), ("nz", ctypes.c_int)]
+                ("ny", ctypes.c_int), ("nz", ctypes.c_int), ("grid_off", ctypes.c_longlong * 2)]
 
 
 _dp = ctypes.POINTER(ctypes.c_double)

@@ -64,6 +64,9 @@ def main():
     ap.add_argument("--steps", type=int, default=12)
     ap.add_argument("--halo", choices=["exchange", "peer"], default="exchange",
                     help="exchange: SlabRunner (NCCL/gloo P2P); peer: PeerRunner (fused push over CUDA IPC)")
+    ap.add_argument("--suballoc", action="store_true",
+                    help="population grids from a torch-backed dev_alloc that returns pointers 4 KiB inside "
+                         "their blocks (the peer path must map them at their offset)")
     args = ap.parse_args()
     # the TB case's small slabs keep their two-step sweeps (below the 2-wave rule of lbm_create)
     os.environ.setdefault("LBM_PEER_TB", "1")
@@ -86,8 +89,20 @@ def main():
         streaming = L.LBM_AA if name.endswith("AA") else L.LBM_PULL
         stream = torch.cuda.Stream()
         torch.cuda.set_stream(stream)
+        allocator = None
+        if args.suballoc:
+            blocks = {}
+
+            def alloc(nbytes, blocks=blocks):
+                t = torch.empty(nbytes + 8192, dtype=torch.uint8, device=f"cuda:{dev}")
+                p = t.data_ptr() + 4096
+                blocks[p] = t
+                return p
+
+            allocator = (alloc, lambda p, blocks=blocks: blocks.pop(p, None))
         lat = L.Lattice(st, space, eq, rates, shape, zero_centered=zc, bc=bc, swe_g=g, device=dev,
-                        stream=stream.cuda_stream, rank=rank, nranks=world, streaming=streaming)
+                        stream=stream.cuda_stream, rank=rank, nranks=world, streaming=streaming,
+                        allocator=allocator)
         r, u = fields(st, eq, shape, lat.offset, lat.extent)
         lat.init_macroscopic(np.ascontiguousarray(r), np.ascontiguousarray(u[:lat.d]))
         runner = (D.PeerRunner if args.halo == "peer" else D.SlabRunner)(lat, rank, world)

@@ -39,3 +39,16 @@ def test_torchrun_slabs_bitwise(nproc, halo):
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
     assert "ALL PASS" in r.stdout
+
+
+def test_torchrun_peer_push_suballocated_grids():
+    """The fused halo push across processes when the population grids come from a dev_alloc
+    that sub-allocates (pointers 4 KiB inside torch caching-allocator blocks): CUDA IPC maps
+    whole blocks, so lbm_peer_info carries each grid's offset inside its block."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "scripts", "slab_check.py"), "--steps", "9", "--halo", "peer", "--suballoc"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert "ALL PASS" in r.stdout
