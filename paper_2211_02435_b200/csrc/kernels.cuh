@@ -504,10 +504,19 @@ __global__ void __launch_bounds__(DIAG_BLOCK) k_diag_partial(const real *mem, co
                                                              const double3 dj) {
   const long long n = (long long)g.nx * g.ny * g.nzl;
   double acc[5] = {0, 0, 0, 0, 0};
+  const bool narrow = n < (1ll << 31);  // 32-bit index arithmetic (64-bit division is slow)
   for (long long c = (long long)blockIdx.x * DIAG_BLOCK + threadIdx.x; c < n; c += (long long)DIAG_GRID * DIAG_BLOCK) {
-    const int x = (int)(c % g.nx);
-    const int y = (int)((c / g.nx) % g.ny);
-    const int zl = (int)(c / ((long long)g.nx * g.ny));
+    int x, y, zl;
+    if (narrow) {
+      const unsigned cu = (unsigned)c, row = cu / (unsigned)g.nx;
+      x = (int)(cu - row * (unsigned)g.nx);
+      y = (int)(row % (unsigned)g.ny);
+      zl = (int)(row / (unsigned)g.ny);
+    } else {
+      x = (int)(c % g.nx);
+      y = (int)((c / g.nx) % g.ny);
+      zl = (int)(c / ((long long)g.nx * g.ny));
+    }
     double s = 0, jx = 0, jy = 0, jz = 0;
     sfor<S::Q>([&](auto i) {
       const double v = (double)mem[Canon<S>::template at<i>(g, x, y, zl, aa, state)];
