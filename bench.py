@@ -453,10 +453,13 @@ def main():
             try:
                 D.PeerRunner(lat, rank, n)  # connects the ring; lbm_step then runs the fused push
                 path = "peer"
-                halo = ("peer: fused boundary-plane push over NVLink peer memory (CUDA IPC), device flags, "
+                # device flags spun on by a one-thread kernel when every neighbour has its own GPU;
+                # host-polled flags when ranks share a GPU (no kernel waits on another rank there)
+                waits = "host-polled flags" if lat.info().peer_wait_host else "device flags"
+                halo = (f"peer: fused boundary-plane push over NVLink peer memory (CUDA IPC), {waits}, "
                         "lbm_step" if cfg["streaming"] == L.LBM_PULL else
                         "peer: AA odd-step boundary kernels access the neighbours' planes over NVLink peer "
-                        "memory (CUDA IPC), device flags, lbm_step")
+                        f"memory (CUDA IPC), {waits}, lbm_step")
             except (L.LbmError, D.PeerUnavailable) as ex:
                 if args.halo == "peer":
                     raise
@@ -544,6 +547,8 @@ def main():
         launches_per_step = 1.0 / tb
     elif path == "peer":
         launches_per_step = 4.5 if tb == 2 else 5
+        if lat.info().peer_wait_host:  # no wait kernels
+            launches_per_step -= 1
     else:
         launches_per_step = 2.5 if tb == 2 else 3
     if resident:  # one cluster launch runs all K steps of lbm_step(K)

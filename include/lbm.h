@@ -230,6 +230,9 @@ typedef struct {
                                step; same collision code, bitwise equal); 0: not used.
                                Environment LBM_RESIDENT=0 disables it, LBM_RESIDENT_CLUSTER=k
                                caps the cluster size (both read per call).                 */
+  int peer_wait_host;       /* 1 when the fused halo push of this connected context orders its
+                               phases on the host (a neighbour shares this GPU; see
+                               lbm_peer_connect), 0 for device-side waits or no peer path.  */
 } lbm_info;
 
 /* Creates a context: validates admissibility, allocates the population grid(s) (two for
@@ -320,12 +323,20 @@ typedef struct {
   long long grid_off[2];         /* byte offset of grid k inside the allocation its IPC handle
                                     names (non-zero when lbm_domain.dev_alloc sub-allocates,
                                     e.g. from a caching allocator; CUDA IPC maps whole blocks) */
+  unsigned char uuid[16];        /* cudaDeviceProp.uuid of the exporting context's GPU        */
 } lbm_peer_info;
 lbm_status lbm_peer_export(lbm_ctx *ctx, lbm_peer_info *out);
 /* Maps the neighbours' grids and flags; LBM_EINVAL if their lattice, stencil, precision or
    ranks do not match this context's ring; LBM_EUNSUPPORTED for Esoteric Pull / Twist or one rank
    (at export); LBM_ECUDA if the memory cannot be mapped (no peer access; nothing stays mapped).
-   Resets the flags.  lower = upper = NULL disconnects (unmaps the neighbours; synchronises). */
+   Resets the flags.  Waits: when both neighbours run on other GPUs (one process per GPU, the
+   deployment case) a one-thread kernel spins on the flags on the device and n >= 32 steps replay
+   captured graphs; when a neighbour shares this GPU (uuid), kernels that wait on one another
+   must not run as separate launches on one device (nothing co-schedules them; across processes
+   a spinning kernel blocks the context switch), so the HOST polls the flags and enqueues each
+   phase's kernels only once its neighbours completed the previous one (no graphs; contexts of
+   one process must then be stepped from one host thread each).  Environment LBM_PEER_WAIT
+   = host | device (read at connect) overrides the choice.  lower = upper = NULL disconnects (unmaps the neighbours; synchronises). */
 lbm_status lbm_peer_connect(lbm_ctx *ctx, const lbm_peer_info *lower, const lbm_peer_info *upper);
 /* PULL: pushes the current grid's boundary planes into the neighbours' ghost planes; AA:
    only the handshake (orders the neighbours' initialisation before the first step). */
@@ -337,11 +348,13 @@ lbm_status lbm_peer_prime(lbm_ctx *ctx);
    planes per slab, no walls) advance pairs of steps: interior planes by the fused sweep, the
    boundary regions by two single steps through 8 scratch planes behind grid 0 with pushes into
    the neighbours' scratch and ghost planes; every rank must call with the same n.
-   LBM_PEER_TB=0 (read at create) keeps single steps.  Several
-   contexts driven from ONE host thread must be stepped in small interleaved chunks: a
-   context's stream waits on the GPU for its neighbours, and enqueuing many of its steps
-   first can fill the launch queue before the neighbours' work is enqueued (one process per
-   GPU, the deployment case, has no such coupling). */
+   LBM_PEER_TB=0 (read at create) keeps single steps.  Device-side waits: several contexts
+   driven from ONE host thread must be stepped in small interleaved chunks (a context's stream
+   waits on the GPU for its neighbours, and enqueuing many of its steps first can fill the
+   launch queue before the neighbours' work is enqueued).  Host-ordered waits (neighbours on
+   this GPU, lbm_info.peer_wait_host): the call returns once its last phase is enqueued, having
+   blocked until the neighbours completed each earlier phase, so every context of a process
+   needs its own host thread. */
 lbm_status lbm_step_peer(lbm_ctx *ctx, int n);
 /* *timed_out = 1 if a wait for a neighbour gave up (results invalid); synchronises. */
 lbm_status lbm_peer_status(lbm_ctx *ctx, int *timed_out);

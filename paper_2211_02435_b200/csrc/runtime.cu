@@ -18,7 +18,9 @@
 #include <nccl.h>    // types only
 #include <unistd.h>  // getpid: same-process peers use plain device pointers
 
+#include <chrono>
 #include <mutex>
+#include <thread>
 
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for Nsight timelines
 
@@ -244,6 +246,14 @@ struct lbm_ctx {
   int n_mapped = 0;
   cudaGraphExec_t peer_graph[2] = {nullptr, nullptr};  // captured lbm_step_peer loops per grid parity
   bool peer_on = false;
+  // host-ordered waits (a neighbour shares this GPU): no kernel spins on a flag another rank
+  // writes; the host polls the flags and enqueues the dependent work only once they are set
+  bool peer_host_wait = false;
+  long long host_phase = 0;             // signals enqueued since connect (the device's flags[3])
+  bool host_timed_out = false;
+  cudaStream_t s_poll = nullptr;        // D2H reads of the flags
+  long long *h_flags = nullptr;         // pinned [2]
+  unsigned char uuid[16] = {};          // this context's device
   cudaStream_t s_int = nullptr;         // interior planes of lbm_step_peer
   cudaEvent_t ev_b = nullptr, ev_i = nullptr;
   // slab decomposition with ghost planes (nranks > 1, or one rank exchanging with itself
@@ -515,6 +525,43 @@ unsigned long long peer_timeout_ns() {
   return (unsigned long long)((s > 0 ? s : 60.0) * 1e9);
 }
 
+// The wait before a phase: on the device (a one-thread k_peer_wait spinning on the flags,
+// the deployment case of one GPU per rank) or, when a neighbour shares this GPU, on the host:
+// kernels that wait on one another must not run as separate launches on ONE GPU (nothing
+// guarantees they are co-scheduled; across processes the spin blocks the context switch), so
+// the host polls the flags (D2H reads on a private stream) and only then enqueues the work of
+// the phase.  The target is the number of signals this context has enqueued, which equals the
+// device-side phase flags[3] the spinning wait reads at the same point of the stream.
+void peer_wait(lbm_ctx *c, unsigned long long timeout_ns) {
+  if (!c->peer_host_wait) {
+    k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, timeout_ns);
+    return;
+  }
+  if (c->host_timed_out) return;  // an earlier wait gave up: do not stall again
+  const long long target = c->host_phase;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    if (cudaMemcpyAsync(c->h_flags, c->peer_flags, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->s_poll) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(c->s_poll) != cudaSuccess) {
+      c->host_timed_out = true;  // reported by lbm_peer_status like a timeout
+      return;
+    }
+    if (c->h_flags[0] >= target && c->h_flags[1] >= target) return;
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (dt * 1e9 > (double)timeout_ns) {
+      c->host_timed_out = true;
+      return;
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+void peer_signal(lbm_ctx *c) {
+  k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_remote[0], c->peer_remote[1]);
+  ++c->host_phase;
+}
+
 // Release of the boundary kernels' stores into peer memory before the completion flag
 // (kernels.cuh peer_release_cta): 1 (default) = a CTA barrier, then one system-scope fence by
 // thread 0 of every CTA, so the halo stores are visible system-wide before the kernel ends
@@ -573,7 +620,7 @@ int enqueue_peer_steps(lbm_ctx *c, int n, int cur) {
       gi.zcount = nzl - 4;
       c->ops->pull2(A, B, gi, c->params, c->swe_g, peer_tb_chunks(c), c->s_int);
       cudaEventRecord(c->ev_i, c->s_int);
-      k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, tmo);
+      peer_wait(c, tmo);
       GridParams g1 = c->g;
       g1.peer_lo = nb_lo7;
       g1.peer_hi = nb_hi0;
@@ -582,8 +629,8 @@ int enqueue_peer_steps(lbm_ctx *c, int n, int cur) {
       c->ops->pull(A, s_lo, g1, c->params, c->swe_g, c->bb, 3, c->stream);
       g1.zbegin = nzl - 3;
       c->ops->pull(A, s_hi, g1, c->params, c->swe_g, c->bb, 3, c->stream);
-      k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_remote[0], c->peer_remote[1]);
-      k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, tmo);
+      peer_signal(c);
+      peer_wait(c, tmo);
       GridParams g2 = c->g;
       g2.peer_lo = c->peer_ghost[1 - cur][0];
       g2.peer_hi = c->peer_ghost[1 - cur][1];
@@ -592,7 +639,7 @@ int enqueue_peer_steps(lbm_ctx *c, int n, int cur) {
       c->ops->pull(s_lo, B, g2, c->params, c->swe_g, c->bb, 2, c->stream);
       g2.zbegin = nzl - 2;
       c->ops->pull(s_hi, B, g2, c->params, c->swe_g, c->bb, 2, c->stream);
-      k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_remote[0], c->peer_remote[1]);
+      peer_signal(c);
       cudaEventRecord(c->ev_b, c->stream);
       cur ^= 1;
     }
@@ -611,7 +658,7 @@ int enqueue_peer_steps(lbm_ctx *c, int n, int cur) {
     cudaStreamWaitEvent(c->s_int, c->ev_b, 0);   // boundary of the previous step
     launch(c->g, 1, nzl - 2, c->s_int);
     cudaEventRecord(c->ev_i, c->s_int);
-    k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, tmo);
+    peer_wait(c, tmo);
     GridParams gb = c->g;
     if (pull || pat == lbm::PAT_AA_ODD) {  // the even AA step touches only its own cells
       const int b = pull ? 1 - cur : 0;
@@ -621,7 +668,7 @@ int enqueue_peer_steps(lbm_ctx *c, int n, int cur) {
     }
     launch(gb, 0, 1, c->stream);
     if (nzl > 1) launch(gb, nzl - 1, 1, c->stream);
-    k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_remote[0], c->peer_remote[1]);
+    peer_signal(c);
     cudaEventRecord(c->ev_b, c->stream);
     cur ^= 1;
   }
@@ -1117,6 +1164,8 @@ lbm_status lbm_destroy(lbm_ctx *c) {
   if (c->ev_i) cudaEventDestroy(c->ev_i);
   if (c->s_int) cudaStreamDestroy(c->s_int);
   if (c->peer_flags) cudaFree(c->peer_flags);
+  if (c->s_poll) cudaStreamDestroy(c->s_poll);
+  if (c->h_flags) cudaFreeHost(c->h_flags);
   if (c->comm) nccl_api().CommDestroy(c->comm);
   for (int k = 0; k < 2; ++k)
     if (c->buf[k]) {
@@ -1149,6 +1198,7 @@ lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
   info->temporal_blocking = (use_temporal_blocking(c) || (c->multi && c->peer_tb_cap)) ? 2 : 1;
   info->resident_cluster = resident_cluster(c);
   info->cuda_graph_steps = (c->nranks == 1 && !info->resident_cluster && use_graphs(c)) ? kGraphSteps : 0;
+  info->peer_wait_host = c->peer_on && c->peer_host_wait;
   return LBM_OK;
 }
 
@@ -1414,6 +1464,10 @@ lbm_status lbm_peer_export(lbm_ctx *c, lbm_peer_info *out) {
   out->nx = c->gnx;
   out->ny = c->gny;
   out->nz = c->gnz;
+  cudaDeviceProp prop{};
+  LBM_CUDA(c, cudaGetDeviceProperties(&prop, c->device));
+  memcpy(out->uuid, &prop.uuid, sizeof(out->uuid));
+  memcpy(c->uuid, &prop.uuid, sizeof(c->uuid));
   return LBM_OK;
 }
 
@@ -1500,6 +1554,19 @@ lbm_status peer_connect_impl(lbm_ctx *c, const lbm_peer_info *lo, const lbm_peer
   c->peer_remote[0] = static_cast<long long *>(f[0]) + 1;  // I am the lower's upper neighbour
   c->peer_remote[1] = static_cast<long long *>(f[1]) + 0;
   LBM_CUDA(c, cudaMemset(c->peer_flags, 0, 4 * sizeof(long long)));
+  // device-side waits only when every neighbour runs on another GPU (peer_wait)
+  {
+    bool shared = false;
+    for (int k = 0; k < 2; ++k) shared |= memcmp(nb[k]->uuid, c->uuid, sizeof(c->uuid)) == 0;
+    const char *env = getenv("LBM_PEER_WAIT");
+    c->peer_host_wait = env && !strcmp(env, "host") ? true : env && !strcmp(env, "device") ? false : shared;
+    c->host_phase = 0;
+    c->host_timed_out = false;
+    if (c->peer_host_wait && !c->s_poll) {
+      LBM_CUDA(c, cudaStreamCreateWithFlags(&c->s_poll, cudaStreamNonBlocking));
+      LBM_CUDA(c, cudaMallocHost(&c->h_flags, 2 * sizeof(long long)));
+    }
+  }
   // load the wait / signal kernels and every step kernel now, before any wait can spin
   // (lazy module loading at a first launch waits for the running kernels: Ops::preload)
   {
@@ -1531,8 +1598,8 @@ lbm_status lbm_peer_prime(lbm_ctx *c) {
   if (s != LBM_OK) return fail(c, s, "layout");
   const size_t E = c->esize, bytes = lay.halo_elems * E;
   if (c->streaming != LBM_PULL) {  // AA: no ghost data; the handshake orders the neighbours' init
-    k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, peer_timeout_ns());
-    k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_remote[0], c->peer_remote[1]);
+    peer_wait(c, peer_timeout_ns());
+    peer_signal(c);
     return check_launch(c, "lbm_peer_prime");
   }
   const int b = c->cur;
@@ -1541,10 +1608,10 @@ lbm_status lbm_peer_prime(lbm_ctx *c) {
   // the ghost plane offsets of the receive blocks (recv_hi lies in plane nzl + 1, recv_lo in 0)
   char *lo_dst = static_cast<char *>(c->peer_ghost[b][0]) - top + lay.recv_hi * E;
   char *hi_dst = static_cast<char *>(c->peer_ghost[b][1]) + lay.recv_lo * E;
-  k_peer_wait<<<1, 1, 0, c->stream>>>(c->peer_flags, peer_timeout_ns());
+  peer_wait(c, peer_timeout_ns());
   LBM_CUDA(c, cudaMemcpyAsync(lo_dst, base + lay.send_lo * E, bytes, cudaMemcpyDefault, c->stream));
   LBM_CUDA(c, cudaMemcpyAsync(hi_dst, base + lay.send_hi * E, bytes, cudaMemcpyDefault, c->stream));
-  k_peer_signal<<<1, 1, 0, c->stream>>>(c->peer_flags, c->peer_remote[0], c->peer_remote[1]);
+  peer_signal(c);
   return check_launch(c, "lbm_peer_prime");
 }
 
@@ -1559,7 +1626,7 @@ lbm_status lbm_step_peer(lbm_ctx *c, int n) {
     if (ps != LBM_OK) return ps;
   }
   int t = 0;
-  if (n >= kGraphSteps && graphs_enabled()) {  // replay captured 32-step loops (same launches)
+  if (n >= kGraphSteps && graphs_enabled() && !c->peer_host_wait) {  // replay captured 32-step loops
     for (int par = 0; par < 2; ++par) {
       if (c->peer_graph[par]) continue;
       cudaGraph_t gr = nullptr;
@@ -1599,7 +1666,7 @@ lbm_status lbm_peer_status(lbm_ctx *c, int *timed_out) {
   LBM_CUDA(c, cudaStreamSynchronize(c->stream));
   long long v = 0;
   LBM_CUDA(c, cudaMemcpy(&v, c->peer_flags + 2, sizeof(v), cudaMemcpyDeviceToHost));
-  *timed_out = v != 0;
+  *timed_out = v != 0 || c->host_timed_out;
   return LBM_OK;
 }
 

@@ -264,17 +264,52 @@ def connect_local(lats):
         l.peer_prime()
 
 
+def on_ranks(lats, fn):
+    """fn(lat) for every context of one process, concurrently from one host thread each (the
+    ctypes calls release the GIL).  Contexts whose neighbours share their GPU order the peer
+    phases on the host (lbm_peer_connect): a context's lbm_step blocks until its neighbours
+    enqueued and completed their previous phase, so each needs its own thread."""
+    import threading
+
+    errs = [None] * len(lats)
+
+    def run(k):
+        try:
+            fn(lats[k])
+        except BaseException as ex:  # noqa: BLE001 — re-raised below
+            errs[k] = ex
+
+    ts = [threading.Thread(target=run, args=(k,)) for k in range(len(lats))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+
+
 def step_peer_local(lats, n: int, chunk: int = 1):
     """n steps of every context of one process with the fused halo push (lbm_step on the
-    connected contexts).  The ranks' launches are interleaved in chunks of `chunk` steps (a
-    context waits on the GPU for its neighbours; chunk = 2 lets the two-step sweeps run across
-    ranks)."""
-    done = 0
-    while done < n:
-        k = min(chunk, n - done)
-        for l in lats:
-            l.step(k)
-        done += k
+    connected contexts).  Host-ordered contexts (neighbours on the same GPU, the only case on
+    a one-GPU box) run in one host thread each; device-ordered ones (every neighbour on another
+    GPU) are enqueued from this thread, interleaved in chunks of `chunk` steps (a context waits
+    on the GPU for its neighbours; chunk = 2 lets the two-step sweeps run across ranks)."""
+    if any(l.info().peer_wait_host for l in lats):
+        def run(l):
+            done = 0
+            while done < n:
+                k = min(chunk, n - done)
+                l.step(k)
+                done += k
+        on_ranks(lats, run)
+    else:
+        done = 0
+        while done < n:
+            k = min(chunk, n - done)
+            for l in lats:
+                l.step(k)
+            done += k
     for l in lats:
         l.sync()
         assert not l.peer_timed_out(), "a neighbour wait timed out"

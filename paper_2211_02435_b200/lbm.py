@@ -73,7 +73,7 @@ class lbm_info(ctypes.Structure):
                 ("bytes_per_element", ctypes.c_size_t), ("device_bytes", ctypes.c_size_t),
                 ("steps_done", ctypes.c_longlong), ("rate_specialization", ctypes.c_int),
                 ("temporal_blocking", ctypes.c_int), ("cuda_graph_steps", ctypes.c_int),
-                ("resident_cluster", ctypes.c_int)]
+                ("resident_cluster", ctypes.c_int), ("peer_wait_host", ctypes.c_int)]
 
 
 class lbm_peer_info(ctypes.Structure):
@@ -81,7 +81,8 @@ class lbm_peer_info(ctypes.Structure):
                 ("grid", ctypes.c_void_p * 2), ("flags", ctypes.c_void_p), ("pid", ctypes.c_longlong),
                 ("device", ctypes.c_int), ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
                 ("stencil", ctypes.c_int), ("precision", ctypes.c_int), ("nx", ctypes.c_int),
-                ("ny", ctypes.c_int), ("nz", ctypes.c_int), ("grid_off", ctypes.c_longlong * 2)]
+                ("ny", ctypes.c_int), ("nz", ctypes.c_int), ("grid_off", ctypes.c_longlong * 2),
+                ("uuid", ctypes.c_ubyte * 16)]
 
 
 _dp = ctypes.POINTER(ctypes.c_double)

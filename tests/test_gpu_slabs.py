@@ -234,8 +234,9 @@ def test_c5_eight_slabs_128squared():
 
 @pytest.mark.parametrize("graphs", ["1", "0"])
 def test_peer_push_graph_replay_bitwise(graphs, monkeypatch):
-    """lbm_step_peer(n >= 32) replays captured 32-step graphs (device-side phase counters);
-    whole calls per context (not interleaved step by step) equal the single-rank run."""
+    """Whole lbm_step_peer(n) calls per context (not interleaved step by step; one host thread
+    per context) equal the single-rank run.  On one GPU the phases are host-ordered (no graphs);
+    with one GPU per rank n >= 32 replays captured graphs (test_peer_device_waits_across_gpus)."""
     monkeypatch.setenv("LBM_CUDA_GRAPHS", graphs)
     st, space, eq, zc = W.D3Q19, W.CENTRAL, W.EQ_DELTA, 1
     shape, nranks = (24, 10, 12), 3
@@ -250,8 +251,7 @@ def test_peer_push_graph_replay_bitwise(graphs, monkeypatch):
         lat.set_populations(np.ascontiguousarray(f0[:, lat.offset:lat.offset + lat.extent]))
     D.connect_local(lats)
     for n in (40, 71):
-        for lat in lats:
-            lat.step_peer(n)
+        D.on_ranks(lats, lambda lat: lat.step_peer(n))
     for lat in lats:
         lat.sync()
         assert not lat.peer_timed_out()
@@ -286,8 +286,8 @@ def test_peer_aa_equals_single_rank_bitwise(st, space, eq, zc, nranks, steps, re
 
 
 def test_peer_aa_graph_replay_and_macroscopic():
-    """AA peer loop replayed from captured graphs (whole calls per context), then the
-    macroscopic fields and the diagnostics at the odd parity match the single-rank run."""
+    """AA peer loop in whole calls per context (captured graphs with one GPU per rank; host-
+    ordered phases on one GPU), then the macroscopic fields and the diagnostics at the odd parity match the single-rank run."""
     st, space, eq, zc = W.D3Q27, W.CUMULANT, W.EQ_ABSOLUTE, 1
     shape, nranks = (24, 10, 12), 3
     rates = W.rate_set_p(st)
@@ -303,8 +303,7 @@ def test_peer_aa_graph_replay_and_macroscopic():
         lat.set_populations(np.ascontiguousarray(f0[:, lat.offset:lat.offset + lat.extent]))
     D.connect_local(lats)
     for n in (33, 32):
-        for lat in lats:
-            lat.step_peer(n)
+        D.on_ranks(lats, lambda lat: lat.step_peer(n))
     for lat in lats:
         lat.sync()
         assert not lat.peer_timed_out()
@@ -406,8 +405,8 @@ def test_peer_two_step_sweeps_match_single_rank(st, space, eq, zc, prec, shape, 
 
 
 def test_peer_two_step_sweeps_graph_replay(monkeypatch):
-    """Two-step sweeps across ranks inside the captured 32-step graphs (16 pairs per graph)
-    plus a remainder of pairs and a single step: equal to the single-rank run to rounding."""
+    """Two-step sweeps across ranks in whole calls (inside captured 32-step graphs, 16 pairs per
+    graph, with one GPU per rank; host-ordered phases on one GPU) plus a remainder of pairs and a single step: equal to the single-rank run to rounding."""
     monkeypatch.setenv("LBM_PEER_TB", "1")
     st, space, eq, zc = W.D3Q19, W.RAW, W.EQ_DELTA, 1
     shape, nranks, steps = (32, 16, 24), 2, 71
@@ -422,8 +421,7 @@ def test_peer_two_step_sweeps_graph_replay(monkeypatch):
         lat.set_populations(np.ascontiguousarray(f0[:, lat.offset:lat.offset + lat.extent]))
     D.connect_local(lats)
     for chunk in (64, 7):  # two graph replays per context, then 3 pairs + 1 single step
-        for lat in lats:
-            lat.step_peer(chunk)
+        D.on_ranks(lats, lambda lat: lat.step_peer(chunk))
     for lat in lats:
         lat.sync()
         assert not lat.peer_timed_out()
@@ -465,3 +463,65 @@ def test_exchange_path_two_step_regions(st, space, eq, zc, shape, nranks, monkey
         lat.close()
     assert gate_error(st, multi, single, zc) < 1e-13
     assert gate_error(st, multi, oracle_run(st, space, eq, zc, rates, shape, f0, steps), zc) < F64_TOL
+
+
+def test_peer_waits_are_host_ordered_when_ranks_share_a_gpu(monkeypatch):
+    """Contexts whose neighbours share their GPU never launch a kernel that spins on another
+    rank's flag (B200_PROFILING: such launches on one GPU are not co-scheduled); the host polls
+    the flags instead (lbm_info.peer_wait_host), no graphs.  LBM_PEER_WAIT overrides at connect."""
+    st, space, eq, zc = W.D3Q19, W.RAW, W.EQ_DELTA, 1
+    shape = (16, 8, 12)
+    rates = W.rate_set_p(st)
+    for env, want in ((None, 1), ("device", 0), ("host", 1)):
+        if env is None:
+            monkeypatch.delenv("LBM_PEER_WAIT", raising=False)
+        else:
+            monkeypatch.setenv("LBM_PEER_WAIT", env)
+        lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, rank=r, nranks=2, device=0)
+                for r in range(2)]
+        infos = [lat.peer_export() for lat in lats]
+        for r, lat in enumerate(lats):
+            lo, hi = D.neighbours(r, 2)
+            lat.peer_connect(infos[lo], infos[hi])
+        assert [lat.info().peer_wait_host for lat in lats] == [want, want]
+        for lat in lats:
+            lat.close()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="device-side peer waits need one GPU per rank")
+@pytest.mark.parametrize("tb", ["0", "1"])
+def test_peer_device_waits_across_gpus(tb, monkeypatch):
+    """The deployment case: every context on its own GPU (in one process), device-side waits,
+    n >= 32 steps from captured graphs, single steps and two-step pairs; equal to the single
+    rank (bitwise for single steps, to rounding for pairs)."""
+    monkeypatch.setenv("LBM_PEER_TB", tb)
+    monkeypatch.delenv("LBM_PEER_WAIT", raising=False)
+    st, space, eq, zc = W.D3Q19, W.RAW, W.EQ_DELTA, 1
+    ndev = torch.cuda.device_count()
+    nranks = min(ndev, 4)
+    shape, steps = (32, 16, 8 * nranks), 71
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc) as lat:
+        lat.set_populations(f0)
+        lat.step(steps)
+        single = lat.get_populations()
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, rank=r, nranks=nranks, device=r)
+            for r in range(nranks)]
+    for lat in lats:
+        lat.set_populations(np.ascontiguousarray(f0[:, lat.offset:lat.offset + lat.extent]))
+    D.connect_local(lats)
+    assert all(lat.info().peer_wait_host == 0 for lat in lats)
+    for chunk in (64, 7):
+        for lat in lats:
+            lat.step_peer(chunk)
+    for lat in lats:
+        lat.sync()
+        assert not lat.peer_timed_out()
+    multi = np.concatenate([lat.get_populations() for lat in lats], axis=1)
+    for lat in lats:
+        lat.close()
+    if tb == "0":
+        np.testing.assert_array_equal(multi, single)
+    else:
+        assert gate_error(st, multi, single, zc) < 1e-13
