@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Cost of the slab decomposition with the fused halo push, measured on ONE GPU: N slab
-contexts of one process (cuda:0, lbm_peer_* over plain device pointers, device-side flags)
-step a 1024 x 1024 x 128 D3Q27 cumulant lattice together; compared with one context stepping
+contexts of one process (cuda:0, lbm_peer_* over plain device pointers; since the
+host-ordered waits, flags polled by the host as on any GPU shared by ranks — the round-1
+numbers in profiles/r1/peer_overhead.txt were taken with device-side waits) step a 1024 x 1024 x 128 D3Q27 cumulant lattice together; compared with one context stepping
 the whole lattice.  Same cells, same bytes: the difference is the boundary/interior split,
 the wait/signal kernels and the halo stores.
 
@@ -94,11 +95,15 @@ def main():
         streams = [torch.cuda.ExternalStream(l.stream) for l in lats]
 
         def run(k):
-            while k > 0:
-                c = min(k, args.chunk)
-                for l in lats:
+            # one host thread per context: on one GPU the peer phases are host-ordered
+            # (lbm_info.peer_wait_host), no kernel waits on another context's flag
+            def ctx(l):
+                j = k
+                while j > 0:
+                    c = min(j, args.chunk)
                     l.step_peer(c)
-                k -= c
+                    j -= c
+            D.on_ranks(lats, ctx)
 
         run(args.chunk)
         ms = timed(run, args.steps, streams)
