@@ -585,6 +585,12 @@ def main():
                 "time_steps_per_launch": tb, "peak_source": peak_src,
                 "kernel": (("k_pull2_2d" if two_d else "k_pull2") + " (two fused steps)" if tb == 2 else
                            "k_pull/k_aa stream-collide") + f" ({kkey})"}
+    if tb == 2:
+        # the single-step kernel's roofline, per time step: what the fused sweep beats
+        roofline["frac_of_single_step_roofline_per_time_step"] = round(tb * achieved / peak, 4)
+        roofline["note"] = ("two fused steps per HBM sweep: the launch moves 2qS B/cell for TWO updates; the "
+                            "sweep is bound by the collision arithmetic at 2-3 CTAs/SM, not by HBM (ncu: fp64 "
+                            "pipe 44 % C2 fp64, issue slots 70 % C2 fp32, fp64 pipe 61 % C5; DESIGN.md 6.2b)")
     if n > 1:
         roofline["note"] = "N > 1: per-step time of boundary + interior launches with the halo " + halo.split(":")[0]
     if resident:
