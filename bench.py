@@ -73,7 +73,7 @@ CONFIGS = {
                    shape=lambda n: (256, 256, 256), slab=2, scaling="strong",
                    desc="D3Q19 raw-moment MRT TGV 256^3, fp32, zero-centered + delta eq, pull"),
     "c1": dict(stencil=W.D2Q9, space=W.POPULATION, eq=W.EQ_DELTA, zc=1, prec=0, streaming=0,
-               shape=lambda n: (64, 64, 1), slab=1, scaling="strong",
+               shape=lambda n: (64, 64, 1), slab=1, scaling="strong", steps=1000,
                desc="D2Q9 BGK TGV 64x64, fp64, zero-centered + delta eq, pull"),
     "c5": dict(stencil=W.D2Q9, space=W.CENTRAL, eq=W.EQ_SWE, zc=0, prec=0, streaming=0,
                shape=lambda n: (8192, 8192, 1), slab=1, scaling="strong",
@@ -358,7 +358,8 @@ def reference_arm(args, cfg, name):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: the workload's own count, C1 1000, else 100)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -376,6 +377,8 @@ def main():
                     help="override the global lattice shape (profiling runs only)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.steps is None:
+        args.steps = cfg.get("steps", 100)
     if args.impl == "reference":
         return reference_arm(args, cfg, args.config)
     if args.warmup < 3:
