@@ -169,3 +169,34 @@ def test_swe_depth_scaling_bitwise(space):
         lat.step(10)
         b = lat.get_populations()
     np.testing.assert_array_equal(b, 2 * a)
+
+
+@pytest.mark.parametrize("st,space,tau,model,streaming", [
+    (W.D2Q9, W.POPULATION, 1.0, 0, L.LBM_PULL),
+    (W.D2Q9, W.CUMULANT, 0.875, 1, L.LBM_PULL),
+    (W.D3Q19, W.RAW, 0.8, 0, L.LBM_AA),
+    (W.D3Q27, W.CUMULANT, 1.1, 0, L.LBM_PULL),
+    (W.D3Q27, W.CENTRAL, 0.65, 1, L.LBM_AA),
+])
+def test_gpu_poiseuille_bounce_back_closed_form(st, space, tau, model, streaming):
+    """The device path (walls + body force, pull and AA in place) against the closed-form
+    steady channel flow of half-way bounce-back (tests/test_oracle_pins.py
+    test_poiseuille_bounce_back_closed_form: u_x(y) = F / (2 nu) [(y + 1/2)(H - 1/2 - y) +
+    (16 Lambda - 3) / 12]) — a pin of reading R18 independent of the oracle."""
+    nx, ny, Fx = 32, 8, 1e-6
+    nz = 1 if W.DIM_OF[st] == 2 else 4
+    nu = (tau - 0.5) / 3
+    rates = [1 / tau] if space == W.POPULATION else W.regularized_rates(st, 1 / tau)
+    lam = (tau - 0.5) * ((tau - 0.5) if space == W.POPULATION else 0.5)
+    bc = [[0, 0], [L.LBM_BC_NOSLIP] * 2, [0, 0]]
+    eq = W.EQ_ABSOLUTE if space == W.CUMULANT else W.EQ_DELTA
+    with L.Lattice(st, space, eq, rates, (nx, ny, nz), zero_centered=True, bc=bc, streaming=streaming) as lat:
+        lat.set_populations(np.zeros((W.Q_OF[st], nz, ny, nx)))
+        lat.set_force([Fx, 0, 0], model=model)
+        lat.step(30000)
+        _, u = lat.get_macroscopic()
+    y = np.arange(ny)
+    ref = Fx / (2 * nu) * ((y + 0.5) * (ny - 0.5 - y) + (16 * lam - 3) / 12)
+    ux = u[0].reshape(nz, ny, nx)
+    assert np.abs(ux - ref[None, :, None]).max() < 1e-9 * ref.max()
+    assert np.abs(u[1:]).max() < 1e-12 * ref.max()

@@ -697,6 +697,42 @@ def test_poiseuille_flow(space, nu, model):
     assert np.abs(u[1]).max() < 1e-12 * ref.max()
 
 
+@pytest.mark.parametrize("st,space,tau,model", [
+    (W.D2Q9, W.POPULATION, 1.0, oracle.GUO), (W.D2Q9, W.POPULATION, 0.65, oracle.HE),
+    (W.D2Q9, W.POPULATION, 0.5 + np.sqrt(3 / 16), oracle.GUO), (W.D2Q9, W.RAW, 0.8, oracle.GUO),
+    (W.D2Q9, W.CENTRAL, 1.1, oracle.GUO), (W.D2Q9, W.CUMULANT, 0.875, oracle.HE),
+    (W.D3Q19, W.RAW, 0.875, oracle.GUO), (W.D3Q27, W.POPULATION, 0.65, oracle.GUO),
+    (W.D3Q27, W.CUMULANT, 1.1, oracle.GUO)])
+def test_poiseuille_bounce_back_closed_form(st, space, tau, model):
+    """Half-way bounce-back (reading R18) pinned by a closed form of the LB literature rather
+    than by the paper (which has no walls): for a force-driven channel the steady discrete
+    solution is EXACTLY the parabola with the walls half a node outside plus a uniform slip,
+        u_x(y) = F / (2 nu) [ (y + 1/2)(H - 1/2 - y) + (16 Lambda - 3) / 12 ],
+    with Lambda = (tau_s - 1/2)(tau_odd - 1/2) the product of the even (shear) and odd
+    relaxation times (BGK: tau_odd = tau_s; the R- methods: odd moments at rate 1, tau_odd = 1);
+    bounce-back is exact at Lambda = 3/16 (Ginzburg & d'Humieres 2003).  A reversed or
+    misplaced bounce, a wrong force sign or half-force velocity shift, or a wrong rate slot all
+    change the slip or the curvature."""
+    nx, ny, Fx = 2, 8, 1e-6
+    nz = 1 if W.DIM_OF[st] == 2 else 2
+    nu = (tau - 0.5) / 3
+    rates = [1 / tau] if space == W.POPULATION else W.regularized_rates(st, 1 / tau)
+    lam = (tau - 0.5) * ((tau - 0.5) if space == W.POPULATION else 0.5)
+    bc = [[W.PERIODIC, W.PERIODIC], [W.NOSLIP, W.NOSLIP], [W.PERIODIC, W.PERIODIC]]
+    eq = W.EQ_ABSOLUTE if space == W.CUMULANT else W.EQ_DELTA
+    sim = oracle.Sim(st, space, eq, 1, rates, (nx, ny, nz), bc=bc)
+    sim.set(np.zeros((W.Q_OF[st], nz, ny, nx)))
+    sim.set_force([Fx, 0, 0], force_model=model)
+    sim.step(30000)  # >= 25 diffusion times H^2 / nu: converged to ~1e-11
+    _, u = sim.macroscopic()
+    y = np.arange(ny)
+    ref = Fx / (2 * nu) * ((y + 0.5) * (ny - 0.5 - y) + (16 * lam - 3) / 12)
+    for z in range(nz):
+        for x in range(nx):
+            assert np.abs(u[0, z, :, x] - ref).max() < 1e-9 * ref.max()
+    assert np.abs(u[1:]).max() < 1e-12 * ref.max()
+
+
 def test_shear_wave_between_walls():
     """Bounce-back pin (reading R18): u_x(y) = u0 sin(pi (y+1/2)/ny) between no-slip
     walls decays as exp(-nu (pi/ny)^2 t)."""
