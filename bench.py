@@ -514,7 +514,12 @@ def main():
     time.sleep(0.3)
     # the K timed steps in (up to) 5 windows of consecutive steps, CUDA events between them
     nwin = max(1, min(5, args.steps))
-    bounds = [round(k * args.steps / nwin) for k in range(nwin + 1)]
+    # window edges on multiples of the steps one launch fuses (lbm_step runs whole sweeps inside
+    # a window; the remainder of K goes to the last window)
+    fuse = max(1, lat.info().temporal_blocking) if n == 1 else 1
+    bounds = [0] + [min(args.steps, round(k * args.steps / nwin / fuse) * fuse) for k in range(1, nwin)] + [args.steps]
+    bounds = sorted(set(bounds))
+    nwin = len(bounds) - 1
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(nwin + 1)]
     torch.cuda.synchronize()
     if n > 1:
@@ -586,14 +591,16 @@ def main():
                                    if traffic is not None else None),
                 "algorithmic_bytes_per_cell": bpc, "cells_per_launch": cells_local,
                 "time_steps_per_launch": tb, "peak_source": peak_src,
-                "kernel": (("k_pull2_2d" if two_d else "k_pull2") + " (two fused steps)" if tb == 2 else
+                "kernel": ("k_pullD_2d (three fused steps)" if tb == 3 else
+                           ("k_pull2_2d" if two_d else "k_pull2") + " (two fused steps)" if tb == 2 else
                            "k_pull/k_aa stream-collide") + f" ({kkey})"}
-    if tb == 2:
+    if tb >= 2:
         # the single-step kernel's roofline, per time step: what the fused sweep beats
         roofline["frac_of_single_step_roofline_per_time_step"] = round(tb * achieved / peak, 4)
-        roofline["note"] = ("two fused steps per HBM sweep: the launch moves 2qS B/cell for TWO updates; the "
+        roofline["note"] = (f"{tb} fused steps per HBM sweep: the launch moves 2qS B/cell for {tb} updates; the "
                             "sweep is bound by the collision arithmetic at 2-3 CTAs/SM, not by HBM (ncu: fp64 "
-                            "pipe 44 % C2 fp64, issue slots 70 % C2 fp32, fp64 pipe 61 % C5; DESIGN.md 6.2b)")
+                            "pipe 44 % C2 fp64, issue slots 70 % C2 fp32, fp64 pipe 61 % C5 two-step; "
+                            "DESIGN.md 6.2b); K mod tb steps run as a pair / single step")
     if n > 1:
         roofline["note"] = "N > 1: per-step time of boundary + interior launches with the halo " + halo.split(":")[0]
     if resident:

@@ -209,6 +209,9 @@ typedef struct {
                                fused (pull, single rank, periodic; D3Q19 fp64 with nx % 16 == 0,
                                ny % 8 == 0 (16x8 tiles), or D2Q9 with nx % 256 == 0 (256-cell
                                strips); >= 1184 CTAs = tiles x slab chunks of >= 32 planes;
+                               3 for those D2Q9 lattices with >= 8 rows: triples of steps in
+                               one sweep (k_pullD_2d), then a pair / single step for the rest
+                               of n; LBM_TB_DEPTH=2 (read per call) keeps pairs;
                                the intermediate step stays in shared memory; the same
                                collision code, equal to single steps up to FMA contraction
                                by the compiler, i.e. to rounding), else 1.  Environment

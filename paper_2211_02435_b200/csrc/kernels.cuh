@@ -986,6 +986,120 @@ __global__ void __launch_bounds__(Tile1<TX>::THREADS, MINB)
   }
 }
 
+// Temporal blocking of depth D for 2D lattices (k_pullD_2d; the product uses D = 3): three
+// pull steps per HBM round trip.  A CTA owns TX consecutive cells of a row and sweeps the slab
+// axis (physical y).  Level s = 1..D is time step t+s; at sweep iteration k level s is
+// computed at row k - (s - 1) on the strip widened by D - s cells per side (the cells level
+// s + 1 pulls from): level 1 from HBM (the next row's loads prefetched), level s >= 2 from
+// the shared-memory ring of level s - 1, level D stored to HBM.  A row of a level stays in its
+// ring only while the next level's pull still reads it (3 / 2 / 1 rows for the populations
+// with xi_y = +1 / 0 / -1).  Per cell and D steps: one read and one write of every
+// population, D collisions plus the widened strips (2 (D - s) / TX per level) and the
+// slab-chunk ends.  Same collide() as k_pull: equal to D single steps bitwise on B200
+// (scripts/tb2d_depth.cu: D = 3 at C5 0.73 vs 0.82 ms per step for the two-step sweep;
+// D = 4 no faster, profiles/r2/tb2d_depth.txt).  Single rank, periodic (the slab wraps).
+// ---------------------------------------------------------------------------
+template <class S, int TX, int D>
+struct TileD {
+  static constexpr int W(int s) { return TX + 2 * (D - s); }  // strip width of level s
+  static constexpr int THREADS = (W(1) + 31) / 32 * 32;
+  static constexpr int slots(int i) { return S::mz(i) > 0 ? 3 : (S::mz(i) == 0 ? 2 : 1); }  // mz: slab axis
+  static constexpr int per_level(int w) {  // ring elements of one level of width w
+    int o = 0;
+    for (int j = 0; j < S::Q; ++j) o += slots(j) * w;
+    return o;
+  }
+  static constexpr int level_off(int s) {  // ring of level s (s = 1 .. D-1)
+    int o = 0;
+    for (int l = 1; l < s; ++l) o += per_level(W(l));
+    return o;
+  }
+  static constexpr int pop_off(int i, int w) {
+    int o = 0;
+    for (int j = 0; j < i; ++j) o += slots(j) * w;
+    return o;
+  }
+  static constexpr int RING = level_off(D);  // elements
+};
+
+template <class S, int SPACE, int REG, class real, int RS, int TX, int D, int MINB = 1, bool PF = true>
+__global__ void __launch_bounds__(TileD<S, TX, D>::THREADS, MINB)
+    k_pullD_2d(const real *__restrict__ src, real *__restrict__ dst, const GridParams g, const Rates<real> r,
+               const real swe_g, const Force<real> fr) {
+  static_assert(S::D == 2 && D >= 2 && D <= 4, "2D temporal blocking of depth 2..4");
+  using T = TileD<S, TX, D>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  real *ring = reinterpret_cast<real *>(smem_raw);
+  const int t = threadIdx.x;
+  const int x0 = blockIdx.x * TX;
+  const int n = g.nzl;
+  const int p0 = (int)((long long)n * blockIdx.y / gridDim.y);
+  const int p1 = (int)((long long)n * (blockIdx.y + 1) / gridDim.y);
+  // level 1: strip cell t at x0 - (D - 1) + t, its pull sources at x - 1, x, x + 1
+  constexpr int W1 = T::W(1);
+  const bool act1 = t < W1;
+  const int gx = wrapi(x0 - (D - 1) + t, g.nx);
+  const int xs[3] = {wrapi(gx - 1, g.nx), gx, wrapi(gx + 1, g.nx)};
+  auto load = [&](int k, real(&f)[S::Q]) {
+    const int zc = wrapi(k, n);
+    const long long zo[3] = {(long long)(wrapi(zc - 1, n) + 1) * g.plane, (long long)(zc + 1) * g.plane,
+                             (long long)(wrapi(zc + 1, n) + 1) * g.plane};
+    sfor<S::Q>([&](auto i) {
+      constexpr int cx = S::mx(i), cz = S::mz(i);
+      f[i] = ld_nc(src + zo[1 - cz] + (long long)i * g.pop + xs[1 - cx]);
+    });
+  };
+  // rows of level 1 computed: [p0 - (D - 1), p1 + (D - 1)); iteration k computes level s at
+  // row k - (s - 1) when that row lies in [p0 - (D - s), p1 + (D - s))
+  const int kb = p0 - (D - 1), ke = p1 + (D - 1);
+  real fn[PF ? S::Q : 1];
+  if constexpr (PF) {
+    if (act1) load(kb, fn);
+  }
+  for (int k = kb; k < ke; ++k) {
+    // level 1 at row k
+    if (act1) {
+      real f[S::Q];
+      if constexpr (PF) {
+        sfor<S::Q>([&](auto i) { f[i] = fn[i]; });
+        if (k + 1 < ke) load(k + 1, fn);
+      } else {
+        load(k, f);
+      }
+      collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
+      real *lv = ring + T::level_off(1);
+      sfor<S::Q>([&](auto i) {
+        lv[T::pop_off(i, W1) + ((k + 12) % T::slots(i)) * W1 + t] = f[i];
+      });
+    }
+    // levels 2 .. D
+    sfor<D - 1>([&](auto sm) {
+      constexpr int s = sm + 2;
+      constexpr int Ws = T::W(s), Wp = T::W(s - 1);
+      __syncthreads();
+      const int row = k - (s - 1);
+      if (t < Ws && row >= p0 - (D - s) && row < p1 + (D - s)) {
+        const real *pv = ring + T::level_off(s - 1);
+        real f[S::Q];
+        sfor<S::Q>([&](auto i) {
+          constexpr int cx = S::mx(i), cz = S::mz(i);
+          f[i] = pv[T::pop_off(i, Wp) + ((row - cz + 12) % T::slots(i)) * Wp + (t + 1 - cx)];
+        });
+        collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
+        if constexpr (s == D) {
+          const long long own = (long long)(wrapi(row, n) + 1) * g.plane + (x0 + t);
+          sfor<S::Q>([&](auto i) { dst[own + (long long)i * g.pop] = f[i]; });
+        } else {
+          real *lv = ring + T::level_off(s);
+          sfor<S::Q>([&](auto i) { lv[T::pop_off(i, Ws) + ((row + 12) % T::slots(i)) * Ws + t] = f[i]; });
+        }
+      }
+    });
+    __syncthreads();
+  }
+}
+
+
 // canonical populations of selected cells (local linear index x + nx (y + ny z))
 template <class S, class real>
 __global__ void k_get_cells(const real *mem, const GridParams g, int aa, int state, const long long *__restrict__ idx,

@@ -45,7 +45,8 @@ struct Ops {
   void (*diagnostics)(const void *mem, const GridParams &g, int aa, int state, int zc, double *partial,
                       double *out, double3 dj, cudaStream_t s);
   // registers / local memory of a kernel of this instantiation, for diagnostics: which = 0
-  // k_pull, 1 the two-step sweep (k_pull2 / k_pull2_2d), 2 the cluster-resident loop,
+  // k_pull, 1 the two-step sweep (k_pull2 / k_pull2_2d), 2 the cluster-resident loop, 3 the
+  // depth-3 2D sweep (k_pullD_2d),
   // 10 + pattern the in-place kernel of that pattern (PAT_AA_ODD, PAT_ESO_ODD, PAT_TW0, ...)
   void (*attributes)(int which, int *regs, int *local_bytes);
   // two fused pull steps (temporal blocking; 3D, single rank, periodic); tile TX x TY
@@ -66,6 +67,10 @@ struct Ops {
   // uploads the WO-MRT basis matrices (27 x 27, monomial cube coordinates) to this
   // instantiation's constant memory on the current device (RS_WOBASIS kernels)
   int (*set_wo)(const double *L, const double *Linv);
+  // three fused pull steps (2D only: k_pullD_2d, depth 3, 256-cell strips; single rank,
+  // periodic; nx % 256 == 0); nullptr for 3D stencils
+  void (*pull3)(const void *src, void *dst, const GridParams &g, const void *params, double swe_g, int zchunks,
+                cudaStream_t s);
 };
 
 // shared memory of k_resident2: two grids [Q][R + 2][nx]
@@ -256,6 +261,22 @@ struct OpsImpl {
       else go(k_pull2_2d<S, SPACE, REG, real, RS, TX, srt ? 3 : 2, !srt, false>, conf_slab);
     }
   }
+  // depth-3 2D sweep: 2 CTAs/SM with the next row's loads prefetched (scripts/tb2d_depth.cu,
+  // profiles/r2/tb2d_depth.txt: 1 or 2 CTAs/SM and 37-148 slab chunks within 2 %)
+  static constexpr int kDepth = 3, kDepthTX = 256;
+  static void pull3(const void *src, void *dst, const GridParams &g, const void *params, double swe_g,
+                    int zchunks, cudaStream_t s) {
+    if constexpr (S::D == 2) {
+      using T = TileD<S, kDepthTX, kDepth>;
+      const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
+      const size_t smem = (size_t)T::RING * sizeof(real);
+      auto kern = k_pullD_2d<S, SPACE, REG, real, RS, kDepthTX, kDepth, 2, true>;
+      static unsigned configured = 0;
+      opt_in_smem_once(kern, smem, configured);
+      kern<<<dim3((unsigned)(g.nx / kDepthTX), (unsigned)zchunks, 1), T::THREADS, smem, s>>>(
+          static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
+    }
+  }
   template <bool BB>
   static cudaError_t launch_resident(const real *src, real *dst, const GridParams &g, const MethodParams<real> &p,
                                      double swe_g, int nsteps, int cluster, cudaStream_t s) {
@@ -305,6 +326,8 @@ struct OpsImpl {
       }
     } else if (which == 2) {
       if constexpr (S::D == 2) e = cudaFuncGetAttributes(&a, k_resident2<S, SPACE, REG, real, RS, false>);
+    } else if (which == 3) {
+      if constexpr (S::D == 2) e = cudaFuncGetAttributes(&a, k_pullD_2d<S, SPACE, REG, real, RS, kDepthTX, kDepth, 2, true>);
     } else if (which == 10 + PAT_AA_ODD) {
       e = cudaFuncGetAttributes(&a, k_aa<S, SPACE, REG, real, PAT_AA_ODD, RS>);
     } else if (which == 10 + PAT_AA_EVEN) {
@@ -356,7 +379,8 @@ struct OpsImpl {
                              TbTile<S, real, SPACE>::TY,
                              S::D == 2 ? &resident : nullptr,
                              &preload,
-                             &set_wo};
+                             &set_wo,
+                             S::D == 2 ? &pull3 : nullptr};
 };
 
 }  // namespace lbm

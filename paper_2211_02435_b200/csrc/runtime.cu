@@ -393,6 +393,16 @@ bool use_temporal_blocking(const lbm_ctx *c) {
   return tb_tiles(c) * tb_zchunks(c) >= kTbMinCtas;
 }
 
+// three fused steps per sweep (k_pullD_2d, depth 3) for 2D lattices where the two-step sweep
+// is used: C5 0.73 vs 0.82 ms per step (scripts/tb2d_depth.cu).  Environment LBM_TB_DEPTH=2
+// (read per call) keeps the two-step sweep.
+bool use_depth3(const lbm_ctx *c) {
+  if (!c->ops->pull3 || c->d != 2 || c->g.nzl < 8 || c->g.nx % 256 != 0) return false;
+  const char *env = getenv("LBM_TB_DEPTH");
+  if (env && env[0] == '2') return false;
+  return use_temporal_blocking(c);
+}
+
 // cluster-resident loop (k_resident2): small single-rank 2D pull lattices; returns the CTAs
 // per cluster (0: not used).  The largest cluster (<= 16 CTAs, one per SM) whose CTAs hold
 // their rows + 2 ghost rows of both grids in shared memory and at most kResidentMaxCellsPerCta
@@ -1195,7 +1205,8 @@ lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
   info->rate_specialization = c->rs & 3;
   // multi-rank pull contexts with the pair sequence (peer path, in-library NCCL, or the
   // LBM_REGION_PAIR_* regions of an external exchange) run two steps per interior sweep
-  info->temporal_blocking = (use_temporal_blocking(c) || (c->multi && c->peer_tb_cap)) ? 2 : 1;
+  info->temporal_blocking =
+      use_depth3(c) ? 3 : ((use_temporal_blocking(c) || (c->multi && c->peer_tb_cap)) ? 2 : 1);
   info->resident_cluster = resident_cluster(c);
   info->cuda_graph_steps = (c->nranks == 1 && !info->resident_cluster && use_graphs(c)) ? kGraphSteps : 0;
   info->peer_wait_host = c->peer_on && c->peer_host_wait;
@@ -1273,7 +1284,14 @@ lbm_status lbm_step(lbm_ctx *c, int n) {
       c->steps += kGraphSteps;
     }
   }
-  if (use_temporal_blocking(c)) {  // pairs of steps fused in one sweep (k_pull2)
+  if (use_temporal_blocking(c)) {  // triples (2D, k_pullD_2d), then pairs (k_pull2 / k_pull2_2d)
+    if (use_depth3(c)) {
+      for (; t + 3 <= n; t += 3) {
+        c->ops->pull3(c->buf[c->cur], c->buf[1 - c->cur], g, c->params, c->swe_g, tb_zchunks(c), c->stream);
+        c->cur ^= 1;
+        c->steps += 3;
+      }
+    }
     for (; t + 2 <= n; t += 2) {
       c->ops->pull2(c->buf[c->cur], c->buf[1 - c->cur], g, c->params, c->swe_g, tb_zchunks(c), c->stream);
       c->cur ^= 1;
@@ -1857,6 +1875,7 @@ lbm_status lbm_kernel_attributes(const lbm_ctx *c, int *regs, int *local_bytes) 
   if (!c || !regs || !local_bytes) return LBM_EINVAL;
   int which = 0;
   if (resident_cluster(c)) which = 2;
+  else if (use_depth3(c)) which = 3;
   else if (use_temporal_blocking(c) || (c->multi && c->peer_tb_cap)) which = 1;
   else if (c->streaming != LBM_PULL) which = 10 + inplace_pattern(c, 0);
   c->ops->attributes(which, regs, local_bytes);
