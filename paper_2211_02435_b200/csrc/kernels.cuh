@@ -999,11 +999,12 @@ __global__ void __launch_bounds__(Tile1<TX>::THREADS, MINB)
 // (scripts/tb2d_depth.cu: D = 3 at C5 0.73 vs 0.82 ms per step for the two-step sweep;
 // D = 4 no faster, profiles/r2/tb2d_depth.txt).  Single rank, periodic (the slab wraps).
 // ---------------------------------------------------------------------------
-template <class S, int TX, int D>
+template <class S, int TX, int D, int X = 0>
 struct TileD {
   static constexpr int W(int s) { return TX + 2 * (D - s); }  // strip width of level s
   static constexpr int THREADS = (W(1) + 31) / 32 * 32;
-  static constexpr int slots(int i) { return S::mz(i) > 0 ? 3 : (S::mz(i) == 0 ? 2 : 1); }  // mz: slab axis
+  // rows kept per population (mz: the slab axis); X extra rows for a skewed sweep
+  static constexpr int slots(int i) { return (S::mz(i) > 0 ? 3 : (S::mz(i) == 0 ? 2 : 1)) + X; }
   static constexpr int per_level(int w) {  // ring elements of one level of width w
     int o = 0;
     for (int j = 0; j < S::Q; ++j) o += slots(j) * w;

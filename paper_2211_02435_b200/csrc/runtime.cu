@@ -396,6 +396,15 @@ bool use_temporal_blocking(const lbm_ctx *c) {
 // three fused steps per sweep (k_pullD_2d, depth 3) for 2D lattices where the two-step sweep
 // is used: C5 0.73 vs 0.82 ms per step (scripts/tb2d_depth.cu).  Environment LBM_TB_DEPTH=2
 // (read per call) keeps the two-step sweep.
+// slab chunks of the depth-3 sweep: twice the two-step sweep's (>= 8 waves of CTAs at 2 per SM;
+// C5 0.73 vs 0.74-0.77 ms per step with 74 vs 37 chunks, profiles/r2/tb2d_one_barrier.txt),
+// chunks of >= 32 rows
+int tb3_zchunks(const lbm_ctx *c) {
+  if (getenv("LBM_TB_ZCHUNKS")) return tb_zchunks(c);  // test hook
+  const int maxch = std::max(1, c->g.nzl / kTbMinChunkPlanes);
+  return std::min(2 * tb_zchunks(c), maxch);
+}
+
 bool use_depth3(const lbm_ctx *c) {
   if (!c->ops->pull3 || c->d != 2 || c->g.nzl < 8 || c->g.nx % 256 != 0) return false;
   const char *env = getenv("LBM_TB_DEPTH");
@@ -1287,7 +1296,7 @@ lbm_status lbm_step(lbm_ctx *c, int n) {
   if (use_temporal_blocking(c)) {  // triples (2D, k_pullD_2d), then pairs (k_pull2 / k_pull2_2d)
     if (use_depth3(c)) {
       for (; t + 3 <= n; t += 3) {
-        c->ops->pull3(c->buf[c->cur], c->buf[1 - c->cur], g, c->params, c->swe_g, tb_zchunks(c), c->stream);
+        c->ops->pull3(c->buf[c->cur], c->buf[1 - c->cur], g, c->params, c->swe_g, tb3_zchunks(c), c->stream);
         c->cur ^= 1;
         c->steps += 3;
       }

@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "tb2d_1b.cuh"
 
 
 using namespace lbm;
@@ -162,35 +163,42 @@ void run_depth(Bench &B, int chunks) {
          smem, nb, md);
 }
 
+template <int TX, int D, int MINB, bool PF>
+void run_1b(Bench &B, int chunks) {
+  using T = TileD<S, TX, D, 1>;
+  auto kern = k_pullD1b_2d<S, SP, RG, double, RSM, TX, D, MINB, PF>;
+  const size_t smem = (size_t)T::RING * 8;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  Force<double> fr{};
+  dim3 grid((unsigned)(B.g.nx / TX), (unsigned)chunks);
+  B.reset();
+  B.reference(D);
+  kern<<<grid, T::THREADS, smem>>>(B.a, B.b, B.g, B.r, B.gg, fr);
+  CK(cudaDeviceSynchronize());
+  const double md = B.diff();
+  int nb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T::THREADS, smem));
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  float ms = time_k([&](int p) { kern<<<grid, T::THREADS, smem>>>(p ? B.b : B.a, p ? B.a : B.b, B.g, B.r, B.gg, fr); });
+  printf("C5 1-barrier depth %d TX %3d minb %d pf %d ch %3d  %7.4f ms/step %8.0f MLUPS  regs %3d  lmem %3zu  smem %6zu  %d CTA/SM  maxdiff %.3e\n",
+         D, TX, MINB, (int)PF, chunks, ms / D, (double)D * B.cells / (ms * 1e-3) / 1e6, fa.numRegs, fa.localSizeBytes,
+         smem, nb, md);
+}
+
 int main(int argc, char **argv) {
   const int n = argc > 1 ? atoi(argv[1]) : 8192;
   Bench B(n, n);
   run_product(B, 37);
-  run_depth<256, 3, 1, true>(B, 37);
-  run_depth<256, 3, 1, true>(B, 74);
-  run_depth<256, 3, 1, true>(B, 148);
   run_depth<256, 3, 2, true>(B, 37);
   run_depth<256, 3, 2, true>(B, 74);
-  run_depth<256, 3, 2, true>(B, 148);
-  run_depth<256, 4, 1, true>(B, 37);
-  run_depth<256, 4, 1, true>(B, 74);
-  run_depth<256, 4, 1, true>(B, 148);
-  run_depth<256, 4, 2, true>(B, 37);
-  run_depth<256, 4, 2, true>(B, 74);
-  run_depth<256, 4, 2, true>(B, 148);
-  run_depth<128, 3, 2, true>(B, 37);
-  run_depth<128, 3, 2, true>(B, 74);
-  run_depth<128, 3, 2, true>(B, 148);
-  run_depth<128, 3, 3, true>(B, 37);
-  run_depth<128, 3, 3, true>(B, 74);
-  run_depth<128, 3, 3, true>(B, 148);
-  run_depth<128, 4, 2, true>(B, 37);
-  run_depth<128, 4, 2, true>(B, 74);
-  run_depth<128, 4, 2, true>(B, 148);
-  run_depth<128, 4, 3, true>(B, 37);
-  run_depth<128, 4, 3, true>(B, 74);
-  run_depth<128, 4, 3, true>(B, 148);
-  run_depth<256, 3, 1, false>(B, 74);
-  run_depth<128, 3, 3, false>(B, 74);
+  run_1b<256, 3, 2, true>(B, 37);
+  run_1b<256, 3, 2, true>(B, 74);
+  run_1b<256, 3, 1, true>(B, 74);
+  run_1b<256, 4, 1, true>(B, 37);
+  run_1b<256, 4, 1, true>(B, 74);
+  run_1b<128, 3, 3, true>(B, 74);
+  run_1b<128, 4, 2, true>(B, 74);
+  run_1b<256, 2, 2, true>(B, 37);
   return 0;
 }
