@@ -365,8 +365,12 @@ int tb_zchunks(const lbm_ctx *c) {
     const int k = atoi(e);
     return k < 1 ? 1 : (k > n ? n : k);
   }
+  // twice the chunks the 4-wave minimum needs (>= 8 waves where the slab allows chunks of >= 32
+  // planes): the tail of the last wave shrinks; C2 256^3 6 vs 3 chunks: fp32 52.6k vs 51.0k,
+  // fp64 30.4k vs 29.9k MLUPS (profiles/r2/tb_zchunks.txt); C5 depth 3 74 vs 37 chunks: 0.73 vs
+  // 0.74-0.77 ms per step (profiles/r2/tb2d_one_barrier.txt)
   const long long tiles = tb_tiles(c);
-  const long long need = (kTbMinCtas + tiles - 1) / tiles;
+  const long long need = 2 * ((kTbMinCtas + tiles - 1) / tiles);
   const int maxch = n / kTbMinChunkPlanes > 1 ? n / kTbMinChunkPlanes : 1;
   return (int)(need < maxch ? need : maxch);
 }
@@ -396,14 +400,8 @@ bool use_temporal_blocking(const lbm_ctx *c) {
 // three fused steps per sweep (k_pullD_2d, depth 3) for 2D lattices where the two-step sweep
 // is used: C5 0.73 vs 0.82 ms per step (scripts/tb2d_depth.cu).  Environment LBM_TB_DEPTH=2
 // (read per call) keeps the two-step sweep.
-// slab chunks of the depth-3 sweep: twice the two-step sweep's (>= 8 waves of CTAs at 2 per SM;
-// C5 0.73 vs 0.74-0.77 ms per step with 74 vs 37 chunks, profiles/r2/tb2d_one_barrier.txt),
-// chunks of >= 32 rows
-int tb3_zchunks(const lbm_ctx *c) {
-  if (getenv("LBM_TB_ZCHUNKS")) return tb_zchunks(c);  // test hook
-  const int maxch = std::max(1, c->g.nzl / kTbMinChunkPlanes);
-  return std::min(2 * tb_zchunks(c), maxch);
-}
+// slab chunks of the depth-3 sweep: those of the two-step sweep
+int tb3_zchunks(const lbm_ctx *c) { return tb_zchunks(c); }
 
 bool use_depth3(const lbm_ctx *c) {
   if (!c->ops->pull3 || c->d != 2 || c->g.nzl < 8 || c->g.nx % 256 != 0) return false;
