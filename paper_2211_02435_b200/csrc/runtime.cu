@@ -397,12 +397,12 @@ bool use_temporal_blocking(const lbm_ctx *c) {
   return tb_tiles(c) * tb_zchunks(c) >= kTbMinCtas;
 }
 
-// three fused steps per sweep (k_pullD_2d, depth 3) for 2D lattices where the two-step sweep
-// is used: C5 0.73 vs 0.82 ms per step (scripts/tb2d_depth.cu).  Environment LBM_TB_DEPTH=2
-// (read per call) keeps the two-step sweep.
 // slab chunks of the depth-3 sweep: those of the two-step sweep
 int tb3_zchunks(const lbm_ctx *c) { return tb_zchunks(c); }
 
+// three fused steps per sweep (k_pullD_2d, depth 3) for 2D lattices where the two-step sweep
+// is used: C5 0.73 vs 0.82 ms per step (scripts/tb2d_depth.cu).  Environment LBM_TB_DEPTH=2
+// (read per call) keeps the two-step sweep.
 bool use_depth3(const lbm_ctx *c) {
   if (!c->ops->pull3 || c->d != 2 || c->g.nzl < 8 || c->g.nx % 256 != 0) return false;
   const char *env = getenv("LBM_TB_DEPTH");
