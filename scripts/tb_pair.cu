@@ -145,32 +145,50 @@ void run_pair(Bench<real> &B, const char *tag) {
          2.0 * B.cells / (ms * 1e-3) / 1e6, fa.numRegs, fa.localSizeBytes, smem, nb, md);
 }
 
+// the product kernel k_pull2 at other tiles / occupancies (maxdiff against the 16x8 product output)
+template <class real, int TX, int TY, int MINB, bool PF, bool TRIM>
+void run_k2(Bench<real> &B, const char *tag) {
+  using S = D3Q19;
+  using T = Tile2<TX, TY>;
+  auto kern = k_pull2<S, SPACE_RAW, REG_DELTA, real, RS_GENERAL, TX, TY, MINB, PF, false, TRIM>;
+  const size_t smem = TRIM ? (size_t)Tile2Trim<TX, TY, S>::RING * sizeof(real) : (size_t)3 * S::Q * T::HW * sizeof(real);
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  Force<real> fr{};
+  dim3 grid((unsigned)(B.g.nx / TX), (unsigned)(B.g.ny / TY), (unsigned)B.zch);
+  B.reset();
+  kern<<<grid, T::THREADS, smem>>>(B.a, B.b, B.g, B.r, real(0), fr);
+  CK(cudaDeviceSynchronize());
+  const double md = B.diff();
+  int nb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T::THREADS, smem));
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  float ms = time_k([&](int p) { kern<<<grid, T::THREADS, smem>>>(p ? B.b : B.a, p ? B.a : B.b, B.g, B.r, real(0), fr); });
+  printf("%-40s %7.3f ms/2 steps %8.0f MLUPS  regs %3d  lmem %3zu  smem %6zu  %d CTA/SM  maxdiff %.3e\n", tag, ms,
+         2.0 * B.cells / (ms * 1e-3) / 1e6, fa.numRegs, fa.localSizeBytes, smem, nb, md);
+}
+
 int main(int argc, char **argv) {
   const int which = argc > 1 ? atoi(argv[1]) : 0;  // 0 both, 1 fp32, 2 fp64
-  const int zch = argc > 2 ? atoi(argv[2]) : 3;
+  const int zch = argc > 2 ? atoi(argv[2]) : 6;
   if (which != 2) {
     Bench<float> B(256, 256, 256, zch);
     run_ref<float, 3, false>(B, "C2 f32 k_pull2 16x8 PF (product)");
-    run_pair<float, 32, 8, 2, true>(B, "C2 f32 pair 32x8 minb 2 pf");
-    run_pair<float, 32, 8, 2, false>(B, "C2 f32 pair 32x8 minb 2");
-    run_pair<float, 32, 8, 1, true>(B, "C2 f32 pair 32x8 minb 1 pf");
-    run_pair<float, 16, 8, 4, true>(B, "C2 f32 pair 16x8 minb 4 pf");
-    run_pair<float, 16, 8, 3, true>(B, "C2 f32 pair 16x8 minb 3 pf");
-    run_pair<float, 16, 8, 4, false>(B, "C2 f32 pair 16x8 minb 4");
-    run_pair<float, 32, 4, 3, true>(B, "C2 f32 pair 32x4 minb 3 pf");
-    run_pair<float, 16, 16, 2, true>(B, "C2 f32 pair 16x16 minb 2 pf");
-    run_pair<float, 32, 16, 1, true>(B, "C2 f32 pair 32x16 minb 1 pf");
+    run_k2<float, 16, 8, 3, true, false>(B, "C2 f32 k2 16x8 minb 3 pf");
+    run_k2<float, 16, 16, 2, true, false>(B, "C2 f32 k2 16x16 minb 2 pf");
+    run_k2<float, 16, 16, 2, true, true>(B, "C2 f32 k2 16x16 minb 2 pf trim");
+    run_k2<float, 32, 8, 2, true, false>(B, "C2 f32 k2 32x8 minb 2 pf");
+    run_k2<float, 32, 8, 2, true, true>(B, "C2 f32 k2 32x8 minb 2 pf trim");
+    run_k2<float, 8, 8, 4, true, false>(B, "C2 f32 k2 8x8 minb 4 pf");
+    run_k2<float, 16, 4, 4, true, false>(B, "C2 f32 k2 16x4 minb 4 pf");
   }
   if (which != 1) {
     Bench<double> B(256, 256, 256, zch);
     run_ref<double, 2, true>(B, "C2 f64 k_pull2 16x8 PF trim (product)");
-    run_pair<double, 32, 8, 1, true>(B, "C2 f64 pair 32x8 minb 1 pf");
-    run_pair<double, 32, 8, 1, false>(B, "C2 f64 pair 32x8 minb 1");
-    run_pair<double, 16, 8, 2, true>(B, "C2 f64 pair 16x8 minb 2 pf");
-    run_pair<double, 16, 8, 2, false>(B, "C2 f64 pair 16x8 minb 2");
-    run_pair<double, 16, 8, 3, false>(B, "C2 f64 pair 16x8 minb 3");
-    run_pair<double, 32, 4, 2, true>(B, "C2 f64 pair 32x4 minb 2 pf");
-    run_pair<double, 16, 16, 1, true>(B, "C2 f64 pair 16x16 minb 1 pf");
+    run_k2<double, 16, 8, 2, true, true>(B, "C2 f64 k2 16x8 minb 2 pf trim");
+    run_k2<double, 16, 16, 1, true, true>(B, "C2 f64 k2 16x16 minb 1 pf trim");
+    run_k2<double, 8, 8, 3, true, true>(B, "C2 f64 k2 8x8 minb 3 pf trim");
+    run_k2<double, 16, 4, 3, true, true>(B, "C2 f64 k2 16x4 minb 3 pf trim");
   }
   return 0;
 }
