@@ -401,6 +401,10 @@ lbm_status lbm_get_diagnostics(lbm_ctx *ctx, lbm_diagnostics *out);
 lbm_status lbm_get_cells(lbm_ctx *ctx, const long long *cells, long long n, double *f);
 /* Sets the canonical state (converted to the storage precision); resets the step counter. */
 lbm_status lbm_set_populations(lbm_ctx *ctx, const double *f);
+/* Sets lbm_info.steps_done (e.g. to the saved count after a checkpoint restart through
+   lbm_set_populations).  Informational only: the canonical state does not depend on it (the
+   storage parity of the in-place patterns is tracked separately).  LBM_EINVAL if steps < 0. */
+lbm_status lbm_set_steps(lbm_ctx *ctx, long long steps);
 /* LBM_ENUMERIC if any stored population of the current state is not finite. */
 lbm_status lbm_check_finite(lbm_ctx *ctx);
 

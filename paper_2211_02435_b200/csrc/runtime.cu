@@ -1824,6 +1824,13 @@ lbm_status lbm_get_cells(lbm_ctx *c, const long long *cells, long long n, double
   return LBM_OK;
 }
 
+lbm_status lbm_set_steps(lbm_ctx *c, long long steps) {
+  if (!c) return LBM_EINVAL;
+  if (steps < 0) return fail(c, LBM_EINVAL, "negative step count");
+  c->steps = steps;
+  return LBM_OK;
+}
+
 lbm_status lbm_set_populations(lbm_ctx *c, const double *f) {
   NvtxRange nvtx_("lbm_set_populations");
   if (!c || !f) return fail(c, LBM_EINVAL, "null argument");

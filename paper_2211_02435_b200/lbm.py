@@ -111,6 +111,7 @@ SIGNATURES = [
     ("lbm_get_macroscopic", ctypes.c_int, [_vp, _dp, _dp]),
     ("lbm_get_populations", ctypes.c_int, [_vp, _dp]),
     ("lbm_set_populations", ctypes.c_int, [_vp, _dp]),
+    ("lbm_set_steps", ctypes.c_int, [_vp, ctypes.c_longlong]),
     ("lbm_get_cells", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_longlong), ctypes.c_longlong, _dp]),
     ("lbm_get_diagnostics", ctypes.c_int, [_vp, ctypes.POINTER(lbm_diagnostics)]),
     ("lbm_set_force", ctypes.c_int, [_vp, _dp]),
@@ -396,8 +397,8 @@ class Lattice:
 
     def load(self, path, rates=None):
         """Restore a checkpoint written by save() for the same method, precision and slab.
-        Returns the saved step count; the context's own counter (lbm_info.steps_done) restarts at
-        zero like after any lbm_set_populations, the canonical state is independent of it.  On
+        Returns the saved step count and restores the context's counter (lbm_info.steps_done,
+        lbm_set_steps) to it; the canonical state is independent of the counter.  On
         several ranks the next lbm_step exchanges the halo first (an external-exchange driver,
         SlabRunner, must call prime())."""
         d = np.load(path)
@@ -412,6 +413,7 @@ class Lattice:
                 d["rates"], np.asarray(rates, dtype=np.float64).reshape(-1)):
             raise ValueError("checkpoint relaxation rates differ")
         self.set_populations(d["f"])
+        _check(lib().lbm_set_steps(self._ctx, int(d["steps"])), self._ctx)
         return int(d["steps"])
 
     def test_collide(self, f_in):

@@ -35,7 +35,9 @@ def test_checkpoint_restart_across_patterns(tmp_path):
     for streaming in (L.LBM_PULL, L.LBM_AA, L.LBM_ESOTERIC_PULL, L.LBM_ESOTERIC_TWIST):
         with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, streaming=streaming) as lat:
             assert lat.load(ck) == 11
+            assert lat.info().steps_done == 11  # lbm_set_steps restores the counter
             lat.step(6)
+            assert lat.info().steps_done == 17
             np.testing.assert_array_equal(lat.get_populations(), ref)
     with L.Lattice(st, W.CENTRAL, eq, rates, shape, zero_centered=zc) as lat:
         with pytest.raises(ValueError):
