@@ -525,3 +525,60 @@ def test_peer_device_waits_across_gpus(tb, monkeypatch):
         np.testing.assert_array_equal(multi, single)
     else:
         assert gate_error(st, multi, single, zc) < 1e-13
+
+
+def _random_slab_config(k):
+    rng = np.random.default_rng(7000 + k)
+    st = [W.D2Q9, W.D3Q19, W.D3Q27][rng.integers(3)]
+    space = [W.POPULATION, W.RAW, W.CENTRAL, W.CUMULANT][rng.integers(4)]
+    regimes = [(W.EQ_ABSOLUTE, 0), (W.EQ_ABSOLUTE, 1)] + ([] if space == W.CUMULANT else [(W.EQ_DELTA, 1)])
+    eq, zc = regimes[rng.integers(len(regimes))]
+    streaming = [L.LBM_PULL, L.LBM_AA][rng.integers(2)]
+    transport = ["peer", "exchange"][rng.integers(2)]
+    nranks = int(rng.integers(2, 5))
+    per = max(int(rng.integers(1, 9)), -(-4 // nranks))  # planes per slab (even split; extents >= 4)
+    d = W.DIM_OF[st]
+    shape = ((int(rng.integers(9, 40)), nranks * per, 1) if d == 2 else
+             (int(rng.integers(9, 30)), int(rng.integers(5, 14)), nranks * per))
+    pairs = streaming == L.LBM_PULL and rng.random() < 0.5
+    steps = int(rng.integers(3, 10))
+    return st, space, eq, zc, streaming, transport, nranks, shape, pairs, steps
+
+
+@pytest.mark.parametrize("k", range(40))
+def test_random_multi_rank_sweep(k, monkeypatch):
+    """Seeded random multi-rank draws (stencil, collision space, regime, pull / AA, fused peer
+    push or the exchange building blocks, 2-4 ranks, slabs of 1-8 planes, two-step
+    sweeps across ranks or single steps) against the single-rank run: bitwise with single
+    steps, to rounding with pairs of steps."""
+    st, space, eq, zc, streaming, transport, nranks, shape, pairs, steps = _random_slab_config(k)
+    monkeypatch.setenv("LBM_PEER_TB", "1" if pairs else "0")
+    rates = np.array([1.37]) if space == W.POPULATION else W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape, seed=W.SEED + 11 * k)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, streaming=streaming) as lat:
+        lat.set_populations(f0)
+        lat.step(steps)
+        single = lat.get_populations()
+    slab_axis = 2 if W.DIM_OF[st] == 2 else 1
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, rank=r, nranks=nranks, streaming=streaming)
+            for r in range(nranks)]
+    for lat in lats:
+        sl = [slice(None)] * 4
+        sl[slab_axis] = slice(lat.offset, lat.offset + lat.extent)
+        lat.set_populations(np.ascontiguousarray(f0[tuple(sl)]))
+    used_pairs = pairs and all(D.supports_pairs(l) for l in lats)
+    if transport == "peer":
+        D.connect_local(lats)
+        D.step_peer_local(lats, steps, chunk=2 if pairs else 1)
+        used_pairs = used_pairs and all(l.info().temporal_blocking == 2 for l in lats)
+    else:
+        D.prime_local(lats)
+        D.step_local(lats, steps, pairs=pairs)
+    multi = np.concatenate([lat.get_populations() for lat in lats], axis=slab_axis)
+    for lat in lats:
+        lat.close()
+    what = (st, space, eq, zc, streaming, transport, nranks, shape, pairs, steps)
+    if used_pairs:
+        assert gate_error(st, multi, single, zc) < 1e-13, what
+    else:
+        np.testing.assert_array_equal(multi, single, err_msg=str(what))
