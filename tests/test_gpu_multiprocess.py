@@ -31,7 +31,7 @@ def free_port():
 @pytest.mark.parametrize("halo", ["exchange", "peer"])
 def test_torchrun_slabs_bitwise(nproc, halo):
     """halo=peer: the fused halo push across processes (CUDA IPC mappings of the
-    neighbours' grids and flags; processes sharing one GPU are time-sliced)."""
+    neighbours' grids and flags; processes sharing one GPU order the phases on the host, no kernel spins)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
            os.path.join(ROOT, "scripts", "slab_check.py"), "--steps", "9", "--halo", halo]
