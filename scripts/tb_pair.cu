@@ -174,21 +174,16 @@ int main(int argc, char **argv) {
   if (which != 2) {
     Bench<float> B(256, 256, 256, zch);
     run_ref<float, 3, false>(B, "C2 f32 k_pull2 16x8 PF (product)");
-    run_k2<float, 16, 8, 3, true, false>(B, "C2 f32 k2 16x8 minb 3 pf");
-    run_k2<float, 16, 16, 2, true, false>(B, "C2 f32 k2 16x16 minb 2 pf");
-    run_k2<float, 16, 16, 2, true, true>(B, "C2 f32 k2 16x16 minb 2 pf trim");
-    run_k2<float, 32, 8, 2, true, false>(B, "C2 f32 k2 32x8 minb 2 pf");
-    run_k2<float, 32, 8, 2, true, true>(B, "C2 f32 k2 32x8 minb 2 pf trim");
-    run_k2<float, 8, 8, 4, true, false>(B, "C2 f32 k2 8x8 minb 4 pf");
-    run_k2<float, 16, 4, 4, true, false>(B, "C2 f32 k2 16x4 minb 4 pf");
+    run_k2<float, 32, 16, 1, true, false>(B, "C2 f32 k2 32x16 minb 1 pf");
+    run_k2<float, 32, 16, 1, true, true>(B, "C2 f32 k2 32x16 minb 1 pf trim");
+    run_k2<float, 32, 16, 1, false, true>(B, "C2 f32 k2 32x16 minb 1 trim");
+    run_k2<float, 16, 32, 1, true, true>(B, "C2 f32 k2 16x32 minb 1 pf trim");
+    run_k2<float, 32, 12, 1, true, true>(B, "C2 f32 k2 32x12 minb 1 pf trim");
   }
   if (which != 1) {
     Bench<double> B(256, 256, 256, zch);
     run_ref<double, 2, true>(B, "C2 f64 k_pull2 16x8 PF trim (product)");
-    run_k2<double, 16, 8, 2, true, true>(B, "C2 f64 k2 16x8 minb 2 pf trim");
-    run_k2<double, 16, 16, 1, true, true>(B, "C2 f64 k2 16x16 minb 1 pf trim");
-    run_k2<double, 8, 8, 3, true, true>(B, "C2 f64 k2 8x8 minb 3 pf trim");
-    run_k2<double, 16, 4, 3, true, true>(B, "C2 f64 k2 16x4 minb 3 pf trim");
+    run_k2<double, 32, 16, 1, false, true>(B, "C2 f64 k2 32x16 minb 1 trim");
   }
   return 0;
 }
