@@ -83,3 +83,21 @@ def test_our_arm_json_line():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900)
+def test_our_arm_three_step_sweep_line():
+    """C5 (three steps per HBM sweep): the roofline object counts three time steps per launch,
+    the window edges and the launch count follow them."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "c5", "--steps", "12",
+                        "--warmup", "3", "--no-cpu", "--no-e2e"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _json_lines(r.stdout)[0]
+    rf = d["roofline"]
+    assert rf["time_steps_per_launch"] == 3 and rf["kernel"].startswith("k_pullD_2d")
+    assert abs(rf["frac_of_single_step_roofline_per_time_step"] - 3 * rf["frac"]) < 1e-3
+    assert d["gpu_launches"] == 4 and d["value"] > 1000
