@@ -4,6 +4,8 @@ connected by LocalTransport, must reproduce the single-rank run BITWISE
 the oracle at full parity."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -536,7 +538,7 @@ def _random_slab_config(k):
     streaming = [L.LBM_PULL, L.LBM_AA][rng.integers(2)]
     transport = ["peer", "exchange"][rng.integers(2)]
     nranks = int(rng.integers(2, 5))
-    per = max(int(rng.integers(1, 9)), -(-4 // nranks))  # planes per slab (even split; extents >= 4)
+    per = max(int(rng.integers(2, 9)), -(-4 // nranks))  # planes per slab (even split, >= 2; extents >= 4)
     d = W.DIM_OF[st]
     shape = ((int(rng.integers(9, 40)), nranks * per, 1) if d == 2 else
              (int(rng.integers(9, 30)), int(rng.integers(5, 14)), nranks * per))
@@ -545,10 +547,10 @@ def _random_slab_config(k):
     return st, space, eq, zc, streaming, transport, nranks, shape, pairs, steps
 
 
-@pytest.mark.parametrize("k", range(40))
+@pytest.mark.parametrize("k", range(int(os.environ.get("LBM_TEST_DRAWS_MULTI", "40"))))
 def test_random_multi_rank_sweep(k, monkeypatch):
     """Seeded random multi-rank draws (stencil, collision space, regime, pull / AA, fused peer
-    push or the exchange building blocks, 2-4 ranks, slabs of 1-8 planes, two-step
+    push or the exchange building blocks, 2-4 ranks, slabs of 2-8 planes, two-step
     sweeps across ranks or single steps) against the single-rank run: bitwise with single
     steps, to rounding with pairs of steps."""
     st, space, eq, zc, streaming, transport, nranks, shape, pairs, steps = _random_slab_config(k)
