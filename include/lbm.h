@@ -351,7 +351,10 @@ lbm_status lbm_peer_prime(lbm_ctx *ctx);
    planes per slab, no walls) advance pairs of steps: interior planes by the fused sweep, the
    boundary regions by two single steps through 8 scratch planes behind grid 0 with pushes into
    the neighbours' scratch and ghost planes; every rank must call with the same n.
-   LBM_PEER_TB=0 (read at create) keeps single steps.  Device-side waits: several contexts
+   LBM_PEER_TB=0 (read at create) keeps single steps.  2D slabs of >= 10 rows (nx % 256 == 0)
+   advance TRIPLES instead (lbm_info.temporal_blocking == 3: the interior by the depth-3 sweep,
+   the boundary regions by three single steps through 22 more scratch planes, three flag phases
+   per triple; LBM_TB_DEPTH=2 keeps pairs); captured graphs then hold 36 steps.  Device-side waits: several contexts
    driven from ONE host thread must be stepped in small interleaved chunks (a context's stream
    waits on the GPU for its neighbours, and enqueuing many of its steps first can fill the
    launch queue before the neighbours' work is enqueued).  Host-ordered waits (neighbours on

@@ -997,7 +997,8 @@ __global__ void __launch_bounds__(Tile1<TX>::THREADS, MINB)
 // population, D collisions plus the widened strips (2 (D - s) / TX per level) and the
 // slab-chunk ends.  Same collide() as k_pull: equal to D single steps bitwise on B200
 // (scripts/tb2d_depth.cu: D = 3 at C5 0.73 vs 0.82 ms per step for the two-step sweep;
-// D = 4 no faster, profiles/r2/tb2d_depth.txt).  Single rank, periodic (the slab wraps).
+// D = 4 no faster, profiles/r2/tb2d_depth.txt).  Single rank, periodic (the slab wraps), or a
+// row range of a rank's slab (RANGE; the interior of three steps across ranks, runtime.cu).
 // ---------------------------------------------------------------------------
 template <class S, int TX, int D, int X = 0>
 struct TileD {
@@ -1023,7 +1024,10 @@ struct TileD {
   static constexpr int RING = level_off(D);  // elements
 };
 
-template <class S, int SPACE, int REG, class real, int RS, int TX, int D, int MINB = 1, bool PF = true>
+// RANGE (across ranks): output rows [zbegin, zbegin + zcount) of a slab, every row the levels
+// pull from inside [0, nzl) (zbegin >= D, zbegin + zcount <= nzl - D): no wrap, no ghost rows.
+template <class S, int SPACE, int REG, class real, int RS, int TX, int D, int MINB = 1, bool PF = true,
+          bool RANGE = false>
 __global__ void __launch_bounds__(TileD<S, TX, D>::THREADS, MINB)
     k_pullD_2d(const real *__restrict__ src, real *__restrict__ dst, const GridParams g, const Rates<real> r,
                const real swe_g, const Force<real> fr) {
@@ -1034,17 +1038,22 @@ __global__ void __launch_bounds__(TileD<S, TX, D>::THREADS, MINB)
   const int t = threadIdx.x;
   const int x0 = blockIdx.x * TX;
   const int n = g.nzl;
-  const int p0 = (int)((long long)n * blockIdx.y / gridDim.y);
-  const int p1 = (int)((long long)n * (blockIdx.y + 1) / gridDim.y);
+  const int zb = RANGE ? g.zbegin : 0, zn = RANGE ? g.zcount : n;
+  const int p0 = zb + (int)((long long)zn * blockIdx.y / gridDim.y);
+  const int p1 = zb + (int)((long long)zn * (blockIdx.y + 1) / gridDim.y);
+  auto zw = [&](int k) {
+    if constexpr (RANGE) return k;
+    else return wrapi(k, n);
+  };
   // level 1: strip cell t at x0 - (D - 1) + t, its pull sources at x - 1, x, x + 1
   constexpr int W1 = T::W(1);
   const bool act1 = t < W1;
   const int gx = wrapi(x0 - (D - 1) + t, g.nx);
   const int xs[3] = {wrapi(gx - 1, g.nx), gx, wrapi(gx + 1, g.nx)};
   auto load = [&](int k, real(&f)[S::Q]) {
-    const int zc = wrapi(k, n);
-    const long long zo[3] = {(long long)(wrapi(zc - 1, n) + 1) * g.plane, (long long)(zc + 1) * g.plane,
-                             (long long)(wrapi(zc + 1, n) + 1) * g.plane};
+    const int zc = zw(k);
+    const long long zo[3] = {(long long)(zw(zc - 1) + 1) * g.plane, (long long)(zc + 1) * g.plane,
+                             (long long)(zw(zc + 1) + 1) * g.plane};
     sfor<S::Q>([&](auto i) {
       constexpr int cx = S::mx(i), cz = S::mz(i);
       f[i] = ld_nc(src + zo[1 - cz] + (long long)i * g.pop + xs[1 - cx]);
@@ -1088,7 +1097,7 @@ __global__ void __launch_bounds__(TileD<S, TX, D>::THREADS, MINB)
         });
         collide<S, SPACE, REG, real, RS>(f, r, swe_g, fr);
         if constexpr (s == D) {
-          const long long own = (long long)(wrapi(row, n) + 1) * g.plane + (x0 + t);
+          const long long own = (long long)(zw(row) + 1) * g.plane + (x0 + t);
           sfor<S::Q>([&](auto i) { dst[own + (long long)i * g.pop] = f[i]; });
         } else {
           real *lv = ring + T::level_off(s);

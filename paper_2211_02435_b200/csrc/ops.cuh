@@ -270,11 +270,15 @@ struct OpsImpl {
       using T = TileD<S, kDepthTX, kDepth>;
       const MethodParams<real> &p = *static_cast<const MethodParams<real> *>(params);
       const size_t smem = (size_t)T::RING * sizeof(real);
-      auto kern = k_pullD_2d<S, SPACE, REG, real, RS, kDepthTX, kDepth, 2, true>;
-      static unsigned configured = 0;
-      opt_in_smem_once(kern, smem, configured);
-      kern<<<dim3((unsigned)(g.nx / kDepthTX), (unsigned)zchunks, 1), T::THREADS, smem, s>>>(
-          static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
+      // whole slab with periodic wrap (single rank) or a row range without wrap (across ranks)
+      auto go = [&](auto kern, unsigned &configured) {
+        opt_in_smem_once(kern, smem, configured);
+        kern<<<dim3((unsigned)(g.nx / kDepthTX), (unsigned)zchunks, 1), T::THREADS, smem, s>>>(
+            static_cast<const real *>(src), static_cast<real *>(dst), g, p.rates, (real)swe_g, p.force);
+      };
+      static unsigned conf_slab = 0, conf_range = 0;
+      if (g.zcount) go(k_pullD_2d<S, SPACE, REG, real, RS, kDepthTX, kDepth, 2, true, true>, conf_range);
+      else go(k_pullD_2d<S, SPACE, REG, real, RS, kDepthTX, kDepth, 2, true, false>, conf_slab);
     }
   }
   template <bool BB>
@@ -363,6 +367,7 @@ struct OpsImpl {
     } else if constexpr (S::D == 2) {
       constexpr bool srt = SPACE == SPACE_POPULATION;
       cudaFuncGetAttributes(&a, k_pull2_2d<S, SPACE, REG, real, RS, TT::TX, srt ? 3 : 2, !srt, true>);
+      cudaFuncGetAttributes(&a, k_pullD_2d<S, SPACE, REG, real, RS, kDepthTX, kDepth, 2, true, true>);
     }
     cudaGetLastError();
   }

@@ -245,6 +245,7 @@ struct lbm_ctx {
   long long peer_pid[6] = {};
   int n_mapped = 0;
   cudaGraphExec_t peer_graph[2] = {nullptr, nullptr};  // captured lbm_step_peer loops per grid parity
+  int peer_graph_steps = 0;                            // steps per captured loop (32 or 36)
   bool peer_on = false;
   // host-ordered waits (a neighbour shares this GPU): no kernel spins on a flag another rank
   // writes; the host polls the flags and enqueues the dependent work only once they are set
@@ -380,6 +381,16 @@ int tb_zchunks(const lbm_ctx *c) {
 bool use_peer_tb(const lbm_ctx *c) {
   return c->peer_tb_cap && (c->peer_on || c->comm) && c->streaming == LBM_PULL;
 }
+// three fused steps per triple across ranks (2D, fused peer push): the interior rows [3, nzl - 3)
+// by the depth-3 sweep, the boundary regions by three single steps through the scratch
+// planes 8..29 (enqueue_peer_steps); >= 10 rows per slab; LBM_TB_DEPTH=2 keeps pairs
+bool use_peer_tb3(const lbm_ctx *c) {
+  if (!use_peer_tb(c) || !c->peer_on || c->d != 2 || !c->ops->pull3 || c->g.nzl < 10 || c->g.nx % 256 != 0)
+    return false;
+  const char *env = getenv("LBM_TB_DEPTH");
+  return !(env && env[0] == '2');
+}
+
 int peer_tb_chunks(const lbm_ctx *c) {
   const long long tiles = tb_tiles(c);
   const long long need = (kTbMinCtas + tiles - 1) / tiles;
@@ -613,6 +624,65 @@ int enqueue_peer_steps(lbm_ctx *c, int n, int cur) {
   cudaEventRecord(c->ev_b, c->stream);
   cudaEventRecord(c->ev_i, c->stream);
   int t = 0;
+  if (use_peer_tb3(c)) {
+    // Triples t -> t+3 (2D): on s_int the depth-3 sweep of the interior rows [3, nzl - 3) (its
+    // widened levels reach rows 1 .. nzl - 2 of A, no ghost data); on the context stream three
+    // phases, each wait / two boundary launches / signal: step t+1 of rows {0..4} and
+    // {nzl-5..nzl-1} from A into the level-1 scratch (rows -1..4 at scratch planes 8..13,
+    // nzl-5..nzl at 14..19), step t+2 of rows {0..3} and {nzl-4..nzl-1} from it into the
+    // level-2 scratch (rows -1..3 at 20..24, nzl-4..nzl at 25..29), step t+3 of rows {0,1,2} and
+    // {nzl-3..nzl-1} from it into B.  Rows 0 and nzl-1 push their slab-crossing populations into
+    // the neighbours' ghost rows of the same level (their rows nzl and -1), level 3 into their
+    // ghost planes of B.  Three flag phases per triple, as three single steps.
+    const long long PB = (long long)c->g.plane * (long long)c->esize;
+    char *scr = static_cast<char *>(c->buf[0]) + c->scratch_off * c->esize;
+    char *lo = static_cast<char *>(c->peer_scr[0]), *hi = static_cast<char *>(c->peer_scr[1]);
+    void *l1b = scr + 8 * PB, *l1t = scr + (18 - (long long)nzl) * PB;  // row z at base + (z + 1) P
+    void *l2b = scr + 20 * PB, *l2t = scr + (28 - (long long)nzl) * PB;
+    for (; t + 3 <= n; t += 3) {
+      void *A = c->buf[cur], *B = c->buf[1 - cur];
+      cudaStreamWaitEvent(c->stream, c->ev_i, 0);
+      cudaStreamWaitEvent(c->s_int, c->ev_b, 0);
+      GridParams gi = c->g;
+      gi.zbegin = 3;
+      gi.zcount = nzl - 6;
+      c->ops->pull3(A, B, gi, c->params, c->swe_g, peer_tb_chunks(c), c->s_int);
+      cudaEventRecord(c->ev_i, c->s_int);
+      GridParams g1 = c->g;
+      g1.peer_fence = peer_fence();
+      // level 1: row 0 -> the lower's level-1 row nzl (its plane 19), row nzl-1 -> the upper's row -1 (plane 8)
+      g1.peer_lo = lo + 19 * PB;
+      g1.peer_hi = hi + 8 * PB;
+      peer_wait(c, tmo);
+      g1.zbegin = 0;
+      c->ops->pull(A, l1b, g1, c->params, c->swe_g, c->bb, 5, c->stream);
+      g1.zbegin = nzl - 5;
+      c->ops->pull(A, l1t, g1, c->params, c->swe_g, c->bb, 5, c->stream);
+      peer_signal(c);
+      // level 2: into the lower's level-2 row nzl (plane 29) and the upper's row -1 (plane 20)
+      GridParams g2 = g1;
+      g2.peer_lo = lo + 29 * PB;
+      g2.peer_hi = hi + 20 * PB;
+      peer_wait(c, tmo);
+      g2.zbegin = 0;
+      c->ops->pull(l1b, l2b, g2, c->params, c->swe_g, c->bb, 4, c->stream);
+      g2.zbegin = nzl - 4;
+      c->ops->pull(l1t, l2t, g2, c->params, c->swe_g, c->bb, 4, c->stream);
+      peer_signal(c);
+      // level 3: into the neighbours' ghost planes of B
+      GridParams g3 = g1;
+      g3.peer_lo = c->peer_ghost[1 - cur][0];
+      g3.peer_hi = c->peer_ghost[1 - cur][1];
+      peer_wait(c, tmo);
+      g3.zbegin = 0;
+      c->ops->pull(l2b, B, g3, c->params, c->swe_g, c->bb, 3, c->stream);
+      g3.zbegin = nzl - 3;
+      c->ops->pull(l2t, B, g3, c->params, c->swe_g, c->bb, 3, c->stream);
+      peer_signal(c);
+      cudaEventRecord(c->ev_b, c->stream);
+      cur ^= 1;
+    }
+  }
   if (use_peer_tb(c)) {
     // Pairs of steps t -> t+2 (A = current grid, B = next): on s_int the two-step sweep of
     // the interior planes [2, nzl - 2) (its step-(t+1) halo planes 1 and nzl - 2 are recomputed
@@ -1134,7 +1204,9 @@ lbm_status lbm_create(lbm_stencil stencil, lbm_space collision_space, lbm_equili
       c->peer_tb_cap = false;
     c->scratch_off = c->grid_elems;
   }
-  const size_t alloc_elems = c->grid_elems + (c->peer_tb_cap ? (size_t)8 * g.plane : 0);
+  // scratch planes behind grid 0: 8 for pairs of steps across ranks, 22 more (planes 8..29) for
+  // the triples of 2D contexts on the peer path (use_peer_tb3)
+  const size_t alloc_elems = c->grid_elems + (c->peer_tb_cap ? (size_t)(two_d ? 30 : 8) * g.plane : 0);
   const int ngrids = (D.streaming == LBM_PULL) ? 2 : 1;
   for (int k = 0; k < ngrids; ++k) {
     if (c->dev_alloc) {
@@ -1212,8 +1284,9 @@ lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
   info->rate_specialization = c->rs & 3;
   // multi-rank pull contexts with the pair sequence (peer path, in-library NCCL, or the
   // LBM_REGION_PAIR_* regions of an external exchange) run two steps per interior sweep
-  info->temporal_blocking =
-      use_depth3(c) ? 3 : ((use_temporal_blocking(c) || (c->multi && c->peer_tb_cap)) ? 2 : 1);
+  info->temporal_blocking = (use_depth3(c) || use_peer_tb3(c))
+                                ? 3
+                                : ((use_temporal_blocking(c) || (c->multi && c->peer_tb_cap)) ? 2 : 1);
   info->resident_cluster = resident_cluster(c);
   info->cuda_graph_steps = (c->nranks == 1 && !info->resident_cluster && use_graphs(c)) ? kGraphSteps : 0;
   info->peer_wait_host = c->peer_on && c->peer_host_wait;
@@ -1651,13 +1724,19 @@ lbm_status lbm_step_peer(lbm_ctx *c, int n) {
     if (ps != LBM_OK) return ps;
   }
   int t = 0;
-  if (n >= kGraphSteps && graphs_enabled() && !c->peer_host_wait) {  // replay captured 32-step loops
+  // steps per captured loop: an even number of grid swaps (32 single steps or pairs; 36 = 12
+  // triples on the 2D peer path), so a graph ends on the parity it started from
+  const int gsteps = use_peer_tb3(c) ? 36 : kGraphSteps;
+  if ((c->peer_graph[0] || c->peer_graph[1]) && c->peer_graph_steps != gsteps) drop_graphs(c);
+  if (n >= gsteps && graphs_enabled() && !c->peer_host_wait) {  // replay captured step loops
+    c->peer_graph_steps = gsteps;
     for (int par = 0; par < 2; ++par) {
       if (c->peer_graph[par]) continue;
       cudaGraph_t gr = nullptr;
       LBM_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-      enqueue_peer_steps(c, kGraphSteps, par);  // par: pull grid / AA state
+      const int endp = enqueue_peer_steps(c, gsteps, par);  // par: pull grid / AA state
       cudaError_t e = cudaStreamEndCapture(c->stream, &gr);
+      if (e == cudaSuccess && endp != par) e = cudaErrorInvalidValue;  // odd number of swaps
       if (e == cudaSuccess) e = cudaGetLastError();
       if (e == cudaSuccess) e = cudaGraphInstantiate(&c->peer_graph[par], gr, 0);
       if (gr) cudaGraphDestroy(gr);
@@ -1667,9 +1746,9 @@ lbm_status lbm_step_peer(lbm_ctx *c, int n) {
       }
     }
     const int par = pull_parity(c);
-    for (; t + kGraphSteps <= n; t += kGraphSteps) {  // even: the parity is unchanged
+    for (; t + gsteps <= n; t += gsteps) {  // an even number of swaps: the parity is unchanged
       LBM_CUDA(c, cudaGraphLaunch(c->peer_graph[par], c->stream));
-      c->steps += kGraphSteps;
+      c->steps += gsteps;
     }
   }
   if (t < n) {

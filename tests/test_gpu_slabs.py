@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import workloads as W
-from gpu_helpers import F64_TOL, gate_error, initial_state, oracle_run
+from gpu_helpers import F64_TOL, gate_error, initial_state, oracle_run, round_to
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -538,9 +538,9 @@ def _random_slab_config(k):
     streaming = [L.LBM_PULL, L.LBM_AA][rng.integers(2)]
     transport = ["peer", "exchange"][rng.integers(2)]
     nranks = int(rng.integers(2, 5))
-    per = max(int(rng.integers(2, 9)), -(-4 // nranks))  # planes per slab (even split, >= 2; extents >= 4)
+    per = max(int(rng.integers(2, 15)), -(-4 // nranks))  # planes per slab (even split, >= 2; extents >= 4)
     d = W.DIM_OF[st]
-    shape = ((int(rng.integers(9, 40)), nranks * per, 1) if d == 2 else
+    shape = ((256 if rng.random() < 0.5 else int(rng.integers(9, 40)), nranks * per, 1) if d == 2 else
              (int(rng.integers(9, 30)), int(rng.integers(5, 14)), nranks * per))
     pairs = streaming == L.LBM_PULL and rng.random() < 0.5
     steps = int(rng.integers(3, 10))
@@ -550,7 +550,7 @@ def _random_slab_config(k):
 @pytest.mark.parametrize("k", range(int(os.environ.get("LBM_TEST_DRAWS_MULTI", "40"))))
 def test_random_multi_rank_sweep(k, monkeypatch):
     """Seeded random multi-rank draws (stencil, collision space, regime, pull / AA, fused peer
-    push or the exchange building blocks, 2-4 ranks, slabs of 2-8 planes, two-step
+    push or the exchange building blocks, 2-4 ranks, slabs of 2-14 planes, two-step
     sweeps across ranks or single steps) against the single-rank run: bitwise with single
     steps, to rounding with pairs of steps."""
     st, space, eq, zc, streaming, transport, nranks, shape, pairs, steps = _random_slab_config(k)
@@ -571,8 +571,8 @@ def test_random_multi_rank_sweep(k, monkeypatch):
     used_pairs = pairs and all(D.supports_pairs(l) for l in lats)
     if transport == "peer":
         D.connect_local(lats)
-        D.step_peer_local(lats, steps, chunk=2 if pairs else 1)
-        used_pairs = used_pairs and all(l.info().temporal_blocking == 2 for l in lats)
+        D.step_peer_local(lats, steps, chunk=steps if pairs else 1)
+        used_pairs = used_pairs and all(l.info().temporal_blocking >= 2 for l in lats)
     else:
         D.prime_local(lats)
         D.step_local(lats, steps, pairs=pairs)
@@ -584,3 +584,50 @@ def test_random_multi_rank_sweep(k, monkeypatch):
         assert gate_error(st, multi, single, zc) < 1e-13, what
     else:
         np.testing.assert_array_equal(multi, single, err_msg=str(what))
+
+
+@pytest.mark.parametrize("space,eq,zc,prec,nranks,rows,steps", [
+    (W.CENTRAL, W.EQ_SWE, 0, L.LBM_FP64, 2, 12, 9),
+    (W.CUMULANT, W.EQ_SWE, 1, L.LBM_FP64, 3, 10, 11),
+    (W.CENTRAL, W.EQ_ABSOLUTE, 1, L.LBM_FP64, 4, 16, 8),
+    (W.RAW, W.EQ_DELTA, 1, L.LBM_FP32, 2, 20, 7),
+    (W.POPULATION, W.EQ_DELTA, 1, L.LBM_FP64, 3, 11, 36 + 5),
+])
+def test_peer_three_step_sweeps_2d_match_single_rank(space, eq, zc, prec, nranks, rows, steps, monkeypatch):
+    """2D slabs on the fused peer push advance TRIPLES of steps (interior rows by the depth-3
+    sweep, boundary regions by three single steps through the level-1 / level-2 scratch with
+    pushes into the neighbours' ghost rows; lbm_info.temporal_blocking == 3), then a pair or a
+    single step: equal to the single-rank run to rounding and to the oracle."""
+    monkeypatch.setenv("LBM_PEER_TB", "1")
+    st = W.D2Q9
+    shape = (256, rows * nranks, 1)
+    g = W.swe_lattice_parameters()[0] if eq == W.EQ_SWE else 0.0
+    rates = (W.regularized_rates(st, W.swe_lattice_parameters()[2]) if eq == W.EQ_SWE else
+             (np.array([1.37]) if space == W.POPULATION else W.rate_set_p(st)))
+    if eq == W.EQ_SWE:
+        f0 = initial_state(st, space, eq, zc, shape, g=g, noise=0.0, dam=(60.0, 6.25, 1.25))
+    else:
+        f0 = round_to(initial_state(st, space, eq, zc, shape), prec)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, precision=prec, swe_g=g) as lat:
+        lat.set_populations(f0)
+        lat.step(steps)
+        single = lat.get_populations()
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, precision=prec, swe_g=g, rank=r,
+                      nranks=nranks) for r in range(nranks)]
+    for lat in lats:
+        lat.set_populations(np.ascontiguousarray(f0[:, :, lat.offset:lat.offset + lat.extent]))
+    D.connect_local(lats)
+    assert all(lat.info().temporal_blocking == 3 for lat in lats)
+    D.on_ranks(lats, lambda lat: lat.step_peer(steps))
+    for lat in lats:
+        lat.sync()
+        assert not lat.peer_timed_out()
+    multi = np.concatenate([lat.get_populations() for lat in lats], axis=2)
+    for lat in lats:
+        lat.close()
+    norm = "cell" if eq == W.EQ_SWE else "population"
+    tol = 1e-13 if prec == L.LBM_FP64 else 2e-6
+    assert gate_error(st, multi, single, zc, norm=norm) < tol
+    if prec == L.LBM_FP64 and eq != W.EQ_SWE:
+        ref = oracle_run(st, space, eq, zc, rates, shape, f0, steps, g=g)
+        assert gate_error(st, multi, ref, zc) < F64_TOL
