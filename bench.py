@@ -573,8 +573,8 @@ def main():
     # across ranks: interior sweep + 4 boundary (+ 2 waits + 2 signals on the peer path)
     if n == 1:
         launches_per_step = 1.0 / tb
-    elif path == "peer":
-        launches_per_step = 4.5 if tb == 2 else 5
+    elif path == "peer":  # per sweep: interior + 2 boundary launches, a wait and a signal per phase
+        launches_per_step = {1: 5.0, 2: 4.5, 3: 13.0 / 3.0}.get(tb, 5.0)
         if lat.info().peer_wait_host:  # no wait kernels
             launches_per_step -= 1
     else:
