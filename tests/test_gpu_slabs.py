@@ -372,8 +372,8 @@ def test_peer_two_step_sweeps_match_single_rank(st, space, eq, zc, prec, shape, 
     the boundary regions by two single steps through the scratch planes with pushes into the
     neighbours' scratch and ghost planes; pairs plus a trailing single step match the
     single-rank run to rounding and the oracle at full parity."""
-    from gpu_helpers import round_to
     monkeypatch.setenv("LBM_PEER_TB", "1")  # small lattices: pairs despite < 2 waves of CTAs
+    monkeypatch.setenv("LBM_TB_DEPTH", "2")  # 2D slabs would otherwise advance triples
     g = W.swe_lattice_parameters()[0] if eq == W.EQ_SWE else 0.0
     rates = W.rate_set_p(st) if space != W.POPULATION else [1.3]
     if eq == W.EQ_SWE:
