@@ -381,12 +381,12 @@ int tb_zchunks(const lbm_ctx *c) {
 bool use_peer_tb(const lbm_ctx *c) {
   return c->peer_tb_cap && (c->peer_on || c->comm) && c->streaming == LBM_PULL;
 }
-// three fused steps per triple across ranks (2D, fused peer push): the interior rows [3, nzl - 3)
-// by the depth-3 sweep, the boundary regions by three single steps through the scratch
-// planes 8..29 (enqueue_peer_steps); >= 10 rows per slab; LBM_TB_DEPTH=2 keeps pairs
+// three fused steps per triple across ranks (2D; fused peer push or in-library NCCL): the
+// interior rows [3, nzl - 3) by the depth-3 sweep, the boundary regions by three single steps
+// through the scratch planes 8..29 (enqueue_peer_steps / enqueue_nccl_steps); >= 10 rows per
+// slab; LBM_TB_DEPTH=2 keeps pairs
 bool use_peer_tb3(const lbm_ctx *c) {
-  if (!use_peer_tb(c) || !c->peer_on || c->d != 2 || !c->ops->pull3 || c->g.nzl < 10 || c->g.nx % 256 != 0)
-    return false;
+  if (!use_peer_tb(c) || c->d != 2 || !c->ops->pull3 || c->g.nzl < 10 || c->g.nx % 256 != 0) return false;
   const char *env = getenv("LBM_TB_DEPTH");
   return !(env && env[0] == '2');
 }
@@ -794,6 +794,17 @@ lbm_status peer_refresh(lbm_ctx *c) {
 void halo_blocks(lbm_ctx *c, const lbm_layout &lay, int which, int grid, char *p[4]) {
   const size_t E = c->esize;
   size_t o[4] = {lay.send_lo, lay.send_hi, lay.recv_lo, lay.recv_hi};
+  if (which == 3 || which == 4) {  // level-1 / level-2 scratch rows of the triples (2D)
+    char *scr = static_cast<char *>(c->buf[0]) + c->scratch_off * E;
+    const long long P = c->g.plane, nzl = c->g.nzl;
+    const long long bot = which == 3 ? 8 * P : 20 * P;                      // row z at + (z + 1) P
+    const long long top = which == 3 ? (18 - nzl) * P : (28 - nzl) * P;
+    p[0] = scr + (bot + (long long)o[0]) * (long long)E;
+    p[1] = scr + (top + (long long)o[1]) * (long long)E;
+    p[2] = scr + (bot + (long long)o[2]) * (long long)E;
+    p[3] = scr + (top + (long long)o[3]) * (long long)E;
+    return;
+  }
   if (which == 2) {
     char *scr = static_cast<char *>(c->buf[0]) + c->scratch_off * E;
     const size_t shift = (size_t)(c->g.nzl - 6) * (size_t)c->g.plane;
@@ -856,6 +867,41 @@ lbm_status enqueue_nccl_steps(lbm_ctx *c, int n, int &cur) {
   LBM_CUDA(c, cudaEventRecord(c->ev_b, c->stream));
   LBM_CUDA(c, cudaEventRecord(c->ev_i, c->stream));
   int t = 0;
+  if (use_peer_tb3(c)) {  // triples (2D): as enqueue_peer_steps, an exchange after each level
+    const long long PB = (long long)c->g.plane * (long long)c->esize;
+    char *scr = static_cast<char *>(c->buf[0]) + c->scratch_off * c->esize;
+    void *l1b = scr + 8 * PB, *l1t = scr + (18 - (long long)nzl) * PB;
+    void *l2b = scr + 20 * PB, *l2t = scr + (28 - (long long)nzl) * PB;
+    for (; t + 3 <= n; t += 3) {
+      void *A = c->buf[cur], *B = c->buf[1 - cur];
+      cudaStreamWaitEvent(c->stream, c->ev_i, 0);
+      cudaStreamWaitEvent(c->s_int, c->ev_b, 0);
+      GridParams gi = c->g;
+      gi.zbegin = 3;
+      gi.zcount = nzl - 6;
+      c->ops->pull3(A, B, gi, c->params, c->swe_g, peer_tb_chunks(c), c->s_int);
+      cudaEventRecord(c->ev_i, c->s_int);
+      GridParams gb = c->g;
+      gb.zbegin = 0;
+      c->ops->pull(A, l1b, gb, c->params, c->swe_g, c->bb, 5, c->stream);
+      gb.zbegin = nzl - 5;
+      c->ops->pull(A, l1t, gb, c->params, c->swe_g, c->bb, 5, c->stream);
+      if ((s = nccl_exchange(c, lay, 3, cur, c->stream)) != LBM_OK) return s;
+      gb.zbegin = 0;
+      c->ops->pull(l1b, l2b, gb, c->params, c->swe_g, c->bb, 4, c->stream);
+      gb.zbegin = nzl - 4;
+      c->ops->pull(l1t, l2t, gb, c->params, c->swe_g, c->bb, 4, c->stream);
+      if ((s = nccl_exchange(c, lay, 4, cur, c->stream)) != LBM_OK) return s;
+      gb.zbegin = 0;
+      c->ops->pull(l2b, B, gb, c->params, c->swe_g, c->bb, 3, c->stream);
+      gb.zbegin = nzl - 3;
+      c->ops->pull(l2t, B, gb, c->params, c->swe_g, c->bb, 3, c->stream);
+      if ((s = nccl_exchange(c, lay, 1, cur, c->stream)) != LBM_OK) return s;
+      cudaEventRecord(c->ev_b, c->stream);
+      cur ^= 1;
+      c->steps += 3;
+    }
+  }
   if (use_peer_tb(c)) {
     const size_t PB = (size_t)c->g.plane * c->esize;
     char *scr = static_cast<char *>(c->buf[0]) + c->scratch_off * c->esize;

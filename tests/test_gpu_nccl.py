@@ -157,3 +157,28 @@ def test_device_allocator_hook():
     np.testing.assert_array_equal(lat.get_populations(), ref)
     lat.close()
     assert not live
+
+
+@pytest.mark.parametrize("space,eq,zc,steps", [(W.CENTRAL, W.EQ_SWE, 0, 10), (W.RAW, W.EQ_DELTA, 1, 8)])
+def test_nccl_self_exchange_three_step_sweeps_2d(space, eq, zc, steps, monkeypatch):
+    """2D triples across the NCCL exchange (interior depth-3 sweep + three boundary steps through
+    the level-1 / level-2 scratch, an exchange after each level) plus a trailing single step or
+    pair: to rounding against the single-rank run."""
+    monkeypatch.setenv("LBM_PEER_TB", "1")
+    st, shape = W.D2Q9, (256, 24, 1)
+    g = W.swe_lattice_parameters()[0] if eq == W.EQ_SWE else 0.0
+    rates = W.regularized_rates(st, W.swe_lattice_parameters()[2]) if eq == W.EQ_SWE else W.rate_set_p(st)
+    if eq == W.EQ_SWE:
+        f0 = initial_state(st, space, eq, zc, shape, g=g, noise=0.0, dam=(60.0, 6.25, 1.25))
+    else:
+        f0 = initial_state(st, space, eq, zc, shape)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, swe_g=g) as lat:
+        lat.set_populations(f0)
+        lat.step(steps)
+        ref = lat.get_populations()
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc, swe_g=g, nccl_id=L.nccl_get_unique_id()) as lat:
+        assert lat.info().temporal_blocking == 3
+        lat.set_populations(f0)
+        lat.step(steps)
+        got = lat.get_populations()
+    assert gate_error(st, got, ref, zc, norm="cell" if eq == W.EQ_SWE else "population") < 1e-13
