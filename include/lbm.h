@@ -140,7 +140,15 @@ typedef enum {
      lbm_get_halo(1) and lbm_swap once (PAIR_BOUNDARY2 counts the pair's first step). */
   LBM_REGION_PAIR_INTERIOR = 3,
   LBM_REGION_PAIR_BOUNDARY1 = 4,
-  LBM_REGION_PAIR_BOUNDARY2 = 5
+  LBM_REGION_PAIR_BOUNDARY2 = 5,
+  /* three fused steps (2D slabs of >= 10 rows, nx % 256 == 0: lbm_get_halo(3) succeeds): TRIPLE_INTERIOR
+     (rows [3, nzl-3), any stream, concurrently with the rest), TRIPLE_BOUNDARY1, exchange
+     lbm_get_halo(3) (level-1 scratch rows), TRIPLE_BOUNDARY2, exchange lbm_get_halo(4)
+     (level-2 scratch rows), TRIPLE_BOUNDARY3, exchange lbm_get_halo(1), lbm_swap. */
+  LBM_REGION_TRIPLE_INTERIOR = 6,
+  LBM_REGION_TRIPLE_BOUNDARY1 = 7,
+  LBM_REGION_TRIPLE_BOUNDARY2 = 8,
+  LBM_REGION_TRIPLE_BOUNDARY3 = 9
 } lbm_region;
 
 typedef struct {
@@ -286,7 +294,9 @@ lbm_status lbm_nccl_get_unique_id(void *out128);
 lbm_status lbm_step_region(lbm_ctx *ctx, lbm_region region, void *stream);
 lbm_status lbm_swap(lbm_ctx *ctx);
 /* PULL: which = 0 the current grid, 1 the next grid, 2 the scratch of the two-step regions
-   (LBM_REGION_PAIR_*).  AA: which = 0 pre-odd, 1 post-odd. */
+   (LBM_REGION_PAIR_*), 3 / 4 the level-1 / level-2 scratch of the three-step regions
+   (LBM_REGION_TRIPLE_*; LBM_EUNSUPPORTED where the context has none).  AA: which = 0 pre-odd,
+   1 post-odd. */
 lbm_status lbm_get_halo(lbm_ctx *ctx, int which, lbm_halo *out);
 
 lbm_status lbm_sync(lbm_ctx *ctx);

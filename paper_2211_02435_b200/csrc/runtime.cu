@@ -385,11 +385,16 @@ bool use_peer_tb(const lbm_ctx *c) {
 // interior rows [3, nzl - 3) by the depth-3 sweep, the boundary regions by three single steps
 // through the scratch planes 8..29 (enqueue_peer_steps / enqueue_nccl_steps); >= 10 rows per
 // slab; LBM_TB_DEPTH=2 keeps pairs
-bool use_peer_tb3(const lbm_ctx *c) {
-  if (!use_peer_tb(c) || c->d != 2 || !c->ops->pull3 || c->g.nzl < 10 || c->g.nx % 256 != 0) return false;
+// the context has the three-step regions (2D slab with the pair scratch, >= 10 rows, 256-cell strips)
+bool tb3_cap(const lbm_ctx *c) {
+  if (!c->peer_tb_cap || c->streaming != LBM_PULL || c->d != 2 || !c->ops->pull3 || c->g.nzl < 10 ||
+      c->g.nx % 256 != 0)
+    return false;
   const char *env = getenv("LBM_TB_DEPTH");
   return !(env && env[0] == '2');
 }
+
+bool use_peer_tb3(const lbm_ctx *c) { return use_peer_tb(c) && tb3_cap(c); }
 
 int peer_tb_chunks(const lbm_ctx *c) {
   const long long tiles = tb_tiles(c);
@@ -1330,7 +1335,7 @@ lbm_status lbm_get_info(const lbm_ctx *c, lbm_info *info) {
   info->rate_specialization = c->rs & 3;
   // multi-rank pull contexts with the pair sequence (peer path, in-library NCCL, or the
   // LBM_REGION_PAIR_* regions of an external exchange) run two steps per interior sweep
-  info->temporal_blocking = (use_depth3(c) || use_peer_tb3(c))
+  info->temporal_blocking = (use_depth3(c) || (c->multi && tb3_cap(c)))
                                 ? 3
                                 : ((use_temporal_blocking(c) || (c->multi && c->peer_tb_cap)) ? 2 : 1);
   info->resident_cluster = resident_cluster(c);
@@ -1490,6 +1495,44 @@ lbm_status lbm_step_region(lbm_ctx *c, lbm_region region, void *stream) {
       }
       break;
     }
+    case LBM_REGION_TRIPLE_INTERIOR:
+    case LBM_REGION_TRIPLE_BOUNDARY1:
+    case LBM_REGION_TRIPLE_BOUNDARY2:
+    case LBM_REGION_TRIPLE_BOUNDARY3: {
+      // three fused steps across ranks with an external exchange (the triple sequence of
+      // enqueue_peer_steps without the peer pushes; scratch planes 8..29)
+      if (!tb3_cap(c))
+        return fail(c, LBM_EUNSUPPORTED, "three-step regions need a 2D multi-rank pull slab of >= 10 rows");
+      void *A = c->buf[c->cur], *B = c->buf[1 - c->cur];
+      const long long PB = (long long)g.plane * (long long)c->esize;
+      char *scr = static_cast<char *>(c->buf[0]) + c->scratch_off * c->esize;
+      void *l1b = scr + 8 * PB, *l1t = scr + (18 - (long long)n) * PB;
+      void *l2b = scr + 20 * PB, *l2t = scr + (28 - (long long)n) * PB;
+      GridParams gb = c->g;
+      if (region == LBM_REGION_TRIPLE_INTERIOR) {
+        gb.zbegin = 3;
+        gb.zcount = n - 6;
+        c->ops->pull3(A, B, gb, c->params, c->swe_g, peer_tb_chunks(c), s);
+      } else if (region == LBM_REGION_TRIPLE_BOUNDARY1) {
+        gb.zbegin = 0;
+        c->ops->pull(A, l1b, gb, c->params, c->swe_g, c->bb, 5, s);
+        gb.zbegin = n - 5;
+        c->ops->pull(A, l1t, gb, c->params, c->swe_g, c->bb, 5, s);
+      } else if (region == LBM_REGION_TRIPLE_BOUNDARY2) {
+        gb.zbegin = 0;
+        c->ops->pull(l1b, l2b, gb, c->params, c->swe_g, c->bb, 4, s);
+        gb.zbegin = n - 4;
+        c->ops->pull(l1t, l2t, gb, c->params, c->swe_g, c->bb, 4, s);
+        c->steps++;  // the triple's first step
+      } else {
+        gb.zbegin = 0;
+        c->ops->pull(l2b, B, gb, c->params, c->swe_g, c->bb, 3, s);
+        gb.zbegin = n - 3;
+        c->ops->pull(l2t, B, gb, c->params, c->swe_g, c->bb, 3, s);
+        c->steps++;  // the second (lbm_swap counts the third)
+      }
+      break;
+    }
     default: return fail(c, LBM_EINVAL, "unknown region");
   }
   return check_launch(c, "stream_collide(region)");
@@ -1509,13 +1552,25 @@ lbm_status lbm_get_halo(lbm_ctx *c, int which, lbm_halo *out) {
     return fail(c, LBM_EUNSUPPORTED, "Esoteric Pull / Push / Twist are single-rank");
   if (which == 2 && !c->peer_tb_cap)
     return fail(c, LBM_EUNSUPPORTED, "no scratch halo: the context does not run two-step sweeps across ranks");
-  if (which < 0 || which > 2) return fail(c, LBM_EINVAL, "which must be 0, 1 or 2");
+  if ((which == 3 || which == 4) && !tb3_cap(c))
+    return fail(c, LBM_EUNSUPPORTED, "no level scratch halo: the context does not run three-step sweeps across ranks");
+  if (which < 0 || which > 4) return fail(c, LBM_EINVAL, "which must be 0 .. 4");
   lbm_layout lay;
   lbm_status s = lbm_grid_layout((lbm_stencil)c->stencil, (lbm_precision)c->prec, c->gnx, c->gny, c->gnz,
                                  c->nranks, &lay);
   if (s != LBM_OK) return fail(c, s, "layout");
   const size_t E = c->esize;
   size_t o[4] = {lay.send_lo, lay.send_hi, lay.recv_lo, lay.recv_hi};
+  if (which == 3 || which == 4) {  // level-1 / level-2 scratch rows of the three-step regions
+    char *p[4];
+    halo_blocks(c, lay, which, c->cur, p);
+    out->send_lo = p[0];
+    out->send_hi = p[1];
+    out->recv_lo = p[2];
+    out->recv_hi = p[3];
+    out->bytes = lay.halo_elems * E;
+    return LBM_OK;
+  }
   if (which == 2) {  // the scratch of the two-step regions: planes -1, 0 at scratch planes 0, 1
     // (the grid's offsets), planes nzl - 1, nzl at scratch planes 6, 7
     char *scr = static_cast<char *>(c->buf[0]) + c->scratch_off * E;

@@ -154,10 +154,42 @@ def supports_pairs(lat: "L.Lattice") -> bool:
         return False
 
 
+def supports_triples(lat: "L.Lattice") -> bool:
+    """The context runs three-step sweeps across ranks (LBM_REGION_TRIPLE_*, lbm_get_halo(3/4):
+    2D slabs of >= 10 rows)."""
+    try:
+        lat.get_halo(3)
+        return True
+    except L.LbmError:
+        return False
+
+
 def step_local(lats, n: int, pairs: bool = False):
     """n time steps of all slab contexts of one process (LocalTransport), with the
-    same boundary/interior split as the multi-process driver (pairs: the two-step regions)."""
+    same boundary/interior split as the multi-process driver (pairs: the fused-step regions,
+    triples where every context has them, then pairs)."""
     tr = LocalTransport(lats)
+    if pairs and all(supports_triples(l) for l in lats):
+        while n >= 3:
+            for l in lats:
+                l.step_region(L.LBM_REGION_TRIPLE_INTERIOR)
+                l.step_region(L.LBM_REGION_TRIPLE_BOUNDARY1)
+            for l in lats:
+                l.sync()
+            tr.exchange_all(3)
+            for l in lats:
+                l.step_region(L.LBM_REGION_TRIPLE_BOUNDARY2)
+            for l in lats:
+                l.sync()
+            tr.exchange_all(4)
+            for l in lats:
+                l.step_region(L.LBM_REGION_TRIPLE_BOUNDARY3)
+            for l in lats:
+                l.sync()
+            tr.exchange_all(1)
+            for l in lats:
+                l.swap()
+            n -= 3
     if pairs and all(supports_pairs(l) for l in lats):
         while n >= 2:
             for l in lats:
@@ -211,6 +243,7 @@ class SlabRunner:
         if pairs and not can:
             raise ValueError("this context has no two-step regions (LBM_REGION_PAIR_*)")
         self.pairs = can if pairs is None else bool(pairs)
+        self.triples = self.pairs and supports_triples(lat)  # 2D slabs of >= 10 rows
 
     def prime(self):
         self.lat.sync()
@@ -220,6 +253,21 @@ class SlabRunner:
         import torch
 
         main = self.s_main
+        # three fused steps per triple (2D): the interior sweep on s_int overlaps the three
+        # boundary steps and their exchanges (level-1 / level-2 scratch rows, next-grid halo)
+        while self.triples and n >= 3:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            self.s_int.wait_event(ev)
+            self.lat.step_region(L.LBM_REGION_TRIPLE_INTERIOR, self.s_int.cuda_stream)
+            for region, which in ((L.LBM_REGION_TRIPLE_BOUNDARY1, 3), (L.LBM_REGION_TRIPLE_BOUNDARY2, 4),
+                                  (L.LBM_REGION_TRIPLE_BOUNDARY3, 1)):
+                self.lat.step_region(region, main.cuda_stream)
+                with torch.cuda.stream(main):
+                    self.tr.exchange(which)
+            main.wait_stream(self.s_int)
+            self.lat.swap()
+            n -= 3
         # two fused steps per pair: the interior sweep on s_int overlaps both boundary steps and
         # both exchanges (scratch halo after the first, next-grid halo after the second)
         while self.pairs and n >= 2:

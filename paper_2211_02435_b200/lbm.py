@@ -26,6 +26,8 @@ LBM_BC_PERIODIC, LBM_BC_NOSLIP = 0, 1
 LBM_FORCE_GUO, LBM_FORCE_HE = 0, 1
 LBM_REGION_ALL, LBM_REGION_BOUNDARY, LBM_REGION_INTERIOR = 0, 1, 2
 LBM_REGION_PAIR_INTERIOR, LBM_REGION_PAIR_BOUNDARY1, LBM_REGION_PAIR_BOUNDARY2 = 3, 4, 5
+LBM_REGION_TRIPLE_INTERIOR, LBM_REGION_TRIPLE_BOUNDARY1, LBM_REGION_TRIPLE_BOUNDARY2, LBM_REGION_TRIPLE_BOUNDARY3 = \
+    6, 7, 8, 9
 
 Q_OF = {LBM_D2Q9: 9, LBM_D3Q19: 19, LBM_D3Q27: 27}
 

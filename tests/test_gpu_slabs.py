@@ -631,3 +631,30 @@ def test_peer_three_step_sweeps_2d_match_single_rank(space, eq, zc, prec, nranks
     if prec == L.LBM_FP64 and eq != W.EQ_SWE:
         ref = oracle_run(st, space, eq, zc, rates, shape, f0, steps, g=g)
         assert gate_error(st, multi, ref, zc) < F64_TOL
+
+
+@pytest.mark.parametrize("nranks,rows,steps", [(2, 12, 9), (3, 10, 11), (4, 14, 7)])
+def test_exchange_three_step_regions_2d(nranks, rows, steps, monkeypatch):
+    """The external-exchange building blocks for triples (LBM_REGION_TRIPLE_*, lbm_get_halo(3/4)
+    level scratch halos) driven by the in-process transport: equal to the single-rank run to
+    rounding."""
+    monkeypatch.setenv("LBM_PEER_TB", "1")
+    st, space, eq, zc = W.D2Q9, W.CENTRAL, W.EQ_ABSOLUTE, 1
+    shape = (256, rows * nranks, 1)
+    rates = W.rate_set_p(st)
+    f0 = initial_state(st, space, eq, zc, shape)
+    with L.Lattice(st, space, eq, rates, shape, zero_centered=zc) as lat:
+        lat.set_populations(f0)
+        lat.step(steps)
+        single = lat.get_populations()
+    lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, rank=r, nranks=nranks) for r in range(nranks)]
+    for lat in lats:
+        lat.set_populations(np.ascontiguousarray(f0[:, :, lat.offset:lat.offset + lat.extent]))
+    assert all(D.supports_triples(l) and l.info().temporal_blocking == 3 for l in lats)
+    D.prime_local(lats)
+    D.step_local(lats, steps, pairs=True)
+    multi = np.concatenate([lat.get_populations() for lat in lats], axis=2)
+    assert all(lat.info().steps_done == steps for lat in lats)
+    for lat in lats:
+        lat.close()
+    assert gate_error(st, multi, single, zc) < 1e-13
