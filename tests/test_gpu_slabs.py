@@ -491,17 +491,17 @@ def test_peer_waits_are_host_ordered_when_ranks_share_a_gpu(monkeypatch):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="device-side peer waits need one GPU per rank")
-@pytest.mark.parametrize("tb", ["0", "1"])
-def test_peer_device_waits_across_gpus(tb, monkeypatch):
+@pytest.mark.parametrize("tb,st", [("0", W.D3Q19), ("1", W.D3Q19), ("1", W.D2Q9)])
+def test_peer_device_waits_across_gpus(tb, st, monkeypatch):
     """The deployment case: every context on its own GPU (in one process), device-side waits,
-    n >= 32 steps from captured graphs, single steps and two-step pairs; equal to the single
-    rank (bitwise for single steps, to rounding for pairs)."""
+    n >= 32 steps from captured graphs, single steps, two-step pairs (3D) and triples (2D, 36-step
+    graphs); equal to the single rank (bitwise for single steps, to rounding when fused)."""
     monkeypatch.setenv("LBM_PEER_TB", tb)
     monkeypatch.delenv("LBM_PEER_WAIT", raising=False)
-    st, space, eq, zc = W.D3Q19, W.RAW, W.EQ_DELTA, 1
+    space, eq, zc = W.RAW, W.EQ_DELTA, 1
     ndev = torch.cuda.device_count()
     nranks = min(ndev, 4)
-    shape, steps = (32, 16, 8 * nranks), 71
+    shape, steps = ((256, 12 * nranks, 1) if st == W.D2Q9 else (32, 16, 8 * nranks)), 71
     rates = W.rate_set_p(st)
     f0 = initial_state(st, space, eq, zc, shape)
     with L.Lattice(st, space, eq, rates, shape, zero_centered=zc) as lat:
@@ -510,8 +510,11 @@ def test_peer_device_waits_across_gpus(tb, monkeypatch):
         single = lat.get_populations()
     lats = [L.Lattice(st, space, eq, rates, shape, zero_centered=zc, rank=r, nranks=nranks, device=r)
             for r in range(nranks)]
+    ax = 2 if st == W.D2Q9 else 1
     for lat in lats:
-        lat.set_populations(np.ascontiguousarray(f0[:, lat.offset:lat.offset + lat.extent]))
+        sl = [slice(None)] * 4
+        sl[ax] = slice(lat.offset, lat.offset + lat.extent)
+        lat.set_populations(np.ascontiguousarray(f0[tuple(sl)]))
     D.connect_local(lats)
     assert all(lat.info().peer_wait_host == 0 for lat in lats)
     for chunk in (64, 7):
@@ -520,7 +523,7 @@ def test_peer_device_waits_across_gpus(tb, monkeypatch):
     for lat in lats:
         lat.sync()
         assert not lat.peer_timed_out()
-    multi = np.concatenate([lat.get_populations() for lat in lats], axis=1)
+    multi = np.concatenate([lat.get_populations() for lat in lats], axis=ax)
     for lat in lats:
         lat.close()
     if tb == "0":
