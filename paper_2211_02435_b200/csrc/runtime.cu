@@ -644,7 +644,7 @@ int enqueue_peer_steps(lbm_ctx *c, int n, int cur) {
     char *lo = static_cast<char *>(c->peer_scr[0]), *hi = static_cast<char *>(c->peer_scr[1]);
     void *l1b = scr + 8 * PB, *l1t = scr + (18 - (long long)nzl) * PB;  // row z at base + (z + 1) P
     void *l2b = scr + 20 * PB, *l2t = scr + (28 - (long long)nzl) * PB;
-    for (; t + 3 <= n; t += 3) {
+    for (; t + 3 <= n && n - t != 4; t += 3) {  // a remainder of 4: two pairs, not triple + single
       void *A = c->buf[cur], *B = c->buf[1 - cur];
       cudaStreamWaitEvent(c->stream, c->ev_i, 0);
       cudaStreamWaitEvent(c->s_int, c->ev_b, 0);
@@ -877,7 +877,7 @@ lbm_status enqueue_nccl_steps(lbm_ctx *c, int n, int &cur) {
     char *scr = static_cast<char *>(c->buf[0]) + c->scratch_off * c->esize;
     void *l1b = scr + 8 * PB, *l1t = scr + (18 - (long long)nzl) * PB;
     void *l2b = scr + 20 * PB, *l2t = scr + (28 - (long long)nzl) * PB;
-    for (; t + 3 <= n; t += 3) {
+    for (; t + 3 <= n && n - t != 4; t += 3) {  // a remainder of 4: two pairs, not triple + single
       void *A = c->buf[cur], *B = c->buf[1 - cur];
       cudaStreamWaitEvent(c->stream, c->ev_i, 0);
       cudaStreamWaitEvent(c->s_int, c->ev_b, 0);
@@ -1417,7 +1417,7 @@ lbm_status lbm_step(lbm_ctx *c, int n) {
   }
   if (use_temporal_blocking(c)) {  // triples (2D, k_pullD_2d), then pairs (k_pull2 / k_pull2_2d)
     if (use_depth3(c)) {
-      for (; t + 3 <= n; t += 3) {
+      for (; t + 3 <= n && n - t != 4; t += 3) {  // a remainder of 4: two pairs, not triple + single
         c->ops->pull3(c->buf[c->cur], c->buf[1 - c->cur], g, c->params, c->swe_g, tb3_zchunks(c), c->stream);
         c->cur ^= 1;
         c->steps += 3;
