@@ -226,9 +226,18 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout=5.0):
+        """Block until nvidia-smi has printed its first sample (NVML start-up can take longer
+        than a short timed region), so the region is always bracketed by samples."""
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
     def stop(self):
         if not self.proc:
             return None
+        if not self.lines:
+            self.wait_first(2.0)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -511,7 +520,8 @@ def main():
         dist.barrier()
     sampler = ClockSampler(local_rank)
     sampler.start()
-    time.sleep(0.3)
+    sampler.wait_first()
+    time.sleep(0.15)
     # the K timed steps in (up to) 5 windows of consecutive steps, CUDA events between them
     nwin = max(1, min(5, args.steps))
     # window edges on multiples of the steps one launch fuses (lbm_step runs whole sweeps inside
