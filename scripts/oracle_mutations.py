@@ -47,6 +47,11 @@ MUTANTS = [
     ("pull: push direction", "p[a] = pos[a] - s.m.xi[i][a];", "p[a] = pos[a] + s.m.xi[i][a];"),
     ("bounce-back: same slot instead of the opposite", "f[i] = src[(long long)s.m.opp[i] * N + c];",
      "f[i] = src[(long long)i * N + c];"),
+    # a wall in the wrong place: the bounced population taken from the periodic image across the
+    # wall (pinned by the closed-form channel flow, test_poiseuille_bounce_back_closed_form)
+    ("bounce-back: opposite population of the periodic image instead of the own cell",
+     "f[i] = src[(long long)s.m.opp[i] * N + c];",
+     "f[i] = src[(long long)s.m.opp[i] * N + ((long long)p[2] * ny + p[1]) * nx + p[0]];"),
     ("SWE: printed -u.u/3 (the garble of Eq. 5.3)", "+ xu * xu / R(2) - uu / R(6));", "+ xu * xu / R(2) - uu / R(3));"),
     ("SWE cumulant: cs2 = g h", "const R cs2 = (m.eq == EQ_SWE) ? m.g * rho / R(2) : R(CS2);\n  // discrete",
      "const R cs2 = (m.eq == EQ_SWE) ? m.g * rho : R(CS2);\n  // discrete"),
