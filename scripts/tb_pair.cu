@@ -10,6 +10,7 @@
 
 #include "kernels.cuh"
 #include "tb_pair.cuh"
+#include "tb3d_depth.cuh"
 
 using namespace lbm;
 
@@ -168,22 +169,63 @@ void run_k2(Bench<real> &B, const char *tag) {
          2.0 * B.cells / (ms * 1e-3) / 1e6, fa.numRegs, fa.localSizeBytes, smem, nb, md);
 }
 
+// depth-D 3D sweep (tb3d_depth.cuh) against D single k_pull steps (its own reference)
+template <class real, int TX, int TY, int D, int MINB, bool PF>
+void run_d3(Bench<real> &B, const char *tag) {
+  using S = D3Q19;
+  using T = Tile3D<S, TX, TY, D>;
+  auto kern = k_pullD_3d<S, SPACE_RAW, REG_DELTA, real, RS_GENERAL, TX, TY, D, MINB, PF>;
+  const size_t smem = (size_t)T::RING * sizeof(real);
+  if (smem > 227 * 1024) {
+    printf("%-40s smem %zu too large\n", tag, smem);
+    return;
+  }
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  Force<real> fr{};
+  // reference: D single steps a -> ref (through b)
+  B.reset();
+  {
+    dim3 grid((unsigned)((B.g.nx + BLOCK_X - 1) / BLOCK_X), (unsigned)B.g.ny, (unsigned)B.g.nzl);
+    const real *sp = B.a;
+    for (int k = 0; k < D; ++k) {
+      real *d = ((D - 1 - k) % 2 == 0) ? B.ref : B.b;
+      k_pull<S, SPACE_RAW, REG_DELTA, real, false, RS_GENERAL><<<grid, BLOCK_X>>>(sp, d, B.g, B.r, real(0), fr);
+      sp = d;
+    }
+    CK(cudaDeviceSynchronize());
+  }
+  CK(cudaMemset(B.b, 0, B.elems * sizeof(real)));
+  dim3 grid((unsigned)(B.g.nx / TX), (unsigned)(B.g.ny / TY), (unsigned)B.zch);
+  kern<<<grid, T::THREADS, smem>>>(B.a, B.b, B.g, B.r, real(0), fr);
+  CK(cudaDeviceSynchronize());
+  const double md = B.diff();
+  int nb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T::THREADS, smem));
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  float ms = time_k([&](int p) { kern<<<grid, T::THREADS, smem>>>(p ? B.b : B.a, p ? B.a : B.b, B.g, B.r, real(0), fr); });
+  printf("%-40s %7.3f ms/%d steps %7.4f ms/step %8.0f MLUPS  regs %3d  lmem %3zu  smem %6zu  %d CTA/SM  maxdiff %.3e\n",
+         tag, ms, D, ms / D, D * B.cells / (ms * 1e-3) / 1e6, fa.numRegs, fa.localSizeBytes, smem, nb, md);
+}
+
 int main(int argc, char **argv) {
   const int which = argc > 1 ? atoi(argv[1]) : 0;  // 0 both, 1 fp32, 2 fp64
   const int zch = argc > 2 ? atoi(argv[2]) : 6;
   if (which != 2) {
     Bench<float> B(256, 256, 256, zch);
     run_ref<float, 3, false>(B, "C2 f32 k_pull2 16x8 PF (product)");
-    run_k2<float, 32, 16, 1, true, false>(B, "C2 f32 k2 32x16 minb 1 pf");
-    run_k2<float, 32, 16, 1, true, true>(B, "C2 f32 k2 32x16 minb 1 pf trim");
-    run_k2<float, 32, 16, 1, false, true>(B, "C2 f32 k2 32x16 minb 1 trim");
-    run_k2<float, 16, 32, 1, true, true>(B, "C2 f32 k2 16x32 minb 1 pf trim");
-    run_k2<float, 32, 12, 1, true, true>(B, "C2 f32 k2 32x12 minb 1 pf trim");
+    run_d3<float, 16, 8, 2, 3, true>(B, "C2 f32 depth 2 16x8 minb 3");
+    run_d3<float, 16, 8, 3, 2, true>(B, "C2 f32 depth 3 16x8 minb 2");
+    run_d3<float, 16, 8, 3, 3, true>(B, "C2 f32 depth 3 16x8 minb 3");
+    run_d3<float, 16, 16, 3, 1, true>(B, "C2 f32 depth 3 16x16 minb 1");
+    run_d3<float, 32, 8, 3, 1, true>(B, "C2 f32 depth 3 32x8 minb 1");
   }
   if (which != 1) {
     Bench<double> B(256, 256, 256, zch);
     run_ref<double, 2, true>(B, "C2 f64 k_pull2 16x8 PF trim (product)");
-    run_k2<double, 32, 16, 1, false, true>(B, "C2 f64 k2 32x16 minb 1 trim");
+    run_d3<double, 16, 8, 2, 2, true>(B, "C2 f64 depth 2 16x8 minb 2");
+    run_d3<double, 16, 8, 3, 1, true>(B, "C2 f64 depth 3 16x8 minb 1");
+    run_d3<double, 16, 8, 3, 2, true>(B, "C2 f64 depth 3 16x8 minb 2");
   }
   return 0;
 }
